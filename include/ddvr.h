@@ -1,0 +1,156 @@
+/*
+ * ddvr.h -- C ABI of the B200-native differentiable emission-absorption
+ * raymarcher (DiffDVR, arXiv 2107.12672).
+ *
+ * Drop-in boundary for the reference package ``voldiff`` (pure NumPy; it has
+ * no FFI of its own).  Each entry point replaces one reference function on
+ * the hot path -- the Python host side (paper_2107_12672_b200/_native.py) binds
+ * them with ctypes exactly as a maintainer would from the reference:
+ *
+ *   ddvr_forward      <- voldiff.renderer.render              renderer.py:393-401
+ *                        (_render_scene :376-390, _march_fused :306-357)
+ *   ddvr_adjoint      <- voldiff.renderer.render_adjoint      renderer.py:688-700
+ *                        (_adjoint_scene :655-685, _adjoint_tile :491-652)
+ *   ddvr_ray_setup    <- voldiff.renderer._ray_setup/_step_counts  renderer.py:182-214, 360-368
+ *   ddvr_l1_loss      <- voldiff.objectives.l1_loss            objectives.py:38-54
+ *   ddvr_last_error   <- the message of the raised voldiff error (errors.py:4-33)
+ *
+ * Conventions
+ *   - every pointer marked (device) is CUDA device memory owned by the caller;
+ *     nothing is allocated inside the library;
+ *   - all calls are asynchronous and stream-ordered on ``stream`` (a
+ *     cudaStream_t; NULL = legacy default stream);
+ *   - gradient outputs ACCUMULATE (+=) into caller-zeroed buffers, so views can
+ *     be summed across calls and reduced in place by NCCL;
+ *   - volume layout (X,Y,Z) float32, z fastest (== ``values.ravel()``,
+ *     field.py:311-324); images (V, rows, W, 4) float32 premultiplied rgb +
+ *     alpha, row 0 = top (renderer.py:56-81, field.py:222);
+ *   - return value is a ddvr_status; on error ddvr_last_error() (thread-local)
+ *     holds the message.  Status codes map to the reference exceptions:
+ *     INVALID_PARAMETER -> InvalidParameterError, INVALID_INPUT ->
+ *     InvalidInputError, UNSUPPORTED -> UnsupportedConfigurationError.
+ */
+#ifndef DDVR_H
+#define DDVR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDVR_ABI_VERSION 1
+
+typedef enum {
+  DDVR_OK = 0,
+  DDVR_INVALID_PARAMETER = 1,
+  DDVR_INVALID_INPUT = 2,
+  DDVR_UNSUPPORTED = 3,
+  DDVR_CUDA_ERROR = 4
+} ddvr_status;
+
+/* differentiation targets (renderer.py:47); any non-empty combination */
+typedef enum {
+  DDVR_TARGET_CAMERA = 1,
+  DDVR_TARGET_STEPSIZE = 2,
+  DDVR_TARGET_TF = 4,
+  DDVR_TARGET_VOLUME = 8
+} ddvr_target;
+
+/* transfer-function representations */
+typedef enum {
+  DDVR_TF_TEXTURE = 0,   /* R texels (r,g,b,tau), centres (r+.5)/R, clamp-to-edge (field.py:540-549) */
+  DDVR_TF_PIECEWISE = 1, /* K knots (pos, r,g,b,tau), strictly increasing pos in [0,1] */
+  DDVR_TF_GAUSSIAN = 2   /* G components (mu, sigma, r,g,b,tau): sum of bumps (tasks.py:751-766) */
+} ddvr_tf_kind;
+
+/* density grid on a world box (DensityVolume, field.py:35-77) */
+typedef struct {
+  const float* data;     /* (device) X*Y*Z floats, z fastest */
+  int32_t dims[3];       /* X, Y, Z >= 1 */
+  double box_min[3];
+  double box_max[3];     /* box_max > box_min on every axis */
+} ddvr_volume;
+
+/* transfer function (TransferFunction, field.py:108-127) */
+typedef struct {
+  int32_t kind;          /* ddvr_tf_kind */
+  int32_t count;         /* texture: R >= 1; piecewise: K >= 1; gaussian: G >= 1 */
+  const float* params;   /* (device) texture (R,4); piecewise (K,5); gaussian (G,6) */
+} ddvr_tf;
+
+/* one spherical camera (SphericalCamera, field.py:130-156); arrays of these
+ * live in DEVICE memory, one per view, so camera gradients can flow per view */
+typedef struct {
+  double lon_deg;
+  double lat_deg;        /* |lat| < 90 - 1e-3 (validated by the host side) */
+  double radius;         /* > 0 */
+  double center[3];
+  double fov_y_deg;      /* (0, 180) */
+  double reserved;
+} ddvr_camera;
+
+/* march parameters (RenderConfig, renderer.py:84-106) */
+typedef struct {
+  double dt;             /* stepsize > 0 */
+  int32_t width;         /* image size shared by all views, >= 1 */
+  int32_t height;
+  int32_t row0;          /* rows [row0, row1) are processed (row bands, renderer.py:491) */
+  int32_t row1;          /* row1 <= 0 means height */
+  int32_t early_stop;    /* 1: stop rays at alpha > 1-1e-4 (target "none", renderer.py:331-335) */
+  int32_t flags;         /* reserved, 0 */
+  float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
+                            forward writes the transmittance before every sample,
+                            tape[ray * tape_stride + i]; the adjoint then reads it
+                            instead of inverting.  NULL = inversion mode (default). */
+  int64_t tape_stride;   /* >= max step count of any ray of the call */
+} ddvr_params;
+
+/* Front-to-back march of every view.  image_out (device) (V, rows, W, 4);
+ * trans_out (device, nullable) (V, rows, W) receives the final transmittance
+ * T = prod(1 - a) in full fp32 relative precision, which the adjoint's
+ * inversion starts from (1 - alpha loses it when alpha -> 1). */
+int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                 int32_t n_views, const ddvr_params* p, float* image_out, float* trans_out,
+                 void* stream);
+
+/* Back-to-front adjoint with the inversion trick: per-ray state is O(1); no
+ * per-sample tape.  image (device) (V, rows, W, 4) is the forward output for
+ * the same inputs; trans (device, nullable) its transmittance side output
+ * (if NULL, T = 1 - alpha).  seed (device) (V, rows, W, 4) = dLoss/dImage.
+ * Outputs (device, accumulate, NULL when the target bit is clear):
+ *   d_volume float (X*Y*Z); d_tf double (same shape as tf->params);
+ *   d_camera double (V, 2) per degree [lon, lat]; d_dt double (1). */
+int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                 int32_t n_views, const ddvr_params* p, const float* image, const float* trans,
+                 const float* seed, uint32_t target_mask, float* d_volume, double* d_tf,
+                 double* d_camera, double* d_dt, void* stream);
+
+/* Fused L1 loss + seed (objectives.py:38-54) over n floats: seed_out[i] =
+ * sign(x-y)/count (sign(0)=0) and loss_out[0] += sum|x-y|/count (double).
+ * count is the normaliser (total element count over all views/ranks). */
+int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float* seed_out,
+                 double* loss_out, void* stream);
+
+/* Ray setup only (parity tests): tn_tf (device, nullable) (V, rows, W, 2)
+ * double; n_steps (device) (V, rows, W) int32; flags (device, nullable)
+ * (V, rows, W) int32 = entry_axis | clamped << 2 | miss << 3. */
+int ddvr_ray_setup(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_views,
+                   const ddvr_params* p, double* tn_tf, int32_t* n_steps, int32_t* flags,
+                   void* stream);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* ddvr_last_error(void);
+
+/* DDVR_ABI_VERSION of the loaded library. */
+int32_t ddvr_abi_version(void);
+
+/* Number of kernel launches this library issued since load (process-wide). */
+int64_t ddvr_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DDVR_H */

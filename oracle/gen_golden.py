@@ -1,0 +1,213 @@
+"""Generate tests/golden/*.npz by running the REFERENCE itself -- test infrastructure.
+
+Run in the build container only (it imports ``voldiff`` from
+/root/reference/pkg/src, which does not exist on the GPU box):
+
+    python oracle/gen_golden.py
+
+Every fixture stores the reference's fp64 outputs for fp32-representable inputs
+so that (a) ``tests/test_oracle_golden.py`` pins ``oracle/dvr_oracle.py`` to the
+reference on CPU, and (b) the ``-m gpu`` parity tests compare the CUDA path to
+the same numbers.  Large gradients (C4/C5 row bands) are stored sparsely.
+
+Cases (reference call sites in brackets):
+* kat_*      known-answer scenes of test_renderer.py:98-122, 166-175, 251-259
+* rand_*     gradcheck.random_scene (gradcheck.py:44-68) with L1 seeds, all four
+             targets, inversion and stored memory modes (renderer.py:491-685)
+* C1         the full C1 view: image + every target, dense N(0,1) seed
+* C2..C5     row bands of view 0: image band, n_steps, and the config's targets
+* counts     exact per-config sample totals (renderer.py:209-214)
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(ROOT, "tests", "golden")
+sys.path.insert(0, REF)
+sys.path.insert(0, ROOT)
+
+import voldiff as vd                                   # noqa: E402  (the reference)
+from voldiff import renderer as vr                     # noqa: E402
+from voldiff.gradcheck import random_scene             # noqa: E402
+
+from paper_2107_12672_b200.scenes import CONFIGS       # noqa: E402
+
+TARGETS = ("tf", "volume", "camera", "stepsize")
+BANDS = {"C2": (120, 136), "C3": (250, 258), "C4": (254, 258), "C5": (510, 512)}
+
+
+def f32(a):
+    return np.asarray(a, np.float64).astype(np.float32).astype(np.float64)
+
+
+def grads_of(gs, target):
+    return {"tf": gs.d_tf, "volume": gs.d_volume, "camera": gs.d_camera,
+            "stepsize": np.array([gs.d_stepsize]) if gs.d_stepsize is not None else None}[target]
+
+
+def cam_fields(cam):
+    return np.array([cam.lon_deg, cam.lat_deg, cam.radius, *cam.center, cam.fov_y_deg,
+                     cam.width, cam.height], np.float64)
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"  wrote {name}.npz ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+def scene_case(name, volume, texels, cam, dt, seed, targets=TARGETS, modes=("inversion",),
+               early=True, box=((-0.5, -0.5, -0.5), (0.5, 0.5, 0.5))):
+    volume, texels, seed = f32(volume), f32(texels), f32(seed)
+    V = vd.DensityVolume(volume, np.array(box[0]), np.array(box[1]))
+    T = vd.TransferFunction(texels)
+    out = dict(volume=volume.astype(np.float32), texels=texels.astype(np.float32),
+               box=np.array(box, np.float64), cam=cam_fields(cam), dt=np.float64(dt),
+               seed=seed)
+    if early:
+        out["image_none"] = vd.render(V, T, cam, vd.RenderConfig(dt=dt)).data
+    img = vd.render(V, T, cam, vd.RenderConfig(dt=dt, target="volume")).data
+    out["image"] = img
+    u, v = vr._tile_pixels(cam, 0, cam.height)
+    _, _, slab = vr._ray_setup(("density", V, T), cam, u, v)
+    out["n_steps"] = vr._step_counts(slab[0], slab[1], dt, slab[4]).astype(np.int32)
+    for mode in modes:
+        for t in targets:
+            gs = vd.render_adjoint(V, T, cam, vd.RenderConfig(dt=dt, target=t, memory_mode=mode),
+                                   seed)
+            out[f"{mode}_{t}"] = np.asarray(grads_of(gs, t), np.float64)
+            out[f"{mode}_{t}_state_floats"] = np.int64(gs.state_floats)
+    save(name, **out)
+
+
+def kat_cases():
+    ones = np.ones((8, 8, 8))
+    cam = vd.SphericalCamera(0.0, 0.0, 2.0, fov_y_deg=8.0, width=9, height=9)
+    seed = np.ones((9, 9, 4))
+    for tau0 in (0.1, 1.0, 10.0):               # test_renderer.py:105-112
+        scene_case(f"kat_transparency_{tau0:g}", ones, np.tile([0.5, 0.5, 0.5, tau0], (2, 1)),
+                   cam, 0.05, seed)
+    scene_case("kat_emission", ones, np.tile([0.7, 0.7, 0.7, 2.0], (2, 1)), cam, 0.01, seed)
+    scene_case("kat_stepsize", ones, np.tile([0.4, 0.4, 0.4, 1.3], (2, 1)), cam, 0.05, seed)
+    scene_case("kat_empty", np.zeros((4, 4, 4)), np.array([[0, 0, 0, 0], [1, 1, 1, 2.0]]),
+               vd.SphericalCamera(10.0, 5.0, 2.0, width=6, height=6), 0.05, np.ones((6, 6, 4)))
+    scene_case("kat_miss", np.ones((4, 4, 4)), np.tile([1.0, 1.0, 1.0, 5.0], (2, 1)),
+               vd.SphericalCamera(0.0, 80.0, 50.0, fov_y_deg=0.5, width=4, height=4), 0.1,
+               np.ones((4, 4, 4)))
+    rng = np.random.default_rng(42)             # conftest.py:20-41 fixtures
+    small_tf = np.column_stack([rng.uniform(0.05, 1.0, (8, 3)), rng.uniform(0.3, 2.0, 8)])
+    scene_case("kat_untouched", np.full((8, 8, 8), 0.5), f32(small_tf),
+               vd.SphericalCamera(0.0, 0.0, 2.0, fov_y_deg=2.0, width=4, height=4), 0.05,
+               np.ones((4, 4, 4)), targets=("volume",))
+    # non-cubic grid, off-centre box, non-square image, camera off-centre
+    rng = np.random.default_rng(7)
+    vol = f32(rng.uniform(0.05, 0.95, (6, 9, 5)))
+    tex = f32(np.column_stack([rng.uniform(0.05, 1, (5, 3)), rng.uniform(0.3, 2.5, 5)]))
+    cam = vd.SphericalCamera(200.0, -35.0, 2.2, center=np.array([0.1, -0.05, 0.2]),
+                             fov_y_deg=40.0, width=11, height=7)
+    scene_case("kat_anisotropic", vol, tex, cam, 0.037,
+               f32(rng.normal(size=(7, 11, 4))), modes=("inversion", "stored"),
+               box=((-0.4, -0.6, -0.3), (0.6, 0.5, 0.7)))
+    # R = 1 and R = 2 transfer functions
+    for R in (1, 2):
+        tex = f32(np.column_stack([rng.uniform(0.05, 1, (R, 3)), rng.uniform(0.3, 2.5, R)]))
+        scene_case(f"kat_tf_r{R}", f32(rng.uniform(0.1, 0.9, (8, 8, 8))), tex,
+                   vd.SphericalCamera(40.0, 10.0, 2.5, width=8, height=8), 0.06,
+                   f32(rng.normal(size=(8, 8, 4))))
+
+
+def random_cases():
+    for s, R in ((500, 8), (501, 8), (502, 2), (503, 8), (2000, 2), (2001, 8)):
+        sc = random_scene(s, tf_res=R)
+        vol, tex = f32(sc.volume.values), f32(sc.tf.texels)
+        V, T = vd.DensityVolume(vol), vd.TransferFunction(tex)
+        img = vd.render(V, T, sc.cam, vd.RenderConfig(dt=sc.dt, target="volume"))
+        _, seeds = vd.l1_loss([img], [sc.ref])
+        scene_case(f"rand_{s}", vol, tex, sc.cam, sc.dt, seeds[0],
+                   modes=("inversion", "stored"))
+
+
+def config_cases():
+    rng = np.random.default_rng(1234)
+    for name in ("C1", "C2", "C3", "C4", "C5"):
+        c = CONFIGS[name]
+        t0 = time.time()
+        vol = c.volume().astype(np.float64)
+        tex = f32(c.texels())
+        V, T = vd.DensityVolume(vol), vd.TransferFunction(tex)
+        lon, lat = c.view_poses()[0]
+        cam = vd.SphericalCamera(lon, lat, c.radius, fov_y_deg=c.fov, width=c.image,
+                                 height=c.image)
+        r0, r1 = BANDS.get(name, (0, c.image))
+        scene = ("density", V, T)
+        out = dict(texels=tex.astype(np.float32), cam=cam_fields(cam), dt=np.float64(c.dt),
+                   rows=np.array([r0, r1]),
+                   volume_sum=np.float64(vol.sum()),
+                   volume_probe=vol.reshape(-1)[:: max(1, vol.size // 4096)].copy())
+        u, v = vr._tile_pixels(cam, r0, r1)
+        o, w, slab = vr._ray_setup(scene, cam, u, v)
+        n = vr._step_counts(slab[0], slab[1], c.dt, slab[4])
+        out["n_steps"] = n.astype(np.int32)
+        out["tn_tf"] = np.stack([slab[0], slab[1]]).astype(np.float64)
+        band, _ = vr._march_fused(scene, o, w, c.dt, slab, n)
+        out["image"] = band.reshape(r1 - r0, c.image, 4)
+        seed = np.zeros((c.image, c.image, 4))
+        seed[r0:r1] = rng.normal(size=(r1 - r0, c.image, 4))
+        out["seed_band"] = seed[r0:r1].copy()
+        targets = TARGETS if name == "C1" else c.targets
+        for t in targets:
+            gs = vr._adjoint_tile(scene, cam, vd.RenderConfig(dt=c.dt, target=t),
+                                  seed[r0:r1].reshape(-1, 4), (r0, r1),
+                                  final_rgba=band)
+            g = np.asarray(grads_of(gs, t), np.float64)
+            if t == "volume" and name != "C1":
+                nz = np.flatnonzero(g)
+                out["inversion_volume_idx"] = nz.astype(np.int64)
+                out["inversion_volume_val"] = g.reshape(-1)[nz]
+            else:
+                out[f"inversion_{t}"] = g
+        save(name, **out)
+        print(f"  {name}: {time.time() - t0:.1f}s, band samples {int(n.sum())}")
+
+
+def count_cases():
+    from oracle import dvr_oracle as O
+    out = {}
+    for name, c in CONFIGS.items():
+        vol = vd.DensityVolume(np.zeros((2, 2, 2)))
+        total = 0
+        rays = 0
+        for lon, lat in c.view_poses():
+            cam = vd.SphericalCamera(lon, lat, c.radius, fov_y_deg=c.fov, width=c.image,
+                                     height=c.image)
+            for r0 in range(0, c.image, 256):
+                r1 = min(r0 + 256, c.image)
+                u, v = vr._tile_pixels(cam, r0, r1)
+                _, _, slab = vr._ray_setup(("density", vol, None), cam, u, v)
+                total += int(vr._step_counts(slab[0], slab[1], c.dt, slab[4]).sum())
+                rays += u.shape[0]
+        out[name + "_samples"] = np.int64(total)
+        out[name + "_rays"] = np.int64(rays)
+        print(f"  {name}: {rays} rays, {total} samples")
+    save("counts", **out)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    which = sys.argv[1:] or ["kat", "rand", "config", "count"]
+    if "kat" in which:
+        kat_cases()
+    if "rand" in which:
+        random_cases()
+    if "config" in which:
+        config_cases()
+    if "count" in which:
+        count_cases()

@@ -1,0 +1,51 @@
+"""B200-native differentiable emission-absorption raymarcher (DiffDVR, arXiv 2107.12672).
+
+Two faces over the same sm_100a kernels (libddvr.so, include/ddvr.h):
+
+* the reference-compatible API (drop-in for ``voldiff``): ``render``,
+  ``render_adjoint``, ``l1_loss``, the domain dataclasses and exceptions;
+* the tensor API: ``render_views`` / ``DiffDVR`` (a torch.autograd.Function),
+  ``Rig``, ``forward``/``adjoint``/``l1_loss_seed`` and the view-sharded
+  multi-GPU step in ``distributed``.
+"""
+
+from .errors import (
+    CorruptFileError,
+    DomainError,
+    InvalidInputError,
+    InvalidParameterError,
+    MissingMetadataError,
+    NumericalAbortError,
+    UnsupportedConfigurationError,
+    VoldiffError,
+)
+from .voldiff_api import (
+    EPS_ALPHA,
+    EPS_POLE_DEG,
+    DensityVolume,
+    GradientSet,
+    ImageRGBA,
+    RenderConfig,
+    SphericalCamera,
+    TransferFunction,
+    blend,
+    blend_adjoint,
+    blend_invert,
+    l1_loss,
+    render,
+    render_adjoint,
+)
+from .raymarch import DiffDVR, Rig, adjoint, camera_array, forward, l1_loss_seed, render_views
+from .scenes import CONFIGS, absorption_ramp_texels, fibonacci_poses, phantom, preset_texels
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CorruptFileError", "DomainError", "InvalidInputError", "InvalidParameterError",
+    "MissingMetadataError", "NumericalAbortError", "UnsupportedConfigurationError",
+    "VoldiffError", "EPS_ALPHA", "EPS_POLE_DEG", "DensityVolume", "GradientSet", "ImageRGBA",
+    "RenderConfig", "SphericalCamera", "TransferFunction", "blend", "blend_adjoint",
+    "blend_invert", "l1_loss", "render", "render_adjoint", "DiffDVR", "Rig", "adjoint",
+    "camera_array", "forward", "l1_loss_seed", "render_views", "CONFIGS",
+    "absorption_ramp_texels", "fibonacci_poses", "phantom", "preset_texels",
+]

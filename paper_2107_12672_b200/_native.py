@@ -1,0 +1,127 @@
+"""ctypes binding of libddvr.so (include/ddvr.h) -- the only door to the kernels.
+
+There is no CPU fallback: if the shared library is missing or fails to load,
+every call raises ``NativeLibraryError``.  The library is built in-tree by
+``paper_2107_12672_b200/_build.py`` (``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import (
+    InvalidInputError,
+    InvalidParameterError,
+    UnsupportedConfigurationError,
+    VoldiffError,
+)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libddvr.so")
+ABI_VERSION = 1
+
+TARGET_CAMERA = 1
+TARGET_STEPSIZE = 2
+TARGET_TF = 4
+TARGET_VOLUME = 8
+TARGET_BITS = {"camera": TARGET_CAMERA, "stepsize": TARGET_STEPSIZE, "tf": TARGET_TF,
+               "volume": TARGET_VOLUME}
+
+TF_TEXTURE = 0
+TF_PIECEWISE = 1
+TF_GAUSSIAN = 2
+
+EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_l1_loss", "ddvr_ray_setup",
+            "ddvr_last_error", "ddvr_abi_version", "ddvr_launch_count")
+
+
+class NativeLibraryError(VoldiffError, RuntimeError):
+    """libddvr.so is missing, stale or failed to load (no fallback exists)."""
+
+
+class CudaError(VoldiffError, RuntimeError):
+    """A CUDA launch failed inside libddvr."""
+
+
+class DdvrVolume(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("dims", ctypes.c_int32 * 3),
+                ("box_min", ctypes.c_double * 3), ("box_max", ctypes.c_double * 3)]
+
+
+class DdvrTf(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("count", ctypes.c_int32), ("params", ctypes.c_void_p)]
+
+
+class DdvrParams(ctypes.Structure):
+    _fields_ = [("dt", ctypes.c_double), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("row0", ctypes.c_int32), ("row1", ctypes.c_int32),
+                ("early_stop", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("tape", ctypes.c_void_p), ("tape_stride", ctypes.c_int64)]
+
+
+CAMERA_DOUBLES = 8   # sizeof(ddvr_camera) / 8: lon, lat, radius, cx, cy, cz, fov, reserved
+
+_lib = None
+
+
+def _bind(lib):
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    lib.ddvr_forward.argtypes = [P(DdvrVolume), P(DdvrTf), vp, ctypes.c_int32, P(DdvrParams),
+                                 vp, vp, vp]
+    lib.ddvr_forward.restype = ctypes.c_int
+    lib.ddvr_adjoint.argtypes = [P(DdvrVolume), P(DdvrTf), vp, ctypes.c_int32, P(DdvrParams),
+                                 vp, vp, vp, ctypes.c_uint32, vp, vp, vp, vp, vp]
+    lib.ddvr_adjoint.restype = ctypes.c_int
+    lib.ddvr_l1_loss.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_double, vp, vp, vp]
+    lib.ddvr_l1_loss.restype = ctypes.c_int
+    lib.ddvr_ray_setup.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp, vp,
+                                   vp]
+    lib.ddvr_ray_setup.restype = ctypes.c_int
+    lib.ddvr_last_error.argtypes = []
+    lib.ddvr_last_error.restype = ctypes.c_char_p
+    lib.ddvr_abi_version.argtypes = []
+    lib.ddvr_abi_version.restype = ctypes.c_int32
+    lib.ddvr_launch_count.argtypes = []
+    lib.ddvr_launch_count.restype = ctypes.c_int64
+
+
+def lib():
+    """The loaded library; raises NativeLibraryError if it cannot be loaded."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryError(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (there is no CPU fallback)")
+        try:
+            handle = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:
+            raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+        for name in EXPORTED:
+            if not hasattr(handle, name):
+                raise NativeLibraryError(f"{LIB_PATH} does not export {name}")
+        _bind(handle)
+        if handle.ddvr_abi_version() != ABI_VERSION:
+            raise NativeLibraryError(
+                f"{LIB_PATH} ABI {handle.ddvr_abi_version()} != expected {ABI_VERSION}")
+        _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map a ddvr_status to the reference exception classes (errors.py:4-33)."""
+    if rc == 0:
+        return
+    msg = lib().ddvr_last_error().decode(errors="replace")
+    if rc == 1:
+        raise InvalidParameterError(msg)
+    if rc == 2:
+        raise InvalidInputError(msg)
+    if rc == 3:
+        raise UnsupportedConfigurationError(msg)
+    raise CudaError(msg or f"ddvr status {rc}")
+
+
+def launch_count() -> int:
+    return int(lib().ddvr_launch_count())

@@ -1,0 +1,129 @@
+"""View-sharded optimisation step over N GPUs (one process per GPU, NCCL).
+
+The reference sums per-view gradients in view order on one host
+(``_volume_loss_and_grad``, tasks.py:397-432; TF variant tasks.py:258-270).
+Here views are dealt round-robin to ranks (rank r takes views r, r+N, ...),
+every rank renders and differentiates its own views with the replicated
+volume and TF, and ONE all-reduce(sum) over a flat fp32 buffer
+
+    [ d_volume (X*Y*Z) | d_tf (R*4) | d_stepsize (1) | loss (1) ]
+
+combines them.  The L1 seeds only need the global element count, known
+statically (objectives.py:51-53), so the forward/adjoint need no
+communication at all.  Camera gradients are per view and stay local.
+
+The packing and the collective are plain torch.distributed, so the same code
+runs with ``gloo`` on CPU tensors in the tests and ``nccl`` on the GPUs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from . import raymarch as R
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list[int]:
+    """Round-robin view indices of ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    return list(range(rank, n_views, world))
+
+
+@dataclass
+class FlatGrads:
+    """One contiguous fp32 buffer holding every all-reduced quantity of a step."""
+
+    n_vox: int
+    n_tf: int
+    buf: torch.Tensor
+
+    @classmethod
+    def zeros(cls, n_vox: int, n_tf: int, device) -> "FlatGrads":
+        return cls(n_vox, n_tf, torch.zeros(n_vox + n_tf + 2, dtype=torch.float32, device=device))
+
+    @property
+    def d_volume(self) -> torch.Tensor:
+        return self.buf[: self.n_vox]
+
+    @property
+    def d_tf(self) -> torch.Tensor:
+        return self.buf[self.n_vox: self.n_vox + self.n_tf]
+
+    @property
+    def d_stepsize(self) -> torch.Tensor:
+        return self.buf[self.n_vox + self.n_tf: self.n_vox + self.n_tf + 1]
+
+    @property
+    def loss(self) -> torch.Tensor:
+        return self.buf[self.n_vox + self.n_tf + 1:]
+
+    def allreduce(self, group=None) -> None:
+        """Sum the buffer over all ranks in place (one collective)."""
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=group)
+
+
+class ShardedStep:
+    """One forward + L1 + adjoint + all-reduce step over this rank's views.
+
+    density (X,Y,Z) fp32, texels (R,4) fp32 on this rank's GPU (replicated);
+    refs: (V_local, H, W, 4) fp32 reference images of the local views;
+    lonlat: (V_local, 2) poses; ``total_elements`` = 4*H*W*V_global.
+    """
+
+    def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
+                 total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
+                 group=None):
+        self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
+        self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
+        self.mask = 0
+        for t in targets:
+            self.mask |= N.TARGET_BITS[t]
+        if self.mask & N.TARGET_CAMERA:
+            raise ValueError("camera gradients are per view; use the single-view API")
+        self.count = float(total_elements if total_elements is not None else refs.numel())
+        self.group = group
+        dev = density.device
+        V = self.cams.shape[0]
+        self.flat = FlatGrads.zeros(density.numel(), texels.numel(), dev)
+        self.img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=dev)
+        self.seed = torch.empty_like(self.img)
+        self.trans = torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=dev)
+        self.d_tf64 = torch.zeros(texels.shape, dtype=torch.float64, device=dev)
+        self.d_dt64 = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.loss64 = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def run(self) -> FlatGrads:
+        import ctypes
+        f = self.flat
+        f.buf.zero_()
+        self.d_tf64.zero_()
+        self.d_dt64.zero_()
+        self.loss64.zero_()
+        V = self.cams.shape[0]
+        if V:
+            vol, tf, prm = R._descs(self.density, self.texels, self.rig, self.dt, False)
+            lib = N.lib()
+            st = R._stream_ptr()
+            N.check(lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
+                                     ctypes.byref(prm), self.img.data_ptr(), self.trans.data_ptr(),
+                                     st))
+            N.check(lib.ddvr_l1_loss(self.img.data_ptr(), self.refs.data_ptr(), self.img.numel(),
+                                     self.count, self.seed.data_ptr(), self.loss64.data_ptr(), st))
+            want = lambda bit, t: t.data_ptr() if self.mask & bit else None  # noqa: E731
+            N.check(lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
+                                     ctypes.byref(prm), self.img.data_ptr(),
+                                     self.trans.data_ptr(), self.seed.data_ptr(), self.mask,
+                                     want(N.TARGET_VOLUME, f.d_volume),
+                                     want(N.TARGET_TF, self.d_tf64), None,
+                                     want(N.TARGET_STEPSIZE, self.d_dt64), st))
+        f.d_tf.copy_(self.d_tf64.reshape(-1))
+        f.d_stepsize.copy_(self.d_dt64)
+        f.loss.copy_(self.loss64)
+        f.allreduce(self.group)
+        return f

@@ -1,0 +1,230 @@
+"""Tensor-level raymarcher over CUDA tensors: ops and the autograd Function.
+
+This is the B200 product path: torch owns device memory and streams, every
+compute step is a libddvr kernel reached through the C ABI (``_native``).
+
+    images = render_views(density, texels, lonlat, dt, rig)     # differentiable
+
+``DiffDVR.backward`` launches ONE adjoint kernel whose target mask is
+``ctx.needs_input_grad`` and saves only the output images and the per-pixel
+transmittance: O(pixels) memory, the paper's inversion trick
+(renderer.py:540-543, 576-580).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from .errors import InvalidInputError, InvalidParameterError
+
+EPS_POLE_DEG = 1e-3    # field.py:24
+
+
+@dataclass(frozen=True)
+class Rig:
+    """Static geometry shared by every view of a batch.
+
+    The image size is common to all views (images are (V, H, W, 4));
+    ``rows`` restricts every view to a row band [r0, r1) (renderer.py:491).
+    """
+
+    width: int
+    height: int
+    box_min: tuple = (-0.5, -0.5, -0.5)
+    box_max: tuple = (0.5, 0.5, 0.5)
+    rows: tuple | None = None
+
+    @property
+    def band(self) -> tuple:
+        return self.rows if self.rows is not None else (0, self.height)
+
+    @property
+    def band_rows(self) -> int:
+        r0, r1 = self.band
+        return r1 - r0
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _require(t: torch.Tensor, name: str, dtype, *, ndim=None, align16=False):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidInputError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise InvalidInputError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise InvalidInputError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() != ndim:
+        raise InvalidInputError(f"{name} must have {ndim} dims, got shape {tuple(t.shape)}")
+    if align16 and t.data_ptr() % 16:
+        raise InvalidInputError(f"{name} must be 16-byte aligned")
+
+
+def camera_array(lonlat: torch.Tensor, radius=2.0, center=(0.0, 0.0, 0.0),
+                 fov_y_deg=30.0) -> torch.Tensor:
+    """(V, 8) float64 device array of ddvr_camera records from (V, 2) lon/lat degrees."""
+    ll = lonlat.detach().to(torch.float64)
+    V = ll.shape[0]
+    dev = ll.device
+    rad = torch.as_tensor(radius, dtype=torch.float64, device=dev).reshape(-1, 1).expand(V, 1)
+    ctr = torch.as_tensor(center, dtype=torch.float64, device=dev).reshape(-1, 3).expand(V, 3)
+    fov = torch.as_tensor(fov_y_deg, dtype=torch.float64, device=dev).reshape(-1, 1).expand(V, 1)
+    pad = torch.zeros(V, 1, dtype=torch.float64, device=dev)
+    return torch.cat([ll, rad, ctr, fov, pad], dim=1).contiguous()
+
+
+def validate_cameras(lonlat, radius, fov_y_deg):
+    """Host-side checks of field.py:147-156 (one device->host copy)."""
+    ll = torch.as_tensor(lonlat).detach().to("cpu", torch.float64)
+    if ll.numel() and bool((ll[:, 1].abs() >= 90.0 - EPS_POLE_DEG).any()):
+        raise InvalidParameterError("latitude violates the pole exclusion")
+    if bool((torch.as_tensor(radius, dtype=torch.float64) <= 0).any()):
+        raise InvalidParameterError("camera radius must be positive")
+    f = torch.as_tensor(fov_y_deg, dtype=torch.float64)
+    if bool(((f <= 0) | (f >= 180)).any()):
+        raise InvalidParameterError("vertical field of view must be in (0, 180)")
+
+
+def _descs(density: torch.Tensor, texels: torch.Tensor, rig: Rig, dt: float, early_stop: bool):
+    _require(density, "density", torch.float32, ndim=3)
+    _require(texels, "texels", torch.float32, ndim=2, align16=True)
+    if texels.shape[1] != 4:
+        raise InvalidParameterError("transfer function must have shape (R, 4), R >= 1")
+    vol = N.DdvrVolume(density.data_ptr(), (ctypes.c_int32 * 3)(*density.shape),
+                       (ctypes.c_double * 3)(*rig.box_min), (ctypes.c_double * 3)(*rig.box_max))
+    tf = N.DdvrTf(N.TF_TEXTURE, texels.shape[0], texels.data_ptr())
+    r0, r1 = rig.band
+    prm = N.DdvrParams(float(dt), rig.width, rig.height, r0, r1, 1 if early_stop else 0, 0)
+    return vol, tf, prm
+
+
+def forward(density, texels, cams, dt: float, rig: Rig, *, early_stop=False, with_trans=True):
+    """Images (V, rows, W, 4) fp32 and final transmittance (V, rows, W) (or None)."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    vol, tf, prm = _descs(density, texels, rig, dt, early_stop)
+    V = cams.shape[0]
+    img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=density.device)
+    trans = (torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=density.device)
+             if with_trans else None)
+    N.check(N.lib().ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,
+                                 ctypes.byref(prm), img.data_ptr(),
+                                 trans.data_ptr() if trans is not None else None, _stream_ptr()))
+    return img, trans
+
+
+def adjoint(density, texels, cams, dt: float, rig: Rig, image, trans, seed, mask: int, *,
+            d_volume=None, d_tf=None, d_camera=None, d_dt=None):
+    """Accumulate gradients of sum(seed * image) into the given buffers (+=)."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    vol, tf, prm = _descs(density, texels, rig, dt, False)
+    V = cams.shape[0]
+    shape = (V, rig.band_rows, rig.width, 4)
+    _require(seed, "seed", torch.float32)
+    if tuple(seed.shape) != shape:
+        raise InvalidInputError(f"seed shape {tuple(seed.shape)} does not match image {shape}")
+    if image is not None:
+        _require(image, "image", torch.float32)
+        if tuple(image.shape) != shape:
+            raise InvalidInputError("provided image does not match the camera size")
+    if trans is not None:
+        _require(trans, "transmittance", torch.float32)
+    for buf, name, dt_ in ((d_volume, "d_volume", torch.float32), (d_tf, "d_tf", torch.float64),
+                           (d_camera, "d_camera", torch.float64), (d_dt, "d_dt", torch.float64)):
+        if buf is not None:
+            _require(buf, name, dt_)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    N.check(N.lib().ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,
+                                 ctypes.byref(prm), ptr(image), ptr(trans), seed.data_ptr(),
+                                 mask, ptr(d_volume), ptr(d_tf), ptr(d_camera), ptr(d_dt),
+                                 _stream_ptr()))
+
+
+def l1_loss_seed(images: torch.Tensor, refs: torch.Tensor, count: float | None = None):
+    """(loss (1,) float64, seed like images) of mean |x - y| (objectives.py:38-54)."""
+    _require(images, "images", torch.float32)
+    _require(refs, "refs", torch.float32)
+    if images.shape != refs.shape:
+        raise InvalidInputError(f"image shape {tuple(images.shape)} != reference shape "
+                                f"{tuple(refs.shape)}")
+    count = float(images.numel()) if count is None else float(count)
+    seed = torch.empty_like(images)
+    loss = torch.zeros(1, dtype=torch.float64, device=images.device)
+    N.check(N.lib().ddvr_l1_loss(images.data_ptr(), refs.data_ptr(), images.numel(), count,
+                                 seed.data_ptr(), loss.data_ptr(), _stream_ptr()))
+    return loss, seed
+
+
+def ray_setup(cams, dt: float, rig: Rig, dims=(2, 2, 2)):
+    """(tn_tf (V,rows,W,2) f64, n_steps (V,rows,W) i32, flags i32) for parity tests."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    vol = N.DdvrVolume(None, (ctypes.c_int32 * 3)(*dims), (ctypes.c_double * 3)(*rig.box_min),
+                       (ctypes.c_double * 3)(*rig.box_max))
+    r0, r1 = rig.band
+    prm = N.DdvrParams(float(dt), rig.width, rig.height, r0, r1, 0, 0)
+    V = cams.shape[0]
+    dev = cams.device
+    tn_tf = torch.empty(V, rig.band_rows, rig.width, 2, dtype=torch.float64, device=dev)
+    n = torch.empty(V, rig.band_rows, rig.width, dtype=torch.int32, device=dev)
+    fl = torch.empty_like(n)
+    N.check(N.lib().ddvr_ray_setup(ctypes.byref(vol), cams.data_ptr(), V, ctypes.byref(prm),
+                                   tn_tf.data_ptr(), n.data_ptr(), fl.data_ptr(), _stream_ptr()))
+    return tn_tf, n, fl
+
+
+class DiffDVR(torch.autograd.Function):
+    """images = DiffDVR.apply(density, texels, lonlat, dt, rig, radius, center, fov).
+
+    density (X,Y,Z) fp32, texels (R,4) fp32, lonlat (V,2) degrees, dt a 0-d
+    tensor (stepsize).  Gradients: density, texels, lonlat (per degree), dt.
+    """
+
+    @staticmethod
+    def forward(ctx, density, texels, lonlat, dt, rig: Rig, radius, center, fov):
+        cams = camera_array(lonlat.to(density.device), radius, center, fov)
+        dtv = float(dt)
+        img, trans = forward(density.contiguous(), texels.contiguous(), cams, dtv, rig)
+        ctx.save_for_backward(density, texels, img, trans)
+        ctx.cams, ctx.dt, ctx.rig = cams, dtv, rig
+        ctx.lonlat_meta = (lonlat.dtype, lonlat.device)
+        ctx.dt_meta = (dt.dtype, dt.device) if isinstance(dt, torch.Tensor) else None
+        ctx.mark_non_differentiable(trans)
+        return img
+
+    @staticmethod
+    def backward(ctx, grad_img):
+        density, texels, img, trans = ctx.saved_tensors
+        need = ctx.needs_input_grad
+        mask = ((N.TARGET_VOLUME if need[0] else 0) | (N.TARGET_TF if need[1] else 0)
+                | (N.TARGET_CAMERA if need[2] else 0) | (N.TARGET_STEPSIZE if need[3] else 0))
+        if mask == 0:
+            return (None,) * 8
+        dev = density.device
+        d_vol = torch.zeros_like(density) if need[0] else None
+        d_tf = torch.zeros(texels.shape, dtype=torch.float64, device=dev) if need[1] else None
+        d_cam = (torch.zeros(ctx.cams.shape[0], 2, dtype=torch.float64, device=dev)
+                 if need[2] else None)
+        d_dt = torch.zeros(1, dtype=torch.float64, device=dev) if need[3] else None
+        adjoint(density.contiguous(), texels.contiguous(), ctx.cams, ctx.dt, ctx.rig, img, trans,
+                grad_img.contiguous().to(torch.float32), mask, d_volume=d_vol, d_tf=d_tf,
+                d_camera=d_cam, d_dt=d_dt)
+        g_tf = d_tf.to(texels.dtype) if d_tf is not None else None
+        g_cam = d_cam.to(*ctx.lonlat_meta) if d_cam is not None else None
+        g_dt = None
+        if d_dt is not None and ctx.dt_meta is not None:
+            g_dt = d_dt.reshape(()).to(ctx.dt_meta[0]).to(ctx.dt_meta[1])
+        return d_vol, g_tf, g_cam, g_dt, None, None, None, None
+
+
+def render_views(density, texels, lonlat, dt, rig: Rig, *, radius=2.0, center=(0.0, 0.0, 0.0),
+                 fov_y_deg=30.0):
+    """Differentiable images (V, rows, W, 4) of ``lonlat`` views (autograd-aware)."""
+    if not isinstance(dt, torch.Tensor):
+        dt = torch.tensor(float(dt), dtype=torch.float64)
+    if float(dt) <= 0.0:
+        raise InvalidParameterError("stepsize must be positive")
+    return DiffDVR.apply(density, texels, lonlat, dt, rig, radius, center, fov_y_deg)

@@ -1,0 +1,409 @@
+"""Drop-in replacement for the reference's render / loss API (voldiff).
+
+Same names, signatures, argument meaning and exceptions as
+``voldiff.renderer.render`` (renderer.py:393-401), ``render_adjoint``
+(renderer.py:688-700) and ``voldiff.objectives.l1_loss`` (objectives.py:38-54),
+plus the domain dataclasses they take (field.py:35-156, renderer.py:56-118).
+Inputs may be the reference's own objects (duck-typed ``.values``,
+``.texels``, camera fields) or the classes below.  Results come back as
+float64 NumPy, like the reference.
+
+Every numerical result is computed by libddvr on the current CUDA device; the
+``threads`` keyword is accepted and ignored (the GPU replaces the tile pool,
+renderer.py:243-247).  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import raymarch as R
+from .errors import (
+    InvalidInputError,
+    InvalidParameterError,
+    UnsupportedConfigurationError,
+)
+
+EPS_POLE_DEG = 1e-3      # field.py:24
+EPS_ALPHA = 1e-6         # field.py:25
+TILE_ROWS = 64           # renderer.py:44 (only used for the stored-mode memory counter)
+_TARGETS = ("none", "camera", "stepsize", "tf", "volume")     # renderer.py:47
+_MEMORY_MODES = ("inversion", "stored")                        # renderer.py:48
+
+
+# ---------------------------------------------------------------------------
+# domain types (field.py:35-156; renderer.py:56-118)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class DensityVolume:
+    """3D scalar grid (X,Y,Z) on a world box (field.py:35-77)."""
+
+    values: np.ndarray
+    box_min: np.ndarray = dc_field(default_factory=lambda: np.array([-0.5, -0.5, -0.5]))
+    box_max: np.ndarray = dc_field(default_factory=lambda: np.array([0.5, 0.5, 0.5]))
+
+    def __post_init__(self):
+        self.values = np.asarray(self.values, dtype=np.float64)
+        self.box_min = np.asarray(self.box_min, dtype=np.float64).reshape(3)
+        self.box_max = np.asarray(self.box_max, dtype=np.float64).reshape(3)
+        if self.values.ndim != 3 or min(self.values.shape) < 1:
+            raise InvalidParameterError("volume values must be a non-empty 3D array")
+        if not np.all(np.isfinite(self.values)):
+            raise InvalidParameterError("volume contains non-finite densities")
+        if not np.all(self.box_max > self.box_min):
+            raise InvalidParameterError("world box must have positive extent on each axis")
+
+    @property
+    def dims(self):
+        return self.values.shape
+
+    @property
+    def extent(self):
+        return self.box_max - self.box_min
+
+    @property
+    def voxel_size(self):
+        return self.extent / np.asarray(self.values.shape, dtype=np.float64)
+
+
+@dataclass
+class TransferFunction:
+    """R texels of (r, g, b, tau) with linear interpolation (field.py:108-127)."""
+
+    texels: np.ndarray
+
+    def __post_init__(self):
+        self.texels = np.asarray(self.texels, dtype=np.float64)
+        if self.texels.ndim != 2 or self.texels.shape[1] != 4 or self.texels.shape[0] < 1:
+            raise InvalidParameterError("transfer function must have shape (R, 4), R >= 1")
+        if not np.all(np.isfinite(self.texels)):
+            raise InvalidParameterError("transfer function contains non-finite entries")
+
+    @property
+    def resolution(self):
+        return self.texels.shape[0]
+
+
+@dataclass
+class SphericalCamera:
+    """Camera on a sphere around ``center`` looking at it, up = +Y (field.py:130-156)."""
+
+    lon_deg: float
+    lat_deg: float
+    radius: float
+    center: np.ndarray = dc_field(default_factory=lambda: np.zeros(3))
+    fov_y_deg: float = 30.0
+    width: int = 64
+    height: int = 64
+
+    def __post_init__(self):
+        self.lon_deg = float(self.lon_deg) % 360.0
+        self.lat_deg = float(self.lat_deg)
+        self.radius = float(self.radius)
+        self.center = np.asarray(self.center, dtype=np.float64).reshape(3)
+        if abs(self.lat_deg) >= 90.0 - EPS_POLE_DEG:
+            raise InvalidParameterError(f"latitude {self.lat_deg} deg violates the pole exclusion")
+        if self.radius <= 0.0:
+            raise InvalidParameterError("camera radius must be positive")
+        if not 0.0 < self.fov_y_deg < 180.0:
+            raise InvalidParameterError("vertical field of view must be in (0, 180)")
+        if self.width < 1 or self.height < 1:
+            raise InvalidParameterError("image size must be at least 1x1")
+
+
+@dataclass
+class ImageRGBA:
+    """Premultiplied rgb + accumulated opacity, shape (H, W, 4) (renderer.py:56-81)."""
+
+    data: np.ndarray
+
+    def __post_init__(self):
+        self.data = np.asarray(self.data, dtype=np.float64)
+        if self.data.ndim != 3 or self.data.shape[2] != 4:
+            raise InvalidInputError("image data must have shape (H, W, 4)")
+
+    @classmethod
+    def zeros(cls, width, height):
+        return cls(np.zeros((height, width, 4)))
+
+    @property
+    def width(self):
+        return self.data.shape[1]
+
+    @property
+    def height(self):
+        return self.data.shape[0]
+
+    @property
+    def alpha(self):
+        return self.data[..., 3]
+
+
+@dataclass
+class RenderConfig:
+    """Stepsize, differentiation target and adjoint memory mode (renderer.py:84-106)."""
+
+    dt: float
+    target: str = "none"
+    memory_mode: str = "inversion"
+    precision: str = "double"
+
+    def __post_init__(self):
+        _validate_config(self)
+
+    @property
+    def dtype(self):
+        return np.float64 if self.precision == "double" else np.float32
+
+
+@dataclass
+class GradientSet:
+    """Gradients for the selected target; the others stay None (renderer.py:109-118)."""
+
+    d_stepsize: float | None = None
+    d_camera: np.ndarray | None = None
+    d_tf: np.ndarray | None = None
+    d_volume: np.ndarray | None = None
+    d_color: np.ndarray | None = None
+    state_floats: int = 0
+
+
+def _validate_config(cfg):
+    dt = float(cfg.dt)
+    if not dt > 0.0:
+        raise InvalidParameterError("stepsize must be positive")
+    if cfg.target not in _TARGETS:
+        raise InvalidParameterError(f"unknown differentiation target {cfg.target!r}")
+    if getattr(cfg, "memory_mode", "inversion") not in _MEMORY_MODES:
+        raise InvalidParameterError(f"unknown memory mode {cfg.memory_mode!r}")
+    if getattr(cfg, "precision", "double") not in ("double", "single"):
+        raise InvalidParameterError("precision must be 'double' or 'single'")
+    cfg.dt = dt
+
+
+# ---------------------------------------------------------------------------
+# compositing algebra on single states (renderer.py:126-174); host helpers
+# ---------------------------------------------------------------------------
+
+
+def blend(state, sample):
+    """One front-to-back compositing step (renderer.py:126-138)."""
+    state = np.asarray(state, np.float64)
+    sample = np.asarray(sample, np.float64)
+    vis = 1.0 - state[..., 3:4]
+    out = np.empty(np.broadcast_shapes(state.shape, sample.shape))
+    out[..., :3] = state[..., :3] + vis * sample[..., :3]
+    out[..., 3:4] = state[..., 3:4] + vis * sample[..., 3:4]
+    return out
+
+
+def blend_invert(nxt, sample):
+    """Exact inverse of :func:`blend` given the blended sample (renderer.py:141-152)."""
+    nxt = np.asarray(nxt, np.float64)
+    sample = np.asarray(sample, np.float64)
+    a_s = sample[..., 3]
+    if np.any(a_s > 1.0 - EPS_ALPHA + 1e-15):
+        raise InvalidInputError("sample opacity exceeds the invertibility clamp")
+    a_prev = (a_s - nxt[..., 3]) / (a_s - 1.0)
+    out = np.empty(np.broadcast_shapes(nxt.shape, sample.shape))
+    out[..., :3] = nxt[..., :3] - (1.0 - a_prev)[..., None] * sample[..., :3]
+    out[..., 3] = a_prev
+    return out
+
+
+def blend_adjoint(state, sample, next_hat):
+    """(state_hat, sample_hat) = transpose of the blend Jacobian (renderer.py:155-174)."""
+    state = np.asarray(state, np.float64)
+    sample = np.asarray(sample, np.float64)
+    next_hat = np.asarray(next_hat, np.float64)
+    vis = 1.0 - state[..., 3]
+    shape = np.broadcast_shapes(state.shape, sample.shape, next_hat.shape)
+    state_hat = np.empty(shape)
+    sample_hat = np.empty(shape)
+    state_hat[..., :3] = next_hat[..., :3]
+    state_hat[..., 3] = (1.0 - sample[..., 3]) * next_hat[..., 3] - np.sum(
+        sample[..., :3] * next_hat[..., :3], axis=-1)
+    sample_hat[..., :3] = vis[..., None] * next_hat[..., :3]
+    sample_hat[..., 3] = vis * next_hat[..., 3]
+    return state_hat, sample_hat
+
+
+# ---------------------------------------------------------------------------
+# upload helpers
+# ---------------------------------------------------------------------------
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise N.NativeLibraryError("no CUDA device: the B200 raymarcher has no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _upload(volume, tf, cam, dev):
+    values = np.asarray(volume.values)
+    if values.ndim != 3:
+        raise InvalidParameterError("volume values must be a non-empty 3D array")
+    dens = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
+    tex = torch.from_numpy(np.ascontiguousarray(np.asarray(tf.texels), dtype=np.float32)).to(dev)
+    if tex.dim() != 2 or tex.shape[1] != 4:
+        raise InvalidParameterError("transfer function must have shape (R, 4), R >= 1")
+    ll = torch.tensor([[float(cam.lon_deg), float(cam.lat_deg)]], dtype=torch.float64)
+    cams = R.camera_array(ll.to(dev), float(cam.radius),
+                          tuple(np.asarray(cam.center, np.float64).reshape(3)),
+                          float(cam.fov_y_deg))
+    rig = R.Rig(int(cam.width), int(cam.height),
+                tuple(np.asarray(volume.box_min, np.float64).reshape(3)),
+                tuple(np.asarray(volume.box_max, np.float64).reshape(3)))
+    return dens, tex, cams, rig
+
+
+def _image_from(img, trans):
+    """fp64 ImageRGBA with alpha = 1 - T evaluated in fp64 (keeps T exact for the adjoint)."""
+    data = img[0].to(torch.float64)
+    data[..., 3] = 1.0 - trans[0].to(torch.float64)
+    return ImageRGBA(data.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# public entry points
+# ---------------------------------------------------------------------------
+
+
+def render(volume, tf, cam, cfg, *, threads: int = 1) -> ImageRGBA:
+    """Direct volume rendering (renderer.py:393-401); early termination only for target none."""
+    _validate_config(cfg)
+    dev = _device()
+    dens, tex, cams, rig = _upload(volume, tf, cam, dev)
+    img, trans = R.forward(dens, tex, cams, cfg.dt, rig, early_stop=(cfg.target == "none"))
+    return _image_from(img, trans)
+
+
+def _stored_tape_len(cams, dt, rig):
+    _, n, _ = R.ray_setup(cams, dt, rig)
+    return n
+
+
+def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) -> GradientSet:
+    """Gradient of sum(seed * image) for ``cfg.target`` (renderer.py:688-700, 655-685)."""
+    _validate_config(cfg)
+    if cfg.target == "none":
+        raise UnsupportedConfigurationError("adjoint requires a differentiation target")
+    seed_arr = seed.data if hasattr(seed, "data") and not isinstance(seed, np.ndarray) else seed
+    seed_arr = np.asarray(seed_arr, dtype=np.float64)
+    H, W = int(cam.height), int(cam.width)
+    if seed_arr.shape != (H, W, 4):
+        raise InvalidInputError(f"seed shape {seed_arr.shape} does not match image {(H, W, 4)}")
+    img_arr = None
+    if image is not None:
+        img_arr = image.data if hasattr(image, "data") and not isinstance(image, np.ndarray) \
+            else image
+        img_arr = np.asarray(img_arr, dtype=np.float64)
+        if img_arr.shape != (H, W, 4):
+            raise InvalidInputError("provided image does not match the camera size")
+    dev = _device()
+    dens, tex, cams, rig = _upload(volume, tf, cam, dev)
+    stored = getattr(cfg, "memory_mode", "inversion") == "stored"
+    tape = None
+    n_steps = None
+    if stored:
+        n_steps = _stored_tape_len(cams, cfg.dt, rig)
+        stride = max(int(n_steps.max().item()), 1)
+        tape = torch.empty(H * W * stride, dtype=torch.float32, device=dev)
+        img_t, trans_t = _forward_tape(dens, tex, cams, cfg.dt, rig, tape, stride)
+    elif img_arr is None:
+        img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig)
+    else:
+        img_t = torch.from_numpy(img_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
+        trans_t = torch.from_numpy((1.0 - img_arr[..., 3]).astype(np.float32)).to(dev)
+        trans_t = trans_t.reshape(1, H, W)
+    seed_t = torch.from_numpy(seed_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
+    bit = N.TARGET_BITS[cfg.target]
+    d_vol = torch.zeros_like(dens) if bit == N.TARGET_VOLUME else None
+    d_tf = torch.zeros(tex.shape, dtype=torch.float64, device=dev) if bit == N.TARGET_TF else None
+    d_cam = torch.zeros(1, 2, dtype=torch.float64, device=dev) if bit == N.TARGET_CAMERA else None
+    d_dt = torch.zeros(1, dtype=torch.float64, device=dev) if bit == N.TARGET_STEPSIZE else None
+    if stored:
+        _adjoint_tape(dens, tex, cams, cfg.dt, rig, img_t, trans_t, seed_t, bit, tape, stride,
+                      d_vol, d_tf, d_cam, d_dt)
+    else:
+        R.adjoint(dens, tex, cams, cfg.dt, rig, img_t, trans_t, seed_t, bit, d_volume=d_vol,
+                  d_tf=d_tf, d_camera=d_cam, d_dt=d_dt)
+    # per-ray state: inversion keeps (C, A) and the constant seed, 8 floats per ray,
+    # independent of the step count (renderer.py:513); stored mode keeps a tape
+    # of one transmittance per sample, n_max per 64-row tile.
+    if stored:
+        n_cpu = n_steps[0].cpu().numpy()
+        state = 8 * H * W + sum(int(n_cpu[r:r + TILE_ROWS].max()) * n_cpu[r:r + TILE_ROWS].size
+                                for r in range(0, H, TILE_ROWS))
+    else:
+        state = 8 * H * W
+    out = GradientSet(state_floats=int(state))
+    if d_vol is not None:
+        out.d_volume = d_vol.to(torch.float64).cpu().numpy()
+    if d_tf is not None:
+        out.d_tf = d_tf.cpu().numpy()
+    if d_cam is not None:
+        out.d_camera = d_cam[0].cpu().numpy()
+    if d_dt is not None:
+        out.d_stepsize = float(d_dt.item())
+    return out
+
+
+def _forward_tape(dens, tex, cams, dt, rig, tape, stride):
+    import ctypes
+    vol, tf, prm = R._descs(dens, tex, rig, dt, False)
+    prm.tape = tape.data_ptr()
+    prm.tape_stride = stride
+    img = torch.empty(1, rig.height, rig.width, 4, dtype=torch.float32, device=dens.device)
+    trans = torch.empty(1, rig.height, rig.width, dtype=torch.float32, device=dens.device)
+    N.check(N.lib().ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), 1,
+                                 ctypes.byref(prm), img.data_ptr(), trans.data_ptr(),
+                                 R._stream_ptr()))
+    return img, trans
+
+
+def _adjoint_tape(dens, tex, cams, dt, rig, img, trans, seed, mask, tape, stride, d_vol, d_tf,
+                  d_cam, d_dt):
+    import ctypes
+    vol, tf, prm = R._descs(dens, tex, rig, dt, False)
+    prm.tape = tape.data_ptr()
+    prm.tape_stride = stride
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    N.check(N.lib().ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), 1,
+                                 ctypes.byref(prm), img.data_ptr(), trans.data_ptr(),
+                                 seed.data_ptr(), mask, ptr(d_vol), ptr(d_tf), ptr(d_cam),
+                                 ptr(d_dt), R._stream_ptr()))
+
+
+def l1_loss(images, refs):
+    """(mean |x - y|, [sign(x - y)/count]) over all images (objectives.py:38-54)."""
+    if len(images) != len(refs):
+        raise InvalidInputError("image and reference counts differ")
+    arr = lambda im: im.data if isinstance(im, ImageRGBA) or hasattr(im, "alpha") \
+        else np.asarray(im, np.float64)  # noqa: E731
+    xs = [np.asarray(arr(im), np.float64) for im in images]
+    ys = [np.asarray(arr(r), np.float64) for r in refs]
+    for x, y in zip(xs, ys):
+        if x.shape != y.shape:
+            raise InvalidInputError(f"image shape {x.shape} != reference shape {y.shape}")
+    count = sum(x.size for x in xs)
+    if count == 0:
+        return 0.0, [np.zeros_like(x) for x in xs]
+    dev = _device()
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    seeds = []
+    for x, y in zip(xs, ys):
+        xt = torch.from_numpy(x.astype(np.float32).ravel()).to(dev)
+        yt = torch.from_numpy(y.astype(np.float32).ravel()).to(dev)
+        st = torch.empty_like(xt)
+        N.check(N.lib().ddvr_l1_loss(xt.data_ptr(), yt.data_ptr(), xt.numel(), float(count),
+                                     st.data_ptr(), loss.data_ptr(), R._stream_ptr()))
+        seeds.append(st.to(torch.float64).cpu().numpy().reshape(x.shape))
+    return float(loss.item()), seeds
+
