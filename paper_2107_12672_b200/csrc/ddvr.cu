@@ -38,7 +38,7 @@
 namespace {
 
 constexpr float kEpsAlpha = 1e-6f;      // field.py:25 (EPS_ALPHA)
-constexpr float kStopT = 1e-4f;         // alpha > 1 - 1e-4  <=>  T < 1e-4 (renderer.py:45)
+constexpr float kAlphaStop = 1.f - 1e-4f;   // ALPHA_STOP (renderer.py:45)
 constexpr double kStepEps = 1e-9;       // renderer.py:212
 constexpr double kDeg = 3.14159265358979323846 / 180.0;   // field.py:27
 constexpr int kTile = 16;               // CTA = 16x16 pixels
@@ -73,9 +73,9 @@ struct VolArgs {
   const float* __restrict__ data;
   int X, Y, Z, YZ;
   int Xm2, Ym2, Zm2;       // max(dim-2, 0): highest cell index (field.py:302-304)
-  float fX1, fY1, fZ1;     // dim-1 as float (clamp bound, field.py:299-301)
-  float lox, loy, loz;     // -0.5 - tol  (inside test in grid units)
-  float hix, hiy, hiz;     // dim - 0.5 + tol
+  int X1, Y1, Z1;          // dim-1: clamp bound (field.py:299-301)
+  long long lo[3], hi[3];  // inside test, fixed-point grid units: [-0.5 - tol, dim - 0.5 + tol]
+  long long top[3];        // (dim-1) in fixed point: spatial-gradient liveness (field.py:461-463)
   double bmin[3], bmax[3], scale[3];   // scale = dim / extent
 };
 
@@ -148,9 +148,20 @@ __device__ void make_frame(const ddvr_camera& c, int W, int H, Frame& F) {
 }
 
 // one ray: fp64 geometry and the fp32 march parameters in grid coordinates
+// Sample positions are kept in 32.32 fixed-point GRID coordinates
+// (g = (x - bmin)*scale - 0.5): g_i = g_0 + i*step with integer adds.  The
+// only error is the 2^-33 rounding of g_0 and step: < 5e-7 voxel after 4k
+// steps, a relative stepsize error of ~1e-9 (fp32 grid coordinates would
+// quantise positions to ~1.5e-5 voxel at 256^3, which alone moves the
+// cancellation-heavy camera gradient by ~3e-4), and it makes the adjoint's
+// backward positions bitwise identical to the forward's (g -= step).
+constexpr double kFix = 4294967296.0;           // 2^32
+constexpr float kInvFix = 2.3283064365386963e-10f;   // 2^-32
+
 struct Ray {
-  float g0[3];     // grid coordinate of the entry point (g = (x - bmin)*scale - 0.5)
-  float gw[3];     // grid-space direction per unit t
+  long long g0[3]; // fixed-point grid coordinate of the entry point
+  long long gs[3]; // fixed-point grid step per sample (dt * w * scale)
+  float gw[3];     // grid-space direction per unit t (fp32, for dt gradients)
   int n;           // step count (renderer.py:209-214)
   int axis;        // face axis that decided the entry (renderer.py:198)
   bool clamped, miss;
@@ -205,8 +216,10 @@ __device__ void setup_ray(const Frame& F, const VolArgs& V, double dt, int W, in
   // entry point and grid-space march parameters (renderer.py:315 xo = o + tn*w)
   for (int k = 0; k < 3; ++k) {
     const double xo = da(r.o[k], dm(tn, r.w[k]));
-    r.g0[k] = (float)(dm(ds(xo, V.bmin[k]), V.scale[k]) - 0.5);
-    r.gw[k] = (float)dm(r.w[k], V.scale[k]);
+    const double gw = dm(r.w[k], V.scale[k]);
+    r.g0[k] = __double2ll_rn((dm(ds(xo, V.bmin[k]), V.scale[k]) - 0.5) * kFix);
+    r.gs[k] = __double2ll_rn(dm(dt, gw) * kFix);
+    r.gw[k] = (float)gw;
   }
 }
 
@@ -221,18 +234,28 @@ struct Cell {
   bool inside;
 };
 
-__device__ __forceinline__ void locate(const VolArgs& V, float gx, float gy, float gz, Cell& c) {
-  c.inside = gx >= V.lox && gx <= V.hix && gy >= V.loy && gy <= V.hiy && gz >= V.loz &&
-             gz <= V.hiz;
-  const float cx = fminf(fmaxf(gx, 0.f), V.fX1);
-  const float cy = fminf(fmaxf(gy, 0.f), V.fY1);
-  const float cz = fminf(fmaxf(gz, 0.f), V.fZ1);
-  const int ix = min((int)cx, V.Xm2);
-  const int iy = min((int)cy, V.Ym2);
-  const int iz = min((int)cz, V.Zm2);
-  c.fx = __fsub_rn(cx, (float)ix);
-  c.fy = __fsub_rn(cy, (float)iy);
-  c.fz = __fsub_rn(cz, (float)iz);
+// one axis of _grid_setup (field.py:290-307) on a fixed-point coordinate:
+// gc = clip(g, 0, dim-1); i = clip(floor(gc), 0, dim-2); f = gc - i
+__device__ __forceinline__ void axis_cell(long long g, int d1, int dm2, int& i, float& f) {
+  const int hi = (int)(g >> 32);
+  const float fr = __fmul_rn(__uint2float_rn((unsigned)g), kInvFix);
+  if (hi < 0) {
+    i = 0; f = 0.f;
+  } else if (hi >= d1) {
+    i = dm2; f = d1 > 0 ? 1.f : 0.f;
+  } else {
+    i = hi; f = fr;
+  }
+}
+
+__device__ __forceinline__ void locate(const VolArgs& V, long long gx, long long gy, long long gz,
+                                       Cell& c) {
+  c.inside = gx >= V.lo[0] && gx <= V.hi[0] && gy >= V.lo[1] && gy <= V.hi[1] &&
+             gz >= V.lo[2] && gz <= V.hi[2];
+  int ix, iy, iz;
+  axis_cell(gx, V.X1, V.Xm2, ix, c.fx);
+  axis_cell(gy, V.Y1, V.Ym2, iy, c.fy);
+  axis_cell(gz, V.Z1, V.Zm2, iz, c.fz);
   c.base = (ix * V.Y + iy) * V.Z + iz;
   c.ox = ix + 1 < V.X ? V.YZ : 0;
   c.oy = iy + 1 < V.Y ? V.Z : 0;
@@ -307,13 +330,28 @@ struct Segment {
   bool a_clamped;
 };
 
+// a = 1 - exp(-x) is evaluated without cancellation: for x < ln2/2 by the
+// degree-7 Taylor polynomial of -expm1(-x) (truncation < 5e-9 relative) with
+// e = 1 - a exact to half an ulp; above, a = 1 - exp(-x) is well conditioned.
+// (fp32 1 - __expf(-x) alone loses ~1e-5 relative on a at dt*tau ~ 5e-3.)
 __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
   Segment s;
   s.tau = fmaxf(tau_raw, 0.f);
-  s.e = __expf(-__fmul_rn(dt32, s.tau));
-  s.a_clamped = s.e < kEpsAlpha;
-  s.ome = fmaxf(s.e, kEpsAlpha);
-  s.a = __fsub_rn(1.f, s.ome);
+  const float x = __fmul_rn(dt32, s.tau);
+  float p = __fmaf_rn(-x, 1.f / 5040.f, 1.f / 720.f);
+  p = __fmaf_rn(-x, p, 1.f / 120.f);
+  p = __fmaf_rn(-x, p, 1.f / 24.f);
+  p = __fmaf_rn(-x, p, 1.f / 6.f);
+  p = __fmaf_rn(-x, p, 0.5f);
+  p = __fmaf_rn(-x, p, 1.f);
+  const float a_small = __fmul_rn(x, p);
+  const float e_big = __expf(-x);
+  const bool small = x < 0.34657359f;
+  const float a_raw = small ? a_small : __fsub_rn(1.f, e_big);
+  s.e = small ? __fsub_rn(1.f, a_small) : e_big;
+  s.a_clamped = s.e < kEpsAlpha;                 // a_raw > 1 - EPS_ALPHA
+  s.ome = s.a_clamped ? kEpsAlpha : s.e;
+  s.a = s.a_clamped ? __fsub_rn(1.f, kEpsAlpha) : a_raw;
   return s;
 }
 
@@ -358,14 +396,16 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
 
   const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
   float* tape = G.tape ? G.tape + pix * G.tape_stride : nullptr;
-  float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+  // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
+  // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355)
+  float T = 1.f, A = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+  long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
   for (int i = 0; i < r.n; ++i) {
-    if (EARLY && T < kStopT) break;            // renderer.py:331-335
+    if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
     if (tape) tape[i] = T;                     // stored mode (renderer.py:348-349)
-    const float t = __fmul_rn((float)i, dt32);
     Cell c;
-    locate(V, __fmaf_rn(t, r.gw[0], r.g0[0]), __fmaf_rn(t, r.gw[1], r.g0[1]),
-           __fmaf_rn(t, r.gw[2], r.g0[2]), c);
+    locate(V, gx, gy, gz, c);
+    gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
     float v[8], p0, p1;
     gather8(V, c, v);
     const float d = clamp_density(c.inside, interp(c, v, p0, p1));
@@ -376,9 +416,10 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
     c0 = __fmaf_rn(Ta, s.x, c0);
     c1 = __fmaf_rn(Ta, s.y, c1);
     c2 = __fmaf_rn(Ta, s.z, c2);
+    A = __fadd_rn(A, Ta);
     T = __fmul_rn(T, g.ome);
   }
-  reinterpret_cast<float4*>(image)[pix] = make_float4(c0, c1, c2, 1.f - T);
+  reinterpret_cast<float4*>(image)[pix] = make_float4(c0, c1, c2, A);
   if (trans) trans[pix] = T;
 }
 
@@ -449,13 +490,14 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   // camera / stepsize sums (grid units)
   float s1x = 0, s1y = 0, s1z = 0, s2x = 0, s2y = 0, s2z = 0;
   float dt_bl = 0.f, dt_pos = 0.f;
+  // last sample position; walk back with exact integer steps
+  long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
+  long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
+  long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
 
   for (int i = r.n - 1; i >= 0; --i) {
     const float t = __fmul_rn((float)i, dt32);
     Cell c;
-    const float gx = __fmaf_rn(t, r.gw[0], r.g0[0]);
-    const float gy = __fmaf_rn(t, r.gw[1], r.g0[1]);
-    const float gz = __fmaf_rn(t, r.gw[2], r.g0[2]);
     locate(V, gx, gy, gz, c);
     float v[8], p0, p1;
     gather8(V, c, v);
@@ -542,9 +584,9 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
         const float ddy = ez * ((1.f - c.fx) * (v[2] - v[0]) + c.fx * (v[3] - v[1])) +
                           c.fz * ((1.f - c.fx) * (v[6] - v[4]) + c.fx * (v[7] - v[5]));
         const float ddz = p1 - p0;
-        const float bx = (gx >= 0.f && gx <= V.fX1) ? ddx * d_hat : 0.f;
-        const float by = (gy >= 0.f && gy <= V.fY1) ? ddy * d_hat : 0.f;
-        const float bz = (gz >= 0.f && gz <= V.fZ1) ? ddz * d_hat : 0.f;
+        const float bx = (gx >= 0 && gx <= V.top[0]) ? ddx * d_hat : 0.f;
+        const float by = (gy >= 0 && gy <= V.top[1]) ? ddy * d_hat : 0.f;
+        const float bz = (gz >= 0 && gz <= V.top[2]) ? ddz * d_hat : 0.f;
         if (kCam) {
           s1x += bx; s1y += by; s1z += bz;
           s2x += t * bx; s2y += t * by; s2z += t * bz;
@@ -553,6 +595,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
       }
     }
     T = Tp;
+    gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
   }
 
   // ---- flush per-ray accumulators ----
@@ -703,13 +746,16 @@ int make_vol(const ddvr_volume* vol, VolArgs& V) {
   V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
   V.YZ = V.Y * V.Z;
   V.Xm2 = V.X >= 2 ? V.X - 2 : 0; V.Ym2 = V.Y >= 2 ? V.Y - 2 : 0; V.Zm2 = V.Z >= 2 ? V.Z - 2 : 0;
-  V.fX1 = (float)(V.X - 1); V.fY1 = (float)(V.Y - 1); V.fZ1 = (float)(V.Z - 1);
+  V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
   // inside test in grid units.  Every sample of a march lies in [tn, tf) of the
   // exact slab, so the reference's 1e-9*extent tolerance (field.py:293) only has
-  // to absorb rounding; fp32 grid coordinates need ~1e-3 voxel of slack.
-  const float tol = 1e-3f;
-  V.lox = V.loy = V.loz = -0.5f - tol;
-  V.hix = (float)V.X - 0.5f + tol; V.hiy = (float)V.Y - 0.5f + tol; V.hiz = (float)V.Z - 0.5f + tol;
+  // to absorb rounding of the fixed-point entry point: 1e-6 voxel of slack.
+  const double tol = 1e-6;
+  for (int k = 0; k < 3; ++k) {
+    V.lo[k] = (long long)llrint((-0.5 - tol) * kFix);
+    V.hi[k] = (long long)llrint(((double)vol->dims[k] - 0.5 + tol) * kFix);
+    V.top[k] = (long long)(vol->dims[k] - 1) << 32;
+  }
   for (int k = 0; k < 3; ++k) {
     V.bmin[k] = vol->box_min[k];
     V.bmax[k] = vol->box_max[k];

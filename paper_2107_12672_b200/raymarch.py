@@ -186,7 +186,7 @@ class DiffDVR(torch.autograd.Function):
     @staticmethod
     def forward(ctx, density, texels, lonlat, dt, rig: Rig, radius, center, fov):
         cams = camera_array(lonlat.to(density.device), radius, center, fov)
-        dtv = float(dt)
+        dtv = float(dt.detach()) if isinstance(dt, torch.Tensor) else float(dt)
         img, trans = forward(density.contiguous(), texels.contiguous(), cams, dtv, rig)
         ctx.save_for_backward(density, texels, img, trans)
         ctx.cams, ctx.dt, ctx.rig = cams, dtv, rig
@@ -213,10 +213,11 @@ class DiffDVR(torch.autograd.Function):
                 grad_img.contiguous().to(torch.float32), mask, d_volume=d_vol, d_tf=d_tf,
                 d_camera=d_cam, d_dt=d_dt)
         g_tf = d_tf.to(texels.dtype) if d_tf is not None else None
-        g_cam = d_cam.to(*ctx.lonlat_meta) if d_cam is not None else None
+        g_cam = (d_cam.to(dtype=ctx.lonlat_meta[0], device=ctx.lonlat_meta[1])
+                 if d_cam is not None else None)
         g_dt = None
         if d_dt is not None and ctx.dt_meta is not None:
-            g_dt = d_dt.reshape(()).to(ctx.dt_meta[0]).to(ctx.dt_meta[1])
+            g_dt = d_dt.reshape(()).to(dtype=ctx.dt_meta[0], device=ctx.dt_meta[1])
         return d_vol, g_tf, g_cam, g_dt, None, None, None, None
 
 
@@ -225,6 +226,6 @@ def render_views(density, texels, lonlat, dt, rig: Rig, *, radius=2.0, center=(0
     """Differentiable images (V, rows, W, 4) of ``lonlat`` views (autograd-aware)."""
     if not isinstance(dt, torch.Tensor):
         dt = torch.tensor(float(dt), dtype=torch.float64)
-    if float(dt) <= 0.0:
+    if float(dt.detach()) <= 0.0:
         raise InvalidParameterError("stepsize must be positive")
     return DiffDVR.apply(density, texels, lonlat, dt, rig, radius, center, fov_y_deg)

@@ -264,10 +264,15 @@ def _upload(volume, tf, cam, dev):
 
 
 def _image_from(img, trans):
-    """fp64 ImageRGBA with alpha = 1 - T evaluated in fp64 (keeps T exact for the adjoint)."""
-    data = img[0].to(torch.float64)
-    data[..., 3] = 1.0 - trans[0].to(torch.float64)
-    return ImageRGBA(data.cpu().numpy())
+    """fp64 ImageRGBA; the fp32 transmittance rides along for a later adjoint.
+
+    alpha = A is accurate as A -> 0; T = prod(1 - a) is accurate as T -> 0.
+    ``render_adjoint(image=...)`` starts the inversion from the attached T
+    when the image came from :func:`render`, else from 1 - alpha.
+    """
+    out = ImageRGBA(img[0].to(torch.float64).cpu().numpy())
+    out._ddvr_trans = trans[0].cpu().numpy()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -320,8 +325,10 @@ def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) 
         img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig)
     else:
         img_t = torch.from_numpy(img_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
-        trans_t = torch.from_numpy((1.0 - img_arr[..., 3]).astype(np.float32)).to(dev)
-        trans_t = trans_t.reshape(1, H, W)
+        t_np = getattr(image, "_ddvr_trans", None)
+        if t_np is None or np.shape(t_np) != (H, W):
+            t_np = 1.0 - img_arr[..., 3]
+        trans_t = torch.from_numpy(np.asarray(t_np, np.float32)).to(dev).reshape(1, H, W)
     seed_t = torch.from_numpy(seed_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
     bit = N.TARGET_BITS[cfg.target]
     d_vol = torch.zeros_like(dens) if bit == N.TARGET_VOLUME else None

@@ -1,0 +1,131 @@
+"""The C-ABI library: loads, exports every symbol of include/ddvr.h, maps errors.
+
+Host-side validation in libddvr runs before any CUDA call, so the error paths
+are exercised here without a GPU (no compute calls are made).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "ddvr.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(ddvr_\w+)\s*\(",
+                                 text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2107_12672_b200 import _build, _native
+    _build.build()
+    return _native.lib()
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_l1_loss", "ddvr_ray_setup",
+                            "ddvr_last_error", "ddvr_abi_version", "ddvr_launch_count"])
+
+
+def test_library_exports_every_declared_symbol(lib):
+    handle = ctypes.CDLL(lib._name)
+    for name in _declared():
+        assert hasattr(handle, name), name
+    assert lib.ddvr_abi_version() == 1
+
+
+def test_python_binding_matches_header():
+    from paper_2107_12672_b200 import _native
+    assert sorted(_native.EXPORTED) == _declared()
+    # struct layout: ddvr_params = double + 6 int32 + pointer + int64
+    assert ctypes.sizeof(_native.DdvrParams) == 8 + 6 * 4 + 8 + 8
+    assert ctypes.sizeof(_native.DdvrVolume) == 8 + 12 + 4 + 48
+    assert ctypes.sizeof(_native.DdvrTf) == 16
+
+
+def _descs(dt=0.1, dims=(4, 4, 4), box=((-0.5,) * 3, (0.5,) * 3), R=8, W=8, H=8, rows=(0, 0)):
+    from paper_2107_12672_b200 import _native as N
+    vol = N.DdvrVolume(16, (ctypes.c_int32 * 3)(*dims), (ctypes.c_double * 3)(*box[0]),
+                       (ctypes.c_double * 3)(*box[1]))
+    tf = N.DdvrTf(N.TF_TEXTURE, R, 16)
+    prm = N.DdvrParams(dt, W, H, rows[0], rows[1], 0, 0, None, 0)
+    return vol, tf, prm
+
+
+@pytest.mark.parametrize("kw,code,text", [
+    (dict(dt=0.0), 1, "stepsize"),
+    (dict(dt=-1.0), 1, "stepsize"),
+    (dict(dims=(0, 4, 4)), 1, "non-empty"),
+    (dict(box=((0.5, -0.5, -0.5), (0.5, 0.5, 0.5))), 1, "extent"),
+    (dict(R=0), 1, "(R, 4)"),
+    (dict(W=0), 1, "1x1"),
+    (dict(rows=(5, 3)), 1, "row band"),
+])
+def test_forward_validation(lib, kw, code, text):
+    vol, tf, prm = _descs(**kw)
+    rc = lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, None)
+    assert rc == code
+    assert text in lib.ddvr_last_error().decode()
+
+
+def test_adjoint_without_target_is_unsupported(lib):
+    vol, tf, prm = _descs()
+    rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, 16, 0, None, None, None, None, None)
+    assert rc == 3 and "target" in lib.ddvr_last_error().decode()
+
+
+def test_adjoint_missing_output_is_invalid_input(lib):
+    vol, tf, prm = _descs()
+    rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, 16, 8, None, None, None, None, None)
+    assert rc == 2 and "d_volume" in lib.ddvr_last_error().decode()
+
+
+def test_unbuilt_tf_kind_is_unsupported(lib):
+    from paper_2107_12672_b200 import _native as N
+    vol, tf, prm = _descs()
+    tf.kind = 7
+    rc = lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, None)
+    assert rc == 3
+
+
+def test_status_codes_map_to_reference_exceptions(lib):
+    from paper_2107_12672_b200 import _native as N
+    from paper_2107_12672_b200.errors import (InvalidInputError, InvalidParameterError,
+                                              UnsupportedConfigurationError)
+    vol, tf, prm = _descs(dt=0.0)
+    with pytest.raises(InvalidParameterError):
+        N.check(lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm),
+                                 16, None, None))
+    vol, tf, prm = _descs()
+    with pytest.raises(UnsupportedConfigurationError):
+        N.check(lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm),
+                                 16, None, 16, 0, None, None, None, None, None))
+    with pytest.raises(InvalidInputError):
+        N.check(lib.ddvr_l1_loss(None, None, 4, 1.0, None, None, None))
+
+
+def test_zero_views_is_a_no_op(lib):
+    vol, tf, prm = _descs()
+    assert lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), None, 0, ctypes.byref(prm), 16,
+                            None, None) == 0
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    from paper_2107_12672_b200 import _native as N
+    monkeypatch.setattr(N, "_lib", None)
+    monkeypatch.setattr(N, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(N.NativeLibraryError):
+        N.lib()
