@@ -98,8 +98,11 @@ class ShardedStep:
         self.d_dt64 = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss64 = torch.zeros(1, dtype=torch.float64, device=dev)
 
-    def run(self) -> FlatGrads:
+    def run(self, hook=None) -> FlatGrads:
+        """One step; ``hook(name)`` (optional) is called at "post_forward",
+        "pre_adjoint" and "post_adjoint" in stream order (for CUDA events)."""
         import ctypes
+        hook = hook or (lambda name: None)
         f = self.flat
         f.buf.zero_()
         self.d_tf64.zero_()
@@ -113,15 +116,18 @@ class ShardedStep:
             N.check(lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
                                      ctypes.byref(prm), self.img.data_ptr(), self.trans.data_ptr(),
                                      st))
+            hook("post_forward")
             N.check(lib.ddvr_l1_loss(self.img.data_ptr(), self.refs.data_ptr(), self.img.numel(),
                                      self.count, self.seed.data_ptr(), self.loss64.data_ptr(), st))
             want = lambda bit, t: t.data_ptr() if self.mask & bit else None  # noqa: E731
+            hook("pre_adjoint")
             N.check(lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
                                      ctypes.byref(prm), self.img.data_ptr(),
                                      self.trans.data_ptr(), self.seed.data_ptr(), self.mask,
                                      want(N.TARGET_VOLUME, f.d_volume),
                                      want(N.TARGET_TF, self.d_tf64), None,
                                      want(N.TARGET_STEPSIZE, self.d_dt64), st))
+            hook("post_adjoint")
         f.d_tf.copy_(self.d_tf64.reshape(-1))
         f.d_stepsize.copy_(self.d_dt64)
         f.loss.copy_(self.loss64)
