@@ -71,6 +71,10 @@ typedef struct {
   int32_t dims[3];       /* X, Y, Z >= 1 */
   double box_min[3];
   double box_max[3];     /* box_max > box_min on every axis */
+  const float* cells;    /* (device, nullable, 32-byte aligned) cell-record copy of data
+                            built by ddvr_pack_cells: the 8 corner values of every cell
+                            in one 32-byte record, so a sample is one 256-bit load.
+                            NULL = gather the 8 corners from data. */
 } ddvr_volume;
 
 /* transfer function (TransferFunction, field.py:108-127) */
@@ -121,11 +125,26 @@ int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
  * (if NULL, T = 1 - alpha).  seed (device) (V, rows, W, 4) = dLoss/dImage.
  * Outputs (device, accumulate, NULL when the target bit is clear):
  *   d_volume float (X*Y*Z); d_tf double (same shape as tf->params);
- *   d_camera double (V, 2) per degree [lon, lat]; d_dt double (1). */
+ *   d_camera double (V, 2) per degree [lon, lat]; d_dt double (1).
+ * workspace (device, 32-byte aligned): ddvr_adjoint_workspace_bytes() bytes
+ * (cell-gradient records when vol->cells is set and the volume target is on;
+ * zeroed and folded into d_volume inside the call). */
 int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
                  int32_t n_views, const ddvr_params* p, const float* image, const float* trans,
                  const float* seed, uint32_t target_mask, float* d_volume, double* d_tf,
-                 double* d_camera, double* d_dt, void* stream);
+                 double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
+                 void* stream);
+
+/* Workspace ddvr_adjoint needs for this volume and target mask (0 if none). */
+int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t target_mask);
+
+/* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:
+ * max(X-1,1) * max(Y-1,1) * max(Z-1,1) records of 8 floats. */
+int64_t ddvr_cells_bytes(const int32_t dims[3]);
+
+/* Build the cell records of vol->data into cells_out (device, 32-byte aligned,
+ * ddvr_cells_bytes bytes).  Call again whenever the density changes. */
+int ddvr_pack_cells(const ddvr_volume* vol, float* cells_out, void* stream);
 
 /* Fused L1 loss + seed (objectives.py:38-54) over n floats: seed_out[i] =
  * sign(x-y)/count (sign(0)=0) and loss_out[0] += sum|x-y|/count (double).

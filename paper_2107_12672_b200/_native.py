@@ -31,8 +31,9 @@ TF_TEXTURE = 0
 TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
-EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_l1_loss", "ddvr_ray_setup",
-            "ddvr_last_error", "ddvr_abi_version", "ddvr_launch_count")
+EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes",
+            "ddvr_pack_cells", "ddvr_l1_loss", "ddvr_ray_setup", "ddvr_last_error",
+            "ddvr_abi_version", "ddvr_launch_count")
 
 
 class NativeLibraryError(VoldiffError, RuntimeError):
@@ -45,7 +46,8 @@ class CudaError(VoldiffError, RuntimeError):
 
 class DdvrVolume(ctypes.Structure):
     _fields_ = [("data", ctypes.c_void_p), ("dims", ctypes.c_int32 * 3),
-                ("box_min", ctypes.c_double * 3), ("box_max", ctypes.c_double * 3)]
+                ("box_min", ctypes.c_double * 3), ("box_max", ctypes.c_double * 3),
+                ("cells", ctypes.c_void_p)]
 
 
 class DdvrTf(ctypes.Structure):
@@ -71,8 +73,15 @@ def _bind(lib):
                                  vp, vp, vp]
     lib.ddvr_forward.restype = ctypes.c_int
     lib.ddvr_adjoint.argtypes = [P(DdvrVolume), P(DdvrTf), vp, ctypes.c_int32, P(DdvrParams),
-                                 vp, vp, vp, ctypes.c_uint32, vp, vp, vp, vp, vp]
+                                 vp, vp, vp, ctypes.c_uint32, vp, vp, vp, vp, vp,
+                                 ctypes.c_int64, vp]
     lib.ddvr_adjoint.restype = ctypes.c_int
+    lib.ddvr_adjoint_workspace_bytes.argtypes = [P(DdvrVolume), ctypes.c_uint32]
+    lib.ddvr_adjoint_workspace_bytes.restype = ctypes.c_int64
+    lib.ddvr_cells_bytes.argtypes = [P(ctypes.c_int32)]
+    lib.ddvr_cells_bytes.restype = ctypes.c_int64
+    lib.ddvr_pack_cells.argtypes = [P(DdvrVolume), vp, vp]
+    lib.ddvr_pack_cells.restype = ctypes.c_int
     lib.ddvr_l1_loss.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_double, vp, vp, vp]
     lib.ddvr_l1_loss.restype = ctypes.c_int
     lib.ddvr_ray_setup.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp, vp,

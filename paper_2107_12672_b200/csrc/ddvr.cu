@@ -6,20 +6,25 @@
 //
 // Kernels
 //   dvr_forward_kernel  one thread per ray, 16x16-pixel CTAs (8x4-pixel warps),
-//                       fp64 ray setup, fp32 march in grid coordinates, TF in
-//                       shared memory, float4 image stores.
+//                       fp64 ray setup, exact fixed-point sample positions,
+//                       one 256-bit gather per sample from the cell-record
+//                       volume (8 corners per cell, 32 B), TF in shared
+//                       memory, float4 image stores.
 //   dvr_adjoint_kernel  same mapping; walks each ray back to front and recovers
 //                       the transmittance before every sample by inverting the
-//                       compositing step (T_prev = T / (1 - a)), so per-ray
-//                       state is O(1).  Gradient scatter:
+//                       compositing step (T_prev = T / (1 - a)): O(1) state per
+//                       ray, no tape.  Gradient scatter:
 //                         volume  : per-ray cell-run accumulation of the 8
-//                                   corner weights, flushed with red.global.add
-//                                   when the ray leaves a cell;
+//                                   corner weights, flushed as two 128-bit
+//                                   vector reds into a cell-gradient
+//                                   workspace when the ray leaves a cell;
+//                                   fold_cells_kernel sums them into voxels;
 //                         tf      : per-ray texel-run accumulation, flushed to
-//                                   per-CTA shared memory, then double atomics;
+//                                   per-CTA shared memory, then fp64 atomics;
 //                         camera/stepsize: per-ray sums in registers, fp64
 //                                   Jacobian chain per ray, warp-shuffle + CTA
 //                                   reduction, one fp64 atomic per CTA.
+//   pack_cells_kernel   builds the cell-record copy of a volume.
 //   ray_setup_kernel    parity-test helper (tn, tf, n_steps, flags).
 //   l1_loss_kernel      fused L1 loss value + seed (objectives.py:38-54).
 //
@@ -30,21 +35,31 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
-#include <cstdio>
 #include <cstdint>
+#include <cstdio>
 
 #include "ddvr.h"
 
 namespace {
 
-constexpr float kEpsAlpha = 1e-6f;      // field.py:25 (EPS_ALPHA)
+constexpr float kEpsAlpha = 1e-6f;          // field.py:25 (EPS_ALPHA)
 constexpr float kAlphaStop = 1.f - 1e-4f;   // ALPHA_STOP (renderer.py:45)
-constexpr double kStepEps = 1e-9;       // renderer.py:212
+constexpr double kStepEps = 1e-9;           // renderer.py:212
 constexpr double kDeg = 3.14159265358979323846 / 180.0;   // field.py:27
-constexpr int kTile = 16;               // CTA = 16x16 pixels
+constexpr int kTile = 16;                   // CTA = 16x16 pixels
 constexpr int kThreads = kTile * kTile;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxTfBytes = 96 * 1024;  // TF table + TF gradient in shared memory
+constexpr int kMaxTfBytes = 96 * 1024;      // TF table + TF gradient in shared memory
+
+// Sample positions are kept in 32.32 fixed-point GRID coordinates
+// (g = (x - bmin)*scale - 0.5): g_i = g_0 + i*step with integer adds.  The
+// only error is the 2^-33 rounding of g_0 and step: < 5e-7 voxel after 4k
+// steps, a relative stepsize error of ~1e-9 (fp32 grid coordinates would
+// quantise positions to ~1.5e-5 voxel at 256^3, which alone moves the
+// cancellation-heavy camera gradient by ~3e-4), and it makes the adjoint's
+// backward positions bitwise identical to the forward's (g -= step).
+constexpr double kFix = 4294967296.0;                  // 2^32
+constexpr float kInvFix = 2.3283064365386963e-10f;     // 2^-32
 
 thread_local char g_err[1024] = "";
 std::atomic<int64_t> g_launches{0};
@@ -70,10 +85,13 @@ int check_launch(const char* what) {
 // ---------------------------------------------------------------------------
 
 struct VolArgs {
-  const float* __restrict__ data;
+  const float* __restrict__ data;    // (X,Y,Z) z fastest
+  const float* __restrict__ cells;   // cell records (nullable): 8 corner values per cell
   int X, Y, Z, YZ;
+  int CY, CZ;              // cells along y and z: max(dim-1, 1)
   int Xm2, Ym2, Zm2;       // max(dim-2, 0): highest cell index (field.py:302-304)
   int X1, Y1, Z1;          // dim-1: clamp bound (field.py:299-301)
+  float tX, tY, tZ;        // cell fraction at the top clamp: 1 if dim > 1 else 0
   long long lo[3], hi[3];  // inside test, fixed-point grid units: [-0.5 - tol, dim - 0.5 + tol]
   long long top[3];        // (dim-1) in fixed point: spatial-gradient liveness (field.py:461-463)
   double bmin[3], bmax[3], scale[3];   // scale = dim / extent
@@ -108,8 +126,9 @@ __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b
 __device__ __forceinline__ double dd(double a, double b) { return __ddiv_rn(a, b); }
 
 __device__ void make_frame(const ddvr_camera& c, int W, int H, Frame& F) {
-  const double lon = dm(fmod(c.lon_deg, 360.0) < 0 ? da(fmod(c.lon_deg, 360.0), 360.0)
-                                                    : fmod(c.lon_deg, 360.0), kDeg);
+  double lon_deg = fmod(c.lon_deg, 360.0);          // field.py:143 (lon % 360)
+  if (lon_deg < 0.0) lon_deg = da(lon_deg, 360.0);
+  const double lon = dm(lon_deg, kDeg);
   const double lat = dm(c.lat_deg, kDeg);
   double sl, cl, sp, cp;
   sincos(lat, &sl, &cl);
@@ -147,17 +166,7 @@ __device__ void make_frame(const ddvr_camera& c, int W, int H, Frame& F) {
   F.du[2][0] = -cp * sl * k; F.du[2][1] = -sp * cl * k;
 }
 
-// one ray: fp64 geometry and the fp32 march parameters in grid coordinates
-// Sample positions are kept in 32.32 fixed-point GRID coordinates
-// (g = (x - bmin)*scale - 0.5): g_i = g_0 + i*step with integer adds.  The
-// only error is the 2^-33 rounding of g_0 and step: < 5e-7 voxel after 4k
-// steps, a relative stepsize error of ~1e-9 (fp32 grid coordinates would
-// quantise positions to ~1.5e-5 voxel at 256^3, which alone moves the
-// cancellation-heavy camera gradient by ~3e-4), and it makes the adjoint's
-// backward positions bitwise identical to the forward's (g -= step).
-constexpr double kFix = 4294967296.0;           // 2^32
-constexpr float kInvFix = 2.3283064365386963e-10f;   // 2^-32
-
+// one ray: fp64 geometry and the fixed-point march parameters
 struct Ray {
   long long g0[3]; // fixed-point grid coordinate of the entry point
   long long gs[3]; // fixed-point grid step per sample (dt * w * scale)
@@ -165,8 +174,14 @@ struct Ray {
   int n;           // step count (renderer.py:209-214)
   int axis;        // face axis that decided the entry (renderer.py:198)
   bool clamped, miss;
+  bool all_inside; // first and last samples inside => every sample inside (convex box)
   double o[3], w[3], tn, tf, su, sv, dn;
 };
+
+__device__ __forceinline__ bool inside_fx(const VolArgs& V, long long x, long long y, long long z) {
+  return x >= V.lo[0] && x <= V.hi[0] && y >= V.lo[1] && y <= V.hi[1] && z >= V.lo[2] &&
+         z <= V.hi[2];
+}
 
 // camera ray through pixel (u, v) + slab clipping + step count, fp64
 // (field.py:218-228, renderer.py:182-214, 315)
@@ -221,6 +236,12 @@ __device__ void setup_ray(const Frame& F, const VolArgs& V, double dt, int W, in
     r.gs[k] = __double2ll_rn(dm(dt, gw) * kFix);
     r.gw[k] = (float)gw;
   }
+  // Every sample lies on the segment [first, last]; the box is convex, so the
+  // per-sample inside test of field.py:293-298 reduces to the two endpoints.
+  const long long m = r.n > 0 ? (long long)(r.n - 1) : 0;
+  r.all_inside = inside_fx(V, r.g0[0], r.g0[1], r.g0[2]) &&
+                 inside_fx(V, r.g0[0] + m * r.gs[0], r.g0[1] + m * r.gs[1],
+                           r.g0[2] + m * r.gs[2]);
 }
 
 // ---------------------------------------------------------------------------
@@ -228,51 +249,69 @@ __device__ void setup_ray(const Frame& F, const VolArgs& V, double dt, int W, in
 // ---------------------------------------------------------------------------
 
 struct Cell {
-  int base;            // flat index of corner (ix, iy, iz)
-  int ox, oy, oz;      // flat offsets to the +x/+y/+z corners (0 on a clamped axis)
+  int cell;            // cell-record index (ix * CY + iy) * CZ + iz
+  int base;            // flat voxel index of corner (ix, iy, iz)
+  int ox, oy, oz;      // flat voxel offsets to the +x/+y/+z corners (0 on a clamped axis)
   float fx, fy, fz;    // cell fractions
   bool inside;
 };
 
-// one axis of _grid_setup (field.py:290-307) on a fixed-point coordinate:
-// gc = clip(g, 0, dim-1); i = clip(floor(gc), 0, dim-2); f = gc - i
-__device__ __forceinline__ void axis_cell(long long g, int d1, int dm2, int& i, float& f) {
+// one axis of _grid_setup (field.py:290-307) on a fixed-point coordinate,
+// branch-free: gc = clip(g, 0, dim-1); i = clip(floor(gc), 0, dim-2); f = gc - i
+__device__ __forceinline__ void axis_cell(long long g, int d1, int dm2, float ftop, int& i,
+                                          float& f) {
   const int hi = (int)(g >> 32);
   const float fr = __fmul_rn(__uint2float_rn((unsigned)g), kInvFix);
-  if (hi < 0) {
-    i = 0; f = 0.f;
-  } else if (hi >= d1) {
-    i = dm2; f = d1 > 0 ? 1.f : 0.f;
-  } else {
-    i = hi; f = fr;
+  i = min(max(hi, 0), dm2);
+  f = hi < 0 ? 0.f : (hi >= d1 ? ftop : fr);
+}
+
+template <bool SCALAR>
+__device__ __forceinline__ void locate(const VolArgs& V, long long gx, long long gy, long long gz,
+                                       bool all_inside, Cell& c) {
+  c.inside = all_inside || inside_fx(V, gx, gy, gz);
+  int ix, iy, iz;
+  axis_cell(gx, V.X1, V.Xm2, V.tX, ix, c.fx);
+  axis_cell(gy, V.Y1, V.Ym2, V.tY, iy, c.fy);
+  axis_cell(gz, V.Z1, V.Zm2, V.tZ, iz, c.fz);
+  c.cell = (ix * V.CY + iy) * V.CZ + iz;
+  if (SCALAR) {
+    c.base = (ix * V.Y + iy) * V.Z + iz;
+    c.ox = ix + 1 < V.X ? V.YZ : 0;
+    c.oy = iy + 1 < V.Y ? V.Z : 0;
+    c.oz = iz + 1 < V.Z ? 1 : 0;
   }
 }
 
-__device__ __forceinline__ void locate(const VolArgs& V, long long gx, long long gy, long long gz,
-                                       Cell& c) {
-  c.inside = gx >= V.lo[0] && gx <= V.hi[0] && gy >= V.lo[1] && gy <= V.hi[1] &&
-             gz >= V.lo[2] && gz <= V.hi[2];
-  int ix, iy, iz;
-  axis_cell(gx, V.X1, V.Xm2, ix, c.fx);
-  axis_cell(gy, V.Y1, V.Ym2, iy, c.fy);
-  axis_cell(gz, V.Z1, V.Zm2, iz, c.fz);
-  c.base = (ix * V.Y + iy) * V.Z + iz;
-  c.ox = ix + 1 < V.X ? V.YZ : 0;
-  c.oy = iy + 1 < V.Y ? V.Z : 0;
-  c.oz = iz + 1 < V.Z ? 1 : 0;
+__device__ __forceinline__ void ld256(const float* p, float v[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                 "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
+__device__ __forceinline__ void red128(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
 }
 
 // corner values, bit 0 = +x, bit 1 = +y, bit 2 = +z (field.py:318-322 order)
-__device__ __forceinline__ void gather8(const VolArgs& V, const Cell& c, float v[8]) {
-  const float* p = V.data + c.base;
-  v[0] = __ldg(p);
-  v[1] = __ldg(p + c.ox);
-  v[2] = __ldg(p + c.oy);
-  v[3] = __ldg(p + c.ox + c.oy);
-  v[4] = __ldg(p + c.oz);
-  v[5] = __ldg(p + c.ox + c.oz);
-  v[6] = __ldg(p + c.oy + c.oz);
-  v[7] = __ldg(p + c.ox + c.oy + c.oz);
+template <bool CELLS>
+__device__ __forceinline__ void fetch8(const VolArgs& V, const Cell& c, float v[8]) {
+  if (CELLS) {
+    ld256(V.cells + 8 * (size_t)c.cell, v);
+  } else {
+    const float* p = V.data + c.base;
+    v[0] = __ldg(p);
+    v[1] = __ldg(p + c.ox);
+    v[2] = __ldg(p + c.oy);
+    v[3] = __ldg(p + c.ox + c.oy);
+    v[4] = __ldg(p + c.oz);
+    v[5] = __ldg(p + c.ox + c.oz);
+    v[6] = __ldg(p + c.oy + c.oz);
+    v[7] = __ldg(p + c.ox + c.oy + c.oz);
+  }
 }
 
 // unclamped interpolant (lerp x, then y, then z); also returns the two
@@ -312,8 +351,8 @@ struct TexelTF {
     w = __fsub_rn(f, (float)i0);
     const float4 a = tex[i0];
     const float4 b = tex[i1];
-    float4 dlt = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y), __fsub_rn(b.z, a.z),
-                             __fsub_rn(b.w, a.w));
+    const float4 dlt = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
+                                   __fsub_rn(b.z, a.z), __fsub_rn(b.w, a.w));
     if (want_slope) {
       const bool live = t >= 0.f && t <= fR1;
       const float s = live ? fR : 0.f;
@@ -374,7 +413,7 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 // forward kernel (renderer.py:306-357)
 // ---------------------------------------------------------------------------
 
-template <bool EARLY>
+template <bool EARLY, bool CELLS, bool TAPE>
 __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
                                                              float* __restrict__ image,
                                                              float* __restrict__ trans) {
@@ -391,23 +430,24 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
 
   Ray r;
   setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
-  TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1), max(TFA.count - 2, 0)};
+  const TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1),
+                   max(TFA.count - 2, 0)};
   const float dt32 = (float)G.dt;
 
   const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
-  float* tape = G.tape ? G.tape + pix * G.tape_stride : nullptr;
+  float* tape = TAPE ? G.tape + pix * G.tape_stride : nullptr;
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
   // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355)
   float T = 1.f, A = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
   long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
   for (int i = 0; i < r.n; ++i) {
     if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
-    if (tape) tape[i] = T;                     // stored mode (renderer.py:348-349)
+    if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     Cell c;
-    locate(V, gx, gy, gz, c);
+    locate<!CELLS>(V, gx, gy, gz, r.all_inside, c);
     gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
     float v[8], p0, p1;
-    gather8(V, c, v);
+    fetch8<CELLS>(V, c, v);
     const float d = clamp_density(c.inside, interp(c, v, p0, p1));
     int i0; float w; float4 slope;
     const float4 s = tf.eval(d, i0, w, slope, false);
@@ -434,11 +474,37 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-template <unsigned MASK>
+// flush of one cell run: into the cell-gradient workspace (two 128-bit vector
+// reds) or, without cell records, straight into the voxel gradient
+template <bool CELLS>
+__device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
+                                           float* __restrict__ d_cells, int cell, int base,
+                                           int ox, int oy, int oz, const float acc[8]) {
+  if (CELLS) {
+    float* q = d_cells + 8 * (size_t)cell;
+    red128(q, acc[0], acc[1], acc[2], acc[3]);
+    red128(q + 4, acc[4], acc[5], acc[6], acc[7]);
+  } else {
+    float* q = d_volume + base;
+    atomicAdd(q, acc[0]);
+    if (ox) atomicAdd(q + ox, acc[1]);
+    if (oy) atomicAdd(q + oy, acc[2]);
+    if (ox && oy) atomicAdd(q + ox + oy, acc[3]);
+    if (oz) {
+      atomicAdd(q + oz, acc[4]);
+      if (ox) atomicAdd(q + ox + oz, acc[5]);
+      if (oy) atomicAdd(q + oy + oz, acc[6]);
+      if (ox && oy) atomicAdd(q + ox + oy + oz, acc[7]);
+    }
+  }
+}
+
+template <unsigned MASK, bool CELLS>
 __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
     const float* __restrict__ trans, const float* __restrict__ seed, float* __restrict__ d_volume,
-    double* __restrict__ d_tf, double* __restrict__ d_camera, double* __restrict__ d_dt) {
+    float* __restrict__ d_cells, double* __restrict__ d_tf, double* __restrict__ d_camera,
+    double* __restrict__ d_dt) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
   constexpr bool kStep = MASK & DDVR_TARGET_STEPSIZE;
   constexpr bool kTf = MASK & DDVR_TARGET_TF;
@@ -463,6 +529,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
 
   Ray r;
   r.n = 0;
+  r.all_inside = true;
   float Tn = 1.f;
   float4 sd = make_float4(0, 0, 0, 0);
   const float* tape = nullptr;
@@ -473,14 +540,15 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     sd = reinterpret_cast<const float4*>(seed)[pix];
     Tn = trans ? trans[pix] : 1.f - reinterpret_cast<const float4*>(image)[pix].w;
   }
-  TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1), max(TFA.count - 2, 0)};
+  const TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1),
+                   max(TFA.count - 2, 0)};
   const float dt32 = (float)G.dt;
 
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
   float T = Tn;                       // transmittance after the current sample
   // volume cell-run accumulator
-  int run_base = -1, run_ox = 0, run_oy = 0, run_oz = 0;
+  int run_cell = -1, run_base = 0, run_ox = 0, run_oy = 0, run_oz = 0;
   float acc8[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc8[k] = 0.f;
@@ -496,11 +564,10 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
 
   for (int i = r.n - 1; i >= 0; --i) {
-    const float t = __fmul_rn((float)i, dt32);
     Cell c;
-    locate(V, gx, gy, gz, c);
+    locate<!CELLS>(V, gx, gy, gz, r.all_inside, c);
     float v[8], p0, p1;
-    gather8(V, c, v);
+    fetch8<CELLS>(V, c, v);
     const float raw = interp(c, v, p0, p1);
     const float d = clamp_density(c.inside, raw);
     int i0; float w; float4 slope;
@@ -516,7 +583,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     const float cdot = s.x * sd.x + s.y * sd.y + s.z * sd.z;
     const float seg_a_hat = Tp * (a_hat + cdot);
     const float aT = g.a * Tp;
-    const float4 o4h_rgb = make_float4(aT * sd.x, aT * sd.y, aT * sd.z, 0.f);
+    const float h0 = aT * sd.x, h1 = aT * sd.y, h2 = aT * sd.z;   // d L / d rgb
     a_hat = g.ome * a_hat - g.a * cdot;
     // Beer-Lambert adjoint (renderer.py:592-596)
     const float a_raw_hat = g.a_clamped ? 0.f : seg_a_hat;
@@ -538,32 +605,19 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
         tfa1 = make_float4(0, 0, 0, 0);
       }
       const float w0 = 1.f - w;
-      tfa0.x += w0 * o4h_rgb.x; tfa0.y += w0 * o4h_rgb.y; tfa0.z += w0 * o4h_rgb.z;
-      tfa0.w += w0 * tau_hat;
-      tfa1.x += w * o4h_rgb.x; tfa1.y += w * o4h_rgb.y; tfa1.z += w * o4h_rgb.z;
-      tfa1.w += w * tau_hat;
+      tfa0.x += w0 * h0; tfa0.y += w0 * h1; tfa0.z += w0 * h2; tfa0.w += w0 * tau_hat;
+      tfa1.x += w * h0;  tfa1.y += w * h1;  tfa1.z += w * h2;  tfa1.w += w * tau_hat;
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
-      const float d_hat = slope.x * o4h_rgb.x + slope.y * o4h_rgb.y + slope.z * o4h_rgb.z +
-                          slope.w * tau_hat;
+      const float d_hat = slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat;
       const bool live = c.inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol) {   // renderer.py:607-608, accumulated per cell run
-        if (c.base != run_base) {
-          if (run_base >= 0) {
-            float* q = d_volume + run_base;
-            atomicAdd(q, acc8[0]);
-            if (run_ox) atomicAdd(q + run_ox, acc8[1]);
-            if (run_oy) atomicAdd(q + run_oy, acc8[2]);
-            if (run_ox && run_oy) atomicAdd(q + run_ox + run_oy, acc8[3]);
-            if (run_oz) {
-              atomicAdd(q + run_oz, acc8[4]);
-              if (run_ox) atomicAdd(q + run_ox + run_oz, acc8[5]);
-              if (run_oy) atomicAdd(q + run_oy + run_oz, acc8[6]);
-              if (run_ox && run_oy) atomicAdd(q + run_ox + run_oy + run_oz, acc8[7]);
-            }
-          }
-          run_base = c.base; run_ox = c.ox; run_oy = c.oy; run_oz = c.oz;
+        if (c.cell != run_cell) {
+          if (run_cell >= 0)
+            flush_cell<CELLS>(d_volume, d_cells, run_cell, run_base, run_ox, run_oy, run_oz, acc8);
+          run_cell = c.cell;
+          if (!CELLS) { run_base = c.base; run_ox = c.ox; run_oy = c.oy; run_oz = c.oz; }
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc8[k] = 0.f;
         }
@@ -578,6 +632,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
         acc8[6] += y11 * ex; acc8[7] += y11 * c.fx;
       }
       if (kPos && live) {   // renderer.py:609-623 (spatial gradient, field.py:446-484)
+        const float t = __fmul_rn((float)i, dt32);
         const float ey = 1.f - c.fy, ez = 1.f - c.fz;
         const float ddx = ez * (ey * (v[1] - v[0]) + c.fy * (v[3] - v[2])) +
                           c.fz * (ey * (v[5] - v[4]) + c.fy * (v[7] - v[6]));
@@ -599,19 +654,8 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   }
 
   // ---- flush per-ray accumulators ----
-  if (kVol && run_base >= 0) {
-    float* q = d_volume + run_base;
-    atomicAdd(q, acc8[0]);
-    if (run_ox) atomicAdd(q + run_ox, acc8[1]);
-    if (run_oy) atomicAdd(q + run_oy, acc8[2]);
-    if (run_ox && run_oy) atomicAdd(q + run_ox + run_oy, acc8[3]);
-    if (run_oz) {
-      atomicAdd(q + run_oz, acc8[4]);
-      if (run_ox) atomicAdd(q + run_ox + run_oz, acc8[5]);
-      if (run_oy) atomicAdd(q + run_oy + run_oz, acc8[6]);
-      if (run_ox && run_oy) atomicAdd(q + run_ox + run_oy + run_oz, acc8[7]);
-    }
-  }
+  if (kVol && run_cell >= 0)
+    flush_cell<CELLS>(d_volume, d_cells, run_cell, run_base, run_ox, run_oy, run_oz, acc8);
   if (kTf) {
     if (tf_run >= 0) {
       const int j1 = min(tf_run + 1, TFA.count - 1);
@@ -635,26 +679,29 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
       if (kStep) stp = (double)dt_bl + (double)dt_pos;
       if (kCam) {
         // world-space sums: x_hat = scale * grid-space gradient (chain of g = (x-bmin)*scale)
-        double xo_h[3] = {s1x * V.scale[0], s1y * V.scale[1], s1z * V.scale[2]};
-        double w_h[3] = {s2x * V.scale[0], s2y * V.scale[1], s2z * V.scale[2]};
+        const double xo_h[3] = {s1x * V.scale[0], s1y * V.scale[1], s1z * V.scale[2]};
+        const double w_h[3] = {s2x * V.scale[0], s2y * V.scale[1], s2z * V.scale[2]};
         // entry point xo = o + tn*w moves with the camera (renderer.py:629-639)
         const double sdot = r.w[0] * xo_h[0] + r.w[1] * xo_h[1] + r.w[2] * xo_h[2];
-        double o_h[3] = {xo_h[0], xo_h[1], xo_h[2]};
-        double w_tot[3];
-        for (int k = 0; k < 3; ++k) w_tot[k] = w_h[k] + r.tn * xo_h[k];
-        if (!r.clamped && !r.miss) {
-          const int k = r.axis;
-          o_h[k] -= sdot / r.w[k];
-          w_tot[k] -= sdot * r.tn / r.w[k];
+        const bool need = !r.clamped && !r.miss;
+        double o_h[3], w_tot[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const bool sel = need && r.axis == k;
+          o_h[k] = xo_h[k] - (sel ? sdot / r.w[k] : 0.0);
+          w_tot[k] = w_h[k] + r.tn * xo_h[k] - (sel ? sdot * r.tn / r.w[k] : 0.0);
         }
         // d(direction)/d(lon,lat) at this pixel (field.py:253-271), per degree
         double dj[2];
+#pragma unroll
         for (int j = 0; j < 2; ++j) {
           double draw[3];
+#pragma unroll
           for (int k = 0; k < 3; ++k)
             draw[k] = F.df[k][j] + F.dr[k][j] * r.su + F.du[k][j] * r.sv;
           const double proj = r.w[0] * draw[0] + r.w[1] * draw[1] + r.w[2] * draw[2];
           double acc = 0.0;
+#pragma unroll
           for (int k = 0; k < 3; ++k)
             acc += w_tot[k] * (draw[k] - r.w[k] * proj) / r.dn + o_h[k] * F.jo[k][j];
           dj[j] = acc;
@@ -676,6 +723,67 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
       if (kStep) atomicAdd(d_dt, t2);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// cell-record layout: pack (volume -> cells) and fold (cell gradients -> voxels)
+// ---------------------------------------------------------------------------
+
+// cells[(i*CY + j)*CZ + k][c] = v[min(i+bx, X-1)][min(j+by, Y-1)][min(k+bz, Z-1)],
+// c = bx | by << 1 | bz << 2 (the corner order of field.py:318-322)
+__global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __restrict__ cells,
+                                                       long long ncells) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= ncells) return;
+  const int k = (int)(id % V.CZ);
+  const long long ij = id / V.CZ;
+  const int j = (int)(ij % V.CY);
+  const int i = (int)(ij / V.CY);
+  const int i1 = min(i + 1, V.X - 1), j1 = min(j + 1, V.Y - 1), k1 = min(k + 1, V.Z - 1);
+  const float* p = V.data;
+  auto at = [&](int a, int b, int c) { return __ldg(p + ((size_t)a * V.Y + b) * V.Z + c); };
+  float4 lo = make_float4(at(i, j, k), at(i1, j, k), at(i, j1, k), at(i1, j1, k));
+  float4 hi = make_float4(at(i, j, k1), at(i1, j, k1), at(i, j1, k1), at(i1, j1, k1));
+  float4* q = reinterpret_cast<float4*>(cells + 8 * id);
+  q[0] = lo;
+  q[1] = hi;
+}
+
+// d_volume[x,y,z] += sum of the cell-gradient slots that map to voxel (x,y,z)
+// (transpose of pack_cells_kernel)
+__global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
+                                                       const float* __restrict__ d_cells,
+                                                       float* __restrict__ d_volume,
+                                                       long long nvox) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nvox) return;
+  const int z = (int)(id % V.Z);
+  const long long xy = id / V.Z;
+  const int y = (int)(xy % V.Y);
+  const int x = (int)(xy / V.Y);
+  // per axis, the (cell index, corner bit) pairs that land on this voxel
+  int ci[3][2], cb[3][2], cn[3];
+  const int dims[3] = {V.X, V.Y, V.Z};
+  const int pos[3] = {x, y, z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    int n = 0;
+    if (dims[a] == 1) {
+      ci[a][0] = 0; cb[a][0] = 0; ci[a][1] = 0; cb[a][1] = 1; n = 2;
+    } else {
+      if (pos[a] <= dims[a] - 2) { ci[a][n] = pos[a]; cb[a][n] = 0; ++n; }
+      if (pos[a] >= 1) { ci[a][n] = pos[a] - 1; cb[a][n] = 1; ++n; }
+    }
+    cn[a] = n;
+  }
+  float s = 0.f;
+  for (int a = 0; a < cn[0]; ++a)
+    for (int b = 0; b < cn[1]; ++b)
+      for (int c = 0; c < cn[2]; ++c) {
+        const size_t cell = ((size_t)ci[0][a] * V.CY + ci[1][b]) * V.CZ + ci[2][c];
+        s += d_cells[8 * cell + (cb[0][a] | cb[1][b] << 1 | cb[2][c] << 2)];
+      }
+  d_volume[id] += s;
 }
 
 // ---------------------------------------------------------------------------
@@ -728,7 +836,12 @@ __global__ void __launch_bounds__(256) l1_loss_kernel(const float* __restrict__ 
 // host-side validation and launch
 // ---------------------------------------------------------------------------
 
-int make_vol(const ddvr_volume* vol, VolArgs& V) {
+long long cell_count(const int32_t dims[3]) {
+  return (long long)(dims[0] > 1 ? dims[0] - 1 : 1) * (dims[1] > 1 ? dims[1] - 1 : 1) *
+         (dims[2] > 1 ? dims[2] - 1 : 1);
+}
+
+int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
   if (!vol) return set_error(DDVR_INVALID_PARAMETER, "volume descriptor is NULL");
   for (int k = 0; k < 3; ++k) {
     if (vol->dims[k] < 1)
@@ -741,12 +854,17 @@ int make_vol(const ddvr_volume* vol, VolArgs& V) {
   const long long nvox = (long long)vol->dims[0] * vol->dims[1] * vol->dims[2];
   if (nvox > 0x7fffffffLL)
     return set_error(DDVR_UNSUPPORTED, "volume has more than 2^31 voxels");
-  if (!vol->data) return set_error(DDVR_INVALID_INPUT, "volume data pointer is NULL");
+  if (need_data && !vol->data) return set_error(DDVR_INVALID_INPUT, "volume data pointer is NULL");
+  if (vol->cells && ((uintptr_t)vol->cells & 31) != 0)
+    return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");
   V.data = vol->data;
+  V.cells = vol->cells;
   V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
   V.YZ = V.Y * V.Z;
+  V.CY = V.Y > 1 ? V.Y - 1 : 1; V.CZ = V.Z > 1 ? V.Z - 1 : 1;
   V.Xm2 = V.X >= 2 ? V.X - 2 : 0; V.Ym2 = V.Y >= 2 ? V.Y - 2 : 0; V.Zm2 = V.Z >= 2 ? V.Z - 2 : 0;
   V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
+  V.tX = V.X > 1 ? 1.f : 0.f; V.tY = V.Y > 1 ? 1.f : 0.f; V.tZ = V.Z > 1 ? 1.f : 0.f;
   // inside test in grid units.  Every sample of a march lies in [tn, tf) of the
   // exact slab, so the reference's 1e-9*extent tolerance (field.py:293) only has
   // to absorb rounding of the fixed-point entry point: 1e-6 voxel of slack.
@@ -755,8 +873,6 @@ int make_vol(const ddvr_volume* vol, VolArgs& V) {
     V.lo[k] = (long long)llrint((-0.5 - tol) * kFix);
     V.hi[k] = (long long)llrint(((double)vol->dims[k] - 0.5 + tol) * kFix);
     V.top[k] = (long long)(vol->dims[k] - 1) << 32;
-  }
-  for (int k = 0; k < 3; ++k) {
     V.bmin[k] = vol->box_min[k];
     V.bmax[k] = vol->box_max[k];
     V.scale[k] = (double)vol->dims[k] / (vol->box_max[k] - vol->box_min[k]);
@@ -812,13 +928,27 @@ dim3 grid_of(const Geometry& G, int n_views) {
   return dim3((G.W + kTile - 1) / kTile, (G.row1 - G.row0 + kTile - 1) / kTile, n_views);
 }
 
-template <unsigned M>
+template <typename K>
+void set_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <bool EARLY, bool CELLS, bool TAPE>
+void launch_forward(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
+                    const Geometry& G, float* image, float* trans) {
+  auto k = dvr_forward_kernel<EARLY, CELLS, TAPE>;
+  set_smem(k, smem);
+  k<<<grid, kThreads, smem, st>>>(V, T, G, image, trans);
+}
+
+template <unsigned M, bool CELLS>
 void launch_adjoint(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
                     const Geometry& G, const float* image, const float* trans, const float* seed,
-                    float* dv, double* dtf, double* dcam, double* ddt) {
-  auto k = dvr_adjoint_kernel<M>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<grid, kThreads, smem, st>>>(V, T, G, image, trans, seed, dv, dtf, dcam, ddt);
+                    float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
+  auto k = dvr_adjoint_kernel<M, CELLS>;
+  set_smem(k, smem);
+  k<<<grid, kThreads, smem, st>>>(V, T, G, image, trans, seed, dv, dcells, dtf, dcam, ddt);
 }
 
 }  // namespace
@@ -835,6 +965,30 @@ int32_t ddvr_abi_version(void) { return DDVR_ABI_VERSION; }
 
 int64_t ddvr_launch_count(void) { return g_launches.load(); }
 
+int64_t ddvr_cells_bytes(const int32_t dims[3]) {
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1) return 0;
+  return cell_count(dims) * 8 * (int64_t)sizeof(float);
+}
+
+int ddvr_pack_cells(const ddvr_volume* vol, float* cells_out, void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  int rc;
+  if ((rc = make_vol(vol, V))) return rc;
+  if (!cells_out) return set_error(DDVR_INVALID_INPUT, "cell output pointer is NULL");
+  if (((uintptr_t)cells_out & 31) != 0)
+    return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");
+  const long long n = cell_count(vol->dims);
+  pack_cells_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(V, cells_out,
+                                                                                  n);
+  return check_launch("pack_cells_kernel");
+}
+
+int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t mask) {
+  if (!vol || !vol->cells || !(mask & DDVR_TARGET_VOLUME)) return 0;
+  return ddvr_cells_bytes(vol->dims);
+}
+
 int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
                  int32_t n_views, const ddvr_params* p, float* image_out, float* trans_out,
                  void* stream) {
@@ -850,22 +1004,21 @@ int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid = grid_of(G, n_views);
-  if (p->early_stop) {
-    if (tbl > 48 * 1024)
-      cudaFuncSetAttribute(dvr_forward_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbl);
-    dvr_forward_kernel<true><<<grid, kThreads, tbl, st>>>(V, T, G, image_out, trans_out);
-  } else {
-    if (tbl > 48 * 1024)
-      cudaFuncSetAttribute(dvr_forward_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbl);
-    dvr_forward_kernel<false><<<grid, kThreads, tbl, st>>>(V, T, G, image_out, trans_out);
-  }
+  const bool early = p->early_stop != 0, cells = V.cells != nullptr, tape = G.tape != nullptr;
+#define DDVR_FWD(E, C, P) \
+  if (early == E && cells == C && tape == P) launch_forward<E, C, P>(grid, tbl, st, V, T, G, image_out, trans_out);
+  DDVR_FWD(false, false, false) DDVR_FWD(false, false, true) DDVR_FWD(false, true, false)
+  DDVR_FWD(false, true, true) DDVR_FWD(true, false, false) DDVR_FWD(true, false, true)
+  DDVR_FWD(true, true, false) DDVR_FWD(true, true, true)
+#undef DDVR_FWD
   return check_launch("dvr_forward_kernel");
 }
 
 int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
                  int32_t n_views, const ddvr_params* p, const float* image, const float* trans,
                  const float* seed, uint32_t mask, float* d_volume, double* d_tf,
-                 double* d_camera, double* d_dt, void* stream) {
+                 double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
+                 void* stream) {
   g_err[0] = 0;
   VolArgs V;
   TfArgs T;
@@ -886,14 +1039,32 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
     return set_error(DDVR_INVALID_INPUT, "d_camera is NULL but the camera target is set");
   if ((mask & DDVR_TARGET_STEPSIZE) && !d_dt)
     return set_error(DDVR_INVALID_INPUT, "d_dt is NULL but the stepsize target is set");
+  const int64_t ws_need = ddvr_adjoint_workspace_bytes(vol, mask);
+  if (ws_need > 0 && (!workspace || workspace_bytes < ws_need))
+    return set_error(DDVR_INVALID_INPUT,
+                     "volume target with cell records needs a %lld-byte workspace",
+                     (long long)ws_need);
+  if (workspace && ((uintptr_t)workspace & 31) != 0)
+    return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid = grid_of(G, n_views);
   const size_t smem = (mask & DDVR_TARGET_TF) ? 2 * tbl : tbl;
-#define DDVR_CASE(M)                                                                        \
-  case M:                                                                                   \
-    launch_adjoint<M>(grid, smem, st, V, T, G, image, trans, seed, d_volume, d_tf, d_camera, \
-                      d_dt);                                                                \
+  const bool cells = V.cells != nullptr;
+  float* d_cells = ws_need > 0 ? static_cast<float*>(workspace) : nullptr;
+  if (d_cells) {
+    cudaError_t e = cudaMemsetAsync(d_cells, 0, (size_t)ws_need, st);
+    if (e != cudaSuccess)
+      return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
+  }
+#define DDVR_CASE(M)                                                                       \
+  case M:                                                                                  \
+    if (cells)                                                                             \
+      launch_adjoint<M, true>(grid, smem, st, V, T, G, image, trans, seed, d_volume,       \
+                              d_cells, d_tf, d_camera, d_dt);                              \
+    else                                                                                   \
+      launch_adjoint<M, false>(grid, smem, st, V, T, G, image, trans, seed, d_volume,      \
+                               d_cells, d_tf, d_camera, d_dt);                             \
     break;
   switch (mask) {
     DDVR_CASE(1) DDVR_CASE(2) DDVR_CASE(3) DDVR_CASE(4) DDVR_CASE(5) DDVR_CASE(6) DDVR_CASE(7)
@@ -902,7 +1073,13 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
     default: break;
   }
 #undef DDVR_CASE
-  return check_launch("dvr_adjoint_kernel");
+  if ((rc = check_launch("dvr_adjoint_kernel"))) return rc;
+  if (d_cells) {
+    const long long nvox = (long long)V.X * V.Y * V.Z;
+    fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells, d_volume, nvox);
+    return check_launch("fold_cells_kernel");
+  }
+  return DDVR_OK;
 }
 
 int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float* seed_out,
@@ -926,9 +1103,7 @@ int ddvr_ray_setup(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_vi
   VolArgs V;
   Geometry G;
   int rc;
-  ddvr_volume tmp = *vol;
-  if (!tmp.data) tmp.data = reinterpret_cast<const float*>(16);   // geometry only
-  if ((rc = make_vol(&tmp, V)) || (rc = make_geo(cams, n_views, p, G))) return rc;
+  if ((rc = make_vol(vol, V, false)) || (rc = make_geo(cams, n_views, p, G))) return rc;
   if (!n_steps) return set_error(DDVR_INVALID_INPUT, "n_steps pointer is NULL");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
   ray_setup_kernel<<<grid_of(G, n_views), kThreads, 0, (cudaStream_t)stream>>>(V, G, tn_tf,

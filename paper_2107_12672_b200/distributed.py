@@ -78,7 +78,7 @@ class ShardedStep:
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
-                 group=None):
+                 group=None, layout="cells"):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
@@ -97,6 +97,10 @@ class ShardedStep:
         self.d_tf64 = torch.zeros(texels.shape, dtype=torch.float64, device=dev)
         self.d_dt64 = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss64 = torch.zeros(1, dtype=torch.float64, device=dev)
+        # cell records (rebuilt from the density every step) + adjoint workspace
+        self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
+                      if layout == "cells" else None)
+        self.workspace = R.workspace_for(density, self.mask, self.cells)
 
     def run(self, hook=None) -> FlatGrads:
         """One step; ``hook(name)`` (optional) is called at "post_forward",
@@ -110,7 +114,10 @@ class ShardedStep:
         self.loss64.zero_()
         V = self.cams.shape[0]
         if V:
-            vol, tf, prm = R._descs(self.density, self.texels, self.rig, self.dt, False)
+            if self.cells is not None:
+                R.pack_cells(self.density, self.cells)
+            vol, tf, prm = R._descs(self.density, self.texels, self.rig, self.dt, False,
+                                    self.cells)
             lib = N.lib()
             st = R._stream_ptr()
             N.check(lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
@@ -126,7 +133,11 @@ class ShardedStep:
                                      self.trans.data_ptr(), self.seed.data_ptr(), self.mask,
                                      want(N.TARGET_VOLUME, f.d_volume),
                                      want(N.TARGET_TF, self.d_tf64), None,
-                                     want(N.TARGET_STEPSIZE, self.d_dt64), st))
+                                     want(N.TARGET_STEPSIZE, self.d_dt64),
+                                     want(N.TARGET_VOLUME, self.workspace)
+                                     if self.workspace is not None else None,
+                                     self.workspace.numel() * 4 if self.workspace is not None
+                                     else 0, st))
             hook("post_adjoint")
         f.d_tf.copy_(self.d_tf64.reshape(-1))
         f.d_stepsize.copy_(self.d_dt64)

@@ -285,7 +285,8 @@ def render(volume, tf, cam, cfg, *, threads: int = 1) -> ImageRGBA:
     _validate_config(cfg)
     dev = _device()
     dens, tex, cams, rig = _upload(volume, tf, cam, dev)
-    img, trans = R.forward(dens, tex, cams, cfg.dt, rig, early_stop=(cfg.target == "none"))
+    img, trans = R.forward(dens, tex, cams, cfg.dt, rig, early_stop=(cfg.target == "none"),
+                           cells=R.pack_cells(dens))
     return _image_from(img, trans)
 
 
@@ -313,16 +314,19 @@ def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) 
             raise InvalidInputError("provided image does not match the camera size")
     dev = _device()
     dens, tex, cams, rig = _upload(volume, tf, cam, dev)
+    cells = R.pack_cells(dens)
     stored = getattr(cfg, "memory_mode", "inversion") == "stored"
     tape = None
     n_steps = None
+    stride = 0
     if stored:
         n_steps = _stored_tape_len(cams, cfg.dt, rig)
         stride = max(int(n_steps.max().item()), 1)
         tape = torch.empty(H * W * stride, dtype=torch.float32, device=dev)
-        img_t, trans_t = _forward_tape(dens, tex, cams, cfg.dt, rig, tape, stride)
+        img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig, cells=cells, tape=tape,
+                                   tape_stride=stride)
     elif img_arr is None:
-        img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig)
+        img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig, cells=cells)
     else:
         img_t = torch.from_numpy(img_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
         t_np = getattr(image, "_ddvr_trans", None)
@@ -335,12 +339,8 @@ def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) 
     d_tf = torch.zeros(tex.shape, dtype=torch.float64, device=dev) if bit == N.TARGET_TF else None
     d_cam = torch.zeros(1, 2, dtype=torch.float64, device=dev) if bit == N.TARGET_CAMERA else None
     d_dt = torch.zeros(1, dtype=torch.float64, device=dev) if bit == N.TARGET_STEPSIZE else None
-    if stored:
-        _adjoint_tape(dens, tex, cams, cfg.dt, rig, img_t, trans_t, seed_t, bit, tape, stride,
-                      d_vol, d_tf, d_cam, d_dt)
-    else:
-        R.adjoint(dens, tex, cams, cfg.dt, rig, img_t, trans_t, seed_t, bit, d_volume=d_vol,
-                  d_tf=d_tf, d_camera=d_cam, d_dt=d_dt)
+    R.adjoint(dens, tex, cams, cfg.dt, rig, img_t, trans_t, seed_t, bit, d_volume=d_vol,
+              d_tf=d_tf, d_camera=d_cam, d_dt=d_dt, cells=cells, tape=tape, tape_stride=stride)
     # per-ray state: inversion keeps (C, A) and the constant seed, 8 floats per ray,
     # independent of the step count (renderer.py:513); stored mode keeps a tape
     # of one transmittance per sample, n_max per 64-row tile.
@@ -360,32 +360,6 @@ def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) 
     if d_dt is not None:
         out.d_stepsize = float(d_dt.item())
     return out
-
-
-def _forward_tape(dens, tex, cams, dt, rig, tape, stride):
-    import ctypes
-    vol, tf, prm = R._descs(dens, tex, rig, dt, False)
-    prm.tape = tape.data_ptr()
-    prm.tape_stride = stride
-    img = torch.empty(1, rig.height, rig.width, 4, dtype=torch.float32, device=dens.device)
-    trans = torch.empty(1, rig.height, rig.width, dtype=torch.float32, device=dens.device)
-    N.check(N.lib().ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), 1,
-                                 ctypes.byref(prm), img.data_ptr(), trans.data_ptr(),
-                                 R._stream_ptr()))
-    return img, trans
-
-
-def _adjoint_tape(dens, tex, cams, dt, rig, img, trans, seed, mask, tape, stride, d_vol, d_tf,
-                  d_cam, d_dt):
-    import ctypes
-    vol, tf, prm = R._descs(dens, tex, rig, dt, False)
-    prm.tape = tape.data_ptr()
-    prm.tape_stride = stride
-    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    N.check(N.lib().ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), 1,
-                                 ctypes.byref(prm), img.data_ptr(), trans.data_ptr(),
-                                 seed.data_ptr(), mask, ptr(d_vol), ptr(d_tf), ptr(d_cam),
-                                 ptr(d_dt), R._stream_ptr()))
 
 
 def l1_loss(images, refs):

@@ -32,8 +32,10 @@ def lib():
 
 def test_header_declares_the_boundary():
     names = _declared()
-    assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_l1_loss", "ddvr_ray_setup",
-                            "ddvr_last_error", "ddvr_abi_version", "ddvr_launch_count"])
+    assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes",
+                            "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_l1_loss",
+                            "ddvr_ray_setup", "ddvr_last_error", "ddvr_abi_version",
+                            "ddvr_launch_count"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -48,14 +50,14 @@ def test_python_binding_matches_header():
     assert sorted(_native.EXPORTED) == _declared()
     # struct layout: ddvr_params = double + 6 int32 + pointer + int64
     assert ctypes.sizeof(_native.DdvrParams) == 8 + 6 * 4 + 8 + 8
-    assert ctypes.sizeof(_native.DdvrVolume) == 8 + 12 + 4 + 48
+    assert ctypes.sizeof(_native.DdvrVolume) == 8 + 12 + 4 + 48 + 8
     assert ctypes.sizeof(_native.DdvrTf) == 16
 
 
 def _descs(dt=0.1, dims=(4, 4, 4), box=((-0.5,) * 3, (0.5,) * 3), R=8, W=8, H=8, rows=(0, 0)):
     from paper_2107_12672_b200 import _native as N
     vol = N.DdvrVolume(16, (ctypes.c_int32 * 3)(*dims), (ctypes.c_double * 3)(*box[0]),
-                       (ctypes.c_double * 3)(*box[1]))
+                       (ctypes.c_double * 3)(*box[1]), None)
     tf = N.DdvrTf(N.TF_TEXTURE, R, 16)
     prm = N.DdvrParams(dt, W, H, rows[0], rows[1], 0, 0, None, 0)
     return vol, tf, prm
@@ -81,14 +83,14 @@ def test_forward_validation(lib, kw, code, text):
 def test_adjoint_without_target_is_unsupported(lib):
     vol, tf, prm = _descs()
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
-                          None, 16, 0, None, None, None, None, None)
+                          None, 16, 0, None, None, None, None, None, 0, None)
     assert rc == 3 and "target" in lib.ddvr_last_error().decode()
 
 
 def test_adjoint_missing_output_is_invalid_input(lib):
     vol, tf, prm = _descs()
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
-                          None, 16, 8, None, None, None, None, None)
+                          None, 16, 8, None, None, None, None, None, 0, None)
     assert rc == 2 and "d_volume" in lib.ddvr_last_error().decode()
 
 
@@ -112,9 +114,28 @@ def test_status_codes_map_to_reference_exceptions(lib):
     vol, tf, prm = _descs()
     with pytest.raises(UnsupportedConfigurationError):
         N.check(lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm),
-                                 16, None, 16, 0, None, None, None, None, None))
+                                 16, None, 16, 0, None, None, None, None, None, 0, None))
     with pytest.raises(InvalidInputError):
         N.check(lib.ddvr_l1_loss(None, None, 4, 1.0, None, None, None))
+
+
+def test_cell_layout_sizes(lib):
+    dims = (ctypes.c_int32 * 3)(256, 256, 256)
+    assert lib.ddvr_cells_bytes(dims) == 255 ** 3 * 32
+    assert lib.ddvr_cells_bytes((ctypes.c_int32 * 3)(1, 5, 2)) == 1 * 4 * 1 * 32
+    vol, _, _ = _descs(dims=(9, 5, 3))
+    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 0      # no cell records
+    vol.cells = 32
+    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 8 * 4 * 2 * 32
+    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 4) == 0      # tf target only
+
+
+def test_adjoint_with_cells_requires_workspace(lib):
+    vol, tf, prm = _descs()
+    vol.cells = 32
+    rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, 16, 8, 16, None, None, None, None, 0, None)
+    assert rc == 2 and "workspace" in lib.ddvr_last_error().decode()
 
 
 def test_zero_views_is_a_no_op(lib):

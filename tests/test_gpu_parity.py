@@ -29,7 +29,7 @@ def _torch():
     return torch
 
 
-def _setup(g, dev, volume=None, rows=None):
+def _setup(g, dev, volume=None, rows=None, layout="cells"):
     torch = _torch()
     from paper_2107_12672_b200 import raymarch as R
     cam = g["cam"]
@@ -42,10 +42,12 @@ def _setup(g, dev, volume=None, rows=None):
     box = g.get("box", np.array([[-0.5] * 3, [0.5] * 3]))
     rig = R.Rig(int(W), int(H), tuple(box[0]), tuple(box[1]),
                 rows=tuple(int(r) for r in rows) if rows is not None else None)
-    return dens, tex, cams, rig, float(g["dt"])
+    cells = R.pack_cells(dens) if layout == "cells" else None
+    return dens, tex, cams, rig, float(g["dt"]), cells
 
 
-def _grads(dens, tex, cams, rig, dt, img, trans, seed, targets, stored_tape=None):
+def _grads(dens, tex, cams, rig, dt, img, trans, seed, targets, cells=None, tape=None,
+           stride=0):
     torch = _torch()
     from paper_2107_12672_b200 import raymarch as R
     dev = dens.device
@@ -60,7 +62,8 @@ def _grads(dens, tex, cams, rig, dt, img, trans, seed, targets, stored_tape=None
         "stepsize": torch.zeros(1, dtype=torch.float64, device=dev) if "stepsize" in targets else None,
     }
     R.adjoint(dens, tex, cams, dt, rig, img, trans, seed, mask, d_volume=out["volume"],
-              d_tf=out["tf"], d_camera=out["camera"], d_dt=out["stepsize"])
+              d_tf=out["tf"], d_camera=out["camera"], d_dt=out["stepsize"], cells=cells,
+              tape=tape, tape_stride=stride)
     torch.cuda.synchronize()
     return {k: v.double().cpu().numpy() for k, v in out.items() if v is not None}
 
@@ -72,17 +75,18 @@ SCENES = golden_names("kat_") + golden_names("rand_")
 def test_ray_setup_bit_exact(cuda, name):
     from paper_2107_12672_b200 import raymarch as R
     g = golden(name)
-    dens, tex, cams, rig, dt = _setup(g, cuda)
+    dens, tex, cams, rig, dt, _ = _setup(g, cuda, layout="voxels")
     _, n, _ = R.ray_setup(cams, dt, rig, dims=g["volume"].shape)
     np.testing.assert_array_equal(n[0].cpu().numpy().ravel(), g["n_steps"].ravel())
 
 
 @pytest.mark.parametrize("name", SCENES)
-def test_image_matches_reference(cuda, name):
+@pytest.mark.parametrize("layout", ["cells", "voxels"])
+def test_image_matches_reference(cuda, name, layout):
     from paper_2107_12672_b200 import raymarch as R
     g = golden(name)
-    dens, tex, cams, rig, dt = _setup(g, cuda)
-    img, trans = R.forward(dens, tex, cams, dt, rig)
+    dens, tex, cams, rig, dt, cells = _setup(g, cuda, layout=layout)
+    img, trans = R.forward(dens, tex, cams, dt, rig, cells=cells)
     got = img[0].double().cpu().numpy()
     ref = g["image"]
     if np.linalg.norm(ref) == 0:
@@ -92,7 +96,7 @@ def test_image_matches_reference(cuda, name):
     T = trans[0].double().cpu().numpy()
     np.testing.assert_allclose(1.0 - T, got[..., 3], atol=2e-6)
     if "image_none" in g:   # early ray termination (renderer.py:331-335)
-        img2, _ = R.forward(dens, tex, cams, dt, rig, early_stop=True)
+        img2, _ = R.forward(dens, tex, cams, dt, rig, early_stop=True, cells=cells)
         ref2 = g["image_none"]
         got2 = img2[0].double().cpu().numpy()
         if np.linalg.norm(ref2) == 0:
@@ -103,30 +107,27 @@ def test_image_matches_reference(cuda, name):
 
 @pytest.mark.parametrize("name", SCENES)
 @pytest.mark.parametrize("mode", ["inversion", "stored"])
-def test_gradients_match_reference(cuda, name, mode):
+@pytest.mark.parametrize("layout", ["cells", "voxels"])
+def test_gradients_match_reference(cuda, name, mode, layout):
     torch = _torch()
     from paper_2107_12672_b200 import raymarch as R
     g = golden(name)
     keys = [k for k in g if k.startswith(mode + "_") and not k.endswith("state_floats")]
     if not keys:
         pytest.skip(f"no {mode} fixtures for {name}")
-    dens, tex, cams, rig, dt = _setup(g, cuda)
+    dens, tex, cams, rig, dt, cells = _setup(g, cuda, layout=layout)
     seed = torch.from_numpy(np.asarray(g["seed"], np.float32)).to(cuda)[None].contiguous()
+    tape, stride = None, 0
     if mode == "stored":
-        from paper_2107_12672_b200 import voldiff_api as A
         H, W = rig.height, rig.width
         _, n, _ = R.ray_setup(cams, dt, rig)
         stride = max(int(n.max().item()), 1)
         tape = torch.full((H * W * stride,), float("nan"), dtype=torch.float32, device=cuda)
-        img, trans = A._forward_tape(dens, tex, cams, dt, rig, tape, stride)
-    else:
-        img, trans = R.forward(dens, tex, cams, dt, rig)
+    img, trans = R.forward(dens, tex, cams, dt, rig, cells=cells, tape=tape, tape_stride=stride)
     targets = [k.split("_", 1)[1] for k in keys]
     for t in targets:   # one target per call, as the reference
-        if mode == "stored":
-            got = _stored(dens, tex, cams, rig, dt, img, trans, seed, t, tape, stride)
-        else:
-            got = _grads(dens, tex, cams, rig, dt, img, trans, seed, [t])[t]
+        got = _grads(dens, tex, cams, rig, dt, img, trans, seed, [t], cells=cells, tape=tape,
+                     stride=stride)[t]
         ref = np.asarray(g[f"{mode}_{t}"], np.float64).reshape(got.shape)
         if np.linalg.norm(ref) < 1e-300:
             assert np.abs(got).max() <= 1e-7, (t, np.abs(got).max())
@@ -134,32 +135,19 @@ def test_gradients_match_reference(cuda, name, mode):
             assert rel_l2(got, ref) <= GRAD_TOL, (t, rel_l2(got, ref))
     if mode == "inversion" and len(targets) > 1:
         # all targets in ONE adjoint launch reproduce each single-target result
-        both = _grads(dens, tex, cams, rig, dt, img, trans, seed, targets)
+        both = _grads(dens, tex, cams, rig, dt, img, trans, seed, targets, cells=cells)
         for t in targets:
             ref = np.asarray(g[f"{mode}_{t}"], np.float64).reshape(both[t].shape)
             if np.linalg.norm(ref) > 1e-300:
                 assert rel_l2(both[t], ref) <= GRAD_TOL
 
 
-def _stored(dens, tex, cams, rig, dt, img, trans, seed, t, tape, stride):
-    torch = _torch()
-    from paper_2107_12672_b200 import voldiff_api as A
-    dev = dens.device
-    d_vol = torch.zeros_like(dens) if t == "volume" else None
-    d_tf = torch.zeros(tex.shape, dtype=torch.float64, device=dev) if t == "tf" else None
-    d_cam = torch.zeros(1, 2, dtype=torch.float64, device=dev) if t == "camera" else None
-    d_dt = torch.zeros(1, dtype=torch.float64, device=dev) if t == "stepsize" else None
-    A._adjoint_tape(dens, tex, cams, dt, rig, img, trans, seed, BIT[t], tape, stride, d_vol, d_tf,
-                    d_cam, d_dt)
-    torch.cuda.synchronize()
-    return next(v for v in (d_vol, d_tf, d_cam, d_dt) if v is not None).double().cpu().numpy()
-
-
 CONFIG_CASES = ["C1", "C2", "C3", "C4", "C5"]
 
 
 @pytest.mark.parametrize("name", CONFIG_CASES)
-def test_config_band_matches_reference(cuda, name):
+@pytest.mark.parametrize("layout", ["cells", "voxels"])
+def test_config_band_matches_reference(cuda, name, layout):
     """Full C1 view and row bands of view 0 at C2..C5 against the reference."""
     torch = _torch()
     from paper_2107_12672_b200 import raymarch as R
@@ -171,17 +159,17 @@ def test_config_band_matches_reference(cuda, name):
     np.testing.assert_array_equal(probe, g["volume_probe"])
     rows = g["rows"]
     g = dict(g, volume=vol)
-    dens, tex, cams, rig, dt = _setup(g, cuda, rows=rows)
+    dens, tex, cams, rig, dt, cells = _setup(g, cuda, rows=rows, layout=layout)
     tn_tf, n, _ = R.ray_setup(cams, dt, rig, dims=vol.shape)
     np.testing.assert_array_equal(n[0].cpu().numpy().ravel(), g["n_steps"].ravel())
     np.testing.assert_allclose(tn_tf[0].cpu().numpy().reshape(-1, 2).T, g["tn_tf"], rtol=0,
                                atol=1e-12)
-    img, trans = R.forward(dens, tex, cams, dt, rig)
+    img, trans = R.forward(dens, tex, cams, dt, rig, cells=cells)
     assert rel_l2(img[0].double().cpu().numpy(), g["image"]) <= IMG_TOL
     seed = torch.from_numpy(g["seed_band"].astype(np.float32)).to(cuda)[None].contiguous()
     targets = [k.split("_", 1)[1] for k in g if k.startswith("inversion_")]
     targets = sorted({t.replace("_idx", "").replace("_val", "") for t in targets})
-    got = _grads(dens, tex, cams, rig, dt, img, trans, seed, targets)
+    got = _grads(dens, tex, cams, rig, dt, img, trans, seed, targets, cells=cells)
     for t in targets:
         if t == "volume" and "inversion_volume_idx" in g:
             ref = np.zeros(vol.size)
