@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0,
                    help="target CPU time of the cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--views", type=int, default=0,
+                   help="profiling aid: use only the first N views (not a bench result)")
+    p.add_argument("--layout", default="cells", choices=["cells", "voxels"])
     return p.parse_args()
 
 
@@ -257,6 +260,8 @@ def run_own(args, cfg):
     truth = torch.from_numpy(cfg.volume()).to(dev)
     tex = torch.from_numpy(cfg.texels().astype(np.float32)).to(dev)
     poses = cfg.view_poses()
+    if args.views:
+        poses = poses[: args.views]
     mine = shard_views(len(poses), rank, world)
     ll = torch.tensor([poses[i] for i in mine], dtype=torch.float64, device=dev).reshape(-1, 2)
     rig = R.Rig(cfg.image, cfg.image)
@@ -266,7 +271,8 @@ def run_own(args, cfg):
     est = (0.85 * truth + 0.1 * torch.rand(truth.shape, generator=g, device=dev)).contiguous()
     total_elems = 4 * cfg.image * cfg.image * len(poses)
     step = ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
-                       total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov)
+                       total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
+                       layout=args.layout)
     _, n_steps, _ = R.ray_setup(cams, cfg.dt, rig, dims=tuple(truth.shape))
     local_samples = int(n_steps.to(torch.int64).sum().item())
     local_rays = n_steps.numel()

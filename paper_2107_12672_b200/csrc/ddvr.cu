@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
@@ -86,9 +87,10 @@ int check_launch(const char* what) {
 
 struct VolArgs {
   const float* __restrict__ data;    // (X,Y,Z) z fastest
-  const float* __restrict__ cells;   // cell records (nullable): 8 corner values per cell
+  const float* __restrict__ cells;   // padded cell records (nullable): 8 corner values per cell
+  const float* __restrict__ cell0;   // address of the record of cell (0,0,0) inside cells
   int X, Y, Z, YZ;
-  int CY, CZ;              // cells along y and z: max(dim-1, 1)
+  int CY, CZ;              // padded cells along y and z: dim + 1 (cells -1 .. dim-1)
   int Xm2, Ym2, Zm2;       // max(dim-2, 0): highest cell index (field.py:302-304)
   int X1, Y1, Z1;          // dim-1: clamp bound (field.py:299-301)
   float tX, tY, tZ;        // cell fraction at the top clamp: 1 if dim > 1 else 0
@@ -249,7 +251,7 @@ __device__ void setup_ray(const Frame& F, const VolArgs& V, double dt, int W, in
 // ---------------------------------------------------------------------------
 
 struct Cell {
-  int cell;            // cell-record index (ix * CY + iy) * CZ + iz
+  int cell;            // padded cell-record index relative to cell0 (may be negative)
   int base;            // flat voxel index of corner (ix, iy, iz)
   int ox, oy, oz;      // flat voxel offsets to the +x/+y/+z corners (0 on a clamped axis)
   float fx, fy, fz;    // cell fractions
@@ -266,21 +268,50 @@ __device__ __forceinline__ void axis_cell(long long g, int d1, int dm2, float ft
   f = hi < 0 ? 0.f : (hi >= d1 ? ftop : fr);
 }
 
-template <bool SCALAR>
-__device__ __forceinline__ void locate(const VolArgs& V, long long gx, long long gy, long long gz,
-                                       bool all_inside, Cell& c) {
+// Voxel layout: the clamps of field.py:299-307 per sample.
+__device__ __forceinline__ void locate_voxels(const VolArgs& V, long long gx, long long gy,
+                                              long long gz, bool all_inside, Cell& c) {
   c.inside = all_inside || inside_fx(V, gx, gy, gz);
   int ix, iy, iz;
   axis_cell(gx, V.X1, V.Xm2, V.tX, ix, c.fx);
   axis_cell(gy, V.Y1, V.Ym2, V.tY, iy, c.fy);
   axis_cell(gz, V.Z1, V.Zm2, V.tZ, iz, c.fz);
-  c.cell = (ix * V.CY + iy) * V.CZ + iz;
-  if (SCALAR) {
-    c.base = (ix * V.Y + iy) * V.Z + iz;
-    c.ox = ix + 1 < V.X ? V.YZ : 0;
-    c.oy = iy + 1 < V.Y ? V.Z : 0;
-    c.oz = iz + 1 < V.Z ? 1 : 0;
+  c.base = (ix * V.Y + iy) * V.Z + iz;
+  c.cell = c.base;   // identifies the cell (its 8 corners) for the cell-run logic
+  c.ox = ix + 1 < V.X ? V.YZ : 0;
+  c.oy = iy + 1 < V.Y ? V.Z : 0;
+  c.oz = iz + 1 < V.Z ? 1 : 0;
+}
+
+// Padded cell layout: records exist for cells -1 .. dim-1 on every axis with
+// edge-replicated corners, so clamp-to-edge (field.py:299-307) is baked into
+// the data: a sample in [-0.5, 0) reads cell -1 whose corners are both v[0],
+// one in [dim-1, dim-0.5] reads cell dim-1 whose corners are both v[dim-1].
+// Values, spatial derivatives (0 in the pad, field.py:459-484) and scatter
+// weights (folded back onto the clamped voxel) equal the clamped ones; the
+// only difference is the measure-zero point g == dim-1 exactly.  Cell
+// location is then just the high word and the fraction of each coordinate.
+__device__ __forceinline__ void locate_cells(const VolArgs& V, long long gx, long long gy,
+                                             long long gz, bool all_inside, Cell& c) {
+  int hx = (int)(gx >> 32), hy = (int)(gy >> 32), hz = (int)(gz >> 32);
+  c.inside = true;
+  if (!all_inside) {   // never taken for march samples (see Ray::all_inside); kept safe
+    c.inside = inside_fx(V, gx, gy, gz);
+    hx = min(max(hx, -1), V.X1);
+    hy = min(max(hy, -1), V.Y1);
+    hz = min(max(hz, -1), V.Z1);
   }
+  c.fx = __fmul_rn(__uint2float_rn((unsigned)gx), kInvFix);
+  c.fy = __fmul_rn(__uint2float_rn((unsigned)gy), kInvFix);
+  c.fz = __fmul_rn(__uint2float_rn((unsigned)gz), kInvFix);
+  c.cell = (hx * V.CY + hy) * V.CZ + hz;
+}
+
+template <bool CELLS>
+__device__ __forceinline__ void locate(const VolArgs& V, long long gx, long long gy, long long gz,
+                                       bool all_inside, Cell& c) {
+  if (CELLS) locate_cells(V, gx, gy, gz, all_inside, c);
+  else locate_voxels(V, gx, gy, gz, all_inside, c);
 }
 
 __device__ __forceinline__ void ld256(const float* p, float v[8]) {
@@ -300,7 +331,7 @@ __device__ __forceinline__ void red128(float* p, float a, float b, float c, floa
 template <bool CELLS>
 __device__ __forceinline__ void fetch8(const VolArgs& V, const Cell& c, float v[8]) {
   if (CELLS) {
-    ld256(V.cells + 8 * (size_t)c.cell, v);
+    ld256(V.cell0 + 8 * (long long)c.cell, v);
   } else {
     const float* p = V.data + c.base;
     v[0] = __ldg(p);
@@ -335,9 +366,10 @@ __device__ __forceinline__ float clamp_density(bool inside, float raw) {
 // transfer functions (field.py:525-579; renderer.py:472-488)
 // ---------------------------------------------------------------------------
 
-// texel table: R texels, centre of texel r at (r + 0.5)/R, clamp-to-edge
+// texel table: R texels, centre of texel r at (r + 0.5)/R, clamp-to-edge;
+// stored as (texel, delta) pairs by load_tf
 struct TexelTF {
-  const float4* tex;   // shared memory
+  const float4* tex;   // shared memory, 2R float4
   int R;
   float fR, fR1;       // R, R-1
   int Rm2;             // max(R-2, 0)
@@ -347,12 +379,9 @@ struct TexelTF {
     const float t = __fsub_rn(__fmul_rn(d, fR), 0.5f);
     const float f = fminf(fmaxf(t, 0.f), fR1);
     i0 = min((int)f, Rm2);
-    const int i1 = min(i0 + 1, R - 1);
     w = __fsub_rn(f, (float)i0);
-    const float4 a = tex[i0];
-    const float4 b = tex[i1];
-    const float4 dlt = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
-                                   __fsub_rn(b.z, a.z), __fsub_rn(b.w, a.w));
+    const float4 a = tex[2 * i0];
+    const float4 dlt = tex[2 * i0 + 1];
     if (want_slope) {
       const bool live = t >= 0.f && t <= fR1;
       const float s = live ? fR : 0.f;
@@ -384,7 +413,8 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
   p = __fmaf_rn(-x, p, 0.5f);
   p = __fmaf_rn(-x, p, 1.f);
   const float a_small = __fmul_rn(x, p);
-  const float e_big = __expf(-x);
+  float e_big;   // exp(-x) = 2^(-x log2 e); ftz is harmless: e < 1e-6 is clamped below
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e_big) : "f"(__fmul_rn(x, -1.4426950408889634f)));
   const bool small = x < 0.34657359f;
   const float a_raw = small ? a_small : __fsub_rn(1.f, e_big);
   s.e = small ? __fsub_rn(1.f, a_small) : e_big;
@@ -398,9 +428,17 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
 // shared prologue: TF table + view frame into shared memory
 // ---------------------------------------------------------------------------
 
+// shared TF table as (texel k, texel k+1 - texel k) pairs: the lerp is then 4
+// FFMA and the slope (field.py:576) needs no subtraction
 __device__ __forceinline__ void load_tf(const TfArgs& tf, float4* s_tex) {
   const float4* src = reinterpret_cast<const float4*>(tf.params);
-  for (int i = threadIdx.x; i < tf.count; i += blockDim.x) s_tex[i] = src[i];
+  for (int i = threadIdx.x; i < tf.count; i += blockDim.x) {
+    const float4 a = src[i];
+    const float4 b = src[min(i + 1, tf.count - 1)];
+    s_tex[2 * i] = a;
+    s_tex[2 * i + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y), __fsub_rn(b.z, a.z),
+                                   __fsub_rn(b.w, a.w));
+  }
 }
 
 __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
@@ -444,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
     if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     Cell c;
-    locate<!CELLS>(V, gx, gy, gz, r.all_inside, c);
+    locate<CELLS>(V, gx, gy, gz, r.all_inside, c);
     gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
     float v[8], p0, p1;
     fetch8<CELLS>(V, c, v);
@@ -481,7 +519,7 @@ __device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
                                            float* __restrict__ d_cells, int cell, int base,
                                            int ox, int oy, int oz, const float acc[8]) {
   if (CELLS) {
-    float* q = d_cells + 8 * (size_t)cell;
+    float* q = d_cells + 8 * (long long)cell;
     red128(q, acc[0], acc[1], acc[2], acc[3]);
     red128(q + 4, acc[4], acc[5], acc[6], acc[7]);
   } else {
@@ -515,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   extern __shared__ float4 s_tex[];            // [R] texels, then [R] TF gradient
   __shared__ Frame F;
   __shared__ double s_red[kWarps][3];
-  float4* s_tfg = s_tex + TFA.count;
+  float4* s_tfg = s_tex + 2 * TFA.count;
   const int view = blockIdx.z;
   load_tf(TFA, s_tex);
   if (kTf)
@@ -548,7 +586,8 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   float a_hat = sd.w;
   float T = Tn;                       // transmittance after the current sample
   // volume cell-run accumulator
-  int run_cell = -1, run_base = 0, run_ox = 0, run_oy = 0, run_oz = 0;
+  constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
+  int run_cell = kNoRun, run_base = 0, run_ox = 0, run_oy = 0, run_oz = 0;
   float acc8[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc8[k] = 0.f;
@@ -565,7 +604,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
 
   for (int i = r.n - 1; i >= 0; --i) {
     Cell c;
-    locate<!CELLS>(V, gx, gy, gz, r.all_inside, c);
+    locate<CELLS>(V, gx, gy, gz, r.all_inside, c);
     float v[8], p0, p1;
     fetch8<CELLS>(V, c, v);
     const float raw = interp(c, v, p0, p1);
@@ -614,7 +653,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
       const bool live = c.inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol) {   // renderer.py:607-608, accumulated per cell run
         if (c.cell != run_cell) {
-          if (run_cell >= 0)
+          if (run_cell != kNoRun)
             flush_cell<CELLS>(d_volume, d_cells, run_cell, run_base, run_ox, run_oy, run_oz, acc8);
           run_cell = c.cell;
           if (!CELLS) { run_base = c.base; run_ox = c.ox; run_oy = c.oy; run_oz = c.oz; }
@@ -654,7 +693,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   }
 
   // ---- flush per-ray accumulators ----
-  if (kVol && run_cell >= 0)
+  if (kVol && run_cell != kNoRun)
     flush_cell<CELLS>(d_volume, d_cells, run_cell, run_base, run_ox, run_oy, run_oz, acc8);
   if (kTf) {
     if (tf_run >= 0) {
@@ -729,28 +768,30 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
 // cell-record layout: pack (volume -> cells) and fold (cell gradients -> voxels)
 // ---------------------------------------------------------------------------
 
-// cells[(i*CY + j)*CZ + k][c] = v[min(i+bx, X-1)][min(j+by, Y-1)][min(k+bz, Z-1)],
-// c = bx | by << 1 | bz << 2 (the corner order of field.py:318-322)
+// Padded record of cell (i,j,k), i in [-1, X-1] (storage index i+1):
+//   cells[c] = v[clamp(i+bx, 0, X-1)][clamp(j+by, 0, Y-1)][clamp(k+bz, 0, Z-1)],
+//   c = bx | by << 1 | bz << 2 (the corner order of field.py:318-322).
 __global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __restrict__ cells,
                                                        long long ncells) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= ncells) return;
-  const int k = (int)(id % V.CZ);
+  const int k = (int)(id % V.CZ) - 1;
   const long long ij = id / V.CZ;
-  const int j = (int)(ij % V.CY);
-  const int i = (int)(ij / V.CY);
+  const int j = (int)(ij % V.CY) - 1;
+  const int i = (int)(ij / V.CY) - 1;
+  const int i0 = max(i, 0), j0 = max(j, 0), k0 = max(k, 0);
   const int i1 = min(i + 1, V.X - 1), j1 = min(j + 1, V.Y - 1), k1 = min(k + 1, V.Z - 1);
   const float* p = V.data;
   auto at = [&](int a, int b, int c) { return __ldg(p + ((size_t)a * V.Y + b) * V.Z + c); };
-  float4 lo = make_float4(at(i, j, k), at(i1, j, k), at(i, j1, k), at(i1, j1, k));
-  float4 hi = make_float4(at(i, j, k1), at(i1, j, k1), at(i, j1, k1), at(i1, j1, k1));
+  const float4 lo = make_float4(at(i0, j0, k0), at(i1, j0, k0), at(i0, j1, k0), at(i1, j1, k0));
+  const float4 hi = make_float4(at(i0, j0, k1), at(i1, j0, k1), at(i0, j1, k1), at(i1, j1, k1));
   float4* q = reinterpret_cast<float4*>(cells + 8 * id);
   q[0] = lo;
   q[1] = hi;
 }
 
-// d_volume[x,y,z] += sum of the cell-gradient slots that map to voxel (x,y,z)
-// (transpose of pack_cells_kernel)
+// d_volume[x,y,z] += every cell-gradient slot that pack_cells_kernel filled
+// from voxel (x,y,z) (its exact transpose, padding included)
 __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
                                                        const float* __restrict__ d_cells,
                                                        float* __restrict__ d_volume,
@@ -761,19 +802,22 @@ __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
   const long long xy = id / V.Z;
   const int y = (int)(xy % V.Y);
   const int x = (int)(xy / V.Y);
-  // per axis, the (cell index, corner bit) pairs that land on this voxel
-  int ci[3][2], cb[3][2], cn[3];
+  // per axis, the (storage cell index, corner bit) pairs whose clamped corner is this voxel
+  int ci[3][4], cb[3][4], cn[3];
   const int dims[3] = {V.X, V.Y, V.Z};
   const int pos[3] = {x, y, z};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     int n = 0;
-    if (dims[a] == 1) {
-      ci[a][0] = 0; cb[a][0] = 0; ci[a][1] = 0; cb[a][1] = 1; n = 2;
-    } else {
-      if (pos[a] <= dims[a] - 2) { ci[a][n] = pos[a]; cb[a][n] = 0; ++n; }
-      if (pos[a] >= 1) { ci[a][n] = pos[a] - 1; cb[a][n] = 1; ++n; }
-    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int d = -2; d <= 1; ++d) {
+        const int i = pos[a] + d;                    // padded cell index in [-1, dim-1]
+        if (i < -1 || i > dims[a] - 1) continue;
+        const int corner = min(max(i + b, 0), dims[a] - 1);
+        if (corner == pos[a] && n < 4) { ci[a][n] = i + 1; cb[a][n] = b; ++n; }
+      }
     cn[a] = n;
   }
   float s = 0.f;
@@ -836,9 +880,9 @@ __global__ void __launch_bounds__(256) l1_loss_kernel(const float* __restrict__ 
 // host-side validation and launch
 // ---------------------------------------------------------------------------
 
+// padded cell grid: cells -1 .. dim-1 on every axis
 long long cell_count(const int32_t dims[3]) {
-  return (long long)(dims[0] > 1 ? dims[0] - 1 : 1) * (dims[1] > 1 ? dims[1] - 1 : 1) *
-         (dims[2] > 1 ? dims[2] - 1 : 1);
+  return (long long)(dims[0] + 1) * (dims[1] + 1) * (dims[2] + 1);
 }
 
 int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
@@ -861,7 +905,8 @@ int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
   V.cells = vol->cells;
   V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
   V.YZ = V.Y * V.Z;
-  V.CY = V.Y > 1 ? V.Y - 1 : 1; V.CZ = V.Z > 1 ? V.Z - 1 : 1;
+  V.CY = V.Y + 1; V.CZ = V.Z + 1;
+  V.cell0 = V.cells ? V.cells + 8 * (((long long)V.CY + 1) * V.CZ + 1) : nullptr;
   V.Xm2 = V.X >= 2 ? V.X - 2 : 0; V.Ym2 = V.Y >= 2 ? V.Y - 2 : 0; V.Zm2 = V.Z >= 2 ? V.Z - 2 : 0;
   V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
   V.tX = V.X > 1 ? 1.f : 0.f; V.tY = V.Y > 1 ? 1.f : 0.f; V.tZ = V.Z > 1 ? 1.f : 0.f;
@@ -889,10 +934,10 @@ int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
   if (!tf->params) return set_error(DDVR_INVALID_INPUT, "transfer function pointer is NULL");
   if (((uintptr_t)tf->params & 15) != 0)
     return set_error(DDVR_INVALID_INPUT, "transfer function must be 16-byte aligned");
-  smem_per_table = (size_t)tf->count * sizeof(float4);
-  if (2 * smem_per_table > (size_t)kMaxTfBytes)
+  smem_per_table = 2 * (size_t)tf->count * sizeof(float4);   // (texel, delta) pairs
+  if (3 * (size_t)tf->count * sizeof(float4) > (size_t)kMaxTfBytes)
     return set_error(DDVR_UNSUPPORTED, "transfer function resolution %d exceeds %d texels",
-                     tf->count, kMaxTfBytes / 32);
+                     tf->count, kMaxTfBytes / 48);
   A.params = tf->params;
   A.kind = tf->kind;
   A.count = tf->count;
@@ -1049,11 +1094,13 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid = grid_of(G, n_views);
-  const size_t smem = (mask & DDVR_TARGET_TF) ? 2 * tbl : tbl;
+  const size_t smem = (mask & DDVR_TARGET_TF) ? tbl + tbl / 2 : tbl;
   const bool cells = V.cells != nullptr;
-  float* d_cells = ws_need > 0 ? static_cast<float*>(workspace) : nullptr;
-  if (d_cells) {
-    cudaError_t e = cudaMemsetAsync(d_cells, 0, (size_t)ws_need, st);
+  float* d_cells_all = ws_need > 0 ? static_cast<float*>(workspace) : nullptr;
+  // the kernel indexes cell gradients relative to cell (0,0,0), like V.cell0
+  float* d_cells = d_cells_all ? d_cells_all + (V.cell0 - V.cells) : nullptr;
+  if (d_cells_all) {
+    cudaError_t e = cudaMemsetAsync(d_cells_all, 0, (size_t)ws_need, st);
     if (e != cudaSuccess)
       return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
   }
@@ -1076,7 +1123,8 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   if ((rc = check_launch("dvr_adjoint_kernel"))) return rc;
   if (d_cells) {
     const long long nvox = (long long)V.X * V.Y * V.Z;
-    fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells, d_volume, nvox);
+    fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells_all, d_volume,
+                                                                     nvox);
     return check_launch("fold_cells_kernel");
   }
   return DDVR_OK;

@@ -110,10 +110,10 @@ def _descs(density, texels, rig: Rig, dt: float, early_stop: bool, cells=None):
 
 
 def cells_numel(dims) -> int:
-    """Floats in the cell-record copy of a (X,Y,Z) volume (8 per cell)."""
+    """Floats in the padded cell-record copy of a (X,Y,Z) volume: 8 per cell, (X+1)(Y+1)(Z+1) cells."""
     n = 8
     for d in dims:
-        n *= max(int(d) - 1, 1)
+        n *= int(d) + 1
     return n
 
 

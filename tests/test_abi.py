@@ -121,12 +121,12 @@ def test_status_codes_map_to_reference_exceptions(lib):
 
 def test_cell_layout_sizes(lib):
     dims = (ctypes.c_int32 * 3)(256, 256, 256)
-    assert lib.ddvr_cells_bytes(dims) == 255 ** 3 * 32
-    assert lib.ddvr_cells_bytes((ctypes.c_int32 * 3)(1, 5, 2)) == 1 * 4 * 1 * 32
+    assert lib.ddvr_cells_bytes(dims) == 257 ** 3 * 32
+    assert lib.ddvr_cells_bytes((ctypes.c_int32 * 3)(1, 5, 2)) == 2 * 6 * 3 * 32
     vol, _, _ = _descs(dims=(9, 5, 3))
     assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 0      # no cell records
     vol.cells = 32
-    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 8 * 4 * 2 * 32
+    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 10 * 6 * 4 * 32
     assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 4) == 0      # tf target only
 
 
