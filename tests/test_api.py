@@ -1,0 +1,205 @@
+"""The voldiff drop-in API: same names, validation, exceptions and behaviour.
+
+CPU tests cover the dataclasses, the compositing algebra and the error paths
+that are decided on the host; ``-m gpu`` tests re-run the reference's own
+render/adjoint tests (test_renderer.py) against the drop-in.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2107_12672_b200 as vd
+from conftest import golden, rel_l2
+
+
+# ---------------------------------------------------------------------------
+# CPU: types, algebra, errors
+# ---------------------------------------------------------------------------
+
+
+def test_api_surface_matches_reference_names():
+    for name in ("render", "render_adjoint", "l1_loss", "DensityVolume", "TransferFunction",
+                 "SphericalCamera", "RenderConfig", "ImageRGBA", "GradientSet", "blend",
+                 "blend_invert", "blend_adjoint", "EPS_ALPHA", "EPS_POLE_DEG",
+                 "InvalidParameterError", "InvalidInputError", "UnsupportedConfigurationError",
+                 "VoldiffError", "NumericalAbortError"):
+        assert hasattr(vd, name), name
+
+
+def test_exception_hierarchy():
+    assert issubclass(vd.InvalidParameterError, vd.VoldiffError)
+    assert issubclass(vd.InvalidParameterError, ValueError)
+    assert issubclass(vd.InvalidInputError, ValueError)
+    assert issubclass(vd.UnsupportedConfigurationError, vd.VoldiffError)
+
+
+@pytest.mark.parametrize("kw", [dict(dt=0.0), dict(dt=0.1, target="bogus"),
+                                dict(dt=0.1, memory_mode="tape"),
+                                dict(dt=0.1, precision="half")])
+def test_render_config_validation(kw):
+    with pytest.raises(vd.InvalidParameterError):
+        vd.RenderConfig(**kw)
+
+
+def test_camera_validation():   # field.py:147-156
+    with pytest.raises(vd.InvalidParameterError):
+        vd.SphericalCamera(0.0, 90.0, 2.0)
+    with pytest.raises(vd.InvalidParameterError):
+        vd.SphericalCamera(0.0, -89.9995, 2.0)
+    with pytest.raises(vd.InvalidParameterError):
+        vd.SphericalCamera(0.0, 0.0, 0.0)
+    with pytest.raises(vd.InvalidParameterError):
+        vd.SphericalCamera(0.0, 0.0, 2.0, fov_y_deg=180.0)
+    with pytest.raises(vd.InvalidParameterError):
+        vd.SphericalCamera(0.0, 0.0, 2.0, width=0)
+    assert vd.SphericalCamera(-30.0, 0.0, 2.0).lon_deg == 330.0
+
+
+def test_volume_and_tf_validation():
+    with pytest.raises(vd.InvalidParameterError):
+        vd.DensityVolume(np.zeros((2, 2)))
+    with pytest.raises(vd.InvalidParameterError):
+        vd.DensityVolume(np.full((2, 2, 2), np.nan))
+    with pytest.raises(vd.InvalidParameterError):
+        vd.DensityVolume(np.zeros((2, 2, 2)), box_min=[0, 0, 0], box_max=[1, 0, 1])
+    with pytest.raises(vd.InvalidParameterError):
+        vd.TransferFunction(np.zeros((3, 3)))
+
+
+def test_blend_known_answers():   # test_renderer.py:42-59
+    np.testing.assert_allclose(vd.blend([0.2, 0.0, 0.0, 0.5], [0.4, 0.0, 0.0, 0.5]),
+                               [0.4, 0.0, 0.0, 0.75])
+    np.testing.assert_allclose(vd.blend_invert([0.4, 0.0, 0.0, 0.75], [0.4, 0.0, 0.0, 0.5]),
+                               [0.2, 0.0, 0.0, 0.5])
+    with pytest.raises(vd.InvalidInputError):
+        vd.blend_invert(np.zeros(4), np.array([0.0, 0.0, 0.0, 1.0]))
+
+
+def test_blend_round_trip_and_adjoint():   # test_acceptance.py:119-132, test_renderer.py:84-96
+    rng = np.random.default_rng(4)
+    n = 10_000
+    state = np.concatenate([rng.uniform(0, 1, (n, 3)), rng.uniform(0, 1, (n, 1))], axis=1)
+    sample = np.concatenate([rng.uniform(0, 1, (n, 3)),
+                             rng.uniform(0, 1, (n, 1)) * (1 - 1e-6)], axis=1)
+    assert np.abs(vd.blend_invert(vd.blend(state, sample), sample) - state).max() <= 1e-6
+    s, c, nh = state[0], sample[0], rng.normal(size=4)
+    sh, ch = vd.blend_adjoint(s, c, nh)
+    h = 1e-7
+    for i in range(4):
+        e = np.zeros(4)
+        e[i] = h
+        fd_s = (np.sum(nh * vd.blend(s + e, c)) - np.sum(nh * vd.blend(s - e, c))) / (2 * h)
+        fd_c = (np.sum(nh * vd.blend(s, c + e)) - np.sum(nh * vd.blend(s, c - e))) / (2 * h)
+        assert abs(sh[i] - fd_s) < 1e-6 and abs(ch[i] - fd_c) < 1e-6
+
+
+def test_adjoint_host_side_errors_before_any_gpu_work():   # renderer.py:656-667
+    vol = vd.DensityVolume(np.ones((4, 4, 4)))
+    tf = vd.TransferFunction(np.ones((2, 4)))
+    cam = vd.SphericalCamera(0.0, 0.0, 2.0, width=4, height=4)
+    with pytest.raises(vd.UnsupportedConfigurationError):
+        vd.render_adjoint(vol, tf, cam, vd.RenderConfig(dt=0.1), np.zeros((4, 4, 4)))
+    with pytest.raises(vd.InvalidInputError):
+        vd.render_adjoint(vol, tf, cam, vd.RenderConfig(dt=0.1, target="volume"),
+                          np.zeros((3, 4, 4)))
+    with pytest.raises(vd.InvalidInputError):
+        vd.render_adjoint(vol, tf, cam, vd.RenderConfig(dt=0.1, target="volume"),
+                          np.zeros((4, 4, 4)), image=np.zeros((2, 2, 4)))
+    with pytest.raises(vd.InvalidInputError):
+        vd.l1_loss([np.zeros((2, 2, 4))], [np.zeros((2, 3, 4))])
+
+
+# ---------------------------------------------------------------------------
+# GPU: the reference's own renderer tests against the drop-in
+# ---------------------------------------------------------------------------
+
+
+def _scene(name):
+    g = golden(name)
+    lon, lat, radius, cx, cy, cz, fov, W, H = g["cam"]
+    vol = vd.DensityVolume(g["volume"].astype(np.float64), g["box"][0], g["box"][1])
+    tf = vd.TransferFunction(g["texels"].astype(np.float64))
+    cam = vd.SphericalCamera(lon, lat, radius, (cx, cy, cz), fov, int(W), int(H))
+    return g, vol, tf, cam, float(g["dt"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["rand_500", "rand_2000", "kat_anisotropic", "kat_tf_r1"])
+def test_dropin_render_and_adjoint_match_reference(cuda, name):
+    g, vol, tf, cam, dt = _scene(name)
+    img = vd.render(vol, tf, cam, vd.RenderConfig(dt=dt, target="volume"))
+    assert isinstance(img, vd.ImageRGBA) and img.data.dtype == np.float64
+    assert rel_l2(img.data, g["image"]) <= 1e-5
+    for mode in ("inversion", "stored"):
+        for t in ("tf", "volume", "camera", "stepsize"):
+            key = f"{mode}_{t}"
+            if key not in g:
+                continue
+            cfg = vd.RenderConfig(dt=dt, target=t, memory_mode=mode)
+            for image in (None, img):
+                gs = vd.render_adjoint(vol, tf, cam, cfg, g["seed"], image=image)
+                got = {"tf": gs.d_tf, "volume": gs.d_volume, "camera": gs.d_camera,
+                       "stepsize": gs.d_stepsize}[t]
+                assert rel_l2(np.asarray(got), g[key]) <= 1e-4, (mode, t)
+
+
+@pytest.mark.gpu
+def test_dropin_known_answers(cuda):   # test_renderer.py:98-122
+    vol = vd.DensityVolume(np.zeros((4, 4, 4)))
+    tf = vd.TransferFunction([[0.0, 0.0, 0.0, 0.0], [1.0, 1.0, 1.0, 2.0]])
+    img = vd.render(vol, tf, vd.SphericalCamera(10.0, 5.0, 2.0, width=6, height=6),
+                    vd.RenderConfig(dt=0.05))
+    np.testing.assert_array_equal(img.data, 0.0)
+    ones = vd.DensityVolume(np.ones((8, 8, 8)))
+    cam = vd.SphericalCamera(0.0, 0.0, 2.0, fov_y_deg=8.0, width=9, height=9)
+    for tau0 in (0.125, 1.0, 10.0):   # fp32-exact optical depths
+        tfh = vd.TransferFunction(np.tile([0.5, 0.5, 0.5, tau0], (2, 1)))
+        img = vd.render(ones, tfh, cam, vd.RenderConfig(dt=0.05, target="stepsize"))
+        assert abs((1.0 - img.data[4, 4, 3]) - np.exp(-tau0)) < 1e-5
+    tfe = vd.TransferFunction(np.tile([0.75, 0.75, 0.75, 2.0], (2, 1)))
+    img = vd.render(ones, tfe, cam, vd.RenderConfig(dt=0.01, target="stepsize"))
+    assert abs(img.data[4, 4, 0] - 0.75 * (1.0 - np.exp(-2.0))) < 1e-6
+
+
+@pytest.mark.gpu
+def test_dropin_adjoint_contracts(cuda):   # test_renderer.py:186-268
+    g, vol, tf, cam, dt = _scene("rand_501")
+    for t in ("camera", "stepsize", "tf", "volume"):
+        gs = vd.render_adjoint(vol, tf, cam, vd.RenderConfig(dt=dt, target=t),
+                               np.zeros((cam.height, cam.width, 4)))
+        for val in (gs.d_stepsize, gs.d_camera, gs.d_tf, gs.d_volume):
+            if val is not None:
+                assert not np.any(np.asarray(val))
+    # memory counter: inversion state independent of the step count, stored grows
+    seed = np.ones((cam.height, cam.width, 4))
+    counts = {}
+    for d in (dt, dt / 4):
+        gi = vd.render_adjoint(vol, tf, cam, vd.RenderConfig(dt=d, target="volume"), seed)
+        gs = vd.render_adjoint(vol, tf, cam,
+                               vd.RenderConfig(dt=d, target="volume", memory_mode="stored"), seed)
+        counts[d] = (gi.state_floats, gs.state_floats)
+    assert counts[dt][0] == counts[dt / 4][0]
+    assert counts[dt / 4][1] > 2 * counts[dt][1]
+    # untouched voxels get exactly zero (test_renderer.py:251-259)
+    u = vd.render_adjoint(vd.DensityVolume(np.full((8, 8, 8), 0.5)), tf,
+                          vd.SphericalCamera(0.0, 0.0, 2.0, fov_y_deg=2.0, width=4, height=4),
+                          vd.RenderConfig(dt=0.05, target="volume"), np.ones((4, 4, 4)))
+    assert u.d_volume[0, 0, 0] == 0.0 and u.d_volume[-1, -1, -1] == 0.0
+    assert np.any(u.d_volume != 0.0)
+
+
+@pytest.mark.gpu
+def test_dropin_l1_loss(cuda):   # objectives.py:38-54
+    rng = np.random.default_rng(0)
+    xs = [rng.uniform(0, 1, (5, 7, 4)).astype(np.float32).astype(np.float64) for _ in range(3)]
+    ys = [rng.uniform(0, 1, (5, 7, 4)).astype(np.float32).astype(np.float64) for _ in range(3)]
+    ys[0][0, 0] = xs[0][0, 0]   # sign(0) = 0
+    loss, seeds = vd.l1_loss(xs, ys)
+    count = sum(x.size for x in xs)
+    ref = sum(np.abs(x - y).sum() for x, y in zip(xs, ys)) / count
+    assert abs(loss - ref) <= 1e-7 * ref
+    for x, y, s in zip(xs, ys, seeds):
+        np.testing.assert_allclose(s, np.sign(x - y) / count, rtol=1e-7)
+    assert seeds[0][0, 0, 0] == 0.0
