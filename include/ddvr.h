@@ -71,9 +71,9 @@ typedef struct {
   int32_t dims[3];       /* X, Y, Z >= 1 */
   double box_min[3];
   double box_max[3];     /* box_max > box_min on every axis */
-  const float* cells;    /* (device, nullable, 32-byte aligned) cell-record copy of data
-                            built by ddvr_pack_cells: the 8 corner values of every cell
-                            in one 32-byte record, so a sample is one 256-bit load.
+  const float* cells;    /* (device, nullable, 32-byte aligned) padded cell-record copy of
+                            data built by ddvr_pack_cells: the 8 corner values of every
+                            cell in one 32-byte record, so a sample is one 256-bit load.
                             NULL = gather the 8 corners from data. */
 } ddvr_volume;
 
@@ -112,17 +112,20 @@ typedef struct {
 } ddvr_params;
 
 /* Front-to-back march of every view.  image_out (device) (V, rows, W, 4);
- * trans_out (device, nullable) (V, rows, W) receives the final transmittance
- * T = prod(1 - a) in full fp32 relative precision, which the adjoint's
- * inversion starts from (1 - alpha loses it when alpha -> 1). */
+ * depth_out (device, nullable) (V, rows, W) receives each ray's optical depth
+ * S = sum_i -ln(1 - a_i) = sum_i min(dt*tau_i, -ln EPS_ALPHA), summed in fp64
+ * (transmittance T = exp(-S)).  The adjoint's inversion starts from it; it
+ * never underflows, unlike T, and 1 - alpha loses T as alpha -> 1. */
 int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, float* image_out, float* trans_out,
+                 int32_t n_views, const ddvr_params* p, float* image_out, float* depth_out,
                  void* stream);
 
 /* Back-to-front adjoint with the inversion trick: per-ray state is O(1); no
  * per-sample tape.  image (device) (V, rows, W, 4) is the forward output for
- * the same inputs; trans (device, nullable) its transmittance side output
- * (if NULL, T = 1 - alpha).  seed (device) (V, rows, W, 4) = dLoss/dImage.
+ * the same inputs; depth (device, nullable) its optical-depth side output (if
+ * NULL, S = -ln(1 - alpha)).  The walk inverts each compositing step exactly
+ * in optical-depth form, S_prev = S + ln(1 - a), in fp64.
+ * seed (device) (V, rows, W, 4) = dLoss/dImage.
  * Outputs (device, accumulate, NULL when the target bit is clear):
  *   d_volume float (X*Y*Z); d_tf double (same shape as tf->params);
  *   d_camera double (V, 2) per degree [lon, lat]; d_dt double (1).
@@ -130,7 +133,7 @@ int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
  * (cell-gradient records when vol->cells is set and the volume target is on;
  * zeroed and folded into d_volume inside the call). */
 int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, const float* image, const float* trans,
+                 int32_t n_views, const ddvr_params* p, const float* image, const float* depth,
                  const float* seed, uint32_t target_mask, float* d_volume, double* d_tf,
                  double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
                  void* stream);
@@ -139,7 +142,9 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
 int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t target_mask);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:
- * max(X-1,1) * max(Y-1,1) * max(Z-1,1) records of 8 floats. */
+ * (X+1) * (Y+1) * (Z+1) records of 8 floats -- cells -1 .. dim-1 on every
+ * axis with edge-replicated corners, so clamp-to-edge (field.py:299-307)
+ * needs no per-sample clamping. */
 int64_t ddvr_cells_bytes(const int32_t dims[3]);
 
 /* Build the cell records of vol->data into cells_out (device, 32-byte aligned,

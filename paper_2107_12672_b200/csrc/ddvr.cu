@@ -395,8 +395,11 @@ struct TexelTF {
 // Beer-Lambert segment opacity with the invertibility clamp (field.py:587-600)
 struct Segment {
   float tau, e, ome, a;   // ome = 1 - a = max(e, EPS)
+  float od;               // segment optical depth -ln(1 - a) = min(dt*tau, -ln EPS), exact
   bool a_clamped;
 };
+
+constexpr float kNegLnEps = 13.815510557964274f;   // -ln(EPS_ALPHA)
 
 // a = 1 - exp(-x) is evaluated without cancellation: for x < ln2/2 by the
 // degree-7 Taylor polynomial of -expm1(-x) (truncation < 5e-9 relative) with
@@ -421,6 +424,7 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
   s.a_clamped = s.e < kEpsAlpha;                 // a_raw > 1 - EPS_ALPHA
   s.ome = s.a_clamped ? kEpsAlpha : s.e;
   s.a = s.a_clamped ? __fsub_rn(1.f, kEpsAlpha) : a_raw;
+  s.od = s.a_clamped ? kNegLnEps : x;
   return s;
 }
 
@@ -454,7 +458,7 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 template <bool EARLY, bool CELLS, bool TAPE>
 __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
                                                              float* __restrict__ image,
-                                                             float* __restrict__ trans) {
+                                                             float* __restrict__ depth) {
   extern __shared__ float4 s_tex[];
   __shared__ Frame F;
   const int view = blockIdx.z;
@@ -475,8 +479,10 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
   const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
   float* tape = TAPE ? G.tape + pix * G.tape_stride : nullptr;
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
-  // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355)
+  // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355).
+  // S, the ray's optical depth (T = exp(-S)), is summed in fp64 for the adjoint.
   float T = 1.f, A = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+  double S = 0.0;
   long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
   for (int i = 0; i < r.n; ++i) {
     if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
@@ -496,9 +502,10 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
     c2 = __fmaf_rn(Ta, s.z, c2);
     A = __fadd_rn(A, Ta);
     T = __fmul_rn(T, g.ome);
+    S += (double)g.od;
   }
   reinterpret_cast<float4*>(image)[pix] = make_float4(c0, c1, c2, A);
-  if (trans) trans[pix] = T;
+  if (depth) depth[pix] = (float)S;
 }
 
 // ---------------------------------------------------------------------------
@@ -540,7 +547,7 @@ __device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
 template <unsigned MASK, bool CELLS>
 __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
-    const float* __restrict__ trans, const float* __restrict__ seed, float* __restrict__ d_volume,
+    const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
     float* __restrict__ d_cells, double* __restrict__ d_tf, double* __restrict__ d_camera,
     double* __restrict__ d_dt) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
@@ -568,7 +575,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   Ray r;
   r.n = 0;
   r.all_inside = true;
-  float Tn = 1.f;
+  double S = 0.0;   // optical depth after the current sample (T = exp(-S))
   float4 sd = make_float4(0, 0, 0, 0);
   const float* tape = nullptr;
   if (valid) {
@@ -576,7 +583,9 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
     if (G.tape) tape = G.tape + pix * G.tape_stride;
     sd = reinterpret_cast<const float4*>(seed)[pix];
-    Tn = trans ? trans[pix] : 1.f - reinterpret_cast<const float4*>(image)[pix].w;
+    // the forward's exact optical depth; without it, S = -ln(1 - alpha)
+    S = depth ? (double)depth[pix]
+              : -log1p(-(double)reinterpret_cast<const float4*>(image)[pix].w);
   }
   const TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1),
                    max(TFA.count - 2, 0)};
@@ -584,7 +593,6 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
 
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
-  float T = Tn;                       // transmittance after the current sample
   // volume cell-run accumulator
   constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
   int run_cell = kNoRun, run_base = 0, run_ox = 0, run_oy = 0, run_oz = 0;
@@ -594,9 +602,10 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   // TF texel-run accumulator (texel i0 and i0+1)
   int tf_run = -1;
   float4 tfa0 = make_float4(0, 0, 0, 0), tfa1 = make_float4(0, 0, 0, 0);
-  // camera / stepsize sums (grid units)
-  float s1x = 0, s1y = 0, s1z = 0, s2x = 0, s2y = 0, s2z = 0;
-  float dt_bl = 0.f, dt_pos = 0.f;
+  // camera / stepsize per-ray sums (grid units) in fp64: thousands of terms with
+  // cancellation (the per-sample terms stay fp32)
+  double s1x = 0, s1y = 0, s1z = 0, s2x = 0, s2y = 0, s2z = 0;
+  double dt_bl = 0.0, dt_pos = 0.0;
   // last sample position; walk back with exact integer steps
   long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
   long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
@@ -613,10 +622,19 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     const float4 s = tf.eval(d, i0, w, slope, kDhat);
     const Segment g = segment(s.w, dt32);
 
-    // invert the compositing step: transmittance before this sample
-    // (renderer.py:579 a_prev = (a - A)/(a - 1), carried as T for fp32)
-    // ("stored" mode reads it from the tape instead, renderer.py:576-577)
-    const float Tp = tape ? tape[i] : __fdividef(T, g.ome);
+    // Invert the compositing step (renderer.py:579, a_prev = (a - A)/(a - 1)).
+    // In optical-depth form the inverse is exact: -ln(1 - a) = g.od, so the
+    // depth before this sample is S - od (fp64, no drift over thousands of
+    // steps) and T_prev = exp(-S_prev) is computed fresh each step.  The fp32
+    // chain T_prev = T/(1 - a) drifts to ~1e-4 on camera gradients by 2.6k steps.
+    // ("stored" mode reads T_prev from the tape instead, renderer.py:576-577)
+    S -= (double)g.od;
+    float Tp;
+    if (tape) {
+      Tp = tape[i];
+    } else {
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(Tp) : "f"((float)S * -1.4426950408889634f));
+    }
 
     // blend adjoint (renderer.py:583-589)
     const float cdot = s.x * sd.x + s.y * sd.y + s.z * sd.z;
@@ -628,7 +646,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     const float a_raw_hat = g.a_clamped ? 0.f : seg_a_hat;
     const float ea = g.e * a_raw_hat;
     const float tau_hat = s.w < 0.f ? 0.f : dt32 * ea;
-    if (kStep) dt_bl += g.tau * ea;
+    if (kStep) dt_bl += (double)(g.tau * ea);
 
     if (kTf) {   // renderer.py:602-604: texels i0 and i0+1 with weights (1-w), w
       if (i0 != tf_run) {
@@ -683,12 +701,11 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
         const float bz = (gz >= 0 && gz <= V.top[2]) ? ddz * d_hat : 0.f;
         if (kCam) {
           s1x += bx; s1y += by; s1z += bz;
-          s2x += t * bx; s2y += t * by; s2z += t * bz;
+          s2x += (double)(t * bx); s2y += (double)(t * by); s2z += (double)(t * bz);
         }
-        if (kStep) dt_pos += (float)i * (r.gw[0] * bx + r.gw[1] * by + r.gw[2] * bz);
+        if (kStep) dt_pos += (double)((float)i * (r.gw[0] * bx + r.gw[1] * by + r.gw[2] * bz));
       }
     }
-    T = Tp;
     gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
   }
 
@@ -715,7 +732,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   if (kPos) {
     double cam0 = 0.0, cam1 = 0.0, stp = 0.0;
     if (valid && r.n > 0) {
-      if (kStep) stp = (double)dt_bl + (double)dt_pos;
+      if (kStep) stp = dt_bl + dt_pos;
       if (kCam) {
         // world-space sums: x_hat = scale * grid-space gradient (chain of g = (x-bmin)*scale)
         const double xo_h[3] = {s1x * V.scale[0], s1y * V.scale[1], s1z * V.scale[2]};
@@ -981,19 +998,19 @@ void set_smem(K kernel, size_t smem) {
 
 template <bool EARLY, bool CELLS, bool TAPE>
 void launch_forward(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
-                    const Geometry& G, float* image, float* trans) {
+                    const Geometry& G, float* image, float* depth) {
   auto k = dvr_forward_kernel<EARLY, CELLS, TAPE>;
   set_smem(k, smem);
-  k<<<grid, kThreads, smem, st>>>(V, T, G, image, trans);
+  k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth);
 }
 
 template <unsigned M, bool CELLS>
 void launch_adjoint(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
-                    const Geometry& G, const float* image, const float* trans, const float* seed,
+                    const Geometry& G, const float* image, const float* depth, const float* seed,
                     float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
   auto k = dvr_adjoint_kernel<M, CELLS>;
   set_smem(k, smem);
-  k<<<grid, kThreads, smem, st>>>(V, T, G, image, trans, seed, dv, dcells, dtf, dcam, ddt);
+  k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
 }
 
 }  // namespace
@@ -1035,7 +1052,7 @@ int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t mask) {
 }
 
 int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, float* image_out, float* trans_out,
+                 int32_t n_views, const ddvr_params* p, float* image_out, float* depth_out,
                  void* stream) {
   g_err[0] = 0;
   VolArgs V;
@@ -1051,7 +1068,7 @@ int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   const dim3 grid = grid_of(G, n_views);
   const bool early = p->early_stop != 0, cells = V.cells != nullptr, tape = G.tape != nullptr;
 #define DDVR_FWD(E, C, P) \
-  if (early == E && cells == C && tape == P) launch_forward<E, C, P>(grid, tbl, st, V, T, G, image_out, trans_out);
+  if (early == E && cells == C && tape == P) launch_forward<E, C, P>(grid, tbl, st, V, T, G, image_out, depth_out);
   DDVR_FWD(false, false, false) DDVR_FWD(false, false, true) DDVR_FWD(false, true, false)
   DDVR_FWD(false, true, true) DDVR_FWD(true, false, false) DDVR_FWD(true, false, true)
   DDVR_FWD(true, true, false) DDVR_FWD(true, true, true)
@@ -1060,7 +1077,7 @@ int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
 }
 
 int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, const float* image, const float* trans,
+                 int32_t n_views, const ddvr_params* p, const float* image, const float* depth,
                  const float* seed, uint32_t mask, float* d_volume, double* d_tf,
                  double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
                  void* stream) {
@@ -1075,7 +1092,7 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
   if (!seed) return set_error(DDVR_INVALID_INPUT, "seed pointer is NULL");
-  if (!image && !trans) return set_error(DDVR_INVALID_INPUT, "image and transmittance are NULL");
+  if (!image && !depth) return set_error(DDVR_INVALID_INPUT, "image and optical depth are NULL");
   if ((mask & DDVR_TARGET_VOLUME) && !d_volume)
     return set_error(DDVR_INVALID_INPUT, "d_volume is NULL but the volume target is set");
   if ((mask & DDVR_TARGET_TF) && !d_tf)
@@ -1107,10 +1124,10 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
 #define DDVR_CASE(M)                                                                       \
   case M:                                                                                  \
     if (cells)                                                                             \
-      launch_adjoint<M, true>(grid, smem, st, V, T, G, image, trans, seed, d_volume,       \
+      launch_adjoint<M, true>(grid, smem, st, V, T, G, image, depth, seed, d_volume,       \
                               d_cells, d_tf, d_camera, d_dt);                              \
     else                                                                                   \
-      launch_adjoint<M, false>(grid, smem, st, V, T, G, image, trans, seed, d_volume,      \
+      launch_adjoint<M, false>(grid, smem, st, V, T, G, image, depth, seed, d_volume,      \
                                d_cells, d_tf, d_camera, d_dt);                             \
     break;
   switch (mask) {

@@ -93,7 +93,7 @@ class ShardedStep:
         self.flat = FlatGrads.zeros(density.numel(), texels.numel(), dev)
         self.img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=dev)
         self.seed = torch.empty_like(self.img)
-        self.trans = torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=dev)
+        self.depth = torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=dev)
         self.d_tf64 = torch.zeros(texels.shape, dtype=torch.float64, device=dev)
         self.d_dt64 = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss64 = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -121,7 +121,7 @@ class ShardedStep:
             lib = N.lib()
             st = R._stream_ptr()
             N.check(lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
-                                     ctypes.byref(prm), self.img.data_ptr(), self.trans.data_ptr(),
+                                     ctypes.byref(prm), self.img.data_ptr(), self.depth.data_ptr(),
                                      st))
             hook("post_forward")
             N.check(lib.ddvr_l1_loss(self.img.data_ptr(), self.refs.data_ptr(), self.img.numel(),
@@ -130,7 +130,7 @@ class ShardedStep:
             hook("pre_adjoint")
             N.check(lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,
                                      ctypes.byref(prm), self.img.data_ptr(),
-                                     self.trans.data_ptr(), self.seed.data_ptr(), self.mask,
+                                     self.depth.data_ptr(), self.seed.data_ptr(), self.mask,
                                      want(N.TARGET_VOLUME, f.d_volume),
                                      want(N.TARGET_TF, self.d_tf64), None,
                                      want(N.TARGET_STEPSIZE, self.d_dt64),

@@ -7,7 +7,7 @@ compute step is a libddvr kernel reached through the C ABI (``_native``).
 
 ``DiffDVR.backward`` launches ONE adjoint kernel whose target mask is
 ``ctx.needs_input_grad`` and saves only the output images and the per-pixel
-transmittance: O(pixels) memory, the paper's inversion trick
+optical depth: O(pixels) memory, the paper's inversion trick
 (renderer.py:540-543, 576-580; PAPER.md:299-310).
 """
 
@@ -142,20 +142,20 @@ def _set_tape(prm, tape, tape_stride):
         prm.tape_stride = int(tape_stride)
 
 
-def forward(density, texels, cams, dt: float, rig: Rig, *, early_stop=False, with_trans=True,
+def forward(density, texels, cams, dt: float, rig: Rig, *, early_stop=False, with_depth=True,
             cells=None, tape=None, tape_stride=0):
-    """Images (V, rows, W, 4) fp32 and final transmittance (V, rows, W) (or None)."""
+    """Images (V, rows, W, 4) fp32 and ray optical depth S (V, rows, W), T = exp(-S) (or None)."""
     _require(cams, "cameras", torch.float64, ndim=2)
     vol, tf, prm = _descs(density, texels, rig, dt, early_stop, cells)
     _set_tape(prm, tape, tape_stride)
     V = cams.shape[0]
     img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=density.device)
-    trans = (torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=density.device)
-             if with_trans else None)
+    depth = (torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=density.device)
+             if with_depth else None)
     N.check(N.lib().ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,
                                  ctypes.byref(prm), img.data_ptr(),
-                                 trans.data_ptr() if trans is not None else None, _stream_ptr()))
-    return img, trans
+                                 depth.data_ptr() if depth is not None else None, _stream_ptr()))
+    return img, depth
 
 
 def workspace_for(density, mask: int, cells=None, rig: Rig | None = None):
@@ -165,7 +165,7 @@ def workspace_for(density, mask: int, cells=None, rig: Rig | None = None):
     return torch.empty(cells_numel(density.shape), dtype=torch.float32, device=density.device)
 
 
-def adjoint(density, texels, cams, dt: float, rig: Rig, image, trans, seed, mask: int, *,
+def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask: int, *,
             d_volume=None, d_tf=None, d_camera=None, d_dt=None, cells=None, workspace=None,
             tape=None, tape_stride=0):
     """Accumulate gradients of sum(seed * image) into the given buffers (+=)."""
@@ -181,8 +181,8 @@ def adjoint(density, texels, cams, dt: float, rig: Rig, image, trans, seed, mask
         _require(image, "image", torch.float32)
         if tuple(image.shape) != shape:
             raise InvalidInputError("provided image does not match the camera size")
-    if trans is not None:
-        _require(trans, "transmittance", torch.float32)
+    if depth is not None:
+        _require(depth, "optical depth", torch.float32)
     for buf, name, dt_ in ((d_volume, "d_volume", torch.float32), (d_tf, "d_tf", torch.float64),
                            (d_camera, "d_camera", torch.float64), (d_dt, "d_dt", torch.float64)):
         if buf is not None:
@@ -192,7 +192,7 @@ def adjoint(density, texels, cams, dt: float, rig: Rig, image, trans, seed, mask
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,
-                                 ctypes.byref(prm), ptr(image), ptr(trans), seed.data_ptr(),
+                                 ctypes.byref(prm), ptr(image), ptr(depth), seed.data_ptr(),
                                  mask, ptr(d_volume), ptr(d_tf), ptr(d_camera), ptr(d_dt),
                                  ptr(workspace), ws_bytes, _stream_ptr()))
 
@@ -244,17 +244,17 @@ class DiffDVR(torch.autograd.Function):
         dtv = float(dt.detach()) if isinstance(dt, torch.Tensor) else float(dt)
         density = density.contiguous()
         cells = pack_cells(density) if layout == "cells" else None
-        img, trans = forward(density, texels.contiguous(), cams, dtv, rig, cells=cells)
-        ctx.save_for_backward(density, texels, img, trans)
+        img, depth = forward(density, texels.contiguous(), cams, dtv, rig, cells=cells)
+        ctx.save_for_backward(density, texels, img, depth)
         ctx.cams, ctx.dt, ctx.rig, ctx.cells = cams, dtv, rig, cells
         ctx.lonlat_meta = (lonlat.dtype, lonlat.device)
         ctx.dt_meta = (dt.dtype, dt.device) if isinstance(dt, torch.Tensor) else None
-        ctx.mark_non_differentiable(trans)
+        ctx.mark_non_differentiable(depth)
         return img
 
     @staticmethod
     def backward(ctx, grad_img):
-        density, texels, img, trans = ctx.saved_tensors
+        density, texels, img, depth = ctx.saved_tensors
         need = ctx.needs_input_grad
         mask = ((N.TARGET_VOLUME if need[0] else 0) | (N.TARGET_TF if need[1] else 0)
                 | (N.TARGET_CAMERA if need[2] else 0) | (N.TARGET_STEPSIZE if need[3] else 0))
@@ -266,7 +266,7 @@ class DiffDVR(torch.autograd.Function):
         d_cam = (torch.zeros(ctx.cams.shape[0], 2, dtype=torch.float64, device=dev)
                  if need[2] else None)
         d_dt = torch.zeros(1, dtype=torch.float64, device=dev) if need[3] else None
-        adjoint(density.contiguous(), texels.contiguous(), ctx.cams, ctx.dt, ctx.rig, img, trans,
+        adjoint(density.contiguous(), texels.contiguous(), ctx.cams, ctx.dt, ctx.rig, img, depth,
                 grad_img.contiguous().to(torch.float32), mask, d_volume=d_vol, d_tf=d_tf,
                 d_camera=d_cam, d_dt=d_dt, cells=ctx.cells)
         g_tf = d_tf.to(texels.dtype) if d_tf is not None else None

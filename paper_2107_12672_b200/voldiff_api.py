@@ -263,15 +263,15 @@ def _upload(volume, tf, cam, dev):
     return dens, tex, cams, rig
 
 
-def _image_from(img, trans):
-    """fp64 ImageRGBA; the fp32 transmittance rides along for a later adjoint.
+def _image_from(img, depth):
+    """fp64 ImageRGBA; the ray optical depth S (T = exp(-S)) rides along.
 
-    alpha = A is accurate as A -> 0; T = prod(1 - a) is accurate as T -> 0.
-    ``render_adjoint(image=...)`` starts the inversion from the attached T
-    when the image came from :func:`render`, else from 1 - alpha.
+    alpha = A is accurate as A -> 0; S keeps T accurate as T -> 0.
+    ``render_adjoint(image=...)`` starts the inversion from the attached S
+    when the image came from :func:`render`, else from S = -ln(1 - alpha).
     """
     out = ImageRGBA(img[0].to(torch.float64).cpu().numpy())
-    out._ddvr_trans = trans[0].cpu().numpy()
+    out._ddvr_depth = depth[0].cpu().numpy()
     return out
 
 
@@ -285,9 +285,9 @@ def render(volume, tf, cam, cfg, *, threads: int = 1) -> ImageRGBA:
     _validate_config(cfg)
     dev = _device()
     dens, tex, cams, rig = _upload(volume, tf, cam, dev)
-    img, trans = R.forward(dens, tex, cams, cfg.dt, rig, early_stop=(cfg.target == "none"),
+    img, depth = R.forward(dens, tex, cams, cfg.dt, rig, early_stop=(cfg.target == "none"),
                            cells=R.pack_cells(dens))
-    return _image_from(img, trans)
+    return _image_from(img, depth)
 
 
 def _stored_tape_len(cams, dt, rig):
@@ -323,23 +323,24 @@ def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) 
         n_steps = _stored_tape_len(cams, cfg.dt, rig)
         stride = max(int(n_steps.max().item()), 1)
         tape = torch.empty(H * W * stride, dtype=torch.float32, device=dev)
-        img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig, cells=cells, tape=tape,
+        img_t, depth_t = R.forward(dens, tex, cams, cfg.dt, rig, cells=cells, tape=tape,
                                    tape_stride=stride)
     elif img_arr is None:
-        img_t, trans_t = R.forward(dens, tex, cams, cfg.dt, rig, cells=cells)
+        img_t, depth_t = R.forward(dens, tex, cams, cfg.dt, rig, cells=cells)
     else:
         img_t = torch.from_numpy(img_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
-        t_np = getattr(image, "_ddvr_trans", None)
-        if t_np is None or np.shape(t_np) != (H, W):
-            t_np = 1.0 - img_arr[..., 3]
-        trans_t = torch.from_numpy(np.asarray(t_np, np.float32)).to(dev).reshape(1, H, W)
+        s_np = getattr(image, "_ddvr_depth", None)
+        if s_np is None or np.shape(s_np) != (H, W):
+            with np.errstate(divide="ignore"):
+                s_np = -np.log1p(-np.clip(img_arr[..., 3], 0.0, 1.0))
+        depth_t = torch.from_numpy(np.asarray(s_np, np.float32)).to(dev).reshape(1, H, W)
     seed_t = torch.from_numpy(seed_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
     bit = N.TARGET_BITS[cfg.target]
     d_vol = torch.zeros_like(dens) if bit == N.TARGET_VOLUME else None
     d_tf = torch.zeros(tex.shape, dtype=torch.float64, device=dev) if bit == N.TARGET_TF else None
     d_cam = torch.zeros(1, 2, dtype=torch.float64, device=dev) if bit == N.TARGET_CAMERA else None
     d_dt = torch.zeros(1, dtype=torch.float64, device=dev) if bit == N.TARGET_STEPSIZE else None
-    R.adjoint(dens, tex, cams, cfg.dt, rig, img_t, trans_t, seed_t, bit, d_volume=d_vol,
+    R.adjoint(dens, tex, cams, cfg.dt, rig, img_t, depth_t, seed_t, bit, d_volume=d_vol,
               d_tf=d_tf, d_camera=d_cam, d_dt=d_dt, cells=cells, tape=tape, tape_stride=stride)
     # per-ray state: inversion keeps (C, A) and the constant seed, 8 floats per ray,
     # independent of the step count (renderer.py:513); stored mode keeps a tape

@@ -93,7 +93,7 @@ def test_image_matches_reference(cuda, name, layout):
         assert np.abs(got).max() == 0.0
     else:
         assert rel_l2(got, ref) <= IMG_TOL
-    T = trans[0].double().cpu().numpy()
+    T = np.exp(-trans[0].double().cpu().numpy())      # forward's optical depth S, T = exp(-S)
     np.testing.assert_allclose(1.0 - T, got[..., 3], atol=2e-6)
     if "image_none" in g:   # early ray termination (renderer.py:331-335)
         img2, _ = R.forward(dens, tex, cams, dt, rig, early_stop=True, cells=cells)
