@@ -102,12 +102,15 @@ struct VolArgs {
 struct TfArgs {
   const float* __restrict__ params;
   int kind, count;
+  float fR, fR1;     // R, R-1
+  int Rm2;           // max(R-2, 0)
 };
 
 struct Geometry {
   const ddvr_camera* __restrict__ cams;
   int W, H, row0, row1;
   double dt;
+  float dt32;             // (float)dt: the stepsize of the fp32 march
   float* tape;            // stored memory mode (nullable)
   long long tape_stride;
 };
@@ -366,31 +369,30 @@ __device__ __forceinline__ float clamp_density(bool inside, float raw) {
 // transfer functions (field.py:525-579; renderer.py:472-488)
 // ---------------------------------------------------------------------------
 
-// texel table: R texels, centre of texel r at (r + 0.5)/R, clamp-to-edge;
-// stored as (texel, delta) pairs by load_tf
-struct TexelTF {
-  const float4* tex;   // shared memory, 2R float4
-  int R;
-  float fR, fR1;       // R, R-1
-  int Rm2;             // max(R-2, 0)
+// Dynamic shared memory of every kernel: the TF as (texel k, texel k+1 -
+// texel k) pairs, then (adjoint, tf target) the per-CTA TF gradient.  A
+// file-scope symbol keeps loads in the shared window (no generic->shared
+// conversion per access).
+extern __shared__ float4 g_smem[];
 
-  __device__ __forceinline__ float4 eval(float d, int& i0, float& w, float4& slope,
-                                         bool want_slope) const {
-    const float t = __fsub_rn(__fmul_rn(d, fR), 0.5f);
-    const float f = fminf(fmaxf(t, 0.f), fR1);
-    i0 = min((int)f, Rm2);
-    w = __fsub_rn(f, (float)i0);
-    const float4 a = tex[2 * i0];
-    const float4 dlt = tex[2 * i0 + 1];
-    if (want_slope) {
-      const bool live = t >= 0.f && t <= fR1;
-      const float s = live ? fR : 0.f;
-      slope = make_float4(dlt.x * s, dlt.y * s, dlt.z * s, dlt.w * s);
-    }
-    return make_float4(__fmaf_rn(w, dlt.x, a.x), __fmaf_rn(w, dlt.y, a.y),
-                       __fmaf_rn(w, dlt.z, a.z), __fmaf_rn(w, dlt.w, a.w));
+// texel table: R texels, centre of texel r at (r + 0.5)/R, clamp-to-edge
+// (field.py:540-549); fR, fR1, Rm2 are precomputed on the host (TfArgs)
+__device__ __forceinline__ float4 tf_eval(const TfArgs& T, float d, int& i0, float& w,
+                                          float4& slope, bool want_slope) {
+  const float t = __fsub_rn(__fmul_rn(d, T.fR), 0.5f);
+  const float f = fminf(fmaxf(t, 0.f), T.fR1);
+  i0 = min((int)f, T.Rm2);
+  w = __fsub_rn(f, (float)i0);
+  const float4 a = g_smem[2 * i0];
+  const float4 dlt = g_smem[2 * i0 + 1];
+  if (want_slope) {   // field.py:575-576: zero in the clamp bands
+    const bool live = t >= 0.f && t <= T.fR1;
+    const float sc = live ? T.fR : 0.f;
+    slope = make_float4(dlt.x * sc, dlt.y * sc, dlt.z * sc, dlt.w * sc);
   }
-};
+  return make_float4(__fmaf_rn(w, dlt.x, a.x), __fmaf_rn(w, dlt.y, a.y),
+                     __fmaf_rn(w, dlt.z, a.z), __fmaf_rn(w, dlt.w, a.w));
+}
 
 // Beer-Lambert segment opacity with the invertibility clamp (field.py:587-600)
 struct Segment {
@@ -401,14 +403,31 @@ struct Segment {
 
 constexpr float kNegLnEps = 13.815510557964274f;   // -ln(EPS_ALPHA)
 
-// a = 1 - exp(-x) is evaluated without cancellation: for x < ln2/2 by the
-// degree-7 Taylor polynomial of -expm1(-x) (truncation < 5e-9 relative) with
-// e = 1 - a exact to half an ulp; above, a = 1 - exp(-x) is well conditioned.
-// (fp32 1 - __expf(-x) alone loses ~1e-5 relative on a at dt*tau ~ 5e-3.)
+// How a = 1 - exp(-x), x = dt*tau, is evaluated.  Each CTA picks the cheapest
+// mode that is exact to fp32 for x <= x_max = dt * max(tau texel):
+//   kSegP3  x_max < 0.00896: a = x - x^2/2 + x^3/6 (truncation < 3e-8 relative)
+//   kSegP7  x_max < ln2/2:   degree-7 Taylor polynomial of -expm1(-x) (< 5e-9)
+//   kSegGen otherwise:       polynomial below ln2/2, 1 - exp(-x) above, EPS clamp
+// In the polynomial modes e = 1 - a >= 0.7 is exact to half an ulp and the
+// clamp cannot trigger.  (fp32 1 - __expf(-x) alone loses ~1e-5 relative on a
+// at dt*tau ~ 5e-3.)
+constexpr int kSegP3 = 0, kSegP7 = 1, kSegGen = 2;
+
+template <int SEG>
 __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
   Segment s;
   s.tau = fmaxf(tau_raw, 0.f);
   const float x = __fmul_rn(dt32, s.tau);
+  if (SEG == kSegP3) {
+    float p = __fmaf_rn(-x, 1.f / 6.f, 0.5f);
+    p = __fmaf_rn(-x, p, 1.f);
+    s.a = __fmul_rn(x, p);
+    s.e = __fsub_rn(1.f, s.a);
+    s.ome = s.e;
+    s.a_clamped = false;
+    s.od = x;
+    return s;
+  }
   float p = __fmaf_rn(-x, 1.f / 5040.f, 1.f / 720.f);
   p = __fmaf_rn(-x, p, 1.f / 120.f);
   p = __fmaf_rn(-x, p, 1.f / 24.f);
@@ -416,6 +435,14 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
   p = __fmaf_rn(-x, p, 0.5f);
   p = __fmaf_rn(-x, p, 1.f);
   const float a_small = __fmul_rn(x, p);
+  if (SEG == kSegP7) {
+    s.a = a_small;
+    s.e = __fsub_rn(1.f, a_small);
+    s.ome = s.e;
+    s.a_clamped = false;
+    s.od = x;
+    return s;
+  }
   float e_big;   // exp(-x) = 2^(-x log2 e); ftz is harmless: e < 1e-6 is clamped below
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e_big) : "f"(__fmul_rn(x, -1.4426950408889634f)));
   const bool small = x < 0.34657359f;
@@ -433,16 +460,26 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
 // ---------------------------------------------------------------------------
 
 // shared TF table as (texel k, texel k+1 - texel k) pairs: the lerp is then 4
-// FFMA and the slope (field.py:576) needs no subtraction
-__device__ __forceinline__ void load_tf(const TfArgs& tf, float4* s_tex) {
+// FFMA and the slope (field.py:576) needs no subtraction.  Returns (to every
+// thread, after the barrier the caller issues) the segment mode of the CTA.
+__device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_maxtau) {
   const float4* src = reinterpret_cast<const float4*>(tf.params);
+  float mx = 0.f;
   for (int i = threadIdx.x; i < tf.count; i += blockDim.x) {
     const float4 a = src[i];
     const float4 b = src[min(i + 1, tf.count - 1)];
-    s_tex[2 * i] = a;
-    s_tex[2 * i + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y), __fsub_rn(b.z, a.z),
-                                   __fsub_rn(b.w, a.w));
+    g_smem[2 * i] = a;
+    g_smem[2 * i + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
+                                    __fsub_rn(b.z, a.z), __fsub_rn(b.w, a.w));
+    mx = fmaxf(mx, a.w);   // interpolated tau never exceeds the largest texel
   }
+  // non-negative floats order like their bit patterns
+  if (mx > 0.f) atomicMax(s_maxtau, __float_as_uint(mx));
+}
+
+__device__ __forceinline__ int seg_mode(float dt32, unsigned maxtau_bits) {
+  const float xmax = dt32 * __uint_as_float(maxtau_bits);
+  return xmax < 0.00896f ? kSegP3 : (xmax < 0.34657359f ? kSegP7 : kSegGen);
 }
 
 __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
@@ -455,29 +492,12 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 // forward kernel (renderer.py:306-357)
 // ---------------------------------------------------------------------------
 
-template <bool EARLY, bool CELLS, bool TAPE>
-__global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
-                                                             float* __restrict__ image,
-                                                             float* __restrict__ depth) {
-  extern __shared__ float4 s_tex[];
-  __shared__ Frame F;
-  const int view = blockIdx.z;
-  load_tf(TFA, s_tex);
-  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
-  __syncthreads();
-
-  int px, py;
-  pixel_of(G, px, py);
-  if (px >= G.W || py >= G.row1) return;
-
-  Ray r;
-  setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
-  const TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1),
-                   max(TFA.count - 2, 0)};
-  const float dt32 = (float)G.dt;
-
-  const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
-  float* tape = TAPE ? G.tape + pix * G.tape_stride : nullptr;
+// The march of one ray.  INSIDE: every lane of the warp has all_inside (the
+// per-sample inside test and clamps are compiled out); SEG: segment mode.
+template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE>
+__device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
+                                          const Ray& r, float* __restrict__ tape, float4& rgba,
+                                          double& depth) {
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
   // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355).
   // S, the ray's optical depth (T = exp(-S)), is summed in fp64 for the adjoint.
@@ -488,14 +508,14 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
     if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     Cell c;
-    locate<CELLS>(V, gx, gy, gz, r.all_inside, c);
+    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
     gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
     float v[8], p0, p1;
     fetch8<CELLS>(V, c, v);
-    const float d = clamp_density(c.inside, interp(c, v, p0, p1));
+    const float d = clamp_density(INSIDE || c.inside, interp(c, v, p0, p1));
     int i0; float w; float4 slope;
-    const float4 s = tf.eval(d, i0, w, slope, false);
-    const Segment g = segment(s.w, dt32);
+    const float4 s = tf_eval(TF, d, i0, w, slope, false);
+    const Segment g = segment<SEG>(s.w, dt32);
     const float Ta = __fmul_rn(T, g.a);
     c0 = __fmaf_rn(Ta, s.x, c0);
     c1 = __fmaf_rn(Ta, s.y, c1);
@@ -504,7 +524,50 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
     T = __fmul_rn(T, g.ome);
     S += (double)g.od;
   }
-  reinterpret_cast<float4*>(image)[pix] = make_float4(c0, c1, c2, A);
+  rgba = make_float4(c0, c1, c2, A);
+  depth = S;
+}
+
+template <bool EARLY, bool CELLS, bool TAPE>
+__global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
+                                                             float* __restrict__ image,
+                                                             float* __restrict__ depth) {
+  __shared__ Frame F;
+  __shared__ unsigned s_maxtau;
+  const int view = blockIdx.z;
+  if (threadIdx.x == 0) s_maxtau = 0u;
+  __syncthreads();
+  load_tf(TFA, &s_maxtau);
+  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
+  __syncthreads();
+  const int mode = seg_mode(G.dt32, s_maxtau);
+
+  int px, py;
+  pixel_of(G, px, py);
+  const bool valid = px < G.W && py < G.row1;
+  Ray r;
+  r.n = 0;
+  r.all_inside = true;
+  if (valid) setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
+  const bool warp_inside = CELLS && __all_sync(0xffffffffu, r.all_inside);
+  if (!valid) return;
+
+  const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
+  float* tape = TAPE ? G.tape + pix * G.tape_stride : nullptr;
+  float4 rgba;
+  double S;
+#define DDVR_MARCH(SEG, INS) march_ray<EARLY, CELLS, TAPE, SEG, INS>(V, TFA, G.dt32, r, tape, rgba, S)
+  if (warp_inside) {
+    if (mode == kSegP3) DDVR_MARCH(kSegP3, true);
+    else if (mode == kSegP7) DDVR_MARCH(kSegP7, true);
+    else DDVR_MARCH(kSegGen, true);
+  } else {
+    if (mode == kSegP3) DDVR_MARCH(kSegP3, false);
+    else if (mode == kSegP7) DDVR_MARCH(kSegP7, false);
+    else DDVR_MARCH(kSegGen, false);
+  }
+#undef DDVR_MARCH
+  reinterpret_cast<float4*>(image)[pix] = rgba;
   if (depth) depth[pix] = (float)S;
 }
 
@@ -544,12 +607,35 @@ __device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
   }
 }
 
-template <unsigned MASK, bool CELLS>
-__global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
-    VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
-    const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
-    float* __restrict__ d_cells, double* __restrict__ d_tf, double* __restrict__ d_camera,
-    double* __restrict__ d_dt) {
+__device__ __forceinline__ void tf_flush_run(float4* s_tfg, int R, int run, const float4& a0,
+                                             const float4& a1) {
+  const int j1 = min(run + 1, R - 1);
+  atomicAdd(&s_tfg[run].x, a0.x); atomicAdd(&s_tfg[run].y, a0.y);
+  atomicAdd(&s_tfg[run].z, a0.z); atomicAdd(&s_tfg[run].w, a0.w);
+  atomicAdd(&s_tfg[j1].x, a1.x); atomicAdd(&s_tfg[j1].y, a1.y);
+  atomicAdd(&s_tfg[j1].z, a1.z); atomicAdd(&s_tfg[j1].w, a1.w);
+}
+
+constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
+
+// Per-ray adjoint accumulators that outlive the walk
+struct AdjState {
+  int run_cell, run_base, run_ox, run_oy, run_oz;   // volume cell run
+  float acc8[8];
+  int tf_run;                                       // TF texel run (texels i0, i0+1)
+  float4 tfa0, tfa1;
+  // camera / stepsize per-ray sums (grid units) in fp64: thousands of terms
+  // with cancellation (the per-sample terms stay fp32)
+  double s1x, s1y, s1z, s2x, s2y, s2z, dt_bl, dt_pos;
+};
+
+// The backward walk of one ray (renderer.py:547-626).
+template <unsigned MASK, bool CELLS, int SEG, bool INSIDE>
+__device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
+                                            const Ray& r, double S, float4 sd,
+                                            const float* __restrict__ tape, float4* s_tfg,
+                                            float* __restrict__ d_volume,
+                                            float* __restrict__ d_cells, AdjState& st) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
   constexpr bool kStep = MASK & DDVR_TARGET_STEPSIZE;
   constexpr bool kTf = MASK & DDVR_TARGET_TF;
@@ -557,55 +643,8 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   constexpr bool kPos = kCam || kStep;
   constexpr bool kDhat = kPos || kVol;
 
-  extern __shared__ float4 s_tex[];            // [R] texels, then [R] TF gradient
-  __shared__ Frame F;
-  __shared__ double s_red[kWarps][3];
-  float4* s_tfg = s_tex + 2 * TFA.count;
-  const int view = blockIdx.z;
-  load_tf(TFA, s_tex);
-  if (kTf)
-    for (int i = threadIdx.x; i < TFA.count; i += blockDim.x) s_tfg[i] = make_float4(0, 0, 0, 0);
-  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
-  __syncthreads();
-
-  int px, py;
-  pixel_of(G, px, py);
-  const bool valid = px < G.W && py < G.row1;
-
-  Ray r;
-  r.n = 0;
-  r.all_inside = true;
-  double S = 0.0;   // optical depth after the current sample (T = exp(-S))
-  float4 sd = make_float4(0, 0, 0, 0);
-  const float* tape = nullptr;
-  if (valid) {
-    setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
-    const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
-    if (G.tape) tape = G.tape + pix * G.tape_stride;
-    sd = reinterpret_cast<const float4*>(seed)[pix];
-    // the forward's exact optical depth; without it, S = -ln(1 - alpha)
-    S = depth ? (double)depth[pix]
-              : -log1p(-(double)reinterpret_cast<const float4*>(image)[pix].w);
-  }
-  const TexelTF tf{s_tex, TFA.count, (float)TFA.count, (float)(TFA.count - 1),
-                   max(TFA.count - 2, 0)};
-  const float dt32 = (float)G.dt;
-
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
-  // volume cell-run accumulator
-  constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
-  int run_cell = kNoRun, run_base = 0, run_ox = 0, run_oy = 0, run_oz = 0;
-  float acc8[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) acc8[k] = 0.f;
-  // TF texel-run accumulator (texel i0 and i0+1)
-  int tf_run = -1;
-  float4 tfa0 = make_float4(0, 0, 0, 0), tfa1 = make_float4(0, 0, 0, 0);
-  // camera / stepsize per-ray sums (grid units) in fp64: thousands of terms with
-  // cancellation (the per-sample terms stay fp32)
-  double s1x = 0, s1y = 0, s1z = 0, s2x = 0, s2y = 0, s2z = 0;
-  double dt_bl = 0.0, dt_pos = 0.0;
   // last sample position; walk back with exact integer steps
   long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
   long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
@@ -613,14 +652,15 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
 
   for (int i = r.n - 1; i >= 0; --i) {
     Cell c;
-    locate<CELLS>(V, gx, gy, gz, r.all_inside, c);
+    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
     float v[8], p0, p1;
     fetch8<CELLS>(V, c, v);
     const float raw = interp(c, v, p0, p1);
-    const float d = clamp_density(c.inside, raw);
+    const bool inside = INSIDE || c.inside;
+    const float d = clamp_density(inside, raw);
     int i0; float w; float4 slope;
-    const float4 s = tf.eval(d, i0, w, slope, kDhat);
-    const Segment g = segment(s.w, dt32);
+    const float4 s = tf_eval(TF, d, i0, w, slope, kDhat);
+    const Segment g = segment<SEG>(s.w, dt32);
 
     // Invert the compositing step (renderer.py:579, a_prev = (a - A)/(a - 1)).
     // In optical-depth form the inverse is exact: -ln(1 - a) = g.od, so the
@@ -646,47 +686,42 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     const float a_raw_hat = g.a_clamped ? 0.f : seg_a_hat;
     const float ea = g.e * a_raw_hat;
     const float tau_hat = s.w < 0.f ? 0.f : dt32 * ea;
-    if (kStep) dt_bl += (double)(g.tau * ea);
+    if (kStep) st.dt_bl += (double)(g.tau * ea);
 
     if (kTf) {   // renderer.py:602-604: texels i0 and i0+1 with weights (1-w), w
-      if (i0 != tf_run) {
-        if (tf_run >= 0) {
-          const int j1 = min(tf_run + 1, TFA.count - 1);
-          atomicAdd(&s_tfg[tf_run].x, tfa0.x); atomicAdd(&s_tfg[tf_run].y, tfa0.y);
-          atomicAdd(&s_tfg[tf_run].z, tfa0.z); atomicAdd(&s_tfg[tf_run].w, tfa0.w);
-          atomicAdd(&s_tfg[j1].x, tfa1.x); atomicAdd(&s_tfg[j1].y, tfa1.y);
-          atomicAdd(&s_tfg[j1].z, tfa1.z); atomicAdd(&s_tfg[j1].w, tfa1.w);
-        }
-        tf_run = i0;
-        tfa0 = make_float4(0, 0, 0, 0);
-        tfa1 = make_float4(0, 0, 0, 0);
+      if (i0 != st.tf_run) {
+        if (st.tf_run >= 0) tf_flush_run(s_tfg, TF.count, st.tf_run, st.tfa0, st.tfa1);
+        st.tf_run = i0;
+        st.tfa0 = make_float4(0, 0, 0, 0);
+        st.tfa1 = make_float4(0, 0, 0, 0);
       }
       const float w0 = 1.f - w;
-      tfa0.x += w0 * h0; tfa0.y += w0 * h1; tfa0.z += w0 * h2; tfa0.w += w0 * tau_hat;
-      tfa1.x += w * h0;  tfa1.y += w * h1;  tfa1.z += w * h2;  tfa1.w += w * tau_hat;
+      st.tfa0.x += w0 * h0; st.tfa0.y += w0 * h1; st.tfa0.z += w0 * h2; st.tfa0.w += w0 * tau_hat;
+      st.tfa1.x += w * h0;  st.tfa1.y += w * h1;  st.tfa1.z += w * h2;  st.tfa1.w += w * tau_hat;
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
       const float d_hat = slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat;
-      const bool live = c.inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
+      const bool live = inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol) {   // renderer.py:607-608, accumulated per cell run
-        if (c.cell != run_cell) {
-          if (run_cell != kNoRun)
-            flush_cell<CELLS>(d_volume, d_cells, run_cell, run_base, run_ox, run_oy, run_oz, acc8);
-          run_cell = c.cell;
-          if (!CELLS) { run_base = c.base; run_ox = c.ox; run_oy = c.oy; run_oz = c.oz; }
+        if (c.cell != st.run_cell) {
+          if (st.run_cell != kNoRun)
+            flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
+                              st.run_oz, st.acc8);
+          st.run_cell = c.cell;
+          if (!CELLS) { st.run_base = c.base; st.run_ox = c.ox; st.run_oy = c.oy; st.run_oz = c.oz; }
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc8[k] = 0.f;
+          for (int k = 0; k < 8; ++k) st.acc8[k] = 0.f;
         }
         const float dh = live ? d_hat : 0.f;
         const float z0 = dh * (1.f - c.fz), z1 = dh * c.fz;
         const float y00 = z0 * (1.f - c.fy), y10 = z0 * c.fy;
         const float y01 = z1 * (1.f - c.fy), y11 = z1 * c.fy;
         const float ex = 1.f - c.fx;
-        acc8[0] += y00 * ex; acc8[1] += y00 * c.fx;
-        acc8[2] += y10 * ex; acc8[3] += y10 * c.fx;
-        acc8[4] += y01 * ex; acc8[5] += y01 * c.fx;
-        acc8[6] += y11 * ex; acc8[7] += y11 * c.fx;
+        st.acc8[0] += y00 * ex; st.acc8[1] += y00 * c.fx;
+        st.acc8[2] += y10 * ex; st.acc8[3] += y10 * c.fx;
+        st.acc8[4] += y01 * ex; st.acc8[5] += y01 * c.fx;
+        st.acc8[6] += y11 * ex; st.acc8[7] += y11 * c.fx;
       }
       if (kPos && live) {   // renderer.py:609-623 (spatial gradient, field.py:446-484)
         const float t = __fmul_rn((float)i, dt32);
@@ -700,26 +735,92 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
         const float by = (gy >= 0 && gy <= V.top[1]) ? ddy * d_hat : 0.f;
         const float bz = (gz >= 0 && gz <= V.top[2]) ? ddz * d_hat : 0.f;
         if (kCam) {
-          s1x += bx; s1y += by; s1z += bz;
-          s2x += (double)(t * bx); s2y += (double)(t * by); s2z += (double)(t * bz);
+          st.s1x += bx; st.s1y += by; st.s1z += bz;
+          st.s2x += (double)(t * bx); st.s2y += (double)(t * by); st.s2z += (double)(t * bz);
         }
-        if (kStep) dt_pos += (double)((float)i * (r.gw[0] * bx + r.gw[1] * by + r.gw[2] * bz));
+        if (kStep)
+          st.dt_pos += (double)((float)i * (r.gw[0] * bx + r.gw[1] * by + r.gw[2] * bz));
       }
     }
     gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
   }
+}
+
+template <unsigned MASK, bool CELLS>
+__global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
+    VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
+    const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
+    float* __restrict__ d_cells, double* __restrict__ d_tf, double* __restrict__ d_camera,
+    double* __restrict__ d_dt) {
+  constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
+  constexpr bool kStep = MASK & DDVR_TARGET_STEPSIZE;
+  constexpr bool kTf = MASK & DDVR_TARGET_TF;
+  constexpr bool kVol = MASK & DDVR_TARGET_VOLUME;
+  constexpr bool kPos = kCam || kStep;
+
+  __shared__ Frame F;
+  __shared__ double s_red[kWarps][3];
+  __shared__ unsigned s_maxtau;
+  float4* s_tfg = g_smem + 2 * TFA.count;       // [R] TF gradient after the pair table
+  const int view = blockIdx.z;
+  if (threadIdx.x == 0) s_maxtau = 0u;
+  __syncthreads();
+  load_tf(TFA, &s_maxtau);
+  if (kTf)
+    for (int i = threadIdx.x; i < TFA.count; i += blockDim.x) s_tfg[i] = make_float4(0, 0, 0, 0);
+  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
+  __syncthreads();
+  const int mode = seg_mode(G.dt32, s_maxtau);
+
+  int px, py;
+  pixel_of(G, px, py);
+  const bool valid = px < G.W && py < G.row1;
+
+  Ray r;
+  r.n = 0;
+  r.all_inside = true;
+  double S = 0.0;   // optical depth after the current sample (T = exp(-S))
+  float4 sd = make_float4(0, 0, 0, 0);
+  const float* tape = nullptr;
+  if (valid) {
+    setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
+    const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
+    if (G.tape) tape = G.tape + pix * G.tape_stride;
+    sd = reinterpret_cast<const float4*>(seed)[pix];
+    // the forward's exact optical depth; without it, S = -ln(1 - alpha)
+    S = depth ? (double)depth[pix]
+              : -log1p(-(double)reinterpret_cast<const float4*>(image)[pix].w);
+  }
+  const bool warp_inside = CELLS && __all_sync(0xffffffffu, r.all_inside);
+
+  AdjState st;
+  st.run_cell = kNoRun; st.run_base = 0; st.run_ox = 0; st.run_oy = 0; st.run_oz = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) st.acc8[k] = 0.f;
+  st.tf_run = -1;
+  st.tfa0 = make_float4(0, 0, 0, 0);
+  st.tfa1 = make_float4(0, 0, 0, 0);
+  st.s1x = st.s1y = st.s1z = st.s2x = st.s2y = st.s2z = st.dt_bl = st.dt_pos = 0.0;
+
+#define DDVR_WALK(SEG, INS) \
+  adjoint_ray<MASK, CELLS, SEG, INS>(V, TFA, G.dt32, r, S, sd, tape, s_tfg, d_volume, d_cells, st)
+  if (warp_inside) {
+    if (mode == kSegP3) DDVR_WALK(kSegP3, true);
+    else if (mode == kSegP7) DDVR_WALK(kSegP7, true);
+    else DDVR_WALK(kSegGen, true);
+  } else {
+    if (mode == kSegP3) DDVR_WALK(kSegP3, false);
+    else if (mode == kSegP7) DDVR_WALK(kSegP7, false);
+    else DDVR_WALK(kSegGen, false);
+  }
+#undef DDVR_WALK
 
   // ---- flush per-ray accumulators ----
-  if (kVol && run_cell != kNoRun)
-    flush_cell<CELLS>(d_volume, d_cells, run_cell, run_base, run_ox, run_oy, run_oz, acc8);
+  if (kVol && st.run_cell != kNoRun)
+    flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
+                      st.run_oz, st.acc8);
   if (kTf) {
-    if (tf_run >= 0) {
-      const int j1 = min(tf_run + 1, TFA.count - 1);
-      atomicAdd(&s_tfg[tf_run].x, tfa0.x); atomicAdd(&s_tfg[tf_run].y, tfa0.y);
-      atomicAdd(&s_tfg[tf_run].z, tfa0.z); atomicAdd(&s_tfg[tf_run].w, tfa0.w);
-      atomicAdd(&s_tfg[j1].x, tfa1.x); atomicAdd(&s_tfg[j1].y, tfa1.y);
-      atomicAdd(&s_tfg[j1].z, tfa1.z); atomicAdd(&s_tfg[j1].w, tfa1.w);
-    }
+    if (st.tf_run >= 0) tf_flush_run(s_tfg, TFA.count, st.tf_run, st.tfa0, st.tfa1);
     __syncthreads();
     for (int k = threadIdx.x; k < TFA.count; k += blockDim.x) {
       const float4 g = s_tfg[k];
@@ -732,11 +833,11 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   if (kPos) {
     double cam0 = 0.0, cam1 = 0.0, stp = 0.0;
     if (valid && r.n > 0) {
-      if (kStep) stp = dt_bl + dt_pos;
+      if (kStep) stp = st.dt_bl + st.dt_pos;
       if (kCam) {
         // world-space sums: x_hat = scale * grid-space gradient (chain of g = (x-bmin)*scale)
-        const double xo_h[3] = {s1x * V.scale[0], s1y * V.scale[1], s1z * V.scale[2]};
-        const double w_h[3] = {s2x * V.scale[0], s2y * V.scale[1], s2z * V.scale[2]};
+        const double xo_h[3] = {st.s1x * V.scale[0], st.s1y * V.scale[1], st.s1z * V.scale[2]};
+        const double w_h[3] = {st.s2x * V.scale[0], st.s2y * V.scale[1], st.s2z * V.scale[2]};
         // entry point xo = o + tn*w moves with the camera (renderer.py:629-639)
         const double sdot = r.w[0] * xo_h[0] + r.w[1] * xo_h[1] + r.w[2] * xo_h[2];
         const bool need = !r.clamped && !r.miss;
@@ -958,6 +1059,9 @@ int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
   A.params = tf->params;
   A.kind = tf->kind;
   A.count = tf->count;
+  A.fR = (float)tf->count;
+  A.fR1 = (float)(tf->count - 1);
+  A.Rm2 = tf->count >= 2 ? tf->count - 2 : 0;
   return DDVR_OK;
 }
 
@@ -979,6 +1083,7 @@ int make_geo(const ddvr_camera* cams, int n_views, const ddvr_params* p, Geometr
     return set_error(DDVR_INVALID_PARAMETER, "row band [%d, %d) outside image height %d", G.row0,
                      G.row1, G.H);
   G.dt = p->dt;
+  G.dt32 = (float)p->dt;
   G.tape = p->tape;
   G.tape_stride = p->tape_stride;
   if (G.tape && G.tape_stride < 0)
