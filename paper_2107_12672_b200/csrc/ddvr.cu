@@ -50,7 +50,7 @@ constexpr double kDeg = 3.14159265358979323846 / 180.0;   // field.py:27
 constexpr int kTile = 16;                   // CTA = 16x16 pixels
 constexpr int kThreads = kTile * kTile;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxTfBytes = 96 * 1024;      // TF table + TF gradient in shared memory
+constexpr int kMaxTfBytes = 200 * 1024;     // TF tables + TF gradient in shared memory (B200: 227 KB/CTA)
 
 // Sample positions are kept in 32.32 fixed-point GRID coordinates
 // (g = (x - bmin)*scale - 0.5): g_i = g_0 + i*step with integer adds.  The
@@ -369,11 +369,34 @@ __device__ __forceinline__ float clamp_density(bool inside, float raw) {
 // transfer functions (field.py:525-579; renderer.py:472-488)
 // ---------------------------------------------------------------------------
 
-// Dynamic shared memory of every kernel: the TF as (texel k, texel k+1 -
-// texel k) pairs, then (adjoint, tf target) the per-CTA TF gradient.  A
-// file-scope symbol keeps loads in the shared window (no generic->shared
+// Dynamic shared memory of every kernel (R = TF texels):
+//   g_smem[0, 2R)        the TF as (texel k, texel k+1 - texel k) float4 pairs
+//   g_smem[2R, 3R)       the per-CTA TF gradient (adjoint, tf target)
+//   g_smem[3R, ...)      (tau_k, tau_k+1 - tau_k) float2 pairs: the table of an
+//                        emission-free TF (rgb texels all zero, e.g. the
+//                        absorption ramp of tasks.py:348-356), one 64-bit load
+// A file-scope symbol keeps loads in the shared window (no generic->shared
 // conversion per access).
 extern __shared__ float4 g_smem[];
+
+__device__ __forceinline__ const float2* tau_table(const TfArgs& T) {
+  return reinterpret_cast<const float2*>(g_smem + 3 * T.count);
+}
+
+// tau-only lookup of an emission-free TF (same arithmetic as tf_eval's w channel)
+__device__ __forceinline__ float tf_eval_tau(const TfArgs& T, float d, int& i0, float& w,
+                                             float& slope_tau, bool want_slope) {
+  const float t = __fsub_rn(__fmul_rn(d, T.fR), 0.5f);
+  const float f = fminf(fmaxf(t, 0.f), T.fR1);
+  i0 = min((int)f, T.Rm2);
+  w = __fsub_rn(f, (float)i0);
+  const float2 q = tau_table(T)[i0];
+  if (want_slope) {
+    const bool live = t >= 0.f && t <= T.fR1;
+    slope_tau = q.y * (live ? T.fR : 0.f);
+  }
+  return __fmaf_rn(w, q.y, q.x);
+}
 
 // texel table: R texels, centre of texel r at (r + 0.5)/R, clamp-to-edge
 // (field.py:540-549); fR, fR1, Rm2 are precomputed on the host (TfArgs)
@@ -462,19 +485,25 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
 // shared TF table as (texel k, texel k+1 - texel k) pairs: the lerp is then 4
 // FFMA and the slope (field.py:576) needs no subtraction.  Returns (to every
 // thread, after the barrier the caller issues) the segment mode of the CTA.
-__device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_maxtau) {
+// s_info[0]: largest tau texel (bits), s_info[1]: 1 if any rgb texel is non-zero
+__device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
   const float4* src = reinterpret_cast<const float4*>(tf.params);
+  float2* tau = reinterpret_cast<float2*>(g_smem + 3 * tf.count);
   float mx = 0.f;
+  bool rgb = false;
   for (int i = threadIdx.x; i < tf.count; i += blockDim.x) {
     const float4 a = src[i];
     const float4 b = src[min(i + 1, tf.count - 1)];
     g_smem[2 * i] = a;
     g_smem[2 * i + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
                                     __fsub_rn(b.z, a.z), __fsub_rn(b.w, a.w));
+    tau[i] = make_float2(a.w, __fsub_rn(b.w, a.w));
     mx = fmaxf(mx, a.w);   // interpolated tau never exceeds the largest texel
+    rgb |= a.x != 0.f || a.y != 0.f || a.z != 0.f;
   }
   // non-negative floats order like their bit patterns
-  if (mx > 0.f) atomicMax(s_maxtau, __float_as_uint(mx));
+  if (mx > 0.f) atomicMax(&s_info[0], __float_as_uint(mx));
+  if (rgb) atomicOr(&s_info[1], 1u);
 }
 
 __device__ __forceinline__ int seg_mode(float dt32, unsigned maxtau_bits) {
@@ -494,7 +523,7 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 
 // The march of one ray.  INSIDE: every lane of the warp has all_inside (the
 // per-sample inside test and clamps are compiled out); SEG: segment mode.
-template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE>
+template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT>
 __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
                                           double& depth) {
@@ -513,13 +542,22 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     float v[8], p0, p1;
     fetch8<CELLS>(V, c, v);
     const float d = clamp_density(INSIDE || c.inside, interp(c, v, p0, p1));
-    int i0; float w; float4 slope;
-    const float4 s = tf_eval(TF, d, i0, w, slope, false);
+    int i0; float w;
+    float4 s;
+    if (EMIT) {
+      float4 slope;
+      s = tf_eval(TF, d, i0, w, slope, false);
+    } else {   // emission-free TF: rgb is identically 0
+      float slope_tau;
+      s = make_float4(0.f, 0.f, 0.f, tf_eval_tau(TF, d, i0, w, slope_tau, false));
+    }
     const Segment g = segment<SEG>(s.w, dt32);
     const float Ta = __fmul_rn(T, g.a);
-    c0 = __fmaf_rn(Ta, s.x, c0);
-    c1 = __fmaf_rn(Ta, s.y, c1);
-    c2 = __fmaf_rn(Ta, s.z, c2);
+    if (EMIT) {
+      c0 = __fmaf_rn(Ta, s.x, c0);
+      c1 = __fmaf_rn(Ta, s.y, c1);
+      c2 = __fmaf_rn(Ta, s.z, c2);
+    }
     A = __fadd_rn(A, Ta);
     T = __fmul_rn(T, g.ome);
     S += (double)g.od;
@@ -533,14 +571,15 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
                                                              float* __restrict__ image,
                                                              float* __restrict__ depth) {
   __shared__ Frame F;
-  __shared__ unsigned s_maxtau;
+  __shared__ unsigned s_info[2];
   const int view = blockIdx.z;
-  if (threadIdx.x == 0) s_maxtau = 0u;
+  if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
   __syncthreads();
-  load_tf(TFA, &s_maxtau);
+  load_tf(TFA, s_info);
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
   __syncthreads();
-  const int mode = seg_mode(G.dt32, s_maxtau);
+  const int mode = seg_mode(G.dt32, s_info[0]);
+  const bool emit = s_info[1] != 0u;
 
   int px, py;
   pixel_of(G, px, py);
@@ -556,16 +595,18 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
   float* tape = TAPE ? G.tape + pix * G.tape_stride : nullptr;
   float4 rgba;
   double S;
-#define DDVR_MARCH(SEG, INS) march_ray<EARLY, CELLS, TAPE, SEG, INS>(V, TFA, G.dt32, r, tape, rgba, S)
+#define DDVR_MARCH(SEG, INS, EM) \
+  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM>(V, TFA, G.dt32, r, tape, rgba, S)
+#define DDVR_MARCH_SEG(INS, EM)                  \
+  if (mode == kSegP3) DDVR_MARCH(kSegP3, INS, EM); \
+  else if (mode == kSegP7) DDVR_MARCH(kSegP7, INS, EM); \
+  else DDVR_MARCH(kSegGen, INS, EM);
   if (warp_inside) {
-    if (mode == kSegP3) DDVR_MARCH(kSegP3, true);
-    else if (mode == kSegP7) DDVR_MARCH(kSegP7, true);
-    else DDVR_MARCH(kSegGen, true);
+    if (emit) { DDVR_MARCH_SEG(true, true) } else { DDVR_MARCH_SEG(true, false) }
   } else {
-    if (mode == kSegP3) DDVR_MARCH(kSegP3, false);
-    else if (mode == kSegP7) DDVR_MARCH(kSegP7, false);
-    else DDVR_MARCH(kSegGen, false);
+    if (emit) { DDVR_MARCH_SEG(false, true) } else { DDVR_MARCH_SEG(false, false) }
   }
+#undef DDVR_MARCH_SEG
 #undef DDVR_MARCH
   reinterpret_cast<float4*>(image)[pix] = rgba;
   if (depth) depth[pix] = (float)S;
@@ -630,7 +671,7 @@ struct AdjState {
 };
 
 // The backward walk of one ray (renderer.py:547-626).
-template <unsigned MASK, bool CELLS, int SEG, bool INSIDE>
+template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT>
 __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                             const Ray& r, double S, float4 sd,
                                             const float* __restrict__ tape, float4* s_tfg,
@@ -658,8 +699,15 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const float raw = interp(c, v, p0, p1);
     const bool inside = INSIDE || c.inside;
     const float d = clamp_density(inside, raw);
-    int i0; float w; float4 slope;
-    const float4 s = tf_eval(TF, d, i0, w, slope, kDhat);
+    int i0; float w;
+    float4 s, slope;
+    if (EMIT) {
+      s = tf_eval(TF, d, i0, w, slope, kDhat);
+    } else {   // emission-free TF (never with the tf target): rgb and its slope are 0
+      float slope_tau = 0.f;
+      s = make_float4(0.f, 0.f, 0.f, tf_eval_tau(TF, d, i0, w, slope_tau, kDhat));
+      slope = make_float4(0.f, 0.f, 0.f, slope_tau);
+    }
     const Segment g = segment<SEG>(s.w, dt32);
 
     // Invert the compositing step (renderer.py:579, a_prev = (a - A)/(a - 1)).
@@ -760,17 +808,19 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
 
   __shared__ Frame F;
   __shared__ double s_red[kWarps][3];
-  __shared__ unsigned s_maxtau;
+  __shared__ unsigned s_info[2];
   float4* s_tfg = g_smem + 2 * TFA.count;       // [R] TF gradient after the pair table
   const int view = blockIdx.z;
-  if (threadIdx.x == 0) s_maxtau = 0u;
+  if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
   __syncthreads();
-  load_tf(TFA, &s_maxtau);
+  load_tf(TFA, s_info);
   if (kTf)
     for (int i = threadIdx.x; i < TFA.count; i += blockDim.x) s_tfg[i] = make_float4(0, 0, 0, 0);
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
   __syncthreads();
-  const int mode = seg_mode(G.dt32, s_maxtau);
+  const int mode = seg_mode(G.dt32, s_info[0]);
+  // the tf target needs the rgb channels even when they are zero
+  const bool emit = kTf || s_info[1] != 0u;
 
   int px, py;
   pixel_of(G, px, py);
@@ -802,17 +852,21 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   st.tfa1 = make_float4(0, 0, 0, 0);
   st.s1x = st.s1y = st.s1z = st.s2x = st.s2y = st.s2z = st.dt_bl = st.dt_pos = 0.0;
 
-#define DDVR_WALK(SEG, INS) \
-  adjoint_ray<MASK, CELLS, SEG, INS>(V, TFA, G.dt32, r, S, sd, tape, s_tfg, d_volume, d_cells, st)
+#define DDVR_WALK(SEG, INS, EM)                                                          \
+  adjoint_ray<MASK, CELLS, SEG, INS, EM>(V, TFA, G.dt32, r, S, sd, tape, s_tfg, d_volume, \
+                                         d_cells, st)
+#define DDVR_WALK_SEG(INS, EM)                  \
+  if (mode == kSegP3) DDVR_WALK(kSegP3, INS, EM); \
+  else if (mode == kSegP7) DDVR_WALK(kSegP7, INS, EM); \
+  else DDVR_WALK(kSegGen, INS, EM);
   if (warp_inside) {
-    if (mode == kSegP3) DDVR_WALK(kSegP3, true);
-    else if (mode == kSegP7) DDVR_WALK(kSegP7, true);
-    else DDVR_WALK(kSegGen, true);
+    if (emit) { DDVR_WALK_SEG(true, true) }
+    else if (!kTf) { DDVR_WALK_SEG(true, kTf) }   // kTf: never taken (EMIT=true re-use)
   } else {
-    if (mode == kSegP3) DDVR_WALK(kSegP3, false);
-    else if (mode == kSegP7) DDVR_WALK(kSegP7, false);
-    else DDVR_WALK(kSegGen, false);
+    if (emit) { DDVR_WALK_SEG(false, true) }
+    else if (!kTf) { DDVR_WALK_SEG(false, kTf) }
   }
+#undef DDVR_WALK_SEG
 #undef DDVR_WALK
 
   // ---- flush per-ray accumulators ----
@@ -1052,10 +1106,11 @@ int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
   if (!tf->params) return set_error(DDVR_INVALID_INPUT, "transfer function pointer is NULL");
   if (((uintptr_t)tf->params & 15) != 0)
     return set_error(DDVR_INVALID_INPUT, "transfer function must be 16-byte aligned");
-  smem_per_table = 2 * (size_t)tf->count * sizeof(float4);   // (texel, delta) pairs
-  if (3 * (size_t)tf->count * sizeof(float4) > (size_t)kMaxTfBytes)
+  // shared layout (see g_smem): 2R pair float4 + R gradient float4 + ceil(R/2) tau-pair float4
+  smem_per_table = (3 * (size_t)tf->count + ((size_t)tf->count + 1) / 2) * sizeof(float4);
+  if (smem_per_table > (size_t)kMaxTfBytes)
     return set_error(DDVR_UNSUPPORTED, "transfer function resolution %d exceeds %d texels",
-                     tf->count, kMaxTfBytes / 48);
+                     tf->count, kMaxTfBytes / 56);
   A.params = tf->params;
   A.kind = tf->kind;
   A.count = tf->count;
@@ -1216,7 +1271,7 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid = grid_of(G, n_views);
-  const size_t smem = (mask & DDVR_TARGET_TF) ? tbl + tbl / 2 : tbl;
+  const size_t smem = tbl;
   const bool cells = V.cells != nullptr;
   float* d_cells_all = ws_need > 0 ? static_cast<float*>(workspace) : nullptr;
   // the kernel indexes cell gradients relative to cell (0,0,0), like V.cell0
