@@ -294,6 +294,94 @@ def tf_eval(texels, d):
     return out, slope, (i0, i1), (1.0 - w, w)
 
 
+class PiecewiseTF:
+    """Piecewise-linear TF on non-uniform knots: params (K,5) = [pos, r, g, b, tau].
+
+    NO REFERENCE IMPLEMENTATION: restated from the texel TF's
+    conventions (field.py:540-549, 575-576) -- linear between knots,
+    clamp-to-edge outside [pos_0, pos_K-1], zero slope in the clamp bands.
+    With knots at (r+0.5)/R it equals the R-texel table.  Gradients cover the
+    knot values and positions.  Parity for this mode is unpinned (no reference);
+    tests check it by the texel equivalence and by finite differences.
+    """
+
+    kind = "piecewise"
+
+    def __init__(self, params):
+        self.params = np.asarray(params, np.float64)
+        self.pos = self.params[:, 0]
+        self.val = self.params[:, 1:]
+
+    def eval(self, d):
+        K = self.pos.shape[0]
+        d = np.clip(d, 0.0, 1.0)
+        k = np.clip(np.searchsorted(self.pos, d, side="right") - 1, 0, max(K - 2, 0))
+        k1 = np.minimum(k + 1, K - 1)
+        span = self.pos[k1] - self.pos[k]
+        inner = (d > self.pos[0]) & (d < self.pos[-1]) & (span > 0)
+        w = np.where(inner, (d - self.pos[k]) / np.where(span > 0, span, 1.0), 0.0)
+        w = np.where(d >= self.pos[-1], 1.0 if K > 1 else 0.0, w)
+        out = (1.0 - w)[:, None] * self.val[k] + w[:, None] * self.val[k1]
+        slope = np.where(inner[:, None],
+                         (self.val[k1] - self.val[k]) / np.where(span > 0, span, 1.0)[:, None],
+                         0.0)
+        return out, slope, k, k1, w
+
+    def grads(self, d, o4):
+        """dL/dparams (K,5) of sum(o4 * eval(d)) (o4 (n,4) the output adjoint)."""
+        out, slope, k, k1, w = self.eval(d)
+        g = np.zeros_like(self.params)
+        np.add.at(g[:, 1:], k, (1.0 - w)[:, None] * o4)
+        np.add.at(g[:, 1:], k1, w[:, None] * o4)
+        dh = np.sum(slope * o4, axis=1)              # d out / d d . o4 (0 in clamp bands)
+        np.add.at(g[:, 0], k, dh * (w - 1.0))
+        np.add.at(g[:, 0], k1, -dh * w)
+        return g
+
+
+class GaussianTF:
+    """Analytic sum-of-Gaussians TF: params (G,6) = [mu, sigma, r, g, b, tau].
+
+    out(d) = sum_j exp(-(d - mu_j)^2 / (2 sigma_j^2)) * (r_j, g_j, b_j, tau_j) on the
+    clamped density.  NO REFERENCE IMPLEMENTATION: the optical model follows the
+    reference's 1-D Gaussian demo (tasks.py:751-766: g = exp(-d^2/2sigma^2),
+    tau = tau_s g, opacity-weighted emission g).  Parity unpinned; checked by
+    finite differences and by that demo's closed form.
+    """
+
+    kind = "gaussian"
+
+    def __init__(self, params):
+        self.params = np.asarray(params, np.float64)
+
+    def _g(self, d):
+        mu, sg = self.params[:, 0], self.params[:, 1]
+        z = (np.clip(d, 0.0, 1.0)[:, None] - mu[None, :])
+        return z, np.exp(-(z * z) / (2.0 * sg[None, :] ** 2))
+
+    def eval(self, d):
+        rgba = self.params[:, 2:]
+        z, g = self._g(d)
+        out = g @ rgba
+        dg = -g * z / self.params[None, :, 1] ** 2
+        return out, dg @ rgba, None, None, None
+
+    def grads(self, d, o4):
+        rgba = self.params[:, 2:]
+        sg = self.params[:, 1]
+        z, g = self._g(d)
+        proj = o4 @ rgba.T                                   # (n, G): o4 . rgba_j
+        gr = np.zeros_like(self.params)
+        gr[:, 2:] = g.T @ o4
+        gr[:, 0] = np.sum(g * z / sg ** 2 * proj, axis=0)
+        gr[:, 1] = np.sum(g * z * z / sg ** 3 * proj, axis=0)
+        return gr
+
+
+def _as_tf(tf):
+    return tf if isinstance(tf, (PiecewiseTF, GaussianTF)) else None
+
+
 def segment_opacity(tau_raw, dt):
     """(tau, e, a, a_clamped) of Beer-Lambert with the 1-EPS clamp (field.py:587-600)."""
     tau = np.maximum(tau_raw, 0.0)
@@ -359,7 +447,8 @@ def march(grid: Grid, texels, band: Band, dt: float, *, early_stop=False, record
                 break
         ti = dt * float(i)
         pts = [band.xo[k] + ti * band.w[k] for k in range(3)]
-        s4, _, _, _ = tf_eval(texels, grid.density(pts))
+        d = grid.density(pts)
+        s4 = texels.eval(d)[0] if _as_tf(texels) else tf_eval(texels, d)[0]
         _, _, a, _ = segment_opacity(s4[:, 3], dt)
         if record:
             tape.append(acc.copy())
@@ -394,7 +483,9 @@ def adjoint_view(grid: Grid, texels, view: View, dt: float, seed, targets, *,
     d_camera (2,), d_stepsize (float).
     """
     targets = set(targets)
-    texels = np.asarray(texels, np.float64)
+    analytic = _as_tf(texels)
+    if not analytic:
+        texels = np.asarray(texels, np.float64)
     r0, r1 = rows if rows is not None else (0, view.height)
     band = make_band(grid, view, dt, r0, r1)
     seed = np.asarray(seed, np.float64).reshape(-1, 4)
@@ -407,7 +498,7 @@ def adjoint_view(grid: Grid, texels, view: View, dt: float, seed, targets, *,
     want_pos = bool(targets & {"camera", "stepsize"})
     want_d = bool(targets & {"camera", "stepsize", "volume"})
 
-    g_tf = np.zeros_like(texels)
+    g_tf = np.zeros_like(analytic.params if analytic else texels)
     g_vol = np.zeros(grid.flat.shape[0])
     g_dt = 0.0
     xo_bar = np.zeros((3, nr))
@@ -423,7 +514,10 @@ def adjoint_view(grid: Grid, texels, view: View, dt: float, seed, targets, *,
         ti = dt * float(i)
         pts = [band.xo[k] + ti * band.w[k] for k in range(3)]
         d, spatial, w8, idx8 = grid.density_and_grads(pts)
-        out4, slope, (i0, i1), (tw0, tw1) = tf_eval(texels, d)
+        if analytic:
+            out4, slope = analytic.eval(d)[:2]
+        else:
+            out4, slope, (i0, i1), (tw0, tw1) = tf_eval(texels, d)
         tau, e, a, a_clamped = segment_opacity(out4[:, 3], dt)
         crgb = out4[:, :3]
         cs = a[:, None] * crgb
@@ -445,7 +539,9 @@ def adjoint_view(grid: Grid, texels, view: View, dt: float, seed, targets, *,
             g_dt += float(np.sum(np.where(act, tau * e * a_raw_bar, 0.0)))
         tau_bar = np.where(out4[:, 3] < 0.0, 0.0, dt * e * a_raw_bar)
         o4 = np.concatenate([crgb_bar, tau_bar[:, None]], axis=1) * act[:, None]
-        if "tf" in targets:                                  # renderer.py:602-604
+        if "tf" in targets and analytic:
+            g_tf += analytic.grads(d, o4)
+        elif "tf" in targets:                                # renderer.py:602-604
             np.add.at(g_tf, i0, tw0[:, None] * o4)
             np.add.at(g_tf, i1, tw1[:, None] * o4)
         if want_d:

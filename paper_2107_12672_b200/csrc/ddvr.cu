@@ -104,6 +104,7 @@ struct TfArgs {
   int kind, count;
   float fR, fR1;     // R, R-1
   int Rm2;           // max(R-2, 0)
+  int stride;        // floats per parameter row: 4 texture, 5 piecewise, 6 gaussian
 };
 
 struct Geometry {
@@ -417,6 +418,86 @@ __device__ __forceinline__ float4 tf_eval(const TfArgs& T, float d, int& i0, flo
                      __fmaf_rn(w, dlt.z, a.z), __fmaf_rn(w, dlt.w, a.w));
 }
 
+// Piecewise-linear TF on non-uniform knots, params (K,5) = [pos, r, g, b, tau].
+// No reference implementation: linear between knots, clamp-to-
+// edge outside [pos_0, pos_K-1] with zero slope there, as the texel table
+// (field.py:540-549, 575-576); equals it for knots at (r+0.5)/R.  Shared layout:
+// float4 val[K], float4 slope[K] ((v_k+1 - v_k)/span_k), float pos[K].
+// Returns the knot interval k (texel-like handle) and its weight w.
+__device__ __forceinline__ float4 pl_eval(const TfArgs& T, float d, int& k, float& w,
+                                          float4& slope, bool want_slope) {
+  const int K = T.count;
+  const float4* val = g_smem;
+  const float4* slp = g_smem + K;
+  const float* pos = reinterpret_cast<const float*>(g_smem + 2 * K);
+  float4 sl = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 out;
+  if (K == 1 || d <= pos[0]) {
+    k = 0; w = 0.f; out = val[0];
+  } else if (d >= pos[K - 1]) {
+    k = K - 2; w = 1.f; out = val[K - 1];
+  } else {   // pos[lo] <= d < pos[hi]
+    int lo = 0, hi = K - 1;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pos[mid] <= d) lo = mid; else hi = mid;
+    }
+    k = lo;
+    sl = slp[k];
+    const float u = __fsub_rn(d, pos[k]);
+    const float4 a = val[k];
+    w = __fdiv_rn(u, __fsub_rn(pos[k + 1], pos[k]));
+    out = make_float4(__fmaf_rn(u, sl.x, a.x), __fmaf_rn(u, sl.y, a.y), __fmaf_rn(u, sl.z, a.z),
+                      __fmaf_rn(u, sl.w, a.w));
+  }
+  if (want_slope) slope = sl;
+  return out;
+}
+
+// Analytic sum-of-Gaussians TF, params (G,6) = [mu, sigma, r, g, b, tau]:
+// out(d) = sum_j exp(-(d-mu_j)^2 / 2 sigma_j^2) rgba_j.  No reference
+// implementation: the optical model of the reference's 1-D demo
+// (tasks.py:751-766).  Shared layout: float4 rgba[G], float4 (mu, log2e/2s^2,
+// 1/s^2, s)[G].
+__device__ __forceinline__ float4 gauss_eval(const TfArgs& T, float d, float4& slope,
+                                             bool want_slope) {
+  const float4* rgba = g_smem;
+  const float4* prm = g_smem + T.count;
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f), sl = out;
+  for (int j = 0; j < T.count; ++j) {
+    const float4 q = prm[j];
+    const float4 c = rgba[j];
+    const float z = __fsub_rn(d, q.x);
+    float g;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(-(z * z) * q.y));
+    out.x += g * c.x; out.y += g * c.y; out.z += g * c.z; out.w += g * c.w;
+    if (want_slope) {
+      const float gd = -g * z * q.z;
+      sl.x += gd * c.x; sl.y += gd * c.y; sl.z += gd * c.z; sl.w += gd * c.w;
+    }
+  }
+  if (want_slope) slope = sl;
+  return out;
+}
+
+constexpr int kTfTexture = DDVR_TF_TEXTURE, kTfPiecewise = DDVR_TF_PIECEWISE,
+              kTfGaussian = DDVR_TF_GAUSSIAN;
+
+// (rgb, tau) of density d and its slope, for TF kind KIND; i0/w identify the
+// texel or knot interval (texture, piecewise).  EMIT=false: emission-free
+// texel table (rgb identically 0).
+template <int KIND, bool EMIT>
+__device__ __forceinline__ float4 tf_sample(const TfArgs& T, float d, int& i0, float& w,
+                                            float4& slope, bool want_slope) {
+  if (KIND == kTfPiecewise) return pl_eval(T, d, i0, w, slope, want_slope);
+  if (KIND == kTfGaussian) { i0 = 0; w = 0.f; return gauss_eval(T, d, slope, want_slope); }
+  if (EMIT) return tf_eval(T, d, i0, w, slope, want_slope);
+  float slope_tau = 0.f;
+  const float tau = tf_eval_tau(T, d, i0, w, slope_tau, want_slope);
+  if (want_slope) slope = make_float4(0.f, 0.f, 0.f, slope_tau);
+  return make_float4(0.f, 0.f, 0.f, tau);
+}
+
 // Beer-Lambert segment opacity with the invertibility clamp (field.py:587-600)
 struct Segment {
   float tau, e, ome, a;   // ome = 1 - a = max(e, EPS)
@@ -487,6 +568,33 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
 // thread, after the barrier the caller issues) the segment mode of the CTA.
 // s_info[0]: largest tau texel (bits), s_info[1]: 1 if any rgb texel is non-zero
 __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
+  if (tf.kind == kTfPiecewise) {
+    const int K = tf.count;
+    float* pos = reinterpret_cast<float*>(g_smem + 2 * K);
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+      const float* a = tf.params + 5 * i;
+      const float* b = tf.params + 5 * min(i + 1, K - 1);
+      const float span = __fsub_rn(b[0], a[0]);
+      const float inv = span > 0.f ? __frcp_rn(span) : 0.f;
+      g_smem[i] = make_float4(a[1], a[2], a[3], a[4]);
+      g_smem[K + i] = make_float4(__fsub_rn(b[1], a[1]) * inv, __fsub_rn(b[2], a[2]) * inv,
+                                  __fsub_rn(b[3], a[3]) * inv, __fsub_rn(b[4], a[4]) * inv);
+      pos[i] = a[0];
+    }
+    if (threadIdx.x == 0) { s_info[0] = 0x7f800000u; s_info[1] = 1u; }   // general segment mode
+    return;
+  }
+  if (tf.kind == kTfGaussian) {
+    const int G = tf.count;
+    for (int j = threadIdx.x; j < G; j += blockDim.x) {
+      const float* a = tf.params + 6 * j;
+      const float s2 = a[1] * a[1];
+      g_smem[j] = make_float4(a[2], a[3], a[4], a[5]);
+      g_smem[G + j] = make_float4(a[0], 1.4426950408889634f / (2.f * s2), 1.f / s2, a[1]);
+    }
+    if (threadIdx.x == 0) { s_info[0] = 0x7f800000u; s_info[1] = 1u; }
+    return;
+  }
   const float4* src = reinterpret_cast<const float4*>(tf.params);
   float2* tau = reinterpret_cast<float2*>(g_smem + 3 * tf.count);
   float mx = 0.f;
@@ -523,7 +631,7 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 
 // The march of one ray.  INSIDE: every lane of the warp has all_inside (the
 // per-sample inside test and clamps are compiled out); SEG: segment mode.
-template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT>
+template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT, int KIND>
 __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
                                           double& depth) {
@@ -543,14 +651,8 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     fetch8<CELLS>(V, c, v);
     const float d = clamp_density(INSIDE || c.inside, interp(c, v, p0, p1));
     int i0; float w;
-    float4 s;
-    if (EMIT) {
-      float4 slope;
-      s = tf_eval(TF, d, i0, w, slope, false);
-    } else {   // emission-free TF: rgb is identically 0
-      float slope_tau;
-      s = make_float4(0.f, 0.f, 0.f, tf_eval_tau(TF, d, i0, w, slope_tau, false));
-    }
+    float4 slope;
+    const float4 s = tf_sample<KIND, EMIT>(TF, d, i0, w, slope, false);
     const Segment g = segment<SEG>(s.w, dt32);
     const float Ta = __fmul_rn(T, g.a);
     if (EMIT) {
@@ -596,12 +698,18 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_kernel(VolArgs V, TfArgs
   float4 rgba;
   double S;
 #define DDVR_MARCH(SEG, INS, EM) \
-  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM>(V, TFA, G.dt32, r, tape, rgba, S)
+  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM, kTfTexture>(V, TFA, G.dt32, r, tape, rgba, S)
 #define DDVR_MARCH_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_MARCH(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_MARCH(kSegP7, INS, EM); \
   else DDVR_MARCH(kSegGen, INS, EM);
-  if (warp_inside) {
+  if (TFA.kind == kTfPiecewise) {
+    march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfPiecewise>(V, TFA, G.dt32, r, tape,
+                                                                       rgba, S);
+  } else if (TFA.kind == kTfGaussian) {
+    march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfGaussian>(V, TFA, G.dt32, r, tape,
+                                                                      rgba, S);
+  } else if (warp_inside) {
     if (emit) { DDVR_MARCH_SEG(true, true) } else { DDVR_MARCH_SEG(true, false) }
   } else {
     if (emit) { DDVR_MARCH_SEG(false, true) } else { DDVR_MARCH_SEG(false, false) }
@@ -648,13 +756,20 @@ __device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
   }
 }
 
-__device__ __forceinline__ void tf_flush_run(float4* s_tfg, int R, int run, const float4& a0,
-                                             const float4& a1) {
-  const int j1 = min(run + 1, R - 1);
-  atomicAdd(&s_tfg[run].x, a0.x); atomicAdd(&s_tfg[run].y, a0.y);
-  atomicAdd(&s_tfg[run].z, a0.z); atomicAdd(&s_tfg[run].w, a0.w);
-  atomicAdd(&s_tfg[j1].x, a1.x); atomicAdd(&s_tfg[j1].y, a1.y);
-  atomicAdd(&s_tfg[j1].z, a1.z); atomicAdd(&s_tfg[j1].w, a1.w);
+// flush of a texel / knot run into the per-CTA TF gradient (rows of `stride`
+// floats; the piecewise rows carry the knot-position gradient in column 0)
+__device__ __forceinline__ void tf_flush_run(float* s_grad, int count, int stride, int run,
+                                             const float4& a0, const float4& a1, float p0,
+                                             float p1) {
+  const int j1 = min(run + 1, count - 1);
+  float* g0 = s_grad + stride * run + (stride - 4);
+  float* g1 = s_grad + stride * j1 + (stride - 4);
+  atomicAdd(g0 + 0, a0.x); atomicAdd(g0 + 1, a0.y); atomicAdd(g0 + 2, a0.z); atomicAdd(g0 + 3, a0.w);
+  atomicAdd(g1 + 0, a1.x); atomicAdd(g1 + 1, a1.y); atomicAdd(g1 + 2, a1.z); atomicAdd(g1 + 3, a1.w);
+  if (stride == 5) {
+    atomicAdd(s_grad + stride * run, p0);
+    atomicAdd(s_grad + stride * j1, p1);
+  }
 }
 
 constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
@@ -663,18 +778,19 @@ constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
 struct AdjState {
   int run_cell, run_base, run_ox, run_oy, run_oz;   // volume cell run
   float acc8[8];
-  int tf_run;                                       // TF texel run (texels i0, i0+1)
+  int tf_run;                                       // TF texel/knot run (i0, i0+1)
   float4 tfa0, tfa1;
+  float tfp0, tfp1;                                 // knot-position gradient (piecewise)
   // camera / stepsize per-ray sums (grid units) in fp64: thousands of terms
   // with cancellation (the per-sample terms stay fp32)
   double s1x, s1y, s1z, s2x, s2y, s2z, dt_bl, dt_pos;
 };
 
 // The backward walk of one ray (renderer.py:547-626).
-template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT>
+template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND>
 __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                             const Ray& r, double S, float4 sd,
-                                            const float* __restrict__ tape, float4* s_tfg,
+                                            const float* __restrict__ tape, float* s_tfg,
                                             float* __restrict__ d_volume,
                                             float* __restrict__ d_cells, AdjState& st) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
@@ -700,14 +816,10 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const bool inside = INSIDE || c.inside;
     const float d = clamp_density(inside, raw);
     int i0; float w;
-    float4 s, slope;
-    if (EMIT) {
-      s = tf_eval(TF, d, i0, w, slope, kDhat);
-    } else {   // emission-free TF (never with the tf target): rgb and its slope are 0
-      float slope_tau = 0.f;
-      s = make_float4(0.f, 0.f, 0.f, tf_eval_tau(TF, d, i0, w, slope_tau, kDhat));
-      slope = make_float4(0.f, 0.f, 0.f, slope_tau);
-    }
+    float4 slope;
+    // (emission-free tables never serve the tf target: rgb and its slope are 0)
+    const float4 s = tf_sample<KIND, EMIT>(TF, d, i0, w, slope,
+                                           kDhat || (kTf && KIND != kTfTexture));
     const Segment g = segment<SEG>(s.w, dt32);
 
     // Invert the compositing step (renderer.py:579, a_prev = (a - A)/(a - 1)).
@@ -736,16 +848,39 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const float tau_hat = s.w < 0.f ? 0.f : dt32 * ea;
     if (kStep) st.dt_bl += (double)(g.tau * ea);
 
-    if (kTf) {   // renderer.py:602-604: texels i0 and i0+1 with weights (1-w), w
+    if (kTf && KIND == kTfGaussian) {   // every component: d out/d(mu, sigma, rgba)
+      const float4* rgba = g_smem;
+      const float4* prm = g_smem + TF.count;
+      for (int j = 0; j < TF.count; ++j) {
+        const float4 q = prm[j];
+        const float4 cj = rgba[j];
+        const float z = __fsub_rn(d, q.x);
+        float gj;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gj) : "f"(-(z * z) * q.y));
+        const float proj = h0 * cj.x + h1 * cj.y + h2 * cj.z + tau_hat * cj.w;
+        float* gr = s_tfg + 6 * j;
+        atomicAdd(gr + 0, gj * z * q.z * proj);
+        atomicAdd(gr + 1, gj * z * z * q.z / q.w * proj);
+        atomicAdd(gr + 2, gj * h0); atomicAdd(gr + 3, gj * h1);
+        atomicAdd(gr + 4, gj * h2); atomicAdd(gr + 5, gj * tau_hat);
+      }
+    } else if (kTf) {   // renderer.py:602-604: texels/knots i0, i0+1 with weights (1-w), w
       if (i0 != st.tf_run) {
-        if (st.tf_run >= 0) tf_flush_run(s_tfg, TF.count, st.tf_run, st.tfa0, st.tfa1);
+        if (st.tf_run >= 0)
+          tf_flush_run(s_tfg, TF.count, TF.stride, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
         st.tf_run = i0;
         st.tfa0 = make_float4(0, 0, 0, 0);
         st.tfa1 = make_float4(0, 0, 0, 0);
+        st.tfp0 = st.tfp1 = 0.f;
       }
       const float w0 = 1.f - w;
       st.tfa0.x += w0 * h0; st.tfa0.y += w0 * h1; st.tfa0.z += w0 * h2; st.tfa0.w += w0 * tau_hat;
       st.tfa1.x += w * h0;  st.tfa1.y += w * h1;  st.tfa1.z += w * h2;  st.tfa1.w += w * tau_hat;
+      if (KIND == kTfPiecewise) {   // d out/d pos_k = slope (w - 1), d out/d pos_k+1 = -slope w
+        const float dh = slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat;
+        st.tfp0 += dh * (w - 1.f);
+        st.tfp1 -= dh * w;
+      }
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
@@ -809,13 +944,15 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   __shared__ Frame F;
   __shared__ double s_red[kWarps][3];
   __shared__ unsigned s_info[2];
-  float4* s_tfg = g_smem + 2 * TFA.count;       // [R] TF gradient after the pair table
+  // per-CTA TF gradient (count x stride floats) after the kind's table
+  float* s_tfg = reinterpret_cast<float*>(g_smem) +
+                 (TFA.kind == kTfTexture ? 8 : TFA.kind == kTfPiecewise ? 9 : 8) * TFA.count;
   const int view = blockIdx.z;
   if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
   __syncthreads();
   load_tf(TFA, s_info);
   if (kTf)
-    for (int i = threadIdx.x; i < TFA.count; i += blockDim.x) s_tfg[i] = make_float4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < TFA.count * TFA.stride; i += blockDim.x) s_tfg[i] = 0.f;
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
   __syncthreads();
   const int mode = seg_mode(G.dt32, s_info[0]);
@@ -850,16 +987,23 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   st.tf_run = -1;
   st.tfa0 = make_float4(0, 0, 0, 0);
   st.tfa1 = make_float4(0, 0, 0, 0);
+  st.tfp0 = st.tfp1 = 0.f;
   st.s1x = st.s1y = st.s1z = st.s2x = st.s2y = st.s2z = st.dt_bl = st.dt_pos = 0.0;
 
-#define DDVR_WALK(SEG, INS, EM)                                                          \
-  adjoint_ray<MASK, CELLS, SEG, INS, EM>(V, TFA, G.dt32, r, S, sd, tape, s_tfg, d_volume, \
-                                         d_cells, st)
+#define DDVR_WALK(SEG, INS, EM)                                                         \
+  adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture>(V, TFA, G.dt32, r, S, sd, tape, s_tfg, \
+                                                     d_volume, d_cells, st)
 #define DDVR_WALK_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_WALK(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_WALK(kSegP7, INS, EM); \
   else DDVR_WALK(kSegGen, INS, EM);
-  if (warp_inside) {
+  if (TFA.kind == kTfPiecewise) {
+    adjoint_ray<MASK, CELLS, kSegGen, false, true, kTfPiecewise>(V, TFA, G.dt32, r, S, sd, tape,
+                                                                 s_tfg, d_volume, d_cells, st);
+  } else if (TFA.kind == kTfGaussian) {
+    adjoint_ray<MASK, CELLS, kSegGen, false, true, kTfGaussian>(V, TFA, G.dt32, r, S, sd, tape,
+                                                                s_tfg, d_volume, d_cells, st);
+  } else if (warp_inside) {
     if (emit) { DDVR_WALK_SEG(true, true) }
     else if (!kTf) { DDVR_WALK_SEG(true, kTf) }   // kTf: never taken (EMIT=true re-use)
   } else {
@@ -874,14 +1018,12 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                       st.run_oz, st.acc8);
   if (kTf) {
-    if (st.tf_run >= 0) tf_flush_run(s_tfg, TFA.count, st.tf_run, st.tfa0, st.tfa1);
+    if (st.tf_run >= 0)
+      tf_flush_run(s_tfg, TFA.count, TFA.stride, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
     __syncthreads();
-    for (int k = threadIdx.x; k < TFA.count; k += blockDim.x) {
-      const float4 g = s_tfg[k];
-      if (g.x != 0.f) atomicAdd(d_tf + 4 * k + 0, (double)g.x);
-      if (g.y != 0.f) atomicAdd(d_tf + 4 * k + 1, (double)g.y);
-      if (g.z != 0.f) atomicAdd(d_tf + 4 * k + 2, (double)g.z);
-      if (g.w != 0.f) atomicAdd(d_tf + 4 * k + 3, (double)g.w);
+    for (int k = threadIdx.x; k < TFA.count * TFA.stride; k += blockDim.x) {
+      const float g = s_tfg[k];
+      if (g != 0.f) atomicAdd(d_tf + k, (double)g);
     }
   }
   if (kPos) {
@@ -1099,15 +1241,25 @@ int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
 
 int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
   if (!tf) return set_error(DDVR_INVALID_PARAMETER, "transfer function descriptor is NULL");
-  if (tf->kind != DDVR_TF_TEXTURE)
+  if (tf->kind != DDVR_TF_TEXTURE && tf->kind != DDVR_TF_PIECEWISE &&
+      tf->kind != DDVR_TF_GAUSSIAN)
     return set_error(DDVR_UNSUPPORTED, "transfer-function kind %d is not built", tf->kind);
+  const int stride = tf->kind == DDVR_TF_TEXTURE ? 4 : tf->kind == DDVR_TF_PIECEWISE ? 5 : 6;
   if (tf->count < 1)
-    return set_error(DDVR_INVALID_PARAMETER, "transfer function must have shape (R, 4), R >= 1");
+    return set_error(DDVR_INVALID_PARAMETER,
+                     "transfer function must have shape (R, %d), R >= 1", stride);
   if (!tf->params) return set_error(DDVR_INVALID_INPUT, "transfer function pointer is NULL");
-  if (((uintptr_t)tf->params & 15) != 0)
-    return set_error(DDVR_INVALID_INPUT, "transfer function must be 16-byte aligned");
-  // shared layout (see g_smem): 2R pair float4 + R gradient float4 + ceil(R/2) tau-pair float4
-  smem_per_table = (3 * (size_t)tf->count + ((size_t)tf->count + 1) / 2) * sizeof(float4);
+  if (((uintptr_t)tf->params & (tf->kind == DDVR_TF_TEXTURE ? 15 : 3)) != 0)
+    return set_error(DDVR_INVALID_INPUT, "transfer function parameters are misaligned");
+  const size_t n = (size_t)tf->count;
+  // shared layouts (see g_smem / pl_eval / gauss_eval), gradient rows included:
+  //   texture   2n pair float4 + n gradient float4 + ceil(n/2) tau-pair float4
+  //   piecewise 2n float4 + n pos floats (pad to 9n floats) + 5n gradient floats
+  //   gaussian  2n float4 + 6n gradient floats
+  smem_per_table = tf->kind == DDVR_TF_TEXTURE ? (3 * n + (n + 1) / 2) * sizeof(float4)
+                   : tf->kind == DDVR_TF_PIECEWISE ? (9 * n + 5 * n) * sizeof(float)
+                                                   : (8 * n + 6 * n) * sizeof(float);
+  A.stride = stride;
   if (smem_per_table > (size_t)kMaxTfBytes)
     return set_error(DDVR_UNSUPPORTED, "transfer function resolution %d exceeds %d texels",
                      tf->count, kMaxTfBytes / 56);

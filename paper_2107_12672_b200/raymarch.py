@@ -24,6 +24,13 @@ from .errors import InvalidInputError, InvalidParameterError
 EPS_POLE_DEG = 1e-3    # field.py:24
 
 
+# transfer-function representation by parameter-row width:
+#   (R, 4) texel table [r, g, b, tau]           (field.py:540-549)
+#   (K, 5) piecewise-linear knots [pos, r, g, b, tau]   (no reference implementation)
+#   (G, 6) Gaussians [mu, sigma, r, g, b, tau]          (tasks.py:751-766 optical model)
+TF_KINDS = {4: N.TF_TEXTURE, 5: N.TF_PIECEWISE, 6: N.TF_GAUSSIAN}
+
+
 @dataclass(frozen=True)
 class Rig:
     """Static geometry shared by every view of a batch.
@@ -92,9 +99,13 @@ def validate_cameras(lonlat, radius, fov_y_deg):
 
 def _descs(density, texels, rig: Rig, dt: float, early_stop: bool, cells=None):
     _require(density, "density", torch.float32, ndim=3)
-    _require(texels, "texels", torch.float32, ndim=2, align16=True)
-    if texels.shape[1] != 4:
-        raise InvalidParameterError("transfer function must have shape (R, 4), R >= 1")
+    _require(texels, "texels", torch.float32, ndim=2)
+    kind = TF_KINDS.get(int(texels.shape[1]))
+    if kind is None or texels.shape[0] < 1:
+        raise InvalidParameterError("transfer function must have shape (R, 4) texels, "
+                                    "(K, 5) piecewise knots or (G, 6) Gaussians")
+    if kind == N.TF_TEXTURE and texels.data_ptr() % 16:
+        raise InvalidInputError("texels must be 16-byte aligned")
     if cells is not None:
         _require(cells, "cells", torch.float32)
         if cells.data_ptr() % 32 or cells.numel() != cells_numel(density.shape):
@@ -102,7 +113,7 @@ def _descs(density, texels, rig: Rig, dt: float, early_stop: bool, cells=None):
     vol = N.DdvrVolume(density.data_ptr(), (ctypes.c_int32 * 3)(*density.shape),
                        (ctypes.c_double * 3)(*rig.box_min), (ctypes.c_double * 3)(*rig.box_max),
                        cells.data_ptr() if cells is not None else None)
-    tf = N.DdvrTf(N.TF_TEXTURE, texels.shape[0], texels.data_ptr())
+    tf = N.DdvrTf(kind, texels.shape[0], texels.data_ptr())
     r0, r1 = rig.band
     prm = N.DdvrParams(float(dt), rig.width, rig.height, r0, r1, 1 if early_stop else 0, 0,
                        None, 0)

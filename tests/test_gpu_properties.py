@@ -203,3 +203,55 @@ def test_inversion_matches_stored_on_saturating_rays(cuda):
         out[mode] = (d, dtf)
     for a, b in zip(out["inversion"], out["stored"]):
         assert float((a - b).norm() / b.norm()) <= 1e-4
+
+
+@pytest.mark.parametrize("kind", ["piecewise", "gaussian", "piecewise_uniform"])
+def test_analytic_tf_modes_match_oracle(cuda, kind):
+    """Piecewise-linear (K,5) and Gaussian (G,6) TFs: forward + every gradient vs the oracle."""
+    torch = _t()
+    from oracle import dvr_oracle as O
+    from paper_2107_12672_b200 import raymarch as R
+    rng = np.random.default_rng(21)
+    vol = rng.uniform(0.05, 0.95, (9, 8, 10)).astype(np.float32)
+    if kind == "gaussian":
+        G = 3
+        params = np.column_stack([rng.uniform(0.2, 0.8, G), rng.uniform(0.08, 0.3, G),
+                                  rng.uniform(0.1, 1.0, (G, 3)), rng.uniform(0.5, 4.0, G)])
+        tf_o = O.GaussianTF(params.astype(np.float32).astype(np.float64))
+    else:
+        K = 7
+        pos = (np.arange(K) + 0.5) / K if kind == "piecewise_uniform" else \
+            np.sort(rng.uniform(0.05, 0.95, K))
+        params = np.column_stack([pos, rng.uniform(0.05, 1, (K, 3)), rng.uniform(0.3, 2.0, K)])
+        tf_o = O.PiecewiseTF(params.astype(np.float32).astype(np.float64))
+    params = params.astype(np.float32)
+    view = O.View(50.0, -20.0, 2.2, fov_y_deg=35.0, width=10, height=9)
+    dt = 0.05
+    seed = rng.normal(size=(9, 10, 4))
+    g = O.Grid(vol.astype(np.float64))
+    img_o = O.render_view(g, tf_o, view, dt)
+    ref = O.adjoint_view(g, tf_o, view, dt, seed, ["tf", "volume", "camera", "stepsize"],
+                         image=img_o)
+    dens = torch.from_numpy(vol).to(cuda)
+    tx = torch.from_numpy(params).to(cuda).contiguous()
+    cams = R.camera_array(torch.tensor([[50.0, -20.0]], dtype=torch.float64, device=cuda), 2.2,
+                          (0.0, 0.0, 0.0), 35.0)
+    rig = R.Rig(10, 9)
+    for cells in (R.pack_cells(dens), None):
+        img, depth = R.forward(dens, tx, cams, dt, rig, cells=cells)
+        assert rel_l2(img[0].cpu().numpy(), img_o) <= 1e-5, kind
+        d = {"volume": torch.zeros_like(dens),
+             "tf": torch.zeros(tx.shape, dtype=torch.float64, device=cuda),
+             "camera": torch.zeros(1, 2, dtype=torch.float64, device=cuda),
+             "stepsize": torch.zeros(1, dtype=torch.float64, device=cuda)}
+        R.adjoint(dens, tx, cams, dt, rig, img, depth,
+                  torch.from_numpy(seed.astype(np.float32)).to(cuda)[None].contiguous(), 15,
+                  d_volume=d["volume"], d_tf=d["tf"], d_camera=d["camera"], d_dt=d["stepsize"],
+                  cells=cells)
+        for k, v in d.items():
+            r_ = np.asarray(ref["d_" + k], np.float64)
+            assert rel_l2(v.double().cpu().numpy().reshape(r_.shape), r_) <= 1e-4, (kind, k)
+    if kind == "piecewise_uniform":   # equals the texel table on the GPU too
+        tex = torch.from_numpy(params[:, 1:].copy()).to(cuda)
+        img_t, _ = R.forward(dens, tex, cams, dt, rig)
+        assert rel_l2(img.cpu().numpy(), img_t.cpu().numpy()) <= 1e-6
