@@ -325,6 +325,17 @@ __device__ __forceinline__ void ld256(const float* p, float v[8]) {
                : "l"(p));
 }
 
+// predicated 128-bit vector red: no branch around it (the cell-run flush of
+// the adjoint would otherwise be a divergent branch taken on most iterations)
+__device__ __forceinline__ void red128_if(bool pred, float* p, float a, float b, float c,
+                                          float d) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
+      "@q red.global.add.v4.f32 [%1], {%2,%3,%4,%5};\n\t}" ::"r"((int)pred),
+      "l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+      : "memory");
+}
+
 __device__ __forceinline__ void red128(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
                "f"(d)
@@ -787,7 +798,7 @@ struct AdjState {
 };
 
 // The backward walk of one ray (renderer.py:547-626).
-template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND>
+template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND, bool TAPE>
 __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                             const Ray& r, double S, float4 sd,
                                             const float* __restrict__ tape, float* s_tfg,
@@ -828,19 +839,21 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     // steps) and T_prev = exp(-S_prev) is computed fresh each step.  The fp32
     // chain T_prev = T/(1 - a) drifts to ~1e-4 on camera gradients by 2.6k steps.
     // ("stored" mode reads T_prev from the tape instead, renderer.py:576-577)
-    S -= (double)g.od;
     float Tp;
-    if (tape) {
+    if (TAPE) {
       Tp = tape[i];
     } else {
+      S -= (double)g.od;
       asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(Tp) : "f"((float)S * -1.4426950408889634f));
     }
 
-    // blend adjoint (renderer.py:583-589)
-    const float cdot = s.x * sd.x + s.y * sd.y + s.z * sd.z;
+    // blend adjoint (renderer.py:583-589); emission-free: the rgb terms are 0
+    const float cdot = EMIT ? s.x * sd.x + s.y * sd.y + s.z * sd.z : 0.f;
     const float seg_a_hat = Tp * (a_hat + cdot);
     const float aT = g.a * Tp;
-    const float h0 = aT * sd.x, h1 = aT * sd.y, h2 = aT * sd.z;   // d L / d rgb
+    const float h0 = EMIT ? aT * sd.x : 0.f;   // d L / d rgb
+    const float h1 = EMIT ? aT * sd.y : 0.f;
+    const float h2 = EMIT ? aT * sd.z : 0.f;
     a_hat = g.ome * a_hat - g.a * cdot;
     // Beer-Lambert adjoint (renderer.py:592-596)
     const float a_raw_hat = g.a_clamped ? 0.f : seg_a_hat;
@@ -884,9 +897,29 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
-      const float d_hat = slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat;
+      const float d_hat = EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
+                               : slope.w * tau_hat;
       const bool live = inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
-      if (kVol) {   // renderer.py:607-608, accumulated per cell run
+      if (kVol && CELLS) {   // renderer.py:607-608, accumulated per cell run
+        // branch-free: flush the finished run with predicated vector reds,
+        // restart the accumulators by scaling them with 0
+        const float dh = live ? d_hat : 0.f;
+        const float z0 = dh * (1.f - c.fz), z1 = dh * c.fz;
+        const float y00 = z0 * (1.f - c.fy), y10 = z0 * c.fy;
+        const float y01 = z1 * (1.f - c.fy), y11 = z1 * c.fy;
+        const float ex = 1.f - c.fx;
+        const bool fresh = c.cell != st.run_cell;
+        const bool flush = fresh && st.run_cell != kNoRun;
+        float* q = d_cells + 8 * (long long)(flush ? st.run_cell : 0);
+        red128_if(flush, q, st.acc8[0], st.acc8[1], st.acc8[2], st.acc8[3]);
+        red128_if(flush, q + 4, st.acc8[4], st.acc8[5], st.acc8[6], st.acc8[7]);
+        const float keep = fresh ? 0.f : 1.f;
+        st.acc8[0] = fmaf(st.acc8[0], keep, y00 * ex); st.acc8[1] = fmaf(st.acc8[1], keep, y00 * c.fx);
+        st.acc8[2] = fmaf(st.acc8[2], keep, y10 * ex); st.acc8[3] = fmaf(st.acc8[3], keep, y10 * c.fx);
+        st.acc8[4] = fmaf(st.acc8[4], keep, y01 * ex); st.acc8[5] = fmaf(st.acc8[5], keep, y01 * c.fx);
+        st.acc8[6] = fmaf(st.acc8[6], keep, y11 * ex); st.acc8[7] = fmaf(st.acc8[7], keep, y11 * c.fx);
+        st.run_cell = c.cell;
+      } else if (kVol) {
         if (c.cell != st.run_cell) {
           if (st.run_cell != kNoRun)
             flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
@@ -990,19 +1023,25 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   st.tfp0 = st.tfp1 = 0.f;
   st.s1x = st.s1y = st.s1z = st.s2x = st.s2y = st.s2z = st.dt_bl = st.dt_pos = 0.0;
 
-#define DDVR_WALK(SEG, INS, EM)                                                         \
-  adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture>(V, TFA, G.dt32, r, S, sd, tape, s_tfg, \
-                                                     d_volume, d_cells, st)
+#define DDVR_WALK(SEG, INS, EM)                                                          \
+  adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture, false>(V, TFA, G.dt32, r, S, sd, tape, \
+                                                            s_tfg, d_volume, d_cells, st)
 #define DDVR_WALK_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_WALK(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_WALK(kSegP7, INS, EM); \
   else DDVR_WALK(kSegGen, INS, EM);
-  if (TFA.kind == kTfPiecewise) {
-    adjoint_ray<MASK, CELLS, kSegGen, false, true, kTfPiecewise>(V, TFA, G.dt32, r, S, sd, tape,
-                                                                 s_tfg, d_volume, d_cells, st);
+  // stored mode (tape) and the analytic TFs take the general variant
+#define DDVR_WALK_GEN(KIND, TP)                                                           \
+  adjoint_ray<MASK, CELLS, kSegGen, false, true, KIND, TP>(V, TFA, G.dt32, r, S, sd, tape, \
+                                                           s_tfg, d_volume, d_cells, st)
+  if (G.tape) {
+    if (TFA.kind == kTfPiecewise) DDVR_WALK_GEN(kTfPiecewise, true);
+    else if (TFA.kind == kTfGaussian) DDVR_WALK_GEN(kTfGaussian, true);
+    else DDVR_WALK_GEN(kTfTexture, true);
+  } else if (TFA.kind == kTfPiecewise) {
+    DDVR_WALK_GEN(kTfPiecewise, false);
   } else if (TFA.kind == kTfGaussian) {
-    adjoint_ray<MASK, CELLS, kSegGen, false, true, kTfGaussian>(V, TFA, G.dt32, r, S, sd, tape,
-                                                                s_tfg, d_volume, d_cells, st);
+    DDVR_WALK_GEN(kTfGaussian, false);
   } else if (warp_inside) {
     if (emit) { DDVR_WALK_SEG(true, true) }
     else if (!kTf) { DDVR_WALK_SEG(true, kTf) }   // kTf: never taken (EMIT=true re-use)
@@ -1011,6 +1050,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     else if (!kTf) { DDVR_WALK_SEG(false, kTf) }
   }
 #undef DDVR_WALK_SEG
+#undef DDVR_WALK_GEN
 #undef DDVR_WALK
 
   // ---- flush per-ray accumulators ----
