@@ -381,32 +381,44 @@ __device__ __forceinline__ float clamp_density(bool inside, float raw) {
 // transfer functions (field.py:525-579; renderer.py:472-488)
 // ---------------------------------------------------------------------------
 
-// Dynamic shared memory of every kernel (R = TF texels):
-//   g_smem[0, 2R)        the TF as (texel k, texel k+1 - texel k) float4 pairs
-//   g_smem[2R, 3R)       the per-CTA TF gradient (adjoint, tf target)
-//   g_smem[3R, ...)      (tau_k, tau_k+1 - tau_k) float2 pairs: the table of an
+// Dynamic shared memory of every kernel (R = TF texels; float offsets):
+//   [0, 8(R+1))          the TF as (texel, next texel - texel) float4 pairs with
+//                        guard entries at both ends (see texel_coord)
+//   [8(R+1), 12R+8)      the per-CTA TF gradient (adjoint, tf target)
+//   [12R+8, 14R+10)      (tau, next tau - tau) float2 pairs: the table of an
 //                        emission-free TF (rgb texels all zero, e.g. the
 //                        absorption ramp of tasks.py:348-356), one 64-bit load
+// (piecewise / Gaussian TFs use their own layouts, see pl_eval / gauss_eval)
 // A file-scope symbol keeps loads in the shared window (no generic->shared
 // conversion per access).
 extern __shared__ float4 g_smem[];
 
+// Texel tables carry guard entries: entry e = i + 1 for texel coordinate
+// i in [-1, R-1], where entries 0 and R are clones of texels 0 and R-1 with a
+// zero delta.  Clamp-to-edge (field.py:543-548) and the zero slope of the
+// clamp bands (field.py:575-576) are then baked into the table: i = floor(t),
+// w = t - i, no clamps and no live test.  (Only the measure-zero point
+// t = R-1 exactly differs: the reference takes the left interval's slope.)
+// Float offsets: pairs [0, 8(R+1)), TF gradient [8(R+1), 12R+8),
+// tau pairs [12R+8, 14R+10).
 __device__ __forceinline__ const float2* tau_table(const TfArgs& T) {
-  return reinterpret_cast<const float2*>(g_smem + 3 * T.count);
+  return reinterpret_cast<const float2*>(g_smem) + (6 * T.count + 4);
+}
+
+// texel coordinate i = floor(d R - 1/2) in [-1, R-1] (d in [0, 1]) and weight w
+__device__ __forceinline__ int texel_coord(const TfArgs& T, float d, float& w) {
+  const float t = __fmaf_rn(d, T.fR, -0.5f);
+  const float fl = floorf(t);
+  w = __fsub_rn(t, fl);
+  return (int)fl;
 }
 
 // tau-only lookup of an emission-free TF (same arithmetic as tf_eval's w channel)
 __device__ __forceinline__ float tf_eval_tau(const TfArgs& T, float d, int& i0, float& w,
                                              float& slope_tau, bool want_slope) {
-  const float t = __fsub_rn(__fmul_rn(d, T.fR), 0.5f);
-  const float f = fminf(fmaxf(t, 0.f), T.fR1);
-  i0 = min((int)f, T.Rm2);
-  w = __fsub_rn(f, (float)i0);
-  const float2 q = tau_table(T)[i0];
-  if (want_slope) {
-    const bool live = t >= 0.f && t <= T.fR1;
-    slope_tau = q.y * (live ? T.fR : 0.f);
-  }
+  i0 = texel_coord(T, d, w);
+  const float2 q = tau_table(T)[i0 + 1];
+  if (want_slope) slope_tau = q.y * T.fR;
   return __fmaf_rn(w, q.y, q.x);
 }
 
@@ -414,17 +426,11 @@ __device__ __forceinline__ float tf_eval_tau(const TfArgs& T, float d, int& i0, 
 // (field.py:540-549); fR, fR1, Rm2 are precomputed on the host (TfArgs)
 __device__ __forceinline__ float4 tf_eval(const TfArgs& T, float d, int& i0, float& w,
                                           float4& slope, bool want_slope) {
-  const float t = __fsub_rn(__fmul_rn(d, T.fR), 0.5f);
-  const float f = fminf(fmaxf(t, 0.f), T.fR1);
-  i0 = min((int)f, T.Rm2);
-  w = __fsub_rn(f, (float)i0);
-  const float4 a = g_smem[2 * i0];
-  const float4 dlt = g_smem[2 * i0 + 1];
-  if (want_slope) {   // field.py:575-576: zero in the clamp bands
-    const bool live = t >= 0.f && t <= T.fR1;
-    const float sc = live ? T.fR : 0.f;
-    slope = make_float4(dlt.x * sc, dlt.y * sc, dlt.z * sc, dlt.w * sc);
-  }
+  i0 = texel_coord(T, d, w);
+  const float4 a = g_smem[2 * i0 + 2];
+  const float4 dlt = g_smem[2 * i0 + 3];
+  if (want_slope)   // guard entries have dlt = 0: the clamp bands' zero slope
+    slope = make_float4(dlt.x * T.fR, dlt.y * T.fR, dlt.z * T.fR, dlt.w * T.fR);
   return make_float4(__fmaf_rn(w, dlt.x, a.x), __fmaf_rn(w, dlt.y, a.y),
                      __fmaf_rn(w, dlt.z, a.z), __fmaf_rn(w, dlt.w, a.w));
 }
@@ -607,16 +613,16 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
     return;
   }
   const float4* src = reinterpret_cast<const float4*>(tf.params);
-  float2* tau = reinterpret_cast<float2*>(g_smem + 3 * tf.count);
+  float2* tau = reinterpret_cast<float2*>(g_smem) + (6 * tf.count + 4);
   float mx = 0.f;
   bool rgb = false;
-  for (int i = threadIdx.x; i < tf.count; i += blockDim.x) {
-    const float4 a = src[i];
-    const float4 b = src[min(i + 1, tf.count - 1)];
-    g_smem[2 * i] = a;
-    g_smem[2 * i + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
+  for (int e = threadIdx.x; e <= tf.count; e += blockDim.x) {   // guard entries 0 and R
+    const float4 a = src[min(max(e - 1, 0), tf.count - 1)];
+    const float4 b = src[min(e, tf.count - 1)];
+    g_smem[2 * e] = a;
+    g_smem[2 * e + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
                                     __fsub_rn(b.z, a.z), __fsub_rn(b.w, a.w));
-    tau[i] = make_float2(a.w, __fsub_rn(b.w, a.w));
+    tau[e] = make_float2(a.w, __fsub_rn(b.w, a.w));
     mx = fmaxf(mx, a.w);   // interpolated tau never exceeds the largest texel
     rgb |= a.x != 0.f || a.y != 0.f || a.z != 0.f;
   }
@@ -769,16 +775,18 @@ __device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
 
 // flush of a texel / knot run into the per-CTA TF gradient (rows of `stride`
 // floats; the piecewise rows carry the knot-position gradient in column 0)
+// (texel runs start at the guard coordinate -1, which maps onto texel 0)
 __device__ __forceinline__ void tf_flush_run(float* s_grad, int count, int stride, int run,
                                              const float4& a0, const float4& a1, float p0,
                                              float p1) {
+  const int j0 = max(run, 0);
   const int j1 = min(run + 1, count - 1);
-  float* g0 = s_grad + stride * run + (stride - 4);
+  float* g0 = s_grad + stride * j0 + (stride - 4);
   float* g1 = s_grad + stride * j1 + (stride - 4);
   atomicAdd(g0 + 0, a0.x); atomicAdd(g0 + 1, a0.y); atomicAdd(g0 + 2, a0.z); atomicAdd(g0 + 3, a0.w);
   atomicAdd(g1 + 0, a1.x); atomicAdd(g1 + 1, a1.y); atomicAdd(g1 + 2, a1.z); atomicAdd(g1 + 3, a1.w);
   if (stride == 5) {
-    atomicAdd(s_grad + stride * run, p0);
+    atomicAdd(s_grad + stride * j0, p0);
     atomicAdd(s_grad + stride * j1, p1);
   }
 }
@@ -879,7 +887,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       }
     } else if (kTf) {   // renderer.py:602-604: texels/knots i0, i0+1 with weights (1-w), w
       if (i0 != st.tf_run) {
-        if (st.tf_run >= 0)
+        if (st.tf_run != kNoRun)
           tf_flush_run(s_tfg, TF.count, TF.stride, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
         st.tf_run = i0;
         st.tfa0 = make_float4(0, 0, 0, 0);
@@ -979,7 +987,8 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   __shared__ unsigned s_info[2];
   // per-CTA TF gradient (count x stride floats) after the kind's table
   float* s_tfg = reinterpret_cast<float*>(g_smem) +
-                 (TFA.kind == kTfTexture ? 8 : TFA.kind == kTfPiecewise ? 9 : 8) * TFA.count;
+                 (TFA.kind == kTfTexture ? 8 * TFA.count + 8
+                                         : (TFA.kind == kTfPiecewise ? 9 : 8) * TFA.count);
   const int view = blockIdx.z;
   if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
   __syncthreads();
@@ -1017,7 +1026,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   st.run_cell = kNoRun; st.run_base = 0; st.run_ox = 0; st.run_oy = 0; st.run_oz = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) st.acc8[k] = 0.f;
-  st.tf_run = -1;
+  st.tf_run = kNoRun;
   st.tfa0 = make_float4(0, 0, 0, 0);
   st.tfa1 = make_float4(0, 0, 0, 0);
   st.tfp0 = st.tfp1 = 0.f;
@@ -1058,7 +1067,7 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                       st.run_oz, st.acc8);
   if (kTf) {
-    if (st.tf_run >= 0)
+    if (st.tf_run != kNoRun)
       tf_flush_run(s_tfg, TFA.count, TFA.stride, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
     __syncthreads();
     for (int k = threadIdx.x; k < TFA.count * TFA.stride; k += blockDim.x) {
@@ -1293,10 +1302,10 @@ int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
     return set_error(DDVR_INVALID_INPUT, "transfer function parameters are misaligned");
   const size_t n = (size_t)tf->count;
   // shared layouts (see g_smem / pl_eval / gauss_eval), gradient rows included:
-  //   texture   2n pair float4 + n gradient float4 + ceil(n/2) tau-pair float4
+  //   texture   2(n+1) pair float4 + 4n gradient floats + (n+1) tau-pair float2
   //   piecewise 2n float4 + n pos floats (pad to 9n floats) + 5n gradient floats
   //   gaussian  2n float4 + 6n gradient floats
-  smem_per_table = tf->kind == DDVR_TF_TEXTURE ? (3 * n + (n + 1) / 2) * sizeof(float4)
+  smem_per_table = tf->kind == DDVR_TF_TEXTURE ? (14 * n + 10) * sizeof(float)
                    : tf->kind == DDVR_TF_PIECEWISE ? (9 * n + 5 * n) * sizeof(float)
                                                    : (8 * n + 6 * n) * sizeof(float);
   A.stride = stride;
