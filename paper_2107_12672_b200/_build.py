@@ -1,50 +1,71 @@
-"""In-tree build of libddvr.so for sm_100a (nvcc cross-compiles without a GPU)."""
+"""In-tree build of libddvr.so for sm_100a (nvcc cross-compiles without a GPU).
+
+The kernels are split over several translation units (csrc/ddvr_*.cu sharing
+csrc/ddvr_device.cuh) that compile in parallel and link into one shared
+library with the static CUDA runtime.
+"""
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "ddvr.cu")
+CSRC = os.path.join(HERE, "csrc")
 HDR = os.path.join(ROOT, "include", "ddvr.h")
 OUT = os.path.join(HERE, "libddvr.so")
+OBJ = os.path.join(ROOT, "build", "ddvr")
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-Xptxas", "-v",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 
 
 def nvcc() -> str:
-    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
-        if cand and (os.path.sep not in cand or os.path.exists(cand)):
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
             return cand
     return "nvcc"
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
 def stale() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    return any(os.path.getmtime(p) > t for p in (SRC, HDR, __file__))
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [HDR, __file__]
+    return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/ddvr.cu into libddvr.so next to this file; return its path."""
-    if not force and not stale():
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", SRC]
+def _run(cmd):
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
         raise RuntimeError(f"nvcc failed ({proc.returncode}): {' '.join(cmd)}")
+    return proc.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into libddvr.so next to this file; return its path."""
+    if not force and not stale():
+        return OUT
+    os.makedirs(OBJ, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    jobs = []
+    for src in sources():
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        jobs.append((obj, [nvcc(), *NVCC_FLAGS, "-Xptxas", "-v", *inc, "-c", "-o", obj, src]))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        logs = list(ex.map(lambda j: _run(j[1]), jobs))
     if verbose:
-        sys.stderr.write(proc.stderr)
+        sys.stderr.write("".join(logs))
+    _run([nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *[o for o, _ in jobs]])
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -1,4 +1,9 @@
-// ddvr.cu -- B200 (sm_100a) kernels and the C ABI of include/ddvr.h.
+#pragma once
+// ddvr_device.cuh -- device code shared by the libddvr translation units.
+//
+// (ddvr_abi.cu: C ABI + small kernels; ddvr_fwd.cu: forward instantiations;
+//  ddvr_adj_*.cu: adjoint instantiations.  Split only to compile in parallel.)
+//
 //
 // Differentiable emission-absorption raymarcher (DiffDVR, arXiv 2107.12672),
 // written for Blackwell from scratch.  The reference (voldiff, pure NumPy) is
@@ -41,7 +46,8 @@
 
 #include "ddvr.h"
 
-namespace {
+namespace ddvr_impl {
+
 
 constexpr float kEpsAlpha = 1e-6f;          // field.py:25 (EPS_ALPHA)
 constexpr float kAlphaStop = 1.f - 1e-4f;   // ALPHA_STOP (renderer.py:45)
@@ -61,25 +67,6 @@ constexpr int kMaxTfBytes = 200 * 1024;     // TF tables + TF gradient in shared
 // backward positions bitwise identical to the forward's (g -= step).
 constexpr double kFix = 4294967296.0;                  // 2^32
 constexpr float kInvFix = 2.3283064365386963e-10f;     // 2^-32
-
-thread_local char g_err[1024] = "";
-std::atomic<int64_t> g_launches{0};
-
-int set_error(int code, const char* fmt, ...) {
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(g_err, sizeof(g_err), fmt, ap);
-  va_end(ap);
-  return code;
-}
-
-int check_launch(const char* what) {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess)
-    return set_error(DDVR_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return DDVR_OK;
-}
 
 // ---------------------------------------------------------------------------
 // kernel-side argument blocks (passed by value)
@@ -115,6 +102,32 @@ struct Geometry {
   float* tape;            // stored memory mode (nullable)
   long long tape_stride;
 };
+
+// Launchers with external linkage: each is defined (with its kernel
+// instantiations) in one translation unit.
+void launch_forward(bool early, bool cells, bool tape, dim3 grid, size_t smem, cudaStream_t st,
+                    const VolArgs& V, const TfArgs& T, const Geometry& G, float* image,
+                    float* depth);
+#define DDVR_ADJ_LAUNCHER(NAME)                                                              \
+  void NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
+            const VolArgs& V, const TfArgs& T, const Geometry& G, const float* image,       \
+            const float* depth, const float* seed, float* dv, float* dcells, double* dtf,   \
+            double* dcam, double* ddt)
+DDVR_ADJ_LAUNCHER(launch_adjoint_g0);   // masks 1-3   (camera / stepsize)
+DDVR_ADJ_LAUNCHER(launch_adjoint_g1);   // masks 4-7   (tf [+ camera / stepsize])
+DDVR_ADJ_LAUNCHER(launch_adjoint_g2);   // masks 8-11  (volume [+ camera / stepsize])
+DDVR_ADJ_LAUNCHER(launch_adjoint_g3);   // masks 12-15 (volume + tf [+ ...])
+
+template <typename K>
+inline void set_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+}  // namespace ddvr_impl
+
+namespace {
+using namespace ddvr_impl;
 
 // per-view camera frame, computed once per CTA in fp64 (field.py:194-222)
 struct Frame {
@@ -1127,414 +1140,4 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_kernel(
   }
 }
 
-// ---------------------------------------------------------------------------
-// cell-record layout: pack (volume -> cells) and fold (cell gradients -> voxels)
-// ---------------------------------------------------------------------------
-
-// Padded record of cell (i,j,k), i in [-1, X-1] (storage index i+1):
-//   cells[c] = v[clamp(i+bx, 0, X-1)][clamp(j+by, 0, Y-1)][clamp(k+bz, 0, Z-1)],
-//   c = bx | by << 1 | bz << 2 (the corner order of field.py:318-322).
-__global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __restrict__ cells,
-                                                       long long ncells) {
-  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= ncells) return;
-  const int k = (int)(id % V.CZ) - 1;
-  const long long ij = id / V.CZ;
-  const int j = (int)(ij % V.CY) - 1;
-  const int i = (int)(ij / V.CY) - 1;
-  const int i0 = max(i, 0), j0 = max(j, 0), k0 = max(k, 0);
-  const int i1 = min(i + 1, V.X - 1), j1 = min(j + 1, V.Y - 1), k1 = min(k + 1, V.Z - 1);
-  const float* p = V.data;
-  auto at = [&](int a, int b, int c) { return __ldg(p + ((size_t)a * V.Y + b) * V.Z + c); };
-  const float4 lo = make_float4(at(i0, j0, k0), at(i1, j0, k0), at(i0, j1, k0), at(i1, j1, k0));
-  const float4 hi = make_float4(at(i0, j0, k1), at(i1, j0, k1), at(i0, j1, k1), at(i1, j1, k1));
-  float4* q = reinterpret_cast<float4*>(cells + 8 * id);
-  q[0] = lo;
-  q[1] = hi;
-}
-
-// d_volume[x,y,z] += every cell-gradient slot that pack_cells_kernel filled
-// from voxel (x,y,z) (its exact transpose, padding included)
-__global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
-                                                       const float* __restrict__ d_cells,
-                                                       float* __restrict__ d_volume,
-                                                       long long nvox) {
-  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= nvox) return;
-  const int z = (int)(id % V.Z);
-  const long long xy = id / V.Z;
-  const int y = (int)(xy % V.Y);
-  const int x = (int)(xy / V.Y);
-  // per axis, the (storage cell index, corner bit) pairs whose clamped corner is this voxel
-  int ci[3][4], cb[3][4], cn[3];
-  const int dims[3] = {V.X, V.Y, V.Z};
-  const int pos[3] = {x, y, z};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    int n = 0;
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int d = -2; d <= 1; ++d) {
-        const int i = pos[a] + d;                    // padded cell index in [-1, dim-1]
-        if (i < -1 || i > dims[a] - 1) continue;
-        const int corner = min(max(i + b, 0), dims[a] - 1);
-        if (corner == pos[a] && n < 4) { ci[a][n] = i + 1; cb[a][n] = b; ++n; }
-      }
-    cn[a] = n;
-  }
-  float s = 0.f;
-  for (int a = 0; a < cn[0]; ++a)
-    for (int b = 0; b < cn[1]; ++b)
-      for (int c = 0; c < cn[2]; ++c) {
-        const size_t cell = ((size_t)ci[0][a] * V.CY + ci[1][b]) * V.CZ + ci[2][c];
-        s += d_cells[8 * cell + (cb[0][a] | cb[1][b] << 1 | cb[2][c] << 2)];
-      }
-  d_volume[id] += s;
-}
-
-// ---------------------------------------------------------------------------
-// ray setup (parity helper) and fused L1 loss
-// ---------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(kThreads) ray_setup_kernel(VolArgs V, Geometry G,
-                                                           double* __restrict__ tn_tf,
-                                                           int32_t* __restrict__ n_steps,
-                                                           int32_t* __restrict__ flags) {
-  __shared__ Frame F;
-  const int view = blockIdx.z;
-  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
-  __syncthreads();
-  int px, py;
-  pixel_of(G, px, py);
-  if (px >= G.W || py >= G.row1) return;
-  Ray r;
-  setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
-  const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
-  n_steps[pix] = r.n;
-  if (tn_tf) { tn_tf[2 * pix] = r.tn; tn_tf[2 * pix + 1] = r.tf; }
-  if (flags) flags[pix] = r.axis | (r.clamped ? 4 : 0) | (r.miss ? 8 : 0);
-}
-
-__global__ void __launch_bounds__(256) l1_loss_kernel(const float* __restrict__ x,
-                                                    const float* __restrict__ y, int64_t n,
-                                                    float inv_count, double inv_count_d,
-                                                    float* __restrict__ seed,
-                                                    double* __restrict__ loss) {
-  __shared__ double s_part[8];
-  double part = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const float dlt = x[i] - y[i];
-    part += fabs((double)dlt);
-    if (seed) seed[i] = dlt > 0.f ? inv_count : (dlt < 0.f ? -inv_count : 0.f);
-  }
-  part = warp_sum(part);
-  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
-  __syncthreads();
-  if (threadIdx.x == 0 && loss) {
-    double t = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_part[k];
-    atomicAdd(loss, t * inv_count_d);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// host-side validation and launch
-// ---------------------------------------------------------------------------
-
-// padded cell grid: cells -1 .. dim-1 on every axis
-long long cell_count(const int32_t dims[3]) {
-  return (long long)(dims[0] + 1) * (dims[1] + 1) * (dims[2] + 1);
-}
-
-int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
-  if (!vol) return set_error(DDVR_INVALID_PARAMETER, "volume descriptor is NULL");
-  for (int k = 0; k < 3; ++k) {
-    if (vol->dims[k] < 1)
-      return set_error(DDVR_INVALID_PARAMETER, "volume values must be a non-empty 3D array");
-    if (!(vol->box_max[k] > vol->box_min[k]) || !std::isfinite(vol->box_min[k]) ||
-        !std::isfinite(vol->box_max[k]))
-      return set_error(DDVR_INVALID_PARAMETER,
-                       "world box must have positive extent on each axis");
-  }
-  const long long nvox = (long long)vol->dims[0] * vol->dims[1] * vol->dims[2];
-  if (nvox > 0x7fffffffLL)
-    return set_error(DDVR_UNSUPPORTED, "volume has more than 2^31 voxels");
-  if (need_data && !vol->data) return set_error(DDVR_INVALID_INPUT, "volume data pointer is NULL");
-  if (vol->cells && ((uintptr_t)vol->cells & 31) != 0)
-    return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");
-  V.data = vol->data;
-  V.cells = vol->cells;
-  V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
-  V.YZ = V.Y * V.Z;
-  V.CY = V.Y + 1; V.CZ = V.Z + 1;
-  V.cell0 = V.cells ? V.cells + 8 * (((long long)V.CY + 1) * V.CZ + 1) : nullptr;
-  V.Xm2 = V.X >= 2 ? V.X - 2 : 0; V.Ym2 = V.Y >= 2 ? V.Y - 2 : 0; V.Zm2 = V.Z >= 2 ? V.Z - 2 : 0;
-  V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
-  V.tX = V.X > 1 ? 1.f : 0.f; V.tY = V.Y > 1 ? 1.f : 0.f; V.tZ = V.Z > 1 ? 1.f : 0.f;
-  // inside test in grid units.  Every sample of a march lies in [tn, tf) of the
-  // exact slab, so the reference's 1e-9*extent tolerance (field.py:293) only has
-  // to absorb rounding of the fixed-point entry point: 1e-6 voxel of slack.
-  const double tol = 1e-6;
-  for (int k = 0; k < 3; ++k) {
-    V.lo[k] = (long long)llrint((-0.5 - tol) * kFix);
-    V.hi[k] = (long long)llrint(((double)vol->dims[k] - 0.5 + tol) * kFix);
-    V.top[k] = (long long)(vol->dims[k] - 1) << 32;
-    V.bmin[k] = vol->box_min[k];
-    V.bmax[k] = vol->box_max[k];
-    V.scale[k] = (double)vol->dims[k] / (vol->box_max[k] - vol->box_min[k]);
-  }
-  return DDVR_OK;
-}
-
-int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
-  if (!tf) return set_error(DDVR_INVALID_PARAMETER, "transfer function descriptor is NULL");
-  if (tf->kind != DDVR_TF_TEXTURE && tf->kind != DDVR_TF_PIECEWISE &&
-      tf->kind != DDVR_TF_GAUSSIAN)
-    return set_error(DDVR_UNSUPPORTED, "transfer-function kind %d is not built", tf->kind);
-  const int stride = tf->kind == DDVR_TF_TEXTURE ? 4 : tf->kind == DDVR_TF_PIECEWISE ? 5 : 6;
-  if (tf->count < 1)
-    return set_error(DDVR_INVALID_PARAMETER,
-                     "transfer function must have shape (R, %d), R >= 1", stride);
-  if (!tf->params) return set_error(DDVR_INVALID_INPUT, "transfer function pointer is NULL");
-  if (((uintptr_t)tf->params & (tf->kind == DDVR_TF_TEXTURE ? 15 : 3)) != 0)
-    return set_error(DDVR_INVALID_INPUT, "transfer function parameters are misaligned");
-  const size_t n = (size_t)tf->count;
-  // shared layouts (see g_smem / pl_eval / gauss_eval), gradient rows included:
-  //   texture   2(n+1) pair float4 + 4n gradient floats + (n+1) tau-pair float2
-  //   piecewise 2n float4 + n pos floats (pad to 9n floats) + 5n gradient floats
-  //   gaussian  2n float4 + 6n gradient floats
-  smem_per_table = tf->kind == DDVR_TF_TEXTURE ? (14 * n + 10) * sizeof(float)
-                   : tf->kind == DDVR_TF_PIECEWISE ? (9 * n + 5 * n) * sizeof(float)
-                                                   : (8 * n + 6 * n) * sizeof(float);
-  A.stride = stride;
-  if (smem_per_table > (size_t)kMaxTfBytes)
-    return set_error(DDVR_UNSUPPORTED, "transfer function resolution %d exceeds %d texels",
-                     tf->count, kMaxTfBytes / 56);
-  A.params = tf->params;
-  A.kind = tf->kind;
-  A.count = tf->count;
-  A.fR = (float)tf->count;
-  A.fR1 = (float)(tf->count - 1);
-  A.Rm2 = tf->count >= 2 ? tf->count - 2 : 0;
-  return DDVR_OK;
-}
-
-int make_geo(const ddvr_camera* cams, int n_views, const ddvr_params* p, Geometry& G) {
-  if (!p) return set_error(DDVR_INVALID_PARAMETER, "params is NULL");
-  if (!(p->dt > 0.0) || !std::isfinite(p->dt))
-    return set_error(DDVR_INVALID_PARAMETER, "stepsize must be positive");
-  if (p->width < 1 || p->height < 1)
-    return set_error(DDVR_INVALID_PARAMETER, "image size must be at least 1x1");
-  if (n_views < 0 || n_views > 65535)
-    return set_error(DDVR_INVALID_PARAMETER, "view count %d out of range", n_views);
-  if (n_views > 0 && !cams) return set_error(DDVR_INVALID_INPUT, "camera array is NULL");
-  G.cams = cams;
-  G.W = p->width;
-  G.H = p->height;
-  G.row0 = p->row0;
-  G.row1 = p->row1 <= 0 ? p->height : p->row1;
-  if (G.row0 < 0 || G.row0 > G.row1 || G.row1 > G.H)
-    return set_error(DDVR_INVALID_PARAMETER, "row band [%d, %d) outside image height %d", G.row0,
-                     G.row1, G.H);
-  G.dt = p->dt;
-  G.dt32 = (float)p->dt;
-  G.tape = p->tape;
-  G.tape_stride = p->tape_stride;
-  if (G.tape && G.tape_stride < 0)
-    return set_error(DDVR_INVALID_PARAMETER, "negative tape stride");
-  return DDVR_OK;
-}
-
-dim3 grid_of(const Geometry& G, int n_views) {
-  return dim3((G.W + kTile - 1) / kTile, (G.row1 - G.row0 + kTile - 1) / kTile, n_views);
-}
-
-template <typename K>
-void set_smem(K kernel, size_t smem) {
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-template <bool EARLY, bool CELLS, bool TAPE>
-void launch_forward(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
-                    const Geometry& G, float* image, float* depth) {
-  auto k = dvr_forward_kernel<EARLY, CELLS, TAPE>;
-  set_smem(k, smem);
-  k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth);
-}
-
-template <unsigned M, bool CELLS>
-void launch_adjoint(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
-                    const Geometry& G, const float* image, const float* depth, const float* seed,
-                    float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
-  auto k = dvr_adjoint_kernel<M, CELLS>;
-  set_smem(k, smem);
-  k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-}
-
 }  // namespace
-
-// ---------------------------------------------------------------------------
-// C ABI
-// ---------------------------------------------------------------------------
-
-extern "C" {
-
-const char* ddvr_last_error(void) { return g_err; }
-
-int32_t ddvr_abi_version(void) { return DDVR_ABI_VERSION; }
-
-int64_t ddvr_launch_count(void) { return g_launches.load(); }
-
-int64_t ddvr_cells_bytes(const int32_t dims[3]) {
-  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1) return 0;
-  return cell_count(dims) * 8 * (int64_t)sizeof(float);
-}
-
-int ddvr_pack_cells(const ddvr_volume* vol, float* cells_out, void* stream) {
-  g_err[0] = 0;
-  VolArgs V;
-  int rc;
-  if ((rc = make_vol(vol, V))) return rc;
-  if (!cells_out) return set_error(DDVR_INVALID_INPUT, "cell output pointer is NULL");
-  if (((uintptr_t)cells_out & 31) != 0)
-    return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");
-  const long long n = cell_count(vol->dims);
-  pack_cells_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(V, cells_out,
-                                                                                  n);
-  return check_launch("pack_cells_kernel");
-}
-
-int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t mask) {
-  if (!vol || !vol->cells || !(mask & DDVR_TARGET_VOLUME)) return 0;
-  return ddvr_cells_bytes(vol->dims);
-}
-
-int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, float* image_out, float* depth_out,
-                 void* stream) {
-  g_err[0] = 0;
-  VolArgs V;
-  TfArgs T;
-  Geometry G;
-  size_t tbl;
-  int rc;
-  if ((rc = make_vol(vol, V)) || (rc = make_tf(tf, T, tbl)) || (rc = make_geo(cams, n_views, p, G)))
-    return rc;
-  if (!image_out) return set_error(DDVR_INVALID_INPUT, "image output pointer is NULL");
-  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  const dim3 grid = grid_of(G, n_views);
-  const bool early = p->early_stop != 0, cells = V.cells != nullptr, tape = G.tape != nullptr;
-#define DDVR_FWD(E, C, P) \
-  if (early == E && cells == C && tape == P) launch_forward<E, C, P>(grid, tbl, st, V, T, G, image_out, depth_out);
-  DDVR_FWD(false, false, false) DDVR_FWD(false, false, true) DDVR_FWD(false, true, false)
-  DDVR_FWD(false, true, true) DDVR_FWD(true, false, false) DDVR_FWD(true, false, true)
-  DDVR_FWD(true, true, false) DDVR_FWD(true, true, true)
-#undef DDVR_FWD
-  return check_launch("dvr_forward_kernel");
-}
-
-int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, const float* image, const float* depth,
-                 const float* seed, uint32_t mask, float* d_volume, double* d_tf,
-                 double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
-                 void* stream) {
-  g_err[0] = 0;
-  VolArgs V;
-  TfArgs T;
-  Geometry G;
-  size_t tbl;
-  int rc;
-  if ((rc = make_vol(vol, V)) || (rc = make_tf(tf, T, tbl)) || (rc = make_geo(cams, n_views, p, G)))
-    return rc;
-  if (mask == 0 || (mask & ~15u))
-    return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
-  if (!seed) return set_error(DDVR_INVALID_INPUT, "seed pointer is NULL");
-  if (!image && !depth) return set_error(DDVR_INVALID_INPUT, "image and optical depth are NULL");
-  if ((mask & DDVR_TARGET_VOLUME) && !d_volume)
-    return set_error(DDVR_INVALID_INPUT, "d_volume is NULL but the volume target is set");
-  if ((mask & DDVR_TARGET_TF) && !d_tf)
-    return set_error(DDVR_INVALID_INPUT, "d_tf is NULL but the tf target is set");
-  if ((mask & DDVR_TARGET_CAMERA) && !d_camera)
-    return set_error(DDVR_INVALID_INPUT, "d_camera is NULL but the camera target is set");
-  if ((mask & DDVR_TARGET_STEPSIZE) && !d_dt)
-    return set_error(DDVR_INVALID_INPUT, "d_dt is NULL but the stepsize target is set");
-  const int64_t ws_need = ddvr_adjoint_workspace_bytes(vol, mask);
-  if (ws_need > 0 && (!workspace || workspace_bytes < ws_need))
-    return set_error(DDVR_INVALID_INPUT,
-                     "volume target with cell records needs a %lld-byte workspace",
-                     (long long)ws_need);
-  if (workspace && ((uintptr_t)workspace & 31) != 0)
-    return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
-  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  const dim3 grid = grid_of(G, n_views);
-  const size_t smem = tbl;
-  const bool cells = V.cells != nullptr;
-  float* d_cells_all = ws_need > 0 ? static_cast<float*>(workspace) : nullptr;
-  // the kernel indexes cell gradients relative to cell (0,0,0), like V.cell0
-  float* d_cells = d_cells_all ? d_cells_all + (V.cell0 - V.cells) : nullptr;
-  if (d_cells_all) {
-    cudaError_t e = cudaMemsetAsync(d_cells_all, 0, (size_t)ws_need, st);
-    if (e != cudaSuccess)
-      return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
-  }
-#define DDVR_CASE(M)                                                                       \
-  case M:                                                                                  \
-    if (cells)                                                                             \
-      launch_adjoint<M, true>(grid, smem, st, V, T, G, image, depth, seed, d_volume,       \
-                              d_cells, d_tf, d_camera, d_dt);                              \
-    else                                                                                   \
-      launch_adjoint<M, false>(grid, smem, st, V, T, G, image, depth, seed, d_volume,      \
-                               d_cells, d_tf, d_camera, d_dt);                             \
-    break;
-  switch (mask) {
-    DDVR_CASE(1) DDVR_CASE(2) DDVR_CASE(3) DDVR_CASE(4) DDVR_CASE(5) DDVR_CASE(6) DDVR_CASE(7)
-    DDVR_CASE(8) DDVR_CASE(9) DDVR_CASE(10) DDVR_CASE(11) DDVR_CASE(12) DDVR_CASE(13)
-    DDVR_CASE(14) DDVR_CASE(15)
-    default: break;
-  }
-#undef DDVR_CASE
-  if ((rc = check_launch("dvr_adjoint_kernel"))) return rc;
-  if (d_cells) {
-    const long long nvox = (long long)V.X * V.Y * V.Z;
-    fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells_all, d_volume,
-                                                                     nvox);
-    return check_launch("fold_cells_kernel");
-  }
-  return DDVR_OK;
-}
-
-int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float* seed_out,
-                 double* loss_out, void* stream) {
-  g_err[0] = 0;
-  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative element count");
-  if (!(count > 0.0)) return set_error(DDVR_INVALID_PARAMETER, "normaliser must be positive");
-  if (n == 0) return DDVR_OK;
-  if (!x || !y) return set_error(DDVR_INVALID_INPUT, "image or reference pointer is NULL");
-  int blocks = (int)((n + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  l1_loss_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n, (float)(1.0 / count),
-                                                           1.0 / count, seed_out, loss_out);
-  return check_launch("l1_loss_kernel");
-}
-
-int ddvr_ray_setup(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_views,
-                   const ddvr_params* p, double* tn_tf, int32_t* n_steps, int32_t* flags,
-                   void* stream) {
-  g_err[0] = 0;
-  VolArgs V;
-  Geometry G;
-  int rc;
-  if ((rc = make_vol(vol, V, false)) || (rc = make_geo(cams, n_views, p, G))) return rc;
-  if (!n_steps) return set_error(DDVR_INVALID_INPUT, "n_steps pointer is NULL");
-  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
-  ray_setup_kernel<<<grid_of(G, n_views), kThreads, 0, (cudaStream_t)stream>>>(V, G, tn_tf,
-                                                                              n_steps, flags);
-  return check_launch("ray_setup_kernel");
-}
-
-}  // extern "C"
