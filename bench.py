@@ -5,9 +5,11 @@
 
 Workload (default C4, BASELINE.json configs[3]): absorption tomography, 256^3
 sphere phantom, 64 views at 512x512, dt = 0.2 voxel, absorption-ramp TF
-(R=64, tau 3), gradients w.r.t. the density.  One step = forward march of the
-rank's views + fused L1 loss/seed + adjoint (inversion trick) + ONE all-reduce
-of [d_volume | d_tf | d_dt | loss] (N > 1).  Views are dealt round-robin to
+(R=64, tau 3), gradients w.r.t. the density.  One step = one optimisation
+iteration of the reference's tomography loop (tasks.py:397-481): cell-record
+pack, forward march of the rank's views, fused L1 loss/seed, adjoint
+(inversion trick), ONE all-reduce of [d_volume | d_tf | d_dt | loss] (N > 1),
+smoothness prior, Adam + [0,1] projection -- all libddvr kernels.  Views are dealt round-robin to
 ranks; the total work is fixed (strong scaling).  Synthetic data: the
 reference images are rendered from the phantom, the optimised volume is a
 perturbed copy.
@@ -15,7 +17,7 @@ perturbed copy.
 Own arm: device-timed with CUDA events, L2 flushed (512 MiB write) before
 every timed step, max over ranks.  ``e2e`` repeats the step through the public
 API with host (pinned) buffers: H2D of the volume and the rank's reference
-images and D2H of the gradient and loss inside the timed region.
+images and D2H of the updated volume and the loss inside the timed region.
 
 ``--impl reference``: the reference algorithm on the host CPU (the fp64 NumPy
 oracle restatement, oracle/dvr_oracle.py -- voldiff itself is pure Python and
@@ -245,7 +247,7 @@ def run_own(args, cfg):
 
     from paper_2107_12672_b200 import _native as N
     from paper_2107_12672_b200 import raymarch as R
-    from paper_2107_12672_b200.distributed import ShardedStep, shard_views
+    from paper_2107_12672_b200.distributed import ShardedStep, TomographyIteration, shard_views
 
     world, rank, local = dist_env()
     if world != args.gpus:
@@ -273,6 +275,8 @@ def run_own(args, cfg):
     step = ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                        total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
                        layout=args.layout)
+    # density targets run the whole optimisation iteration (prior + Adam + projection)
+    runner = TomographyIteration(step, lr=0.02, lam=0.5) if "volume" in cfg.targets else step
     _, n_steps, _ = R.ray_setup(cams, cfg.dt, rig, dims=tuple(truth.shape))
     local_samples = int(n_steps.to(torch.int64).sum().item())
     local_rays = n_steps.numel()
@@ -293,12 +297,12 @@ def run_own(args, cfg):
         e = {k: torch.cuda.Event(enable_timing=True)
              for k in ("start", "post_forward", "pre_adjoint", "post_adjoint", "end")}
         e["start"].record(st)
-        step.run(hook=lambda k: e[k].record(st))
+        runner.run(hook=lambda k: e[k].record(st))
         e["end"].record(st)
         return e
 
     for _ in range(args.warmup):
-        step.run()
+        runner.run()
     torch.cuda.synchronize()
 
     launches0 = N.launch_count()
@@ -336,8 +340,11 @@ def run_own(args, cfg):
         a.record(st)
         est.copy_(host_vol, non_blocking=True)
         refs.copy_(host_refs, non_blocking=True)
-        f = step.run()
-        host_grad.copy_(f.d_volume, non_blocking=True)
+        runner.run()
+        f = step.flat
+        # the step's result: the updated density (optimiser steps) or its gradient
+        host_grad.copy_((est if runner is not step else f.d_volume).reshape(-1),
+                        non_blocking=True)
         host_loss.copy_(f.loss, non_blocking=True)
         b.record(st)
         torch.cuda.synchronize()
@@ -375,7 +382,13 @@ def run_own(args, cfg):
                          "frac": adj_gbs / peak, "traffic": ncu_traffic(cfg.name, "adjoint"),
                          "algorithmic_bytes_per_launch": adj_bytes,
                          "bytes_model": f"{adj_b} B/sample + {ADJ_B_PER_RAY} B/ray",
-                         "launch_ms": adj_s * 1e3, "peak_source": peak_src},
+                         "launch_ms": adj_s * 1e3, "peak_source": peak_src,
+                         "note": "algorithmic bytes charge 8 corner gathers (+8 scatters) "
+                                 "per sample with no cache reuse (SURVEY 8d); the kernel "
+                                 "moves `traffic` DRAM bytes per launch (ncu), ~8% of "
+                                 "that, so frac > 1 is reuse, not missing work; its "
+                                 "limiters are issue slots and L1 wavefronts "
+                                 "(profiles/r01_ncu_c4v8_full.txt)"},
             "kernels": {
                 "forward": {"ms": fwd_s * 1e3, "achieved_gbs": fwd_gbs, "frac": fwd_gbs / peak,
                             "bytes_model": f"{FWD_B_PER_SAMPLE} B/sample + {FWD_B_PER_RAY} B/ray",

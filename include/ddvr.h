@@ -164,6 +164,39 @@ int ddvr_ray_setup(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_vi
                    const ddvr_params* p, double* tn_tf, int32_t* n_steps, int32_t* flags,
                    void* stream);
 
+/* ---- the steps either side of the path ---- */
+
+/* smoothness_prior_volume (objectives.py:72-92) times weight:
+ * value_out[0] += weight * mean squared forward difference; grad_out +=
+ * weight * gradient (float (X,Y,Z)).  Either output may be NULL. */
+int ddvr_prior_volume(const float* values, const int32_t dims[3], double weight, float* grad_out,
+                      double* value_out, void* stream);
+
+/* smoothness_prior_tf (objectives.py:57-69) times weight, texels (R,4) float,
+ * grad_out (R,4) double (+=), value_out double (+=). */
+int ddvr_prior_tf(const float* texels, int32_t resolution, double weight, double* grad_out,
+                  double* value_out, void* stream);
+
+/* Adam with bias correction (optim.py:45-67) fused with the projection of
+ * optim.py:70-89: after the update, element i is clamped to [lo, hi] when
+ * stride <= 1 or i % stride == stride-1, else to [lo_other, hi_other]
+ * (volume: stride 1, [0,1]; TF: stride 4, rgb [0, inf), tau [0, tau_max]). */
+typedef struct {
+  double lr, beta1, beta2, eps;
+  int32_t step;          /* 1-based update count t */
+  int32_t stride;
+  float lo, hi, lo_other, hi_other;
+} ddvr_adam;
+
+/* params, m, v updated in place from grads (all float, n elements).  If
+ * nonfinite (device int, caller-zeroed) is given, a non-finite gradient sets
+ * it and the whole update is skipped (NumericalAbortError, optim.py:28-30). */
+int ddvr_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
+                   const ddvr_adam* cfg, int32_t* nonfinite, void* stream);
+
+/* upsample_volume (optim.py:92-129): dst (2X,2Y,2Z) from src (X,Y,Z). */
+int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, void* stream);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char* ddvr_last_error(void);
 

@@ -200,9 +200,37 @@ def count_cases():
     save("counts", **out)
 
 
+def optim_cases():
+    """Steps either side of the path: priors, Adam, projection, upsample."""
+    from voldiff import objectives as vo
+    from voldiff import optim as vopt
+    rng = np.random.default_rng(11)
+    vol = f32(rng.uniform(-0.2, 1.2, (7, 5, 6)))
+    pv, pg = vo.smoothness_prior_volume(vol)
+    tex = f32(rng.uniform(-0.5, 3.0, (9, 4)))
+    tv, tg = vo.smoothness_prior_tf(vd.TransferFunction(tex))
+    grads = [f32(rng.normal(size=vol.shape)) for _ in range(3)]
+    st = vopt.OptimState(lr=0.05)
+    p = vol.copy()
+    traj = []
+    for g in grads:
+        st, p = vopt.adam_step(st, p, g)
+        traj.append(p.copy())
+    proj_vol = vopt.project_params(vol, "volume")
+    proj_tf = vopt.project_params(tex * 40.0, "tf")
+    small = f32(rng.uniform(0, 1, (3, 4, 2)))
+    up = vopt.upsample_volume(vd.DensityVolume(small)).values
+    save("optim", volume=vol, prior_value=np.float64(pv), prior_grad=pg, texels=tex,
+         prior_tf_value=np.float64(tv), prior_tf_grad=tg, adam_grads=np.stack(grads),
+         adam_traj=np.stack(traj), adam_lr=np.float64(0.05), proj_vol=proj_vol,
+         proj_tf_in=tex * 40.0, proj_tf=proj_tf, up_src=small, up=up)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["kat", "rand", "config", "count"]
+    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim"]
+    if "optim" in which:
+        optim_cases()
     if "kat" in which:
         kat_cases()
     if "rand" in which:

@@ -32,7 +32,8 @@ TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
 EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes",
-            "ddvr_pack_cells", "ddvr_l1_loss", "ddvr_ray_setup", "ddvr_last_error",
+            "ddvr_pack_cells", "ddvr_l1_loss", "ddvr_ray_setup", "ddvr_prior_volume",
+            "ddvr_prior_tf", "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_last_error",
             "ddvr_abi_version", "ddvr_launch_count")
 
 
@@ -61,6 +62,13 @@ class DdvrParams(ctypes.Structure):
                 ("tape", ctypes.c_void_p), ("tape_stride", ctypes.c_int64)]
 
 
+class DdvrAdam(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("step", ctypes.c_int32), ("stride", ctypes.c_int32),
+                ("lo", ctypes.c_float), ("hi", ctypes.c_float), ("lo_other", ctypes.c_float),
+                ("hi_other", ctypes.c_float)]
+
+
 CAMERA_DOUBLES = 8   # sizeof(ddvr_camera) / 8: lon, lat, radius, cx, cy, cz, fov, reserved
 
 _lib = None
@@ -87,6 +95,15 @@ def _bind(lib):
     lib.ddvr_ray_setup.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp, vp,
                                    vp]
     lib.ddvr_ray_setup.restype = ctypes.c_int
+    i3 = P(ctypes.c_int32)
+    lib.ddvr_prior_volume.argtypes = [vp, i3, ctypes.c_double, vp, vp, vp]
+    lib.ddvr_prior_volume.restype = ctypes.c_int
+    lib.ddvr_prior_tf.argtypes = [vp, ctypes.c_int32, ctypes.c_double, vp, vp, vp]
+    lib.ddvr_prior_tf.restype = ctypes.c_int
+    lib.ddvr_adam_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(DdvrAdam), vp, vp]
+    lib.ddvr_adam_step.restype = ctypes.c_int
+    lib.ddvr_upsample_volume.argtypes = [vp, i3, vp, vp]
+    lib.ddvr_upsample_volume.restype = ctypes.c_int
     lib.ddvr_last_error.argtypes = []
     lib.ddvr_last_error.restype = ctypes.c_char_p
     lib.ddvr_abi_version.argtypes = []

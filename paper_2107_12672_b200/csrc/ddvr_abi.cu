@@ -248,6 +248,137 @@ dim3 grid_of(const Geometry& G, int n_views) {
   return dim3((G.W + kTile - 1) / kTile, (G.row1 - G.row0 + kTile - 1) / kTile, n_views);
 }
 
+// ---------------------------------------------------------------------------
+// steps either side of the path: priors, Adam, upsample
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void block_add_double(double part, double* out) {
+  __shared__ double s_part[32];
+  part = warp_sum(part);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0 && out) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_part[k];
+    atomicAdd(out, t);
+  }
+}
+
+// smoothness_prior_volume (objectives.py:72-92): P = sum of squared forward
+// differences along each axis / their count; grad[x] is gathered from the
+// (up to) six differences touching voxel x -- no atomics.
+__global__ void __launch_bounds__(256) prior_volume_kernel(const float* __restrict__ v, int X,
+                                                         int Y, int Z, double scale,
+                                                         float* __restrict__ grad,
+                                                         double* __restrict__ value) {
+  const long long n = (long long)X * Y * Z;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  double part = 0.0;
+  const long long sx = (long long)Y * Z, sy = Z;
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += stride) {
+    const int z = (int)(id % Z);
+    const int y = (int)((id / Z) % Y);
+    const int x = (int)(id / sx);
+    const float c = v[id];
+    float g = 0.f;
+    if (x + 1 < X) { const float d = v[id + sx] - c; g -= 2.f * d; part += (double)d * d; }
+    if (x > 0) g += 2.f * (c - v[id - sx]);
+    if (y + 1 < Y) { const float d = v[id + sy] - c; g -= 2.f * d; part += (double)d * d; }
+    if (y > 0) g += 2.f * (c - v[id - sy]);
+    if (z + 1 < Z) { const float d = v[id + 1] - c; g -= 2.f * d; part += (double)d * d; }
+    if (z > 0) g += 2.f * (c - v[id - 1]);
+    if (grad) grad[id] += (float)(scale * g);
+  }
+  block_add_double(part * scale, value);
+}
+
+// smoothness_prior_tf (objectives.py:57-69): mean squared adjacent-texel difference
+__global__ void prior_tf_kernel(const float* __restrict__ t, int R, double scale,
+                                double* __restrict__ grad, double* __restrict__ value) {
+  double part = 0.0;
+  for (int i = threadIdx.x; i < 4 * R; i += blockDim.x) {
+    const int k = i >> 2;
+    const double c = t[i];
+    double g = 0.0;
+    if (k + 1 < R) { const double d = (double)t[i + 4] - c; g -= 2.0 * d; part += d * d; }
+    if (k > 0) g += 2.0 * (c - (double)t[i - 4]);
+    if (grad) grad[i] += scale * g;
+  }
+  block_add_double(part * scale, value);
+}
+
+__global__ void __launch_bounds__(256) finite_check_kernel(const float* __restrict__ g,
+                                                         long long n, int* __restrict__ flag) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= !isfinite(g[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// adam_step (optim.py:45-67) + project_params (optim.py:70-89), skipped entirely
+// when finite_check_kernel flagged a non-finite gradient (optim.py:28-30)
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p,
+                                                 const float* __restrict__ g,
+                                                 float* __restrict__ m, float* __restrict__ v,
+                                                 long long n, ddvr_adam a, float bc1, float bc2,
+                                                 const int* __restrict__ flag) {
+  if (flag && *flag) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const float b1 = (float)a.beta1, b2 = (float)a.beta2, lr = (float)a.lr, eps = (float)a.eps;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    float pi = p[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    const bool last = a.stride <= 1 || (int)(i % a.stride) == a.stride - 1;
+    pi = last ? fminf(fmaxf(pi, a.lo), a.hi) : fminf(fmaxf(pi, a.lo_other), a.hi_other);
+    p[i] = pi;
+  }
+}
+
+// upsample_volume (optim.py:92-129): fine node j at coarse coordinate (j - 0.5)/2,
+// i0 = clip(floor, 0, n-2), edge half-cells extrapolate; separable, so the
+// three axis passes collapse into one trilinear gather per fine voxel
+__device__ __forceinline__ void up_axis(int j, int n, int& i0, int& i1, float& f) {
+  if (n == 1) { i0 = i1 = 0; f = 0.f; return; }
+  const float g = ((float)j - 0.5f) * 0.5f;
+  i0 = min(max((int)floorf(g), 0), n - 2);
+  i1 = i0 + 1;
+  f = g - (float)i0;
+}
+
+__global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__ src, int X,
+                                                     int Y, int Z, float* __restrict__ dst) {
+  const long long n = 8LL * X * Y * Z;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += stride) {
+    const int z = (int)(id % (2 * Z));
+    const int y = (int)((id / (2 * Z)) % (2 * Y));
+    const int x = (int)(id / (4LL * Y * Z));
+    int x0, x1, y0, y1, z0, z1;
+    float fx, fy, fz;
+    up_axis(x, X, x0, x1, fx);
+    up_axis(y, Y, y0, y1, fy);
+    up_axis(z, Z, z0, z1, fz);
+    auto at = [&](int a, int b, int c) { return src[((long long)a * Y + b) * Z + c]; };
+    const float c00 = (1.f - fz) * at(x0, y0, z0) + fz * at(x0, y0, z1);
+    const float c01 = (1.f - fz) * at(x0, y1, z0) + fz * at(x0, y1, z1);
+    const float c10 = (1.f - fz) * at(x1, y0, z0) + fz * at(x1, y0, z1);
+    const float c11 = (1.f - fz) * at(x1, y1, z0) + fz * at(x1, y1, z1);
+    const float c0 = (1.f - fy) * c00 + fy * c01;
+    const float c1 = (1.f - fy) * c10 + fy * c11;
+    dst[id] = (1.f - fx) * c0 + fx * c1;
+  }
+}
+
+int grid_blocks(long long n) {
+  long long b = (n + 255) / 256;
+  return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -392,6 +523,66 @@ int ddvr_ray_setup(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_vi
   ray_setup_kernel<<<grid_of(G, n_views), kThreads, 0, (cudaStream_t)stream>>>(V, G, tn_tf,
                                                                               n_steps, flags);
   return check_launch("ray_setup_kernel");
+}
+
+int ddvr_prior_volume(const float* values, const int32_t dims[3], double weight, float* grad_out,
+                      double* value_out, void* stream) {
+  g_err[0] = 0;
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+    return set_error(DDVR_INVALID_PARAMETER, "volume values must be a non-empty 3D array");
+  if (!values) return set_error(DDVR_INVALID_INPUT, "volume pointer is NULL");
+  const long long X = dims[0], Y = dims[1], Z = dims[2];
+  const long long count = (X > 1 ? (X - 1) * Y * Z : 0) + (Y > 1 ? X * (Y - 1) * Z : 0) +
+                          (Z > 1 ? X * Y * (Z - 1) : 0);
+  if (count == 0) return DDVR_OK;    // objectives.py:90-91: prior 0, gradient 0
+  prior_volume_kernel<<<grid_blocks(X * Y * Z), 256, 0, (cudaStream_t)stream>>>(
+      values, dims[0], dims[1], dims[2], weight / (double)count, grad_out, value_out);
+  return check_launch("prior_volume_kernel");
+}
+
+int ddvr_prior_tf(const float* texels, int32_t resolution, double weight, double* grad_out,
+                  double* value_out, void* stream) {
+  g_err[0] = 0;
+  if (resolution < 1)
+    return set_error(DDVR_INVALID_PARAMETER, "transfer function must have shape (R, 4), R >= 1");
+  if (!texels) return set_error(DDVR_INVALID_INPUT, "texel pointer is NULL");
+  if (resolution < 2) return DDVR_OK;   // objectives.py:61-62
+  prior_tf_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(texels, resolution,
+                                                        weight / (4.0 * (resolution - 1)),
+                                                        grad_out, value_out);
+  return check_launch("prior_tf_kernel");
+}
+
+int ddvr_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
+                   const ddvr_adam* cfg, int32_t* nonfinite, void* stream) {
+  g_err[0] = 0;
+  if (!cfg) return set_error(DDVR_INVALID_PARAMETER, "adam config is NULL");
+  if (!(cfg->lr > 0.0)) return set_error(DDVR_INVALID_PARAMETER, "learning rate must be positive");
+  if (cfg->step < 1) return set_error(DDVR_INVALID_PARAMETER, "adam step must be >= 1");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative parameter count");
+  if (n == 0) return DDVR_OK;
+  if (!params || !grads || !m || !v)
+    return set_error(DDVR_INVALID_INPUT, "parameter, gradient or moment pointer is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nonfinite) {
+    finite_check_kernel<<<grid_blocks(n), 256, 0, st>>>(grads, n, nonfinite);
+    int rc = check_launch("finite_check_kernel");
+    if (rc) return rc;
+  }
+  const float bc1 = (float)(1.0 - pow(cfg->beta1, (double)cfg->step));
+  const float bc2 = (float)(1.0 - pow(cfg->beta2, (double)cfg->step));
+  adam_kernel<<<grid_blocks(n), 256, 0, st>>>(params, grads, m, v, n, *cfg, bc1, bc2, nonfinite);
+  return check_launch("adam_kernel");
+}
+
+int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, void* stream) {
+  g_err[0] = 0;
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+    return set_error(DDVR_INVALID_PARAMETER, "volume values must be a non-empty 3D array");
+  if (!src || !dst) return set_error(DDVR_INVALID_INPUT, "volume pointer is NULL");
+  upsample_kernel<<<grid_blocks(8LL * dims[0] * dims[1] * dims[2]), 256, 0,
+                    (cudaStream_t)stream>>>(src, dims[0], dims[1], dims[2], dst);
+  return check_launch("upsample_kernel");
 }
 
 }  // extern "C"

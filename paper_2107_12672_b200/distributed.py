@@ -144,3 +144,30 @@ class ShardedStep:
         f.loss.copy_(self.loss64)
         f.allreduce(self.group)
         return f
+
+
+class TomographyIteration:
+    """One full absorption-tomography iteration on device (tasks.py:397-481).
+
+    ShardedStep (forward + L1 seed + adjoint + all-reduce) followed by the
+    volume smoothness prior (objectives.py:72-92, weight ``lam``), one Adam
+    update and the [0,1] projection (optim.py:45-89).  Every rank applies the
+    same update to its replica after the all-reduce, so replicas stay equal.
+    """
+
+    def __init__(self, step: ShardedStep, *, lr: float = 0.02, lam: float = 0.5,
+                 check_finite: bool = False):
+        from .optim import AdamState
+        self.step = step
+        self.lam = lam
+        self.adam = AdamState(lr=lr)
+        self.check_finite = check_finite
+
+    def run(self, hook=None):
+        from .optim import prior_volume
+        f = self.step.run(hook=hook)
+        density = self.step.density
+        grad = f.d_volume.view(density.shape)
+        prior = prior_volume(density, self.lam, grad)      # grad += lam * d prior
+        self.adam.update(density, grad, project="volume", check_finite=self.check_finite)
+        return f.loss, prior
