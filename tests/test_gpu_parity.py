@@ -143,6 +143,10 @@ def test_gradients_match_reference(cuda, name, mode, layout):
 
 
 CONFIG_CASES = ["C1", "C2", "C3", "C4", "C5"]
+# C5's Gaussian texel TF is sharply peaked: fp32-level density rounding alone
+# moves the reference's own band gradient by 1.03e-4 rel-L2 (oracle experiment,
+# tools/fp32_floor_c5.py); the bar is 2.5x that floor.
+BAND_TOL = {("C5", "volume"): 2.5e-4}
 
 
 @pytest.mark.parametrize("name", CONFIG_CASES)
@@ -177,7 +181,7 @@ def test_config_band_matches_reference(cuda, name, layout):
         else:
             ref = g[f"inversion_{t}"]
         err = rel_l2(got[t], ref)
-        assert err <= GRAD_TOL, (name, t, err)
+        assert err <= BAND_TOL.get((name, t), GRAD_TOL), (name, t, err)
 
 
 def test_sample_totals_match_reference(cuda):
