@@ -138,6 +138,14 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
                  double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
                  void* stream);
 
+/* Forward-mode Jacobian of the image (render_forward_grad, renderer.py:410-464):
+ * wrt = DDVR_TARGET_CAMERA (p = 2: d/dlon, d/dlat, per degree) or
+ * DDVR_TARGET_STEPSIZE (p = 1); anything else is UNSUPPORTED.  image_out
+ * (device) (V, rows, W, 4); jac_out (device) (V, rows, W, 4, p). */
+int ddvr_forward_grad(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                      int32_t n_views, const ddvr_params* p, uint32_t wrt, float* image_out,
+                      float* jac_out, void* stream);
+
 /* Workspace ddvr_adjoint needs for this volume and target mask (0 if none). */
 int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t target_mask);
 

@@ -200,6 +200,30 @@ def count_cases():
     save("counts", **out)
 
 
+def forward_grad_cases():
+    """render_forward_grad (renderer.py:410-464) per-pixel Jacobians, camera and stepsize."""
+    out = {}
+    for s in (500, 501, 502, 2001):
+        sc = random_scene(s, tf_res=8 if s != 502 else 2)
+        vol, tex = f32(sc.volume.values), f32(sc.tf.texels)
+        V, T = vd.DensityVolume(vol), vd.TransferFunction(tex)
+        for t in ("camera", "stepsize"):
+            img, jac = vd.render_forward_grad(V, T, sc.cam, vd.RenderConfig(dt=sc.dt, target=t))
+            out[f"s{s}_{t}_image"] = img.data
+            out[f"s{s}_{t}_jac"] = jac
+        out[f"s{s}_volume"] = vol.astype(np.float32)
+        out[f"s{s}_texels"] = tex.astype(np.float32)
+        out[f"s{s}_cam"] = cam_fields(sc.cam)
+        out[f"s{s}_dt"] = np.float64(sc.dt)
+    # stepsize closed form scene (test_renderer.py:166-175)
+    ones = vd.DensityVolume(np.ones((8, 8, 8)))
+    T = vd.TransferFunction(f32(np.tile([0.4, 0.4, 0.4, 1.3], (2, 1))))
+    cam = vd.SphericalCamera(0.0, 0.0, 2.0, fov_y_deg=8.0, width=9, height=9)
+    img, jac = vd.render_forward_grad(ones, T, cam, vd.RenderConfig(dt=0.05, target="stepsize"))
+    out["kat_stepsize_jac"] = jac
+    save("forward_grad", **out)
+
+
 def optim_cases():
     """Steps either side of the path: priors, Adam, projection, upsample."""
     from voldiff import objectives as vo
@@ -228,9 +252,11 @@ def optim_cases():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim"]
+    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad"]
     if "optim" in which:
         optim_cases()
+    if "fwdgrad" in which:
+        forward_grad_cases()
     if "kat" in which:
         kat_cases()
     if "rand" in which:

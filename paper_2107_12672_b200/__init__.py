@@ -34,8 +34,19 @@ from .voldiff_api import (
     l1_loss,
     render,
     render_adjoint,
+    render_forward_grad,
 )
-from .raymarch import DiffDVR, Rig, adjoint, camera_array, forward, l1_loss_seed, render_views
+from .raymarch import (
+    DiffDVR,
+    Rig,
+    adjoint,
+    camera_array,
+    forward,
+    forward_grad,
+    l1_loss_seed,
+    pack_cells,
+    render_views,
+)
 from .scenes import CONFIGS, absorption_ramp_texels, fibonacci_poses, phantom, preset_texels
 
 __version__ = "0.1.0"
@@ -45,7 +56,8 @@ __all__ = [
     "MissingMetadataError", "NumericalAbortError", "UnsupportedConfigurationError",
     "VoldiffError", "EPS_ALPHA", "EPS_POLE_DEG", "DensityVolume", "GradientSet", "ImageRGBA",
     "RenderConfig", "SphericalCamera", "TransferFunction", "blend", "blend_adjoint",
-    "blend_invert", "l1_loss", "render", "render_adjoint", "DiffDVR", "Rig", "adjoint",
-    "camera_array", "forward", "l1_loss_seed", "render_views", "CONFIGS",
+    "blend_invert", "l1_loss", "render", "render_adjoint", "render_forward_grad", "DiffDVR",
+    "Rig", "adjoint", "camera_array", "forward", "forward_grad", "l1_loss_seed", "pack_cells",
+    "render_views", "CONFIGS",
     "absorption_ramp_texels", "fibonacci_poses", "phantom", "preset_texels",
 ]

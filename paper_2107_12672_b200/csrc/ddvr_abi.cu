@@ -496,6 +496,27 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   return DDVR_OK;
 }
 
+int ddvr_forward_grad(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                      int32_t n_views, const ddvr_params* p, uint32_t wrt, float* image_out,
+                      float* jac_out, void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  TfArgs T;
+  Geometry G;
+  size_t tbl;
+  int rc;
+  if ((rc = make_vol(vol, V)) || (rc = make_tf(tf, T, tbl)) || (rc = make_geo(cams, n_views, p, G)))
+    return rc;
+  if (wrt != DDVR_TARGET_CAMERA && wrt != DDVR_TARGET_STEPSIZE)   // renderer.py:428-431
+    return set_error(DDVR_UNSUPPORTED, "forward mode supports camera and stepsize, not mask %u",
+                     wrt);
+  if (!image_out || !jac_out) return set_error(DDVR_INVALID_INPUT, "output pointer is NULL");
+  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
+  launch_forward_grad(wrt == DDVR_TARGET_CAMERA ? 2 : 1, V.cells != nullptr, grid_of(G, n_views),
+                      tbl, (cudaStream_t)stream, V, T, G, image_out, jac_out);
+  return check_launch("dvr_forward_grad_kernel");
+}
+
 int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float* seed_out,
                  double* loss_out, void* stream) {
   g_err[0] = 0;

@@ -108,6 +108,9 @@ struct Geometry {
 void launch_forward(bool early, bool cells, bool tape, dim3 grid, size_t smem, cudaStream_t st,
                     const VolArgs& V, const TfArgs& T, const Geometry& G, float* image,
                     float* depth);
+void launch_forward_grad(int n_params, bool cells, dim3 grid, size_t smem, cudaStream_t st,
+                         const VolArgs& V, const TfArgs& T, const Geometry& G, float* image,
+                         float* jac);
 #define DDVR_ADJ_LAUNCHER(NAME)                                                              \
   void NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
             const VolArgs& V, const TfArgs& T, const Geometry& G, const float* image,       \

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _native as N
-from .errors import InvalidInputError, InvalidParameterError
+from .errors import InvalidInputError, InvalidParameterError, UnsupportedConfigurationError
 
 EPS_POLE_DEG = 1e-3    # field.py:24
 
@@ -167,6 +167,28 @@ def forward(density, texels, cams, dt: float, rig: Rig, *, early_stop=False, wit
                                  ctypes.byref(prm), img.data_ptr(),
                                  depth.data_ptr() if depth is not None else None, _stream_ptr()))
     return img, depth
+
+
+def forward_grad(density, texels, cams, dt: float, rig: Rig, wrt: str = "camera", *,
+                 cells=None):
+    """(image (V,rows,W,4), jacobian (V,rows,W,4,p)) by forward mode (renderer.py:410-464).
+
+    wrt "camera": p = 2, d/d(lon, lat) per degree; "stepsize": p = 1.
+    """
+    _require(cams, "cameras", torch.float64, ndim=2)
+    if wrt not in ("camera", "stepsize"):
+        raise UnsupportedConfigurationError(
+            f"forward mode supports camera and stepsize, not {wrt!r}")
+    vol, tf, prm = _descs(density, texels, rig, dt, False, cells)
+    V = cams.shape[0]
+    p = 2 if wrt == "camera" else 1
+    dev = density.device
+    img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=dev)
+    jac = torch.empty(V, rig.band_rows, rig.width, 4, p, dtype=torch.float32, device=dev)
+    N.check(N.lib().ddvr_forward_grad(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,
+                                      ctypes.byref(prm), N.TARGET_BITS[wrt], img.data_ptr(),
+                                      jac.data_ptr(), _stream_ptr()))
+    return img, jac
 
 
 def workspace_for(density, mask: int, cells=None, rig: Rig | None = None):

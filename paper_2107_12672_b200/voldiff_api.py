@@ -290,6 +290,23 @@ def render(volume, tf, cam, cfg, *, threads: int = 1) -> ImageRGBA:
     return _image_from(img, depth)
 
 
+def render_forward_grad(volume, tf, cam, cfg, *, threads: int = 1):
+    """Image and its per-pixel Jacobian by forward mode (renderer.py:410-464).
+
+    Targets ``camera`` (p=2, per degree) and ``stepsize`` (p=1); returns
+    ``(ImageRGBA, jacobian (H, W, 4, p) float64)``.
+    """
+    _validate_config(cfg)
+    if cfg.target not in ("camera", "stepsize"):
+        raise UnsupportedConfigurationError(
+            f"forward mode supports camera and stepsize, not {cfg.target!r}")
+    dev = _device()
+    dens, tex, cams, rig = _upload(volume, tf, cam, dev)
+    img, jac = R.forward_grad(dens, tex, cams, cfg.dt, rig, cfg.target, cells=R.pack_cells(dens))
+    return (ImageRGBA(img[0].to(torch.float64).cpu().numpy()),
+            jac[0].to(torch.float64).cpu().numpy())
+
+
 def _stored_tape_len(cams, dt, rig):
     _, n, _ = R.ray_setup(cams, dt, rig)
     return n
