@@ -146,6 +146,17 @@ int ddvr_forward_grad(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_came
                       int32_t n_views, const ddvr_params* p, uint32_t wrt, float* image_out,
                       float* jac_out, void* stream);
 
+/* Pre-shaded colour volumes (render_colorvol / render_colorvol_adjoint,
+ * renderer.py:404-407, 703-709): cv->data is (X,Y,Z,4) float (r, g, b
+ * emission, tau per voxel, 16-byte aligned), trilinear per channel without
+ * the [0,1] clamp; cv->cells must be NULL.  Outputs as ddvr_forward /
+ * ddvr_adjoint; d_color (device) (X,Y,Z,4) float accumulates (+=). */
+int ddvr_forward_color(const ddvr_volume* cv, const ddvr_camera* cams, int32_t n_views,
+                       const ddvr_params* p, float* image_out, float* depth_out, void* stream);
+int ddvr_adjoint_color(const ddvr_volume* cv, const ddvr_camera* cams, int32_t n_views,
+                       const ddvr_params* p, const float* image, const float* depth,
+                       const float* seed, float* d_color, void* stream);
+
 /* Workspace ddvr_adjoint needs for this volume and target mask (0 if none). */
 int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t target_mask);
 

@@ -593,3 +593,96 @@ def l1_seed(images, refs):
     seeds = [np.sign(np.asarray(x, np.float64) - np.asarray(y, np.float64)) / count
              for x, y in zip(images, refs)]
     return total, seeds
+
+
+# ---------------------------------------------------------------------------
+# pre-shaded colour volumes (renderer.py:404-407, 703-709; field.py:361-376)
+# ---------------------------------------------------------------------------
+
+
+class ColorGrid(Grid):
+    """(X,Y,Z,4) rgb-emission + absorption grid; trilinear per channel, no clamp."""
+
+    def __init__(self, values, box_min=(-0.5, -0.5, -0.5), box_max=(0.5, 0.5, 0.5)):
+        values = np.asarray(values, np.float64)
+        super().__init__(values[..., 0], box_min, box_max)
+        self.rgba = values.reshape(-1, 4)
+        self.cdims = values.shape
+
+    def sample4(self, pts):
+        """(n,4) channel values, 0 outside the box (field.py:361-376)."""
+        _, idx, frac, inside = self._cell(pts)
+        idx8 = self._corners(idx)
+        w8 = self._weights(frac)
+        out = np.einsum("nc,nck->nk", w8, self.rgba[idx8])
+        return np.where(inside[:, None], out, 0.0), w8 * inside[:, None], idx8
+
+
+def march_color(cg: ColorGrid, band: Band, dt: float, *, early_stop=False, record=False):
+    """Front-to-back march of a colour volume (renderer.py:306-357, colour branch)."""
+    nr = band.n.shape[0]
+    acc = np.zeros((nr, 4))
+    tape = [] if record else None
+    steps = int(band.n.max()) if nr else 0
+    for i in range(steps):
+        act = i < band.n
+        if early_stop:
+            act &= acc[:, 3] <= ALPHA_STOP
+            if not act.any():
+                break
+        ti = dt * float(i)
+        s4, _, _ = cg.sample4([band.xo[k] + ti * band.w[k] for k in range(3)])
+        _, _, a, _ = segment_opacity(s4[:, 3], dt)
+        if record:
+            tape.append(acc.copy())
+        vis = np.where(act, 1.0 - acc[:, 3], 0.0)
+        acc[:, :3] = acc[:, :3] + vis[:, None] * (a[:, None] * s4[:, :3])
+        acc[:, 3] = acc[:, 3] + vis * a
+    return acc, tape
+
+
+def render_color_view(cg: ColorGrid, view: View, dt: float, *, early_stop=False):
+    band = make_band(cg, view, dt)
+    rgba, _ = march_color(cg, band, dt, early_stop=early_stop)
+    return rgba.reshape(view.height, view.width, 4)
+
+
+def adjoint_color_view(cg: ColorGrid, view: View, dt: float, seed, *, image=None, stored=False):
+    """d sum(seed * image) / d colour values (X,Y,Z,4) (renderer.py:491-652, colour branch).
+
+    Same inversion walk as adjoint_view; the per-corner sensitivity is
+    w8 (inside-masked) times the full out4 adjoint (renderer.py:611-613).
+    """
+    band = make_band(cg, view, dt)
+    seed = np.asarray(seed, np.float64).reshape(-1, 4)
+    if stored or image is None:
+        final, tape = march_color(cg, band, dt, record=stored)
+    else:
+        final, tape = np.asarray(image, np.float64).reshape(-1, 4), None
+    steps = int(band.n.max()) if band.n.size else 0
+    g = np.zeros_like(cg.rgba)
+    rgb_bar, alpha_bar = seed[:, :3].copy(), seed[:, 3].copy()
+    col, alp = final[:, :3].copy(), final[:, 3].copy()
+    for i in range(steps - 1, -1, -1):
+        act = i < band.n
+        ti = dt * float(i)
+        out4, w8, idx8 = cg.sample4([band.xo[k] + ti * band.w[k] for k in range(3)])
+        tau, e, a, a_clamped = segment_opacity(out4[:, 3], dt)
+        crgb = out4[:, :3]
+        cs = a[:, None] * crgb
+        if stored:
+            col_prev, alp_prev = tape[i][:, :3], tape[i][:, 3]
+        else:
+            alp_prev = np.where(act, (a - alp) / (a - 1.0), alp)
+            col_prev = np.where(act[:, None], col - (1.0 - alp_prev)[:, None] * cs, col)
+        vis = 1.0 - alp_prev
+        cs_bar = vis[:, None] * rgb_bar
+        seg_a_bar = vis * alpha_bar + np.sum(crgb * cs_bar, axis=-1)
+        alpha_bar_next = (1.0 - a) * alpha_bar - np.sum(cs * rgb_bar, axis=-1)
+        a_raw_bar = np.where(a_clamped, 0.0, seg_a_bar)
+        tau_bar = np.where(out4[:, 3] < 0.0, 0.0, dt * e * a_raw_bar)
+        o4 = np.concatenate([a[:, None] * cs_bar, tau_bar[:, None]], axis=1) * act[:, None]
+        np.add.at(g, idx8, w8[:, :, None] * o4[:, None, :])
+        alpha_bar = np.where(act, alpha_bar_next, alpha_bar)
+        col, alp = col_prev, alp_prev
+    return g.reshape(cg.cdims)

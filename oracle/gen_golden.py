@@ -200,6 +200,38 @@ def count_cases():
     save("counts", **out)
 
 
+def color_cases():
+    """render_colorvol (renderer.py:404-407) + render_colorvol_adjoint (:703-709)."""
+    rng = np.random.default_rng(31)
+    out = {}
+    specs = [("a", (7, 8, 6), ((-0.5,) * 3, (0.5,) * 3),
+              vd.SphericalCamera(35.0, 20.0, 2.3, fov_y_deg=35.0, width=9, height=8), 0.06),
+             ("b", (5, 9, 4), ((-0.4, -0.6, -0.3), (0.6, 0.5, 0.7)),
+              vd.SphericalCamera(210.0, -30.0, 2.2, center=np.array([0.1, -0.05, 0.2]),
+                                 fov_y_deg=40.0, width=10, height=7), 0.045),
+             ("c", (8, 8, 8), ((-0.5,) * 3, (0.5,) * 3),
+              vd.SphericalCamera(0.0, 0.0, 0.3, fov_y_deg=60.0, width=6, height=6), 0.05)]
+    for key, dims, box, cam, dt in specs:
+        vals = np.concatenate([rng.uniform(0.0, 1.0, dims + (3,)),
+                               rng.uniform(-0.2, 3.0, dims + (1,))], axis=-1)   # tau < 0 too
+        vals = f32(vals)
+        cv = vd.ColorVolume(vals, np.array(box[0]), np.array(box[1]))
+        seed = f32(rng.normal(size=(cam.height, cam.width, 4)))
+        img = vd.render_colorvol(cv, cam, vd.RenderConfig(dt=dt, target="volume")).data
+        out[f"{key}_values"] = vals.astype(np.float32)
+        out[f"{key}_box"] = np.array(box, np.float64)
+        out[f"{key}_cam"] = cam_fields(cam)
+        out[f"{key}_dt"] = np.float64(dt)
+        out[f"{key}_seed"] = seed
+        out[f"{key}_image"] = img
+        out[f"{key}_image_none"] = vd.render_colorvol(cv, cam, vd.RenderConfig(dt=dt)).data
+        for mode in ("inversion", "stored"):
+            gs = vd.render_colorvol_adjoint(
+                cv, cam, vd.RenderConfig(dt=dt, target="volume", memory_mode=mode), seed)
+            out[f"{key}_{mode}_d_color"] = gs.d_color
+    save("color", **out)
+
+
 def forward_grad_cases():
     """render_forward_grad (renderer.py:410-464) per-pixel Jacobians, camera and stepsize."""
     out = {}
@@ -252,7 +284,9 @@ def optim_cases():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad"]
+    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad", "color"]
+    if "color" in which:
+        color_cases()
     if "optim" in which:
         optim_cases()
     if "fwdgrad" in which:

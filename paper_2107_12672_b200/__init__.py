@@ -22,6 +22,7 @@ from .errors import (
 from .voldiff_api import (
     EPS_ALPHA,
     EPS_POLE_DEG,
+    ColorVolume,
     DensityVolume,
     GradientSet,
     ImageRGBA,
@@ -34,6 +35,8 @@ from .voldiff_api import (
     l1_loss,
     render,
     render_adjoint,
+    render_colorvol,
+    render_colorvol_adjoint,
     render_forward_grad,
 )
 from .raymarch import (
@@ -56,7 +59,8 @@ __all__ = [
     "MissingMetadataError", "NumericalAbortError", "UnsupportedConfigurationError",
     "VoldiffError", "EPS_ALPHA", "EPS_POLE_DEG", "DensityVolume", "GradientSet", "ImageRGBA",
     "RenderConfig", "SphericalCamera", "TransferFunction", "blend", "blend_adjoint",
-    "blend_invert", "l1_loss", "render", "render_adjoint", "render_forward_grad", "DiffDVR",
+    "blend_invert", "l1_loss", "render", "render_adjoint", "render_forward_grad",
+    "ColorVolume", "render_colorvol", "render_colorvol_adjoint", "DiffDVR",
     "Rig", "adjoint", "camera_array", "forward", "forward_grad", "l1_loss_seed", "pack_cells",
     "render_views", "CONFIGS",
     "absorption_ramp_texels", "fibonacci_poses", "phantom", "preset_texels",

@@ -32,7 +32,8 @@ TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
 EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes",
-            "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_l1_loss", "ddvr_ray_setup",
+            "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
+            "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_ray_setup",
             "ddvr_prior_volume",
             "ddvr_prior_tf", "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_last_error",
             "ddvr_abi_version", "ddvr_launch_count")
@@ -88,6 +89,12 @@ def _bind(lib):
     lib.ddvr_forward_grad.argtypes = [P(DdvrVolume), P(DdvrTf), vp, ctypes.c_int32,
                                       P(DdvrParams), ctypes.c_uint32, vp, vp, vp]
     lib.ddvr_forward_grad.restype = ctypes.c_int
+    lib.ddvr_forward_color.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp,
+                                       vp]
+    lib.ddvr_forward_color.restype = ctypes.c_int
+    lib.ddvr_adjoint_color.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp,
+                                       vp, vp, vp]
+    lib.ddvr_adjoint_color.restype = ctypes.c_int
     lib.ddvr_adjoint_workspace_bytes.argtypes = [P(DdvrVolume), ctypes.c_uint32]
     lib.ddvr_adjoint_workspace_bytes.restype = ctypes.c_int64
     lib.ddvr_cells_bytes.argtypes = [P(ctypes.c_int32)]

@@ -517,6 +517,42 @@ int ddvr_forward_grad(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_came
   return check_launch("dvr_forward_grad_kernel");
 }
 
+int ddvr_forward_color(const ddvr_volume* cv, const ddvr_camera* cams, int32_t n_views,
+                       const ddvr_params* p, float* image_out, float* depth_out, void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  Geometry G;
+  int rc;
+  if ((rc = make_vol(cv, V)) || (rc = make_geo(cams, n_views, p, G))) return rc;
+  if (cv->cells) return set_error(DDVR_UNSUPPORTED, "colour volumes use the voxel layout");
+  if (((uintptr_t)cv->data & 15) != 0)
+    return set_error(DDVR_INVALID_INPUT, "colour volume must be 16-byte aligned");
+  if (!image_out) return set_error(DDVR_INVALID_INPUT, "image output pointer is NULL");
+  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
+  launch_forward_color(p->early_stop != 0, G.tape != nullptr, grid_of(G, n_views),
+                       (cudaStream_t)stream, V, G, image_out, depth_out);
+  return check_launch("dvr_forward_color_kernel");
+}
+
+int ddvr_adjoint_color(const ddvr_volume* cv, const ddvr_camera* cams, int32_t n_views,
+                       const ddvr_params* p, const float* image, const float* depth,
+                       const float* seed, float* d_color, void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  Geometry G;
+  int rc;
+  if ((rc = make_vol(cv, V)) || (rc = make_geo(cams, n_views, p, G))) return rc;
+  if (cv->cells) return set_error(DDVR_UNSUPPORTED, "colour volumes use the voxel layout");
+  if (((uintptr_t)cv->data & 15) != 0 || (d_color && ((uintptr_t)d_color & 15) != 0))
+    return set_error(DDVR_INVALID_INPUT, "colour volume and gradient must be 16-byte aligned");
+  if (!seed || !d_color) return set_error(DDVR_INVALID_INPUT, "seed or d_color pointer is NULL");
+  if (!image && !depth) return set_error(DDVR_INVALID_INPUT, "image and optical depth are NULL");
+  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
+  launch_adjoint_color(grid_of(G, n_views), (cudaStream_t)stream, V, G, image, depth, seed,
+                       d_color);
+  return check_launch("dvr_adjoint_color_kernel");
+}
+
 int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float* seed_out,
                  double* loss_out, void* stream) {
   g_err[0] = 0;

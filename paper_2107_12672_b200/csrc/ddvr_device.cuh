@@ -111,6 +111,11 @@ void launch_forward(bool early, bool cells, bool tape, dim3 grid, size_t smem, c
 void launch_forward_grad(int n_params, bool cells, dim3 grid, size_t smem, cudaStream_t st,
                          const VolArgs& V, const TfArgs& T, const Geometry& G, float* image,
                          float* jac);
+void launch_forward_color(bool early, bool tape, dim3 grid, cudaStream_t st, const VolArgs& V,
+                          const Geometry& G, float* image, float* depth);
+void launch_adjoint_color(dim3 grid, cudaStream_t st, const VolArgs& V, const Geometry& G,
+                          const float* image, const float* depth, const float* seed,
+                          float* d_color);
 #define DDVR_ADJ_LAUNCHER(NAME)                                                              \
   void NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
             const VolArgs& V, const TfArgs& T, const Geometry& G, const float* image,       \

@@ -191,6 +191,51 @@ def forward_grad(density, texels, cams, dt: float, rig: Rig, wrt: str = "camera"
     return img, jac
 
 
+def _color_descs(color, rig: Rig, dt: float, early_stop: bool, tape=None, tape_stride=0):
+    _require(color, "colour volume", torch.float32, ndim=4, align16=True)
+    if color.shape[3] != 4:
+        raise InvalidParameterError("color volume must have shape (X, Y, Z, 4)")
+    vol = N.DdvrVolume(color.data_ptr(), (ctypes.c_int32 * 3)(*color.shape[:3]),
+                       (ctypes.c_double * 3)(*rig.box_min), (ctypes.c_double * 3)(*rig.box_max),
+                       None)
+    r0, r1 = rig.band
+    prm = N.DdvrParams(float(dt), rig.width, rig.height, r0, r1, 1 if early_stop else 0, 0,
+                       None, 0)
+    _set_tape(prm, tape, tape_stride)
+    return vol, prm
+
+
+def forward_color(color, cams, dt: float, rig: Rig, *, early_stop=False, tape=None,
+                  tape_stride=0):
+    """Images and optical depth of a pre-shaded (X,Y,Z,4) colour volume (renderer.py:404-407)."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    vol, prm = _color_descs(color, rig, dt, early_stop, tape, tape_stride)
+    V = cams.shape[0]
+    img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=color.device)
+    depth = torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=color.device)
+    N.check(N.lib().ddvr_forward_color(ctypes.byref(vol), cams.data_ptr(), V, ctypes.byref(prm),
+                                       img.data_ptr(), depth.data_ptr(), _stream_ptr()))
+    return img, depth
+
+
+def adjoint_color(color, cams, dt: float, rig: Rig, image, depth, seed, d_color, *, tape=None,
+                  tape_stride=0):
+    """d_color += d sum(seed * image) / d colour values (renderer.py:703-709)."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    vol, prm = _color_descs(color, rig, dt, False, tape, tape_stride)
+    V = cams.shape[0]
+    shape = (V, rig.band_rows, rig.width, 4)
+    _require(seed, "seed", torch.float32)
+    if tuple(seed.shape) != shape:
+        raise InvalidInputError(f"seed shape {tuple(seed.shape)} does not match image {shape}")
+    _require(d_color, "d_color", torch.float32, align16=True)
+    N.check(N.lib().ddvr_adjoint_color(
+        ctypes.byref(vol), cams.data_ptr(), V, ctypes.byref(prm),
+        image.data_ptr() if image is not None else None,
+        depth.data_ptr() if depth is not None else None, seed.data_ptr(), d_color.data_ptr(),
+        _stream_ptr()))
+
+
 def workspace_for(density, mask: int, cells=None, rig: Rig | None = None):
     """Device workspace the adjoint needs for this layout and mask (or None)."""
     if cells is None or not mask & N.TARGET_VOLUME:

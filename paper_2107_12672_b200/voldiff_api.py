@@ -73,6 +73,34 @@ class DensityVolume:
 
 
 @dataclass
+class ColorVolume:
+    """Per-voxel rgb emission plus absorption, shape (X, Y, Z, 4) (field.py:80-105)."""
+
+    values: np.ndarray
+    box_min: np.ndarray = dc_field(default_factory=lambda: np.array([-0.5, -0.5, -0.5]))
+    box_max: np.ndarray = dc_field(default_factory=lambda: np.array([0.5, 0.5, 0.5]))
+
+    def __post_init__(self):
+        self.values = np.asarray(self.values, dtype=np.float64)
+        self.box_min = np.asarray(self.box_min, dtype=np.float64).reshape(3)
+        self.box_max = np.asarray(self.box_max, dtype=np.float64).reshape(3)
+        if self.values.ndim != 4 or self.values.shape[3] != 4:
+            raise InvalidParameterError("color volume must have shape (X, Y, Z, 4)")
+        if not np.all(np.isfinite(self.values)):
+            raise InvalidParameterError("color volume contains non-finite entries")
+        if not np.all(self.box_max > self.box_min):
+            raise InvalidParameterError("world box must have positive extent on each axis")
+
+    @property
+    def dims(self):
+        return self.values.shape[:3]
+
+    @property
+    def voxel_size(self):
+        return (self.box_max - self.box_min) / np.asarray(self.values.shape[:3], dtype=np.float64)
+
+
+@dataclass
 class TransferFunction:
     """R texels of (r, g, b, tau) with linear interpolation (field.py:108-127)."""
 
@@ -305,6 +333,75 @@ def render_forward_grad(volume, tf, cam, cfg, *, threads: int = 1):
     img, jac = R.forward_grad(dens, tex, cams, cfg.dt, rig, cfg.target, cells=R.pack_cells(dens))
     return (ImageRGBA(img[0].to(torch.float64).cpu().numpy()),
             jac[0].to(torch.float64).cpu().numpy())
+
+
+def _upload_color(cv, cam, dev):
+    values = np.asarray(cv.values)
+    if values.ndim != 4 or values.shape[3] != 4:
+        raise InvalidParameterError("color volume must have shape (X, Y, Z, 4)")
+    col = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
+    ll = torch.tensor([[float(cam.lon_deg), float(cam.lat_deg)]], dtype=torch.float64)
+    cams = R.camera_array(ll.to(dev), float(cam.radius),
+                          tuple(np.asarray(cam.center, np.float64).reshape(3)),
+                          float(cam.fov_y_deg))
+    rig = R.Rig(int(cam.width), int(cam.height),
+                tuple(np.asarray(cv.box_min, np.float64).reshape(3)),
+                tuple(np.asarray(cv.box_max, np.float64).reshape(3)))
+    return col, cams, rig
+
+
+def render_colorvol(cv, cam, cfg, *, threads: int = 1) -> ImageRGBA:
+    """Render a pre-shaded colour volume (renderer.py:404-407)."""
+    _validate_config(cfg)
+    dev = _device()
+    col, cams, rig = _upload_color(cv, cam, dev)
+    img, depth = R.forward_color(col, cams, cfg.dt, rig, early_stop=(cfg.target == "none"))
+    return _image_from(img, depth)
+
+
+def render_colorvol_adjoint(cv, cam, cfg, seed, *, threads: int = 1, image=None) -> GradientSet:
+    """Adjoint for the pre-shaded colour volume; target must be ``volume`` (renderer.py:703-709)."""
+    _validate_config(cfg)
+    if cfg.target != "volume":
+        raise UnsupportedConfigurationError("color volumes differentiate per-voxel rgba only")
+    seed_arr = seed.data if hasattr(seed, "data") and not isinstance(seed, np.ndarray) else seed
+    seed_arr = np.asarray(seed_arr, dtype=np.float64)
+    H, W = int(cam.height), int(cam.width)
+    if seed_arr.shape != (H, W, 4):
+        raise InvalidInputError(f"seed shape {seed_arr.shape} does not match image {(H, W, 4)}")
+    dev = _device()
+    col, cams, rig = _upload_color(cv, cam, dev)
+    stored = getattr(cfg, "memory_mode", "inversion") == "stored"
+    tape, stride, n_steps = None, 0, None
+    if stored:
+        n_steps = _stored_tape_len(cams, cfg.dt, rig)
+        stride = max(int(n_steps.max().item()), 1)
+        tape = torch.empty(H * W * stride, dtype=torch.float32, device=dev)
+    if image is None or stored:
+        img_t, depth_t = R.forward_color(col, cams, cfg.dt, rig, tape=tape, tape_stride=stride)
+    else:
+        img_arr = image.data if hasattr(image, "data") and not isinstance(image, np.ndarray) \
+            else image
+        img_arr = np.asarray(img_arr, np.float64)
+        if img_arr.shape != (H, W, 4):
+            raise InvalidInputError("provided image does not match the camera size")
+        img_t = torch.from_numpy(img_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
+        s_np = getattr(image, "_ddvr_depth", None)
+        if s_np is None or np.shape(s_np) != (H, W):
+            with np.errstate(divide="ignore"):
+                s_np = -np.log1p(-np.clip(img_arr[..., 3], 0.0, 1.0))
+        depth_t = torch.from_numpy(np.asarray(s_np, np.float32)).to(dev).reshape(1, H, W)
+    seed_t = torch.from_numpy(seed_arr.astype(np.float32)).to(dev).reshape(1, H, W, 4)
+    d_col = torch.zeros_like(col)
+    R.adjoint_color(col, cams, cfg.dt, rig, img_t, depth_t, seed_t, d_col, tape=tape,
+                    tape_stride=stride)
+    if stored:
+        n_cpu = n_steps[0].cpu().numpy()
+        state = 8 * H * W + sum(int(n_cpu[r:r + TILE_ROWS].max()) * n_cpu[r:r + TILE_ROWS].size
+                                for r in range(0, H, TILE_ROWS))
+    else:
+        state = 8 * H * W
+    return GradientSet(d_color=d_col.to(torch.float64).cpu().numpy(), state_floats=int(state))
 
 
 def _stored_tape_len(cams, dt, rig):

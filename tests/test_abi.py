@@ -34,6 +34,7 @@ def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes",
                             "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
+                            "ddvr_forward_color", "ddvr_adjoint_color",
                             "ddvr_l1_loss",
                             "ddvr_ray_setup", "ddvr_prior_volume", "ddvr_prior_tf",
                             "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_last_error",

@@ -66,6 +66,12 @@ def test_volume_and_tf_validation():
         vd.DensityVolume(np.zeros((2, 2, 2)), box_min=[0, 0, 0], box_max=[1, 0, 1])
     with pytest.raises(vd.InvalidParameterError):
         vd.TransferFunction(np.zeros((3, 3)))
+    with pytest.raises(vd.InvalidParameterError):     # field.py:80-105
+        vd.ColorVolume(np.zeros((2, 2, 2, 3)))
+    with pytest.raises(vd.InvalidParameterError):
+        vd.ColorVolume(np.full((2, 2, 2, 4), np.inf))
+    cv = vd.ColorVolume(np.zeros((3, 4, 5, 4)), box_min=[0, 0, 0], box_max=[3, 2, 1])
+    assert cv.dims == (3, 4, 5) and np.allclose(cv.voxel_size, [1.0, 0.5, 0.2])
 
 
 def test_blend_known_answers():   # test_renderer.py:42-59

@@ -130,3 +130,20 @@ def test_inversion_equals_stored_in_fixtures():
         g = golden(name)
         for t in ("tf", "volume", "camera", "stepsize"):
             assert rel_max(g[f"inversion_{t}"], g[f"stored_{t}"]) < 1e-5
+
+
+@pytest.mark.parametrize("key", ["a", "b", "c"])
+def test_oracle_color_volume(key):
+    """render_colorvol / render_colorvol_adjoint (renderer.py:404-407, 703-709)."""
+    g = golden("color")
+    lon, lat, radius, cx, cy, cz, fov, W, H = g[f"{key}_cam"]
+    cg = O.ColorGrid(g[f"{key}_values"].astype(np.float64), g[f"{key}_box"][0],
+                     g[f"{key}_box"][1])
+    view = O.View(lon, lat, radius, (cx, cy, cz), fov, int(W), int(H))
+    dt = float(g[f"{key}_dt"])
+    assert rel_max(O.render_color_view(cg, view, dt), g[f"{key}_image"]) <= TOL
+    assert rel_max(O.render_color_view(cg, view, dt, early_stop=True),
+                   g[f"{key}_image_none"]) <= TOL
+    for mode in ("inversion", "stored"):
+        got = O.adjoint_color_view(cg, view, dt, g[f"{key}_seed"], stored=(mode == "stored"))
+        assert rel_max(got, g[f"{key}_{mode}_d_color"]) <= TOL
