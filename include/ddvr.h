@@ -216,6 +216,24 @@ int ddvr_adam_step(float* params, const float* grads, float* m, float* v, int64_
 /* upsample_volume (optim.py:92-129): dst (2X,2Y,2Z) from src (X,Y,Z). */
 int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, void* stream);
 
+/* ---- wire / disk formats (fileio.py:27-127) ------------------------------ */
+
+/* Raw volume file -> device volume.  `raw` holds the file's little-endian f32
+ * values in x-fastest order (fileio.py:32, 65: order="F"), already copied to
+ * the device; `dst` receives the (X,Y,Z) z-fastest layout every other entry
+ * point takes.  value_range = NULL or {lo, hi}: fused (v - lo) / (hi - lo)
+ * normalisation (fileio.py:66-70), hi > lo.  Replaces the numpy reshape in
+ * voldiff.fileio.load_volume (fileio.py:45-71). */
+int ddvr_volume_from_raw(const float* raw, const int32_t dims[3], const double* value_range,
+                         float* dst, void* stream);
+
+/* Device (X,Y,Z) volume -> x-fastest raw file body (save_volume, fileio.py:27-40). */
+int ddvr_volume_to_raw(const float* src, const int32_t dims[3], float* raw, void* stream);
+
+/* n_pixels premultiplied rgba float4 -> 3*n_pixels bytes of binary-PPM body
+ * composited over white (save_image, fileio.py:104-110). */
+int ddvr_image_to_ppm(const float* images, int64_t n_pixels, uint8_t* out, void* stream);
+
 /* Thread-local message of the last failing call ("" if none). */
 const char* ddvr_last_error(void);
 

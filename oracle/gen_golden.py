@@ -282,9 +282,45 @@ def optim_cases():
          proj_tf_in=tex * 40.0, proj_tf=proj_tf, up_src=small, up=up)
 
 
+def io_cases():
+    """Files written by the reference's fileio (fileio.py:27-127) + fibonacci_views poses."""
+    import json
+    from voldiff import fileio as vf
+    from voldiff import tasks as vt
+    d = os.path.join(OUT, "io")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(12)
+    vol = vd.DensityVolume(f32(rng.uniform(0, 1, (5, 6, 7))), [-1, -2, -3], [1, 2, 3])
+    vf.save_volume(vol, os.path.join(d, "vol_a"))
+    counts = np.round(rng.uniform(0, 4095, (6, 4, 5))).astype("<f4")
+    vf.save_volume(vd.DensityVolume(counts.astype(np.float64) / 4095.0), os.path.join(d, "vol_r"))
+    with open(os.path.join(d, "vol_r.raw"), "wb") as fh:
+        fh.write(counts.ravel(order="F").tobytes())
+    meta = json.load(open(os.path.join(d, "vol_r.json")))
+    meta["value_range"] = [100.0, 4095.0]
+    with open(os.path.join(d, "vol_r.json"), "w") as fh:
+        json.dump(meta, fh)
+    vol_r = vf.load_volume(os.path.join(d, "vol_r.raw"))
+    tf = vd.TransferFunction(f32(rng.uniform(0, 2, (5, 4))))
+    vf.save_tf(tf, os.path.join(d, "tf.json"))
+    img = np.zeros((5, 7, 4))
+    img[..., 3] = f32(rng.uniform(0, 1, (5, 7)))
+    img[..., :3] = f32(img[..., 3:4] * rng.uniform(0, 1.1, (5, 7, 3)))   # some rgb > alpha
+    img[0, 0] = 0.0
+    img[0, 1] = [1.0, 0.0, 0.0, 1.0]
+    img = vr.ImageRGBA(img)
+    vf.save_image(img, os.path.join(d, "img.ppm"))
+    vf.save_image(img, os.path.join(d, "img.rgba"))
+    views = vt.fibonacci_views(13, 2.5, (0.1, 0.0, -0.2), 35.0, 16, 12)
+    save("io", vol_a=vol.values, vol_r=vol_r.values, texels=tf.texels, image=img.data,
+         fib=np.array([[c.lon_deg, c.lat_deg] for c in views]))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad", "color"]
+    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad", "color", "io"]
+    if "io" in which:
+        io_cases()
     if "color" in which:
         color_cases()
     if "optim" in which:

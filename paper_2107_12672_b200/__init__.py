@@ -32,6 +32,7 @@ from .voldiff_api import (
     blend,
     blend_adjoint,
     blend_invert,
+    fibonacci_views,
     l1_loss,
     render,
     render_adjoint,
@@ -50,6 +51,7 @@ from .raymarch import (
     pack_cells,
     render_views,
 )
+from . import fileio
 from .scenes import CONFIGS, absorption_ramp_texels, fibonacci_poses, phantom, preset_texels
 
 __version__ = "0.1.0"
@@ -60,7 +62,8 @@ __all__ = [
     "VoldiffError", "EPS_ALPHA", "EPS_POLE_DEG", "DensityVolume", "GradientSet", "ImageRGBA",
     "RenderConfig", "SphericalCamera", "TransferFunction", "blend", "blend_adjoint",
     "blend_invert", "l1_loss", "render", "render_adjoint", "render_forward_grad",
-    "ColorVolume", "render_colorvol", "render_colorvol_adjoint", "DiffDVR",
+    "ColorVolume", "render_colorvol", "render_colorvol_adjoint", "fibonacci_views", "fileio",
+    "DiffDVR",
     "Rig", "adjoint", "camera_array", "forward", "forward_grad", "l1_loss_seed", "pack_cells",
     "render_views", "CONFIGS",
     "absorption_ramp_texels", "fibonacci_poses", "phantom", "preset_texels",

@@ -35,7 +35,8 @@ EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes", "ddv
             "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
             "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_ray_setup",
             "ddvr_prior_volume",
-            "ddvr_prior_tf", "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_last_error",
+            "ddvr_prior_tf", "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_volume_from_raw",
+            "ddvr_volume_to_raw", "ddvr_image_to_ppm", "ddvr_last_error",
             "ddvr_abi_version", "ddvr_launch_count")
 
 
@@ -115,6 +116,12 @@ def _bind(lib):
     lib.ddvr_adam_step.restype = ctypes.c_int
     lib.ddvr_upsample_volume.argtypes = [vp, i3, vp, vp]
     lib.ddvr_upsample_volume.restype = ctypes.c_int
+    lib.ddvr_volume_from_raw.argtypes = [vp, i3, P(ctypes.c_double), vp, vp]
+    lib.ddvr_volume_from_raw.restype = ctypes.c_int
+    lib.ddvr_volume_to_raw.argtypes = [vp, i3, vp, vp]
+    lib.ddvr_volume_to_raw.restype = ctypes.c_int
+    lib.ddvr_image_to_ppm.argtypes = [vp, ctypes.c_int64, vp, vp]
+    lib.ddvr_image_to_ppm.restype = ctypes.c_int
     lib.ddvr_last_error.argtypes = []
     lib.ddvr_last_error.restype = ctypes.c_char_p
     lib.ddvr_abi_version.argtypes = []

@@ -374,6 +374,55 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
   }
 }
 
+// Swap the outer and inner axes of a C-order (A,B,C) float array into (C,B,A):
+// the raw file is x-fastest (fileio.py:32, 65), the device volume z-fastest.
+// 32x32 tiles through padded shared memory so both the read (along C) and the
+// write (along A) are 128-byte coalesced; blockIdx.z walks B.  With a value
+// range the load-side normalisation (fileio.py:66-70) is fused, computed in
+// fp64 and rounded once, which is what the reference's float64 result becomes
+// when it is rounded to the device's fp32.
+constexpr int kSwapTile = 32;
+template <bool NORM>
+__global__ void __launch_bounds__(256) swap_xz_kernel(const float* __restrict__ src, int A, int B,
+                                                      int C, double lo, double span,
+                                                      float* __restrict__ dst) {
+  __shared__ float tile[kSwapTile][kSwapTile + 1];
+  const int c0 = blockIdx.x * kSwapTile, a0 = blockIdx.y * kSwapTile;
+  for (int b = blockIdx.z; b < B; b += gridDim.z) {
+    for (int i = threadIdx.y; i < kSwapTile; i += 8) {
+      const int a = a0 + i, c = c0 + threadIdx.x;
+      if (a < A && c < C) {
+        float v = __ldg(src + ((long long)a * B + b) * C + c);
+        if (NORM) v = (float)__ddiv_rn(__dsub_rn((double)v, lo), span);
+        tile[i][threadIdx.x] = v;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < kSwapTile; i += 8) {
+      const int c = c0 + i, a = a0 + threadIdx.x;
+      if (a < A && c < C) dst[((long long)c * B + b) * A + a] = tile[threadIdx.x][i];
+    }
+    __syncthreads();
+  }
+}
+
+// Binary PPM body over white (fileio.py:104-110): rgb + (1 - alpha), clamped to
+// [0,1], x255, rounded half-to-even like np.round; fp64 from the fp32 image.
+__global__ void __launch_bounds__(256) ppm_kernel(const float4* __restrict__ img, long long n,
+                                                  uint8_t* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float4 p = img[i];
+    const double w = 1.0 - (double)p.w;
+    const float ch[3] = {p.x, p.y, p.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double v = fmin(fmax((double)ch[k] + w, 0.0), 1.0);
+      out[3 * i + k] = (uint8_t)__double2int_rn(255.0 * v);
+    }
+  }
+}
+
 int grid_blocks(long long n) {
   long long b = (n + 255) / 256;
   return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -640,6 +689,54 @@ int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, vo
   upsample_kernel<<<grid_blocks(8LL * dims[0] * dims[1] * dims[2]), 256, 0,
                     (cudaStream_t)stream>>>(src, dims[0], dims[1], dims[2], dst);
   return check_launch("upsample_kernel");
+}
+
+static int swap_xz(const float* src, int A, int B, int C, const double* range, float* dst,
+                   void* stream) {
+  const dim3 grid((C + kSwapTile - 1) / kSwapTile, (A + kSwapTile - 1) / kSwapTile,
+                  B < 65535 ? B : 65535);
+  if ((long long)grid.y > 65535) return set_error(DDVR_UNSUPPORTED, "volume axis too large");
+  if (range) {
+    swap_xz_kernel<true><<<grid, dim3(kSwapTile, 8), 0, (cudaStream_t)stream>>>(
+        src, A, B, C, range[0], range[1] - range[0], dst);
+  } else {
+    swap_xz_kernel<false><<<grid, dim3(kSwapTile, 8), 0, (cudaStream_t)stream>>>(
+        src, A, B, C, 0.0, 1.0, dst);
+  }
+  return check_launch("swap_xz_kernel");
+}
+
+int ddvr_volume_from_raw(const float* raw, const int32_t dims[3], const double* value_range,
+                         float* dst, void* stream) {
+  g_err[0] = 0;
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+    return set_error(DDVR_INVALID_PARAMETER, "volume values must be a non-empty 3D array");
+  if (value_range && !(value_range[1] > value_range[0]))
+    return set_error(DDVR_INVALID_PARAMETER, "value_range must be increasing");
+  if (!raw || !dst) return set_error(DDVR_INVALID_INPUT, "volume pointer is NULL");
+  if (raw == dst) return set_error(DDVR_INVALID_INPUT, "in-place layout swap is not supported");
+  return swap_xz(raw, dims[2], dims[1], dims[0], value_range, dst, stream);
+}
+
+int ddvr_volume_to_raw(const float* src, const int32_t dims[3], float* raw, void* stream) {
+  g_err[0] = 0;
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+    return set_error(DDVR_INVALID_PARAMETER, "volume values must be a non-empty 3D array");
+  if (!raw || !src) return set_error(DDVR_INVALID_INPUT, "volume pointer is NULL");
+  if (raw == src) return set_error(DDVR_INVALID_INPUT, "in-place layout swap is not supported");
+  return swap_xz(src, dims[0], dims[1], dims[2], nullptr, raw, stream);
+}
+
+int ddvr_image_to_ppm(const float* images, int64_t n_pixels, uint8_t* out, void* stream) {
+  g_err[0] = 0;
+  if (n_pixels < 0) return set_error(DDVR_INVALID_PARAMETER, "negative pixel count");
+  if (n_pixels == 0) return DDVR_OK;
+  if (!images || !out) return set_error(DDVR_INVALID_INPUT, "image pointer is NULL");
+  if (reinterpret_cast<uintptr_t>(images) & 15)
+    return set_error(DDVR_INVALID_INPUT, "images must be 16-byte aligned");
+  ppm_kernel<<<grid_blocks(n_pixels), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(images), n_pixels, out);
+  return check_launch("ppm_kernel");
 }
 
 }  // extern "C"

@@ -318,6 +318,14 @@ def render(volume, tf, cam, cfg, *, threads: int = 1) -> ImageRGBA:
     return _image_from(img, depth)
 
 
+def fibonacci_views(count: int, radius: float, center=(0.0, 0.0, 0.0), fov_y_deg: float = 30.0,
+                    width: int = 64, height: int = 64):
+    """Golden-angle spiral of cameras on the sphere (tasks.py:118-128)."""
+    from .scenes import fibonacci_poses
+    return [SphericalCamera(lon, lat, radius, center, fov_y_deg, width, height)
+            for lon, lat in fibonacci_poses(count)]
+
+
 def render_forward_grad(volume, tf, cam, cfg, *, threads: int = 1):
     """Image and its per-pixel Jacobian by forward mode (renderer.py:410-464).
 
