@@ -51,23 +51,36 @@ def _run(cmd):
     return proc.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+VARIANTS = os.path.join(HERE, "_variants")
+
+
+def build_variant(name: str, defines) -> str:
+    """Experiment build with extra -D switches into _variants/libddvr_<name>.so
+    (select it at run time with DDVR_LIB=<path>); the product is build()."""
+    return build(force=True, out=os.path.join(VARIANTS, f"libddvr_{name}.so"),
+                 obj=os.path.join(OBJ, "v_" + name), extra=[f"-D{d}" for d in defines])
+
+
+def build(force: bool = False, verbose: bool = False, out: str = OUT, obj: str = OBJ,
+          extra=()) -> str:
     """Compile csrc/*.cu into libddvr.so next to this file; return its path."""
     if not force and not stale():
         return OUT
-    os.makedirs(OBJ, exist_ok=True)
-    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    OUT_, OBJ_ = out, obj
+    os.makedirs(OBJ_, exist_ok=True)
+    os.makedirs(os.path.dirname(OUT_), exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, *extra]
     jobs = []
     for src in sources():
-        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-        jobs.append((obj, [nvcc(), *NVCC_FLAGS, "-Xptxas", "-v", *inc, "-c", "-o", obj, src]))
+        o = os.path.join(OBJ_, os.path.basename(src)[:-3] + ".o")
+        jobs.append((o, [nvcc(), *NVCC_FLAGS, "-Xptxas", "-v", *inc, "-c", "-o", o, src]))
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         logs = list(ex.map(lambda j: _run(j[1]), jobs))
     if verbose:
         sys.stderr.write("".join(logs))
-    _run([nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *[o for o, _ in jobs]])
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    _run([nvcc(), *ARCH, "-shared", "-o", OUT_ + ".tmp", *[o for o, _ in jobs]])
+    os.replace(OUT_ + ".tmp", OUT_)
+    return OUT_
 
 
 if __name__ == "__main__":

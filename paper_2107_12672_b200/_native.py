@@ -17,7 +17,8 @@ from .errors import (
     VoldiffError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libddvr.so")
+LIB_PATH = os.environ.get("DDVR_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                      "libddvr.so")
 ABI_VERSION = 1
 
 TARGET_CAMERA = 1

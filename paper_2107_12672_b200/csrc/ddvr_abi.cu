@@ -28,9 +28,10 @@ int check_launch(const char* what) {
 // cell-record layout: pack (volume -> cells) and fold (cell gradients -> voxels)
 // ---------------------------------------------------------------------------
 
-// Padded record of cell (i,j,k), i in [-1, X-1] (storage index i+1):
-//   cells[c] = v[clamp(i+bx, 0, X-1)][clamp(j+by, 0, Y-1)][clamp(k+bz, 0, Z-1)],
-//   c = bx | by << 1 | bz << 2 (the corner order of field.py:318-322).
+// Padded record of cell (i,j,k), i in [-1, X-1] (storage index i+1): the
+// polynomial coefficients (corners_to_poly) of its 8 edge-clamped corners
+//   v[b] = vol[clamp(i+bx, 0, X-1)][clamp(j+by, 0, Y-1)][clamp(k+bz, 0, Z-1)],
+//   b = bx | by << 1 | bz << 2 (the corner order of field.py:318-322).
 __global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __restrict__ cells,
                                                        long long ncells) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -43,15 +44,33 @@ __global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __res
   const int i1 = min(i + 1, V.X - 1), j1 = min(j + 1, V.Y - 1), k1 = min(k + 1, V.Z - 1);
   const float* p = V.data;
   auto at = [&](int a, int b, int c) { return __ldg(p + ((size_t)a * V.Y + b) * V.Z + c); };
-  const float4 lo = make_float4(at(i0, j0, k0), at(i1, j0, k0), at(i0, j1, k0), at(i1, j1, k0));
-  const float4 hi = make_float4(at(i0, j0, k1), at(i1, j0, k1), at(i0, j1, k1), at(i1, j1, k1));
+  const float v[8] = {at(i0, j0, k0), at(i1, j0, k0), at(i0, j1, k0), at(i1, j1, k0),
+                      at(i0, j0, k1), at(i1, j0, k1), at(i0, j1, k1), at(i1, j1, k1)};
+  float k8[8];
+  corners_to_poly(v, k8);
   float4* q = reinterpret_cast<float4*>(cells + 8 * id);
-  q[0] = lo;
-  q[1] = hi;
+  q[0] = make_float4(k8[0], k8[1], k8[2], k8[3]);
+  q[1] = make_float4(k8[4], k8[5], k8[6], k8[7]);
 }
 
-// d_volume[x,y,z] += every cell-gradient slot that pack_cells_kernel filled
-// from voxel (x,y,z) (its exact transpose, padding included)
+// gradient of corner b of a record from the record's moment gradient m
+// (d rho / d v_b = sum_k L[k][b] phi_k, so g_b = sum_k L[k][b] m_k)
+__device__ __forceinline__ float corner_from_moments(const float4& a, const float4& h, int b) {
+  const float sx = (b & 1) ? 1.f : -1.f, sy = (b & 2) ? 1.f : -1.f, sz = (b & 4) ? 1.f : -1.f;
+  float g = a.x * 0.125f;
+  g = fmaf(0.25f * sx, a.y, g);
+  g = fmaf(0.25f * sy, a.z, g);
+  g = fmaf(0.25f * sz, a.w, g);
+  g = fmaf(0.5f * sx * sy, h.x, g);
+  g = fmaf(0.5f * sx * sz, h.y, g);
+  g = fmaf(0.5f * sy * sz, h.z, g);
+  return fmaf(sx * sy * sz, h.w, g);
+}
+
+// d_volume[x,y,z] += the gradient of every record corner that pack_cells_kernel
+// filled from voxel (x,y,z) (its exact transpose, padding included); the
+// adjoint leaves each record's moment gradient, mapped back per corner here
+// (one 32-byte sector per contributing record, as the corner form read)
 __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
                                                        const float* __restrict__ d_cells,
                                                        float* __restrict__ d_volume,
@@ -85,7 +104,8 @@ __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
     for (int b = 0; b < cn[1]; ++b)
       for (int c = 0; c < cn[2]; ++c) {
         const size_t cell = ((size_t)ci[0][a] * V.CY + ci[1][b]) * V.CZ + ci[2][c];
-        s += d_cells[8 * cell + (cb[0][a] | cb[1][b] << 1 | cb[2][c] << 2)];
+        const float4* m = reinterpret_cast<const float4*>(d_cells + 8 * cell);
+        s += corner_from_moments(m[0], m[1], cb[0][a] | cb[1][b] << 1 | cb[2][c] << 2);
       }
   d_volume[id] += s;
 }

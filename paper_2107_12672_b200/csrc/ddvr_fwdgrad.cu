@@ -68,18 +68,16 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_grad_kernel(VolArgs V, T
   for (int i = 0; i < r.n; ++i) {
     Cell c;
     locate<CELLS>(V, gx, gy, gz, r.all_inside, c);
-    float v[8], p0, p1;
+    float v[8];
     fetch8<CELLS>(V, c, v);
-    const float raw = interp(c, v, p0, p1);
+    const Interp ip = interp(c, v);
+    const float raw = ip.rho;
     const float d = clamp_density(c.inside, raw);
     const bool live = c.inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
     // spatial gradient in grid units, zero where the edge clamp froze the axis
-    const float ey = 1.f - c.fy, ez = 1.f - c.fz;
-    float ddx = ez * (ey * (v[1] - v[0]) + c.fy * (v[3] - v[2])) +
-                c.fz * (ey * (v[5] - v[4]) + c.fy * (v[7] - v[6]));
-    float ddy = ez * ((1.f - c.fx) * (v[2] - v[0]) + c.fx * (v[3] - v[1])) +
-                c.fz * ((1.f - c.fx) * (v[6] - v[4]) + c.fx * (v[7] - v[5]));
-    float ddz = p1 - p0;
+    float ddx = ip.gx;
+    float ddy = interp_gy(c, v);
+    float ddz = interp_gz(c, ip);
     ddx = (live && gx >= 0 && gx <= V.top[0]) ? ddx : 0.f;
     ddy = (live && gy >= 0 && gy <= V.top[1]) ? ddy : 0.f;
     ddz = (live && gz >= 0 && gz <= V.top[2]) ? ddz : 0.f;

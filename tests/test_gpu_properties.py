@@ -72,8 +72,16 @@ def test_autograd_only_requested_targets(cuda):
     assert dens.grad is not None and tx.grad is None and ll.grad is None
 
 
-@pytest.mark.parametrize("case", ["inside_box", "tiny_dt", "big_dt", "R2048", "row_band",
-                                  "one_pixel"])
+# R2048: 2048 independent random texels (slope ~ +-2000, a kink at every texel
+# boundary) put the gradients on the fp32 floor: the fp64 oracle itself moves
+# by up to 1.37e-4 (camera) under fp32-level density noise
+# (tools/fp32_floor_r2048.py), so that case is held to 2.5x its floor; the
+# smooth 2048-texel table (R2048s) keeps the standard bar.
+GRAD_BAR = {"R2048": 3.5e-4}
+
+
+@pytest.mark.parametrize("case", ["inside_box", "tiny_dt", "big_dt", "R2048", "R2048s",
+                                  "row_band", "one_pixel"])
 def test_edge_cases_match_oracle(cuda, case):
     torch = _t()
     from oracle import dvr_oracle as O
@@ -90,6 +98,10 @@ def test_edge_cases_match_oracle(cuda, case):
         dt = 0.7
     elif case == "R2048":
         tex = rng.uniform(0.05, 1.0, (2048, 4)).astype(np.float32)
+    elif case == "R2048s":
+        x = (np.arange(2048) + 0.5) / 2048
+        tex = np.stack([0.5 + 0.4 * np.sin(6 * x + k) for k in range(3)] +
+                       [2.0 + 1.5 * np.sin(9 * x)], axis=1).astype(np.float32)
     elif case == "row_band":
         rows = (3, 6)
     elif case == "one_pixel":
@@ -120,7 +132,7 @@ def test_edge_cases_match_oracle(cuda, case):
             if np.linalg.norm(ref) == 0:
                 assert np.abs(got).max() == 0.0
             else:
-                assert rel_l2(got, ref) <= 1e-4, (case, k, rel_l2(got, ref))
+                assert rel_l2(got, ref) <= GRAD_BAR.get(case, 1e-4), (case, k, rel_l2(got, ref))
 
 
 def _band_oracle(vol, tex, view, dt, seed, rows):
@@ -255,3 +267,45 @@ def test_analytic_tf_modes_match_oracle(cuda, kind):
         tex = torch.from_numpy(params[:, 1:].copy()).to(cuda)
         img_t, _ = R.forward(dens, tex, cams, dt, rig)
         assert rel_l2(img.cpu().numpy(), img_t.cpu().numpy()) <= 1e-6
+
+
+def test_cell_records_are_the_trilinear_polynomial(cuda):
+    """ddvr_pack_cells: padded, edge-clamped records of the polynomial
+    coefficients {c0, cx, cy, cz, cxy, cxz, cyz, cxyz} in u = f - 1/2; the
+    polynomial equals the reference's lerp form (field.py:318-349)."""
+    torch = _t()
+    from paper_2107_12672_b200 import raymarch as R
+    rng = np.random.default_rng(5)
+    vol = rng.uniform(0, 1, (5, 4, 3)).astype(np.float32)
+    cells = R.pack_cells(torch.from_numpy(vol).to(cuda)).cpu().numpy().astype(np.float64)
+    X, Y, Z = vol.shape
+    rec = cells.reshape(X + 1, Y + 1, Z + 1, 8)
+    v64 = vol.astype(np.float64)
+    s = np.array([[(1 if b & 1 << a else -1) for a in range(3)] for b in range(8)], np.float64)
+    for i in range(-1, X):
+        for j in range(-1, Y):
+            for k in range(-1, Z):
+                corner = np.array([v64[min(max(i + (b & 1), 0), X - 1),
+                                       min(max(j + (b >> 1 & 1), 0), Y - 1),
+                                       min(max(k + (b >> 2 & 1), 0), Z - 1)] for b in range(8)])
+                want = np.array([corner.sum() / 8,
+                                 (s[:, 0] * corner).sum() / 4, (s[:, 1] * corner).sum() / 4,
+                                 (s[:, 2] * corner).sum() / 4,
+                                 (s[:, 0] * s[:, 1] * corner).sum() / 2,
+                                 (s[:, 0] * s[:, 2] * corner).sum() / 2,
+                                 (s[:, 1] * s[:, 2] * corner).sum() / 2,
+                                 (s[:, 0] * s[:, 1] * s[:, 2] * corner).sum()])
+                got = rec[i + 1, j + 1, k + 1]
+                np.testing.assert_allclose(got, want, atol=4e-7)
+                for _ in range(3):   # polynomial == x-then-y-then-z lerps
+                    f = rng.uniform(0, 1, 3)
+                    ux, uy, uz = f - 0.5
+                    poly = (got[0] + got[1] * ux + got[2] * uy + got[3] * uz + got[4] * ux * uy
+                            + got[5] * ux * uz + got[6] * uy * uz + got[7] * ux * uy * uz)
+                    a = [corner[b] + f[0] * (corner[b + 1] - corner[b]) for b in (0, 2, 4, 6)]
+                    p0 = a[0] + f[1] * (a[1] - a[0])
+                    p1 = a[2] + f[1] * (a[3] - a[2])
+                    assert abs(poly - (p0 + f[2] * (p1 - p0))) < 1e-6
+                # a replicated (clamped) axis has exactly zero odd coefficients
+                if i in (-1, X - 1):
+                    assert got[1] == got[4] == got[5] == got[7] == 0.0
