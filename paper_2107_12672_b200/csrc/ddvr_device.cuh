@@ -126,10 +126,15 @@ DDVR_ADJ_LAUNCHER(launch_adjoint_g1);   // masks 4-7   (tf [+ camera / stepsize]
 DDVR_ADJ_LAUNCHER(launch_adjoint_g2);   // masks 8-11  (volume [+ camera / stepsize])
 DDVR_ADJ_LAUNCHER(launch_adjoint_g3);   // masks 12-15 (volume + tf [+ ...])
 
+#ifndef DDVR_CARVEOUT
+#define DDVR_CARVEOUT -1
+#endif
 template <typename K>
 inline void set_smem(K kernel, size_t smem) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (DDVR_CARVEOUT >= 0)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, DDVR_CARVEOUT);
 }
 
 }  // namespace ddvr_impl
@@ -356,9 +361,12 @@ __device__ __forceinline__ void ld256(const float* p, float v[8]) {
 // the registers they hold.  A ray stays in one cell for ~3 samples at
 // dt = 0.2 voxel, so reloading only on a cell change cuts the L1 data-pipe
 // wavefronts of the gather (the binding unit) without a divergent branch.
+#ifndef DDVR_L2PF
+#define DDVR_L2PF ".L2::256B"   // measured +1.4% fwd, +0.8% adj at C4 (tools/locality_probe.py)
+#endif
 __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) {
   asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %8, 0;\n\t"
-      "@q ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%9];\n\t}"
+      "@q ld.global.nc" DDVR_L2PF ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%9];\n\t}"
       : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]),
         "+f"(v[7])
       : "r"((int)pred), "l"(p));
@@ -382,6 +390,13 @@ __device__ __forceinline__ void lds128_if(bool pred, const void* p, float4& q) {
 
 #ifndef DDVR_HOLD_CELL
 #define DDVR_HOLD_CELL 1
+#endif
+#ifndef DDVR_PIPE
+#define DDVR_PIPE 0   // measured: +0.6% at C4 (4 CTAs/SM vs 5), -2.9% at 128^3
+#endif
+
+#ifndef DDVR_ABS_WALK
+#define DDVR_ABS_WALK 1
 #endif
 #ifndef DDVR_HOLD_TEX
 #define DDVR_HOLD_TEX 0   // measured: no gain (shared lookups are not the binding wavefronts)
@@ -800,22 +815,11 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
   constexpr bool kHoldCell = CELLS && DDVR_HOLD_CELL;
   constexpr bool kHoldTex = KIND == kTfTexture && DDVR_HOLD_TEX;
-  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  int held = INT_MIN;
   TexHold<EMIT> tex;
-  for (int i = 0; i < r.n; ++i) {
-    if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
+  // one compositing step on a located sample and its record
+  auto composite = [&](const Cell& c, const float* k, int i) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
-    Cell c;
-    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
-    gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
-    if (kHoldCell) {
-      ld256_if(c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
-      held = c.cell;
-    } else {
-      fetch8<CELLS>(V, c, v);
-    }
-    const float d = clamp_density(INSIDE || c.inside, interp(c, v).rho);
+    const float d = clamp_density(INSIDE || c.inside, interp(c, k).rho);
     int i0; float w;
     float4 slope;
     const float4 s = kHoldTex ? tex.sample(TF, d, i0, w, slope, false)
@@ -830,6 +834,54 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     A = __fadd_rn(A, Ta);
     T = __fmul_rn(T, g.ome);
     S += (double)g.od;
+  };
+  if (kHoldCell && DDVR_PIPE) {
+    // Software-pipelined march: two record buffers, the gather of sample i+1
+    // is in flight while sample i composites (the kernel is bound by gather
+    // latency: ~70% of warp time in long-scoreboard stalls, ncu).  Each
+    // buffer keeps its record when its next cell is unchanged.
+    float va[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float vb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int ha = INT_MIN, hb = INT_MIN;
+    Cell ca, cb;
+    const bool ins = INSIDE || r.all_inside;
+    locate<CELLS>(V, gx, gy, gz, ins, ca);
+    ld256_if(r.n > 0, V.cell0 + 8 * (long long)ca.cell, va);
+    ha = ca.cell;
+#pragma unroll 1
+    for (int i = 0; i < r.n; i += 2) {
+      const bool more = i + 1 < r.n;
+      locate<CELLS>(V, gx + r.gs[0], gy + r.gs[1], gz + r.gs[2], ins, cb);
+      ld256_if(more && cb.cell != hb, V.cell0 + 8 * (long long)cb.cell, vb);
+      hb = more ? cb.cell : hb;
+      if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
+      composite(ca, va, i);
+      gx += 2 * r.gs[0]; gy += 2 * r.gs[1]; gz += 2 * r.gs[2];
+      locate<CELLS>(V, gx, gy, gz, ins, ca);
+      const bool next = i + 2 < r.n;
+      ld256_if(next && ca.cell != ha, V.cell0 + 8 * (long long)ca.cell, va);
+      ha = next ? ca.cell : ha;
+      if (!more || (EARLY && A > kAlphaStop)) break;
+      composite(cb, vb, i + 1);
+    }
+    rgba = make_float4(c0, c1, c2, A);
+    depth = S;
+    return;
+  }
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int held = INT_MIN;
+  for (int i = 0; i < r.n; ++i) {
+    if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
+    Cell c;
+    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
+    gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
+    if (kHoldCell) {
+      ld256_if(c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
+      held = c.cell;
+    } else {
+      fetch8<CELLS>(V, c, v);
+    }
+    composite(c, v, i);
   }
   rgba = make_float4(c0, c1, c2, A);
   depth = S;
@@ -984,6 +1036,17 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   constexpr bool kVol = MASK & DDVR_TARGET_VOLUME;
   constexpr bool kPos = kCam || kStep;
   constexpr bool kDhat = kPos || kVol;
+  // Absorption-only walk: with an emission-free TF (rgb texels all zero) and
+  // no TF target, the adjoint chain has a closed form.  The blend adjoint
+  // gives a_hat_i = seed_a * prod_{j>i} (1 - a_j) and T_{i-1} = prod_{j<i}
+  // (1 - a_j), so the Beer-Lambert term e_i * T_{i-1} * a_hat_i equals
+  // seed_a * T_n for every unclamped segment (e_i = 1 - a_i there) and 0 for
+  // a clamped one (renderer.py:583-596): tau_hat is a per-ray constant
+  // dt * seed_a * T_n, T_n = exp(-S) from the forward's optical depth.  No
+  // inversion, exp or fp64 per sample; identical in exact arithmetic to the
+  // inversion walk (and closer to it in fp32 than the walked chain).
+  constexpr bool kAbs = !EMIT && !kTf && !TAPE && KIND == kTfTexture && DDVR_ABS_WALK;
+  const float abs_c = kAbs ? sd.w * (float)exp(-S) : 0.f;   // seed_a * T_n
 
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
@@ -1025,10 +1088,10 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     // steps) and T_prev = exp(-S_prev) is computed fresh each step.  The fp32
     // chain T_prev = T/(1 - a) drifts to ~1e-4 on camera gradients by 2.6k steps.
     // ("stored" mode reads T_prev from the tape instead, renderer.py:576-577)
-    float Tp;
+    float Tp = 0.f;
     if (TAPE) {
       Tp = tape[i];
-    } else {
+    } else if (!kAbs) {
       S -= (double)g.od;
       asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(Tp) : "f"((float)S * -1.4426950408889634f));
     }
@@ -1041,10 +1104,10 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const float h0 = EMIT ? aT * sd.x : 0.f;   // d L / d rgb
     const float h1 = EMIT ? aT * sd.y : 0.f;
     const float h2 = EMIT ? aT * sd.z : 0.f;
-    a_hat = EMIT ? g.ome * a_hat - g.a * cdot : g.ome * a_hat;
+    if (!kAbs) a_hat = EMIT ? g.ome * a_hat - g.a * cdot : g.ome * a_hat;
     // Beer-Lambert adjoint (renderer.py:592-596)
     const float a_raw_hat = g.a_clamped ? 0.f : seg_a_hat;
-    const float ea = g.e * a_raw_hat;
+    const float ea = kAbs ? (g.a_clamped ? 0.f : abs_c) : g.e * a_raw_hat;
     const float tau_hat = s.w < 0.f ? 0.f : dt32 * ea;
     if (kStep) st.dt_bl += (double)(g.tau * ea);
 

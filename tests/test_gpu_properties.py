@@ -309,3 +309,42 @@ def test_cell_records_are_the_trilinear_polynomial(cuda):
                 # a replicated (clamped) axis has exactly zero odd coefficients
                 if i in (-1, X - 1):
                     assert got[1] == got[4] == got[5] == got[7] == 0.0
+
+
+@pytest.mark.parametrize("tau_scale,dt", [(3.0, 0.02), (60.0, 0.02), (4000.0, 0.05)])
+def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt):
+    """Emission-free TF, volume + camera + stepsize targets: the adjoint's
+    closed-form absorption walk (tau_hat = dt seed_a T_n per ray) against the
+    oracle's inversion walk.  The three scales select the degree-3, degree-7
+    and general opacity modes; the last has clamped segments (a > 1 - EPS)."""
+    torch = _t()
+    from oracle import dvr_oracle as O
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.scenes import absorption_ramp_texels
+    rng = np.random.default_rng(11)
+    vol = rng.uniform(0.0, 1.0, (9, 8, 7)).astype(np.float32)
+    tex = absorption_ramp_texels(32, tau_scale).astype(np.float32)
+    view = O.View(47.0, -18.0, 2.0, fov_y_deg=40.0, width=11, height=9)
+    seed = rng.normal(size=(9, 11, 4)).astype(np.float32)
+    targets = ["volume", "camera", "stepsize"]
+    (img_o,), (out,) = _oracle(vol, tex, [view], dt, [seed.astype(np.float64)], targets)
+    if tau_scale > 1000:   # the case must exercise the EPS clamp
+        assert img_o[..., 3].max() > 1 - 2e-6
+    dens = torch.from_numpy(vol).to(cuda)
+    tx = torch.from_numpy(tex).to(cuda)
+    cams = R.camera_array(torch.tensor([[47.0, -18.0]], dtype=torch.float64, device=cuda), 2.0,
+                          (0.0, 0.0, 0.0), 40.0)
+    rig = R.Rig(11, 9)
+    for cells in (R.pack_cells(dens), None):
+        img, depth = R.forward(dens, tx, cams, dt, rig, cells=cells)
+        assert rel_l2(img[0].cpu().numpy(), img_o) <= 1e-5
+        d = {"volume": torch.zeros_like(dens),
+             "camera": torch.zeros(1, 2, dtype=torch.float64, device=cuda),
+             "stepsize": torch.zeros(1, dtype=torch.float64, device=cuda)}
+        R.adjoint(dens, tx, cams, dt, rig, img, depth,
+                  torch.from_numpy(seed).to(cuda)[None].contiguous(), 11, d_volume=d["volume"],
+                  d_camera=d["camera"], d_dt=d["stepsize"], cells=cells)
+        for k in targets:
+            ref = np.asarray(out["d_" + k], np.float64)
+            got = d[k].double().cpu().numpy().reshape(ref.shape)
+            assert rel_l2(got, ref) <= 1e-4, (tau_scale, k, rel_l2(got, ref))
