@@ -816,6 +816,11 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   constexpr bool kHoldCell = CELLS && DDVR_HOLD_CELL;
   constexpr bool kHoldTex = KIND == kTfTexture && DDVR_HOLD_TEX;
   TexHold<EMIT> tex;
+  // Emission-free TF (rgb = 0) without tape or early stop: the compositing
+  // A += (1 - A) a_i (renderer.py:350-355) is exactly A = 1 - prod(1 - a_i)
+  // = -expm1(-S), S = sum of the segment optical depths min(dt tau, -ln EPS)
+  // the march sums anyway (fp64) -- so only S is carried per sample.
+  constexpr bool kAbs = !EMIT && !TAPE && !EARLY && KIND == kTfTexture && DDVR_ABS_WALK;
   // one compositing step on a located sample and its record
   auto composite = [&](const Cell& c, const float* k, int i) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
@@ -824,6 +829,11 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     float4 slope;
     const float4 s = kHoldTex ? tex.sample(TF, d, i0, w, slope, false)
                               : tf_sample<KIND, EMIT>(TF, d, i0, w, slope, false);
+    if (kAbs) {   // segment optical depth only (the EPS clamp of field.py:587-600)
+      const float x = __fmul_rn(dt32, fmaxf(s.w, 0.f));
+      S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
+      return;
+    }
     const Segment g = segment<SEG>(s.w, dt32);
     const float Ta = __fmul_rn(T, g.a);
     if (EMIT) {
@@ -864,12 +874,15 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       if (!more || (EARLY && A > kAlphaStop)) break;
       composite(cb, vb, i + 1);
     }
+    if (kAbs) A = (float)(-expm1(-S));
     rgba = make_float4(c0, c1, c2, A);
     depth = S;
     return;
   }
   float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int held = INT_MIN;
+  // (the emitting variants spill at 48 registers when unrolled)
+#pragma unroll (kAbs ? 4 : 1)
   for (int i = 0; i < r.n; ++i) {
     if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
     Cell c;
@@ -883,6 +896,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     }
     composite(c, v, i);
   }
+  if (kAbs) A = (float)(-expm1(-S));
   rgba = make_float4(c0, c1, c2, A);
   depth = S;
 }
