@@ -553,9 +553,10 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   }
   auto launch = mask <= 3 ? launch_adjoint_g0 : mask <= 7 ? launch_adjoint_g1
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;
-  launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed, d_volume, d_cells, d_tf,
-         d_camera, d_dt);
+  const int n_kernels = launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed,
+                               d_volume, d_cells, d_tf, d_camera, d_dt);
   if ((rc = check_launch("dvr_adjoint_kernel"))) return rc;
+  g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
   if (d_cells) {
     const long long nvox = (long long)V.X * V.Y * V.Z;
     fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells_all, d_volume,

@@ -4,35 +4,37 @@
 namespace ddvr_impl {
 
 template <unsigned M, bool CELLS>
-static void adj(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
-                const Geometry& G, const float* image, const float* depth, const float* seed,
-                float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
-  auto k = dvr_adjoint_kernel<M, CELLS>;
+static int adj(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
+               const Geometry& G, const float* image, const float* depth, const float* seed,
+               float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
+  auto k = dvr_adjoint_kernel<M, CELLS, 0>;
   set_smem(k, smem);
   k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
+  if constexpr (CELLS && !(M & DDVR_TARGET_TF)) {   // the absorption-only walk
+    auto k1 = dvr_adjoint_kernel<M, CELLS, 1>;
+    set_smem(k1, smem);
+    k1<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
+    return 2;
+  }
+  return 1;
 }
 
+#define DDVR_ADJ_ARGS grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt
 DDVR_ADJ_LAUNCHER(launch_adjoint_g1) {
   switch (mask) {
     case 4:
-      if (cells) adj<4, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<4, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<4, true>(DDVR_ADJ_ARGS) : adj<4, false>(DDVR_ADJ_ARGS);
     case 5:
-      if (cells) adj<5, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<5, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<5, true>(DDVR_ADJ_ARGS) : adj<5, false>(DDVR_ADJ_ARGS);
     case 6:
-      if (cells) adj<6, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<6, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<6, true>(DDVR_ADJ_ARGS) : adj<6, false>(DDVR_ADJ_ARGS);
     case 7:
-      if (cells) adj<7, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<7, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<7, true>(DDVR_ADJ_ARGS) : adj<7, false>(DDVR_ADJ_ARGS);
     default:
-      break;
+      return 0;
   }
 }
+
+#undef DDVR_ADJ_ARGS
 
 }  // namespace ddvr_impl

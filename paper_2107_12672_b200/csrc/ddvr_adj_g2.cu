@@ -4,35 +4,37 @@
 namespace ddvr_impl {
 
 template <unsigned M, bool CELLS>
-static void adj(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
-                const Geometry& G, const float* image, const float* depth, const float* seed,
-                float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
-  auto k = dvr_adjoint_kernel<M, CELLS>;
+static int adj(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
+               const Geometry& G, const float* image, const float* depth, const float* seed,
+               float* dv, float* dcells, double* dtf, double* dcam, double* ddt) {
+  auto k = dvr_adjoint_kernel<M, CELLS, 0>;
   set_smem(k, smem);
   k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
+  if constexpr (CELLS && !(M & DDVR_TARGET_TF)) {   // the absorption-only walk
+    auto k1 = dvr_adjoint_kernel<M, CELLS, 1>;
+    set_smem(k1, smem);
+    k1<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
+    return 2;
+  }
+  return 1;
 }
 
+#define DDVR_ADJ_ARGS grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt
 DDVR_ADJ_LAUNCHER(launch_adjoint_g2) {
   switch (mask) {
     case 8:
-      if (cells) adj<8, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<8, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<8, true>(DDVR_ADJ_ARGS) : adj<8, false>(DDVR_ADJ_ARGS);
     case 9:
-      if (cells) adj<9, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<9, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<9, true>(DDVR_ADJ_ARGS) : adj<9, false>(DDVR_ADJ_ARGS);
     case 10:
-      if (cells) adj<10, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<10, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<10, true>(DDVR_ADJ_ARGS) : adj<10, false>(DDVR_ADJ_ARGS);
     case 11:
-      if (cells) adj<11, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      else adj<11, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt);
-      break;
+      return cells ? adj<11, true>(DDVR_ADJ_ARGS) : adj<11, false>(DDVR_ADJ_ARGS);
     default:
-      break;
+      return 0;
   }
 }
+
+#undef DDVR_ADJ_ARGS
 
 }  // namespace ddvr_impl

@@ -117,7 +117,7 @@ void launch_adjoint_color(dim3 grid, cudaStream_t st, const VolArgs& V, const Ge
                           const float* image, const float* depth, const float* seed,
                           float* d_color);
 #define DDVR_ADJ_LAUNCHER(NAME)                                                              \
-  void NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
+  int NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
             const VolArgs& V, const TfArgs& T, const Geometry& G, const float* image,       \
             const float* depth, const float* seed, float* dv, float* dcells, double* dtf,   \
             double* dcam, double* ddt)
@@ -395,6 +395,12 @@ __device__ __forceinline__ void lds128_if(bool pred, const void* p, float4& q) {
 #define DDVR_PIPE 0   // measured: +0.6% at C4 (4 CTAs/SM vs 5), -2.9% at 128^3
 #endif
 
+#ifndef DDVR_ABS_UNROLL
+#define DDVR_ABS_UNROLL 1
+#endif
+#ifndef DDVR_ABS_MINB
+#define DDVR_ABS_MINB 5
+#endif
 #ifndef DDVR_ABS_WALK
 #define DDVR_ABS_WALK 1
 #endif
@@ -908,14 +914,18 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
 // choice swings between 64 and 95 registers for the volume-only walk with
 // unrelated code changes): volume-only fits 64 registers without spills
 // (4 CTAs/SM); the camera/stepsize walks carry fp64 sums (ptxas' choice).
-constexpr int adj_min_blocks(unsigned mask) {
-  return mask == DDVR_TARGET_VOLUME ? 4
+// The absorption-only kernel (ROLE 1) carries none of the emitting walk's
+// state and is compiled for 5 CTAs/SM.
+constexpr int adj_min_blocks(unsigned mask, int role, bool cells) {
+  return !cells ? 2   // voxel layout: 8 scalar gathers per sample, more live state
+         : (role == 1 && mask == DDVR_TARGET_VOLUME) ? DDVR_ABS_MINB
+         : mask == DDVR_TARGET_VOLUME ? 4
          : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? 1 : 3;
 }
 #ifdef DDVR_ADJ_MINB
 #define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, DDVR_ADJ_MINB)
 #else
-#define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, adj_min_blocks(MASK))
+#define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, adj_min_blocks(MASK, ROLE, CELLS))
 #endif
 template <bool EARLY, bool CELLS, bool TAPE>
 __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
@@ -1028,6 +1038,7 @@ constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
 // Per-ray adjoint accumulators that outlive the walk
 struct AdjState {
   int run_cell, run_base, run_ox, run_oy, run_oz;   // volume cell run
+  float* run_q;                                     // its record in the cell workspace
   float acc8[8];
   int tf_run;                                       // TF texel/knot run (i0, i0+1)
   float4 tfa0, tfa1;
@@ -1061,6 +1072,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   // inversion walk (and closer to it in fp32 than the walked chain).
   constexpr bool kAbs = !EMIT && !kTf && !TAPE && KIND == kTfTexture && DDVR_ABS_WALK;
   const float abs_c = kAbs ? sd.w * (float)exp(-S) : 0.f;   // seed_a * T_n
+  const float abs_k = abs_c * dt32 * TF.fR;                   // d_hat per unit texel delta
 
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
@@ -1074,7 +1086,8 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int held = INT_MIN;
   TexHold<EMIT> tex;
-#pragma unroll 1   // (unrolling spills at the 64-register budget)
+  constexpr int kUnroll = kAbs ? DDVR_ABS_UNROLL : 1;   // (the full walk spills when unrolled)
+#pragma unroll (kUnroll)
   for (int i = r.n - 1; i >= 0; --i) {
     Cell c;
     locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
@@ -1089,11 +1102,20 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const bool inside = INSIDE || c.inside;
     const float d = clamp_density(inside, raw);
     int i0; float w;
-    float4 slope;
+    float4 slope, s;
+    float dq = 0.f;   // kAbs: the raw texel delta (the slope is dq * R)
     // (emission-free tables never serve the tf target: rgb and its slope are 0)
     const bool want = kDhat || (kTf && KIND != kTfTexture);
-    const float4 s = kHoldTex ? tex.sample(TF, d, i0, w, slope, want)
-                              : tf_sample<KIND, EMIT>(TF, d, i0, w, slope, want);
+    if (kAbs) {
+      i0 = texel_coord(TF, d, w);
+      const float2 q = tau_table(TF)[i0 + 1];
+      s = make_float4(0.f, 0.f, 0.f, __fmaf_rn(w, q.y, q.x));
+      dq = q.y;
+      slope = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      s = kHoldTex ? tex.sample(TF, d, i0, w, slope, want)
+                   : tf_sample<KIND, EMIT>(TF, d, i0, w, slope, want);
+    }
     const Segment g = segment<SEG>(s.w, dt32);
 
     // Invert the compositing step (renderer.py:579, a_prev = (a - A)/(a - 1)).
@@ -1161,8 +1183,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
-      const float d_hat = EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
-                               : slope.w * tau_hat;
+      const float d_hat = kAbs ? ((s.w < 0.f || g.a_clamped) ? 0.f : dq * abs_k)
+                          : EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
+                                 : slope.w * tau_hat;
       const bool live = inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol && CELLS) {   // renderer.py:607-608, accumulated per cell run
         // The run accumulates the 8 moments sum dh * phi(u), phi = {1, ux, uy,
@@ -1177,9 +1200,10 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
         const bool fresh = c.cell != st.run_cell;
         const bool flush = fresh && st.run_cell != kNoRun;
-        float* q = d_cells + 8 * (long long)(flush ? st.run_cell : 0);
+        float* q = st.run_q;
         red128_if(flush, q, st.acc8[0], st.acc8[1], st.acc8[2], st.acc8[3]);
         red128_if(flush, q + 4, st.acc8[4], st.acc8[5], st.acc8[6], st.acc8[7]);
+        st.run_q = fresh ? d_cells + 8 * (long long)c.cell : st.run_q;
         const float keep = fresh ? 0.f : 1.f;
         st.acc8[0] = fmaf(st.acc8[0], keep, dh);
         st.acc8[1] = fmaf(st.acc8[1], keep, px);
@@ -1232,7 +1256,12 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   }
 }
 
-template <unsigned MASK, bool CELLS>
+// ROLE 0: every walk; ROLE 1: the absorption-only walk (emission-free texel
+// TF, no TF target, no tape, cell records), launched next to ROLE 0 by the
+// host for masks without the TF target.  The TF class is known only on the
+// device (CTA prologue), so each role's CTAs return at once when the class
+// belongs to the other role -- no host synchronisation.
+template <unsigned MASK, bool CELLS, int ROLE>
 __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
     const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
@@ -1259,6 +1288,11 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     for (int i = threadIdx.x; i < TFA.count * TFA.stride; i += blockDim.x) s_tfg[i] = 0.f;
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
   __syncthreads();
+  {
+    const bool abs_class = !kTf && CELLS && DDVR_ABS_WALK && TFA.kind == kTfTexture &&
+                           G.tape == nullptr && s_info[1] == 0u;
+    if (ROLE == 0 ? abs_class : !abs_class) return;   // CTA-uniform
+  }
   const int mode = seg_mode(G.dt32, s_info[0]);
   // the tf target needs the rgb channels even when they are zero
   const bool emit = kTf || s_info[1] != 0u;
@@ -1286,6 +1320,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 
   AdjState st;
   st.run_cell = kNoRun; st.run_base = 0; st.run_ox = 0; st.run_oy = 0; st.run_oz = 0;
+  st.run_q = d_cells;
 #pragma unroll
   for (int k = 0; k < 8; ++k) st.acc8[k] = 0.f;
   st.tf_run = kNoRun;
@@ -1305,7 +1340,9 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 #define DDVR_WALK_GEN(KIND, TP)                                                           \
   adjoint_ray<MASK, CELLS, kSegGen, false, true, KIND, TP>(V, TFA, G.dt32, r, S, sd, tape, \
                                                            s_tfg, d_volume, d_cells, st)
-  if (G.tape) {
+  if (ROLE == 1) {
+    if (warp_inside) { DDVR_WALK_SEG(true, false) } else { DDVR_WALK_SEG(false, false) }
+  } else if (G.tape) {
     if (TFA.kind == kTfPiecewise) DDVR_WALK_GEN(kTfPiecewise, true);
     else if (TFA.kind == kTfGaussian) DDVR_WALK_GEN(kTfGaussian, true);
     else DDVR_WALK_GEN(kTfTexture, true);
