@@ -339,8 +339,7 @@ def run_own(args, cfg):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         est.copy_(host_vol, non_blocking=True)
-        refs.copy_(host_refs, non_blocking=True)
-        runner.run()
+        runner.run(refs_host=host_refs)      # refs H2D overlaps pack + forward
         f = step.flat
         # the step's result: the updated density (optimiser steps) or its gradient
         host_grad.copy_((est if runner is not step else f.d_volume).reshape(-1),

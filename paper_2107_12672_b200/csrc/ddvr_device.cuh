@@ -1286,13 +1286,14 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   load_tf(TFA, s_info);
   if (kTf)
     for (int i = threadIdx.x; i < TFA.count * TFA.stride; i += blockDim.x) s_tfg[i] = 0.f;
-  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
   __syncthreads();
   {
     const bool abs_class = !kTf && CELLS && DDVR_ABS_WALK && TFA.kind == kTfTexture &&
                            G.tape == nullptr && s_info[1] == 0u;
     if (ROLE == 0 ? abs_class : !abs_class) return;   // CTA-uniform
   }
+  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
+  __syncthreads();
   const int mode = seg_mode(G.dt32, s_info[0]);
   // the tf target needs the rgb channels even when they are zero
   const bool emit = kTf || s_info[1] != 0u;

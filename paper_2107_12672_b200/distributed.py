@@ -101,12 +101,35 @@ class ShardedStep:
         self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
                       if layout == "cells" else None)
         self.workspace = R.workspace_for(density, self.mask, self.cells)
+        self._copy_stream = None
 
-    def run(self, hook=None) -> FlatGrads:
+    def _stage_refs(self, refs_host):
+        """Start the host->device copy of this step's reference images on a side
+        stream; return the event the loss kernel waits on.  The refs are first
+        needed by the L1 seed, after the forward march, so the copy overlaps
+        the pack and forward kernels."""
+        if refs_host is None:
+            return None
+        if tuple(refs_host.shape) != tuple(self.refs.shape):
+            raise ValueError(f"refs_host shape {tuple(refs_host.shape)} != {tuple(self.refs.shape)}")
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.refs.device)
+        main = torch.cuda.current_stream(self.refs.device)
+        self._copy_stream.wait_stream(main)          # the previous step's loss read self.refs
+        with torch.cuda.stream(self._copy_stream):
+            self.refs.copy_(refs_host, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self._copy_stream)
+        return done
+
+    def run(self, hook=None, refs_host=None) -> FlatGrads:
         """One step; ``hook(name)`` (optional) is called at "post_forward",
-        "pre_adjoint" and "post_adjoint" in stream order (for CUDA events)."""
+        "pre_adjoint" and "post_adjoint" in stream order (for CUDA events).
+        ``refs_host``: pinned host copy of this step's reference images, copied
+        to the device on a side stream, overlapped with the forward."""
         import ctypes
         hook = hook or (lambda name: None)
+        refs_ready = self._stage_refs(refs_host)
         f = self.flat
         f.buf.zero_()
         self.d_tf64.zero_()
@@ -124,6 +147,8 @@ class ShardedStep:
                                      ctypes.byref(prm), self.img.data_ptr(), self.depth.data_ptr(),
                                      st))
             hook("post_forward")
+            if refs_ready is not None:
+                torch.cuda.current_stream(self.refs.device).wait_event(refs_ready)
             N.check(lib.ddvr_l1_loss(self.img.data_ptr(), self.refs.data_ptr(), self.img.numel(),
                                      self.count, self.seed.data_ptr(), self.loss64.data_ptr(), st))
             want = lambda bit, t: t.data_ptr() if self.mask & bit else None  # noqa: E731
@@ -163,9 +188,9 @@ class TomographyIteration:
         self.adam = AdamState(lr=lr)
         self.check_finite = check_finite
 
-    def run(self, hook=None):
+    def run(self, hook=None, refs_host=None):
         from .optim import prior_volume
-        f = self.step.run(hook=hook)
+        f = self.step.run(hook=hook, refs_host=refs_host)
         density = self.step.density
         grad = f.d_volume.view(density.shape)
         prior = prior_volume(density, self.lam, grad)      # grad += lam * d prior

@@ -1,0 +1,78 @@
+"""The on-device tomography step (distributed.ShardedStep / TomographyIteration).
+
+One step = pack cells, forward over this rank's views, fused L1 loss + seed over
+the global element count (objectives.py:38-54), adjoint, all-reduce (a no-op
+at world size 1).  Checked against the oracle's per-view forward / L1 /
+adjoint sum (the same restatement tests/test_distributed.py reduces over gloo
+ranks), for both volume layouts, with device-resident and host-staged
+reference images.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from test_distributed import _rank_grads, _scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _step(cuda, layout, targets=("volume", "tf", "stepsize")):
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    grid, tex, views, refs, dt = _scene()
+    vol = torch.from_numpy(grid.values.astype(np.float32)).to(cuda)
+    tx = torch.from_numpy(tex.astype(np.float32)).to(cuda)
+    ll = torch.tensor([[v.lon_deg, v.lat_deg] for v in views], dtype=torch.float64, device=cuda)
+    rf = torch.from_numpy(np.stack(refs).astype(np.float32)).to(cuda)
+    step = ShardedStep(vol, tx, ll, rf, dt, R.Rig(6, 5), targets=targets, radius=2.3,
+                       layout=layout)
+    return step, rf
+
+
+@pytest.mark.parametrize("layout", ["cells", "voxels"])
+def test_step_matches_oracle(cuda, layout):
+    step, _ = _step(cuda, layout)
+    f = step.run()
+    ref = _rank_grads(0, 1)
+    assert abs(float(f.loss) - float(ref.loss)) <= 1e-5 * abs(float(ref.loss))
+    for name in ("d_volume", "d_tf", "d_stepsize"):
+        got = getattr(f, name).double().cpu().numpy()
+        want = getattr(ref, name).double().numpy()
+        assert rel_l2(got, want) <= 1e-4, (name, rel_l2(got, want))
+
+
+def test_host_staged_refs_are_identical(cuda):
+    """refs_host: the copy runs on a side stream and the loss kernel waits for it."""
+    step, rf = _step(cuda, "cells")
+    a = step.run().buf.clone()
+    host = rf.cpu().pin_memory()
+    rf.zero_()                        # the step must use the staged copy, not stale data
+    b = step.run(refs_host=host).buf.clone()
+    # (equal up to the order of the fp32 atomic reductions)
+    assert rel_l2(b.double().cpu().numpy(), a.double().cpu().numpy()) <= 1e-6
+    with pytest.raises(ValueError):
+        step.run(refs_host=host[:1])
+
+
+def test_tomography_iterations_reduce_the_loss(cuda):
+    """A few full iterations (step + prior + Adam + projection) recover the
+    density that rendered the references (tasks.py:397-481)."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep, TomographyIteration
+    from paper_2107_12672_b200.scenes import absorption_ramp_texels, fibonacci_poses, phantom
+    truth = torch.from_numpy(phantom("sphere", 24, seed=0).astype(np.float32)).to(cuda)
+    tx = torch.from_numpy(absorption_ramp_texels(32, 3.0).astype(np.float32)).to(cuda)
+    ll = torch.tensor(fibonacci_poses(12), dtype=torch.float64, device=cuda)
+    rig = R.Rig(32, 32)
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    refs, _ = R.forward(truth, tx, cams, 0.2 / 24, rig)
+    est = torch.full_like(truth, 0.3)
+    it = TomographyIteration(ShardedStep(est, tx, ll, refs, 0.2 / 24, rig), lr=0.05, lam=0.0)
+    losses = [float(it.run()[0]) for _ in range(25)]
+    assert losses[-1] < 0.5 * losses[0]
+    assert float(est.min()) >= 0.0 and float(est.max()) <= 1.0   # projection (optim.py:78-89)
