@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DDVR_ABI_VERSION 1
+#define DDVR_ABI_VERSION 2
 
 typedef enum {
   DDVR_OK = 0,
@@ -130,8 +130,9 @@ int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
  *   d_volume float (X*Y*Z); d_tf double (same shape as tf->params);
  *   d_camera double (V, 2) per degree [lon, lat]; d_dt double (1).
  * workspace (device, 32-byte aligned): ddvr_adjoint_workspace_bytes() bytes
- * (cell-gradient records when vol->cells is set and the volume target is on;
- * zeroed and folded into d_volume inside the call). */
+ * (cell-gradient records when vol->cells is set and the volume target is on,
+ * TF-gradient slots when the tf target is on; zeroed, then folded into
+ * d_volume / reduced into d_tf inside the call). */
 int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
                  int32_t n_views, const ddvr_params* p, const float* image, const float* depth,
                  const float* seed, uint32_t target_mask, float* d_volume, double* d_tf,
@@ -157,8 +158,11 @@ int ddvr_adjoint_color(const ddvr_volume* cv, const ddvr_camera* cams, int32_t n
                        const ddvr_params* p, const float* image, const float* depth,
                        const float* seed, float* d_color, void* stream);
 
-/* Workspace ddvr_adjoint needs for this volume and target mask (0 if none). */
-int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t target_mask);
+/* Workspace ddvr_adjoint needs for this volume, TF and target mask (0 if
+ * none): the cell-gradient records (volume target with vol->cells) and the
+ * per-CTA TF-gradient slots (tf target). */
+int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf,
+                                     uint32_t target_mask);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:
  * (X+1) * (Y+1) * (Z+1) records of 8 floats -- cells -1 .. dim-1 on every

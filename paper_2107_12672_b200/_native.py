@@ -19,7 +19,7 @@ from .errors import (
 
 LIB_PATH = os.environ.get("DDVR_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                       "libddvr.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 TARGET_CAMERA = 1
 TARGET_STEPSIZE = 2
@@ -97,7 +97,7 @@ def _bind(lib):
     lib.ddvr_adjoint_color.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp,
                                        vp, vp, vp]
     lib.ddvr_adjoint_color.restype = ctypes.c_int
-    lib.ddvr_adjoint_workspace_bytes.argtypes = [P(DdvrVolume), ctypes.c_uint32]
+    lib.ddvr_adjoint_workspace_bytes.argtypes = [P(DdvrVolume), P(DdvrTf), ctypes.c_uint32]
     lib.ddvr_adjoint_workspace_bytes.restype = ctypes.c_int64
     lib.ddvr_cells_bytes.argtypes = [P(ctypes.c_int32)]
     lib.ddvr_cells_bytes.restype = ctypes.c_int64

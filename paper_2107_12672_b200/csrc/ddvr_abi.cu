@@ -1,5 +1,7 @@
 // ddvr_abi.cu -- the C ABI of include/ddvr.h: validation, launches, small kernels.
 // (Device code: ddvr_device.cuh; kernel instantiations: ddvr_fwd.cu, ddvr_adj_g*.cu.)
+#include <algorithm>
+
 #include "ddvr_device.cuh"
 
 namespace {
@@ -230,6 +232,9 @@ int make_tf(const ddvr_tf* tf, TfArgs& A, size_t& smem_per_table) {
     return set_error(DDVR_UNSUPPORTED, "transfer function resolution %d exceeds %d texels",
                      tf->count, kMaxTfBytes / 56);
   A.params = tf->params;
+  A.slots = nullptr;
+  A.nslot = 0;
+  A.slot_floats = tf_slot_floats(tf->kind, tf->count);
   A.kind = tf->kind;
   A.count = tf->count;
   A.fR = (float)tf->count;
@@ -443,6 +448,38 @@ __global__ void __launch_bounds__(256) ppm_kernel(const float4* __restrict__ img
   }
 }
 
+// d_tf (fp64, the parameter layout count x stride) += sum over the CTA slots
+// (tf_slot layout: rgba rows, then knot positions / (mu, sigma) pairs).
+// 32 outputs x 8 slot lanes per block, reduced through shared memory.
+__global__ void __launch_bounds__(256) tf_slots_reduce_kernel(const float* __restrict__ slots,
+                                                              int nslot, int slot_floats,
+                                                              int kind, int count,
+                                                              double* __restrict__ d_tf) {
+  __shared__ double part[8][33];
+  const int stride = kind == DDVR_TF_TEXTURE ? 4 : kind == DDVR_TF_PIECEWISE ? 5 : 6;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + tx;
+  const int nout = count * stride;
+  int pos = 0;
+  if (k < nout) {
+    const int j = k / stride, c = k % stride;
+    if (kind == DDVR_TF_TEXTURE) pos = 4 * j + c;
+    else if (kind == DDVR_TF_PIECEWISE) pos = c == 0 ? 4 * count + j : 4 * j + c - 1;
+    else pos = c < 2 ? 4 * count + 2 * j + c : 4 * j + c - 2;
+  }
+  double acc = 0.0;
+  if (k < nout)
+    for (int sl = ty; sl < nslot; sl += 8) acc += (double)slots[(size_t)sl * slot_floats + pos];
+  part[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && k < nout) {
+    double t = 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) t += part[r][tx];
+    d_tf[k] += t;
+  }
+}
+
 int grid_blocks(long long n) {
   long long b = (n + 255) / 256;
   return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -481,9 +518,27 @@ int ddvr_pack_cells(const ddvr_volume* vol, float* cells_out, void* stream) {
   return check_launch("pack_cells_kernel");
 }
 
-int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, uint32_t mask) {
+// Workspace layout: [cell-gradient records (volume target, cell layout)]
+// [TF-gradient slots (tf target)], each part 256-byte aligned.
+static int64_t ws_cells_bytes(const ddvr_volume* vol, uint32_t mask) {
   if (!vol || !vol->cells || !(mask & DDVR_TARGET_VOLUME)) return 0;
-  return ddvr_cells_bytes(vol->dims);
+  return (ddvr_cells_bytes(vol->dims) + 255) & ~(int64_t)255;
+}
+
+static int tf_nslot(int slot_floats) {
+  const int64_t budget = 32ll << 20;   // <= 32 MiB of slots
+  const int64_t n = budget / ((int64_t)slot_floats * 4);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, n));
+}
+
+static int64_t ws_tf_bytes(const ddvr_tf* tf, uint32_t mask) {
+  if (!tf || !(mask & DDVR_TARGET_TF) || tf->count < 1) return 0;
+  const int sf = tf_slot_floats(tf->kind, tf->count);
+  return (int64_t)tf_nslot(sf) * sf * 4;
+}
+
+int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf, uint32_t mask) {
+  return ws_cells_bytes(vol, mask) + ws_tf_bytes(tf, mask);
 }
 
 int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
@@ -531,11 +586,12 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
     return set_error(DDVR_INVALID_INPUT, "d_camera is NULL but the camera target is set");
   if ((mask & DDVR_TARGET_STEPSIZE) && !d_dt)
     return set_error(DDVR_INVALID_INPUT, "d_dt is NULL but the stepsize target is set");
-  const int64_t ws_need = ddvr_adjoint_workspace_bytes(vol, mask);
+  const int64_t ws_cells = ws_cells_bytes(vol, mask), ws_tf = ws_tf_bytes(tf, mask);
+  const int64_t ws_need = ws_cells + ws_tf;
   if (ws_need > 0 && (!workspace || workspace_bytes < ws_need))
     return set_error(DDVR_INVALID_INPUT,
-                     "volume target with cell records needs a %lld-byte workspace",
-                     (long long)ws_need);
+                     "this target mask needs a %lld-byte workspace "
+                     "(ddvr_adjoint_workspace_bytes)", (long long)ws_need);
   if (workspace && ((uintptr_t)workspace & 31) != 0)
     return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
@@ -543,11 +599,15 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   const dim3 grid = grid_of(G, n_views);
   const size_t smem = tbl;
   const bool cells = V.cells != nullptr;
-  float* d_cells_all = ws_need > 0 ? static_cast<float*>(workspace) : nullptr;
+  float* d_cells_all = ws_cells > 0 ? static_cast<float*>(workspace) : nullptr;
   // the kernel indexes cell gradients relative to cell (0,0,0), like V.cell0
   float* d_cells = d_cells_all ? d_cells_all + (V.cell0 - V.cells) : nullptr;
-  if (d_cells_all) {
-    cudaError_t e = cudaMemsetAsync(d_cells_all, 0, (size_t)ws_need, st);
+  if (ws_tf > 0) {
+    T.slots = reinterpret_cast<float*>(static_cast<char*>(workspace) + ws_cells);
+    T.nslot = tf_nslot(T.slot_floats);
+  }
+  if (ws_need > 0) {
+    cudaError_t e = cudaMemsetAsync(workspace, 0, (size_t)ws_need, st);
     if (e != cudaSuccess)
       return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
   }
@@ -557,6 +617,12 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
                                d_volume, d_cells, d_tf, d_camera, d_dt);
   if ((rc = check_launch("dvr_adjoint_kernel"))) return rc;
   g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
+  if (ws_tf > 0) {
+    const int nout = T.count * T.stride;
+    tf_slots_reduce_kernel<<<(nout + 31) / 32, 256, 0, st>>>(T.slots, T.nslot, T.slot_floats,
+                                                             T.kind, T.count, d_tf);
+    if ((rc = check_launch("tf_slots_reduce_kernel"))) return rc;
+  }
   if (d_cells) {
     const long long nvox = (long long)V.X * V.Y * V.Z;
     fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells_all, d_volume,

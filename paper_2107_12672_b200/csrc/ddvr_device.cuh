@@ -92,7 +92,19 @@ struct TfArgs {
   float fR, fR1;     // R, R-1
   int Rm2;           // max(R-2, 0)
   int stride;        // floats per parameter row: 4 texture, 5 piecewise, 6 gaussian
+  // adjoint TF-gradient slots in the workspace (tf target): CTA b accumulates
+  // into slot b % nslot, slot_floats floats each: an rgba block (count x 4,
+  // 16-byte rows for vector reds), then count knot positions (piecewise) or
+  // count (mu, sigma) pairs (gaussian)
+  float* __restrict__ slots;
+  int nslot, slot_floats;
 };
+
+// slot size in floats (a multiple of 8: 32-byte aligned slots)
+inline int tf_slot_floats(int kind, int count) {
+  const int extra = kind == DDVR_TF_PIECEWISE ? count : kind == DDVR_TF_GAUSSIAN ? 2 * count : 0;
+  return (4 * count + extra + 7) & ~7;
+}
 
 struct Geometry {
   const ddvr_camera* __restrict__ cams;
@@ -417,6 +429,10 @@ __device__ __forceinline__ void red128_if(bool pred, float* p, float a, float b,
       "@q red.global.add.v4.f32 [%1], {%2,%3,%4,%5};\n\t}" ::"r"((int)pred),
       "l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
       : "memory");
+}
+
+__device__ __forceinline__ void red64(float* p, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
 __device__ __forceinline__ void red128(float* p, float a, float b, float c, float d) {
@@ -1015,21 +1031,22 @@ __device__ __forceinline__ void flush_cell(float* __restrict__ d_volume,
   }
 }
 
-// flush of a texel / knot run into the per-CTA TF gradient (rows of `stride`
-// floats; the piecewise rows carry the knot-position gradient in column 0)
+// flush of a texel / knot run (texel coordinate `run` and run + 1, weights
+// accumulated in a0 / a1) into this CTA's TF-gradient slot: two 128-bit
+// vector reds for the rgba rows (+ the knot-position gradient of a piecewise
+// TF).  Global fp32 reds are native; shared-memory fp32 atomics are CAS loops
+// on sm_100a and serialised on the few hot texels (the earlier design).
 // (texel runs start at the guard coordinate -1, which maps onto texel 0)
-__device__ __forceinline__ void tf_flush_run(float* s_grad, int count, int stride, int run,
+__device__ __forceinline__ void tf_flush_run(float* slot, int count, int kind, int run,
                                              const float4& a0, const float4& a1, float p0,
                                              float p1) {
   const int j0 = max(run, 0);
   const int j1 = min(run + 1, count - 1);
-  float* g0 = s_grad + stride * j0 + (stride - 4);
-  float* g1 = s_grad + stride * j1 + (stride - 4);
-  atomicAdd(g0 + 0, a0.x); atomicAdd(g0 + 1, a0.y); atomicAdd(g0 + 2, a0.z); atomicAdd(g0 + 3, a0.w);
-  atomicAdd(g1 + 0, a1.x); atomicAdd(g1 + 1, a1.y); atomicAdd(g1 + 2, a1.z); atomicAdd(g1 + 3, a1.w);
-  if (stride == 5) {
-    atomicAdd(s_grad + stride * j0, p0);
-    atomicAdd(s_grad + stride * j1, p1);
+  red128(slot + 4 * j0, a0.x, a0.y, a0.z, a0.w);
+  red128(slot + 4 * j1, a1.x, a1.y, a1.z, a1.w);
+  if (kind == kTfPiecewise) {
+    atomicAdd(slot + 4 * count + j0, p0);
+    atomicAdd(slot + 4 * count + j1, p1);
   }
 }
 
@@ -1052,7 +1069,7 @@ struct AdjState {
 template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND, bool TAPE>
 __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                             const Ray& r, double S, float4 sd,
-                                            const float* __restrict__ tape, float* s_tfg,
+                                            const float* __restrict__ tape, float* tf_slot,
                                             float* __restrict__ d_volume,
                                             float* __restrict__ d_cells, AdjState& st) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
@@ -1157,16 +1174,14 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         float gj;
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gj) : "f"(-(z * z) * q.y));
         const float proj = h0 * cj.x + h1 * cj.y + h2 * cj.z + tau_hat * cj.w;
-        float* gr = s_tfg + 6 * j;
-        atomicAdd(gr + 0, gj * z * q.z * proj);
-        atomicAdd(gr + 1, gj * z * z * q.z / q.w * proj);
-        atomicAdd(gr + 2, gj * h0); atomicAdd(gr + 3, gj * h1);
-        atomicAdd(gr + 4, gj * h2); atomicAdd(gr + 5, gj * tau_hat);
+        red128(tf_slot + 4 * j, gj * h0, gj * h1, gj * h2, gj * tau_hat);
+        red64(tf_slot + 4 * TF.count + 2 * j, gj * z * q.z * proj,
+              gj * z * z * q.z / q.w * proj);
       }
     } else if (kTf) {   // renderer.py:602-604: texels/knots i0, i0+1 with weights (1-w), w
       if (i0 != st.tf_run) {
         if (st.tf_run != kNoRun)
-          tf_flush_run(s_tfg, TF.count, TF.stride, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
+          tf_flush_run(tf_slot, TF.count, KIND, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
         st.tf_run = i0;
         st.tfa0 = make_float4(0, 0, 0, 0);
         st.tfa1 = make_float4(0, 0, 0, 0);
@@ -1276,16 +1291,15 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   __shared__ Frame F;
   __shared__ double s_red[kWarps][3];
   __shared__ unsigned s_info[2];
-  // per-CTA TF gradient (count x stride floats) after the kind's table
-  float* s_tfg = reinterpret_cast<float*>(g_smem) +
-                 (TFA.kind == kTfTexture ? 8 * TFA.count + 8
-                                         : (TFA.kind == kTfPiecewise ? 9 : 8) * TFA.count);
+  // this CTA's TF-gradient slot in the workspace
+  float* tf_slot = kTf ? TFA.slots + (size_t)TFA.slot_floats *
+                                         ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
+                                           (size_t)blockIdx.z)) % TFA.nslot)
+                       : nullptr;
   const int view = blockIdx.z;
   if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
   __syncthreads();
   load_tf(TFA, s_info);
-  if (kTf)
-    for (int i = threadIdx.x; i < TFA.count * TFA.stride; i += blockDim.x) s_tfg[i] = 0.f;
   __syncthreads();
   {
     const bool abs_class = !kTf && CELLS && DDVR_ABS_WALK && TFA.kind == kTfTexture &&
@@ -1332,7 +1346,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 
 #define DDVR_WALK(SEG, INS, EM)                                                          \
   adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture, false>(V, TFA, G.dt32, r, S, sd, tape, \
-                                                            s_tfg, d_volume, d_cells, st)
+                                                            tf_slot, d_volume, d_cells, st)
 #define DDVR_WALK_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_WALK(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_WALK(kSegP7, INS, EM); \
@@ -1340,7 +1354,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   // stored mode (tape) and the analytic TFs take the general variant
 #define DDVR_WALK_GEN(KIND, TP)                                                           \
   adjoint_ray<MASK, CELLS, kSegGen, false, true, KIND, TP>(V, TFA, G.dt32, r, S, sd, tape, \
-                                                           s_tfg, d_volume, d_cells, st)
+                                                           tf_slot, d_volume, d_cells, st)
   if (ROLE == 1) {
     if (warp_inside) { DDVR_WALK_SEG(true, false) } else { DDVR_WALK_SEG(false, false) }
   } else if (G.tape) {
@@ -1366,15 +1380,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   if (kVol && st.run_cell != kNoRun)
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                       st.run_oz, st.acc8);
-  if (kTf) {
-    if (st.tf_run != kNoRun)
-      tf_flush_run(s_tfg, TFA.count, TFA.stride, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
-    __syncthreads();
-    for (int k = threadIdx.x; k < TFA.count * TFA.stride; k += blockDim.x) {
-      const float g = s_tfg[k];
-      if (g != 0.f) atomicAdd(d_tf + k, (double)g);
-    }
-  }
+  if (kTf && TFA.kind != kTfGaussian && st.tf_run != kNoRun)
+    tf_flush_run(tf_slot, TFA.count, TFA.kind, st.tf_run, st.tfa0, st.tfa1, st.tfp0, st.tfp1);
   if (kPos) {
     double cam0 = 0.0, cam1 = 0.0, stp = 0.0;
     if (valid && r.n > 0) {

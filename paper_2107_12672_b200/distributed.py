@@ -84,8 +84,6 @@ class ShardedStep:
         self.mask = 0
         for t in targets:
             self.mask |= N.TARGET_BITS[t]
-        if self.mask & N.TARGET_CAMERA:
-            raise ValueError("camera gradients are per view; use the single-view API")
         self.count = float(total_elements if total_elements is not None else refs.numel())
         self.group = group
         dev = density.device
@@ -96,11 +94,14 @@ class ShardedStep:
         self.depth = torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=dev)
         self.d_tf64 = torch.zeros(texels.shape, dtype=torch.float64, device=dev)
         self.d_dt64 = torch.zeros(1, dtype=torch.float64, device=dev)
+        # camera gradients are per view (d/d(lon, lat) per degree, field.py:11), so
+        # they stay with the rank that owns the view: (V_local, 2), not all-reduced
+        self.d_camera = torch.zeros(V, 2, dtype=torch.float64, device=dev)
         self.loss64 = torch.zeros(1, dtype=torch.float64, device=dev)
         # cell records (rebuilt from the density every step) + adjoint workspace
         self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
                       if layout == "cells" else None)
-        self.workspace = R.workspace_for(density, self.mask, self.cells)
+        self.workspace = R.workspace_for(density, self.mask, self.cells, texels)
         self._copy_stream = None
 
     def _stage_refs(self, refs_host):
@@ -134,6 +135,7 @@ class ShardedStep:
         f.buf.zero_()
         self.d_tf64.zero_()
         self.d_dt64.zero_()
+        self.d_camera.zero_()
         self.loss64.zero_()
         V = self.cams.shape[0]
         if V:
@@ -157,9 +159,10 @@ class ShardedStep:
                                      ctypes.byref(prm), self.img.data_ptr(),
                                      self.depth.data_ptr(), self.seed.data_ptr(), self.mask,
                                      want(N.TARGET_VOLUME, f.d_volume),
-                                     want(N.TARGET_TF, self.d_tf64), None,
+                                     want(N.TARGET_TF, self.d_tf64),
+                                     want(N.TARGET_CAMERA, self.d_camera),
                                      want(N.TARGET_STEPSIZE, self.d_dt64),
-                                     want(N.TARGET_VOLUME, self.workspace)
+                                     self.workspace.data_ptr()
                                      if self.workspace is not None else None,
                                      self.workspace.numel() * 4 if self.workspace is not None
                                      else 0, st))

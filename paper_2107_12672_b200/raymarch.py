@@ -236,11 +236,19 @@ def adjoint_color(color, cams, dt: float, rig: Rig, image, depth, seed, d_color,
         _stream_ptr()))
 
 
-def workspace_for(density, mask: int, cells=None, rig: Rig | None = None):
-    """Device workspace the adjoint needs for this layout and mask (or None)."""
-    if cells is None or not mask & N.TARGET_VOLUME:
+def workspace_for(density, mask: int, cells=None, texels=None):
+    """Device workspace ddvr_adjoint needs for this layout, TF and mask (or None):
+    cell-gradient records (volume target, cell layout) + TF-gradient slots
+    (tf target; needs ``texels`` for the TF shape)."""
+    if mask & N.TARGET_TF and texels is None:
+        raise InvalidParameterError("the tf target's workspace depends on the TF: pass texels")
+    if texels is None:
+        texels = torch.zeros(1, 4, dtype=torch.float32, device=density.device)
+    vol, tf, _ = _descs(density, texels, Rig(1, 1), 1.0, False, cells)
+    need = int(N.lib().ddvr_adjoint_workspace_bytes(ctypes.byref(vol), ctypes.byref(tf), mask))
+    if need == 0:
         return None
-    return torch.empty(cells_numel(density.shape), dtype=torch.float32, device=density.device)
+    return torch.empty((need + 3) // 4, dtype=torch.float32, device=density.device)
 
 
 def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask: int, *,
@@ -266,7 +274,7 @@ def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask
         if buf is not None:
             _require(buf, name, dt_)
     if workspace is None:
-        workspace = workspace_for(density, mask, cells)
+        workspace = workspace_for(density, mask, cells, texels)
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,

@@ -46,7 +46,7 @@ def test_library_exports_every_declared_symbol(lib):
     handle = ctypes.CDLL(lib._name)
     for name in _declared():
         assert hasattr(handle, name), name
-    assert lib.ddvr_abi_version() == 1
+    assert lib.ddvr_abi_version() == 2
 
 
 def test_python_binding_matches_header():
@@ -123,15 +123,22 @@ def test_status_codes_map_to_reference_exceptions(lib):
         N.check(lib.ddvr_l1_loss(None, None, 4, 1.0, None, None, None))
 
 
-def test_cell_layout_sizes(lib):
+def test_workspace_layout_sizes(lib):
+    from paper_2107_12672_b200 import _native as N
     dims = (ctypes.c_int32 * 3)(256, 256, 256)
     assert lib.ddvr_cells_bytes(dims) == 257 ** 3 * 32
     assert lib.ddvr_cells_bytes((ctypes.c_int32 * 3)(1, 5, 2)) == 2 * 6 * 3 * 32
-    vol, _, _ = _descs(dims=(9, 5, 3))
-    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 0      # no cell records
+    vol, tf, _ = _descs(dims=(9, 5, 3), R=64)
+    ws = lambda m: lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), ctypes.byref(tf), m)  # noqa
+    assert ws(8) == 0                                        # no cell records
     vol.cells = 32
-    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 8) == 10 * 6 * 4 * 32
-    assert lib.ddvr_adjoint_workspace_bytes(ctypes.byref(vol), 4) == 0      # tf target only
+    cells = (10 * 6 * 4 * 32 + 255) // 256 * 256            # 256-byte aligned part
+    assert ws(8) == cells
+    slots = ws(4)                                            # tf target: per-CTA slots
+    assert slots > 0 and slots % (64 * 4 * 4) == 0 and slots <= 32 << 20
+    assert ws(12) == cells + slots
+    tf.kind, tf.count = N.TF_GAUSSIAN, 7                     # rgba rows + (mu, sigma) pairs
+    assert ws(4) % ((4 * 7 + 2 * 7 + 7) // 8 * 8 * 4) == 0
 
 
 def test_adjoint_with_cells_requires_workspace(lib):

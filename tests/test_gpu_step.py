@@ -76,3 +76,21 @@ def test_tomography_iterations_reduce_the_loss(cuda):
     losses = [float(it.run()[0]) for _ in range(25)]
     assert losses[-1] < 0.5 * losses[0]
     assert float(est.min()) >= 0.0 and float(est.max()) <= 1.0   # projection (optim.py:78-89)
+
+
+def test_step_camera_gradients_stay_per_view(cuda):
+    """C3-style targets: d/d(lon, lat) per view (field.py:11), kept by the owning rank."""
+    from oracle import dvr_oracle as O
+    step, _ = _step(cuda, "cells", targets=("camera", "stepsize"))
+    f = step.run()
+    grid, tex, views, refs, dt = _scene()
+    count = sum(r.size for r in refs)
+    want = []
+    for v, ref in zip(views, refs):
+        img = O.render_view(grid, tex, v, dt)
+        g = O.adjoint_view(grid, tex, v, dt, np.sign(img - ref) / count, ["camera"], image=img)
+        want.append(np.asarray(g["d_camera"], np.float64).reshape(2))
+    got = step.d_camera.cpu().numpy()
+    assert got.shape == (len(views), 2)
+    assert rel_l2(got, np.stack(want)) <= 1e-4
+    assert float(f.d_stepsize) != 0.0
