@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--views", type=int, default=0,
                    help="profiling aid: use only the first N views (not a bench result)")
     p.add_argument("--layout", default="cells", choices=["cells", "voxels"])
+    p.add_argument("--unfused", action="store_true",
+                   help="separate forward / L1 / adjoint launches instead of the fused step")
     return p.parse_args()
 
 
@@ -274,7 +276,7 @@ def run_own(args, cfg):
     total_elems = 4 * cfg.image * cfg.image * len(poses)
     step = ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                        total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
-                       layout=args.layout)
+                       layout=args.layout, fused=not args.unfused)
     # density targets run the whole optimisation iteration (prior + Adam + projection)
     runner = TomographyIteration(step, lr=0.02, lam=0.5) if "volume" in cfg.targets else step
     _, n_steps, _ = R.ray_setup(cams, cfg.dt, rig, dims=tuple(truth.shape))
@@ -364,8 +366,38 @@ def run_own(args, cfg):
         fwd_bytes = FWD_B_PER_SAMPLE * local_samples + FWD_B_PER_RAY * local_rays
         adj_s = float(np.mean(adj_ms)) / 1e3
         fwd_s = float(np.mean(fwd_ms)) / 1e3
+        fused = getattr(step, "fused", False)
+        if fused:   # one kernel marches forward, forms the L1 seed and walks back
+            adj_bytes += fwd_bytes
+            adj_b += FWD_B_PER_SAMPLE
         adj_gbs = adj_bytes / adj_s / 1e9
         fwd_gbs = fwd_bytes / fwd_s / 1e9
+        traffic = ncu_traffic(cfg.name, "fused" if fused else "adjoint")
+        kname = ("dvr_adjoint_kernel<FUSED> (forward + L1 seed + adjoint per ray)" if fused
+                 else "dvr_adjoint_kernel")
+        ray_b = ADJ_B_PER_RAY + (FWD_B_PER_RAY if fused else 0)
+        note = ("algorithmic bytes charge 8 corner gathers (+8 scatters) per sample with no "
+                "cache reuse (SURVEY 8d)")
+        if traffic:
+            note += (f"; ncu measures {traffic / adj_bytes:.2f}x those bytes of DRAM traffic per "
+                     "launch (L1/L2 reuse), so frac > 1 is reuse, not missing work; the "
+                     "limiters are gather latency and L1 wavefronts "
+                     "(profiles/r01_ncu_c4v8_poly.txt)")
+        if fused:
+            kernels = {
+                "pack_cells": {"ms": fwd_s * 1e3},
+                "fused_forward_adjoint": {"ms": adj_s * 1e3, "achieved_gbs": adj_gbs,
+                                          "frac": adj_gbs / peak, "traffic": traffic},
+                "share_of_step": {"pack_cells": fwd_s * 1e3 / ms_per_step,
+                                  "fused_forward_adjoint": adj_s * 1e3 / ms_per_step}}
+        else:
+            kernels = {
+                "forward": {"ms": fwd_s * 1e3, "achieved_gbs": fwd_gbs, "frac": fwd_gbs / peak,
+                            "bytes_model": f"{FWD_B_PER_SAMPLE} B/sample + {FWD_B_PER_RAY} B/ray",
+                            "traffic": ncu_traffic(cfg.name, "forward")},
+                "adjoint": {"ms": adj_s * 1e3, "achieved_gbs": adj_gbs, "frac": adj_gbs / peak},
+                "share_of_step": {"forward": fwd_s * 1e3 / ms_per_step,
+                                  "adjoint": adj_s * 1e3 / ms_per_step}}
         line = {
             "metric": "fwd+adjoint samples/s",
             "value": total_samples / (ms_per_step / 1e3),
@@ -376,25 +408,13 @@ def run_own(args, cfg):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_json(cfg, world),
             "samples_per_step": total_samples, "rays_per_step": total_rays,
-            "roofline": {"bound": "hbm", "kernel": "dvr_adjoint_kernel",
+            "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": adj_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": adj_gbs / peak, "traffic": ncu_traffic(cfg.name, "adjoint"),
+                         "frac": adj_gbs / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": adj_bytes,
-                         "bytes_model": f"{adj_b} B/sample + {ADJ_B_PER_RAY} B/ray",
-                         "launch_ms": adj_s * 1e3, "peak_source": peak_src,
-                         "note": "algorithmic bytes charge 8 corner gathers (+8 scatters) "
-                                 "per sample with no cache reuse (SURVEY 8d); the kernel "
-                                 "moves `traffic` DRAM bytes per launch (ncu), ~8% of "
-                                 "that, so frac > 1 is reuse, not missing work; its "
-                                 "limiters are issue slots and L1 wavefronts "
-                                 "(profiles/r01_ncu_c4v8_full.txt)"},
-            "kernels": {
-                "forward": {"ms": fwd_s * 1e3, "achieved_gbs": fwd_gbs, "frac": fwd_gbs / peak,
-                            "bytes_model": f"{FWD_B_PER_SAMPLE} B/sample + {FWD_B_PER_RAY} B/ray",
-                            "traffic": ncu_traffic(cfg.name, "forward")},
-                "adjoint": {"ms": adj_s * 1e3, "achieved_gbs": adj_gbs, "frac": adj_gbs / peak},
-                "share_of_step": {"forward": fwd_s * 1e3 / ms_per_step,
-                                  "adjoint": adj_s * 1e3 / ms_per_step}},
+                         "bytes_model": f"{adj_b} B/sample + {ray_b} B/ray",
+                         "launch_ms": adj_s * 1e3, "peak_source": peak_src, "note": note},
+            "kernels": kernels,
             "e2e": {"value": total_samples / (e2e_ms_step / 1e3), "unit": "samples/s",
                     "ms_per_step": e2e_ms_step, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},

@@ -95,6 +95,9 @@ typedef struct {
   double reserved;
 } ddvr_camera;
 
+#define DDVR_FLAG_WS_CONTINUE 1
+#define DDVR_FLAG_WS_DEFER 2
+
 /* march parameters (RenderConfig, renderer.py:84-106) */
 typedef struct {
   double dt;             /* stepsize > 0 */
@@ -103,7 +106,13 @@ typedef struct {
   int32_t row0;          /* rows [row0, row1) are processed (row bands, renderer.py:491) */
   int32_t row1;          /* row1 <= 0 means height */
   int32_t early_stop;    /* 1: stop rays at alpha > 1-1e-4 (target "none", renderer.py:331-335) */
-  int32_t flags;         /* reserved, 0 */
+  int32_t flags;         /* 0, or for ddvr_adjoint / ddvr_forward_adjoint_l1 split over
+                            several calls of one step (e.g. view chunks):
+                            DDVR_FLAG_WS_CONTINUE  the workspace already holds this
+                                                   step's partial gradients: not zeroed;
+                            DDVR_FLAG_WS_DEFER     more calls follow: partial gradients
+                                                   stay in the workspace (no fold into
+                                                   d_volume, no reduction into d_tf) */
   float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
                             forward writes the transmittance before every sample,
                             tape[ray * tape_stride + i]; the adjoint then reads it
@@ -138,6 +147,22 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
                  const float* seed, uint32_t target_mask, float* d_volume, double* d_tf,
                  double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
                  void* stream);
+
+/* One fused tomography step over n_views views (the render -> l1_loss ->
+ * render_adjoint body of the reconstruction loop, tasks.py:397-481;
+ * renderer.py:393-401, objectives.py:38-54, renderer.py:688-700): per ray, the
+ * forward march, the L1 seed sign(image - ref) / count and the adjoint walk
+ * run back to back in one kernel (the walk uses the exact fp64 optical depth).
+ * refs (device) (V, rows, W, 4); count = the loss's global element count;
+ * loss_out (device, double) += sum |image - ref| / count.  image_out and
+ * depth_out (device, nullable) receive the rendered images.  Outputs and
+ * workspace as ddvr_adjoint.  Needs vol->cells; no stored (tape) mode. */
+int ddvr_forward_adjoint_l1(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                            int32_t n_views, const ddvr_params* p, const float* refs,
+                            double count, uint32_t target_mask, float* image_out,
+                            float* depth_out, double* loss_out, float* d_volume, double* d_tf,
+                            double* d_camera, double* d_dt, void* workspace,
+                            int64_t workspace_bytes, void* stream);
 
 /* Forward-mode Jacobian of the image (render_forward_grad, renderer.py:410-464):
  * wrt = DDVR_TARGET_CAMERA (p = 2: d/dlon, d/dlat, per degree) or

@@ -28,11 +28,13 @@ TARGET_VOLUME = 8
 TARGET_BITS = {"camera": TARGET_CAMERA, "stepsize": TARGET_STEPSIZE, "tf": TARGET_TF,
                "volume": TARGET_VOLUME}
 
+FLAG_WS_CONTINUE = 1   # ddvr_params.flags (include/ddvr.h)
+FLAG_WS_DEFER = 2
 TF_TEXTURE = 0
 TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
-EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes",
+EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1", "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes",
             "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
             "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_ray_setup",
             "ddvr_prior_volume",
@@ -88,6 +90,10 @@ def _bind(lib):
                                  vp, vp, vp, ctypes.c_uint32, vp, vp, vp, vp, vp,
                                  ctypes.c_int64, vp]
     lib.ddvr_adjoint.restype = ctypes.c_int
+    lib.ddvr_forward_adjoint_l1.argtypes = [P(DdvrVolume), P(DdvrTf), vp, ctypes.c_int32,
+                                            P(DdvrParams), vp, ctypes.c_double, ctypes.c_uint32,
+                                            vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp]
+    lib.ddvr_forward_adjoint_l1.restype = ctypes.c_int
     lib.ddvr_forward_grad.argtypes = [P(DdvrVolume), P(DdvrTf), vp, ctypes.c_int32,
                                       P(DdvrParams), ctypes.c_uint32, vp, vp, vp]
     lib.ddvr_forward_grad.restype = ctypes.c_int

@@ -561,23 +561,20 @@ launch_forward(early, cells, tape, grid, tbl, st, V, T, G, image_out, depth_out)
   return check_launch("dvr_forward_kernel");
 }
 
-int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
-                 int32_t n_views, const ddvr_params* p, const float* image, const float* depth,
-                 const float* seed, uint32_t mask, float* d_volume, double* d_tf,
-                 double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
-                 void* stream) {
-  g_err[0] = 0;
-  VolArgs V;
-  TfArgs T;
-  Geometry G;
-  size_t tbl;
+// Shared body of ddvr_adjoint and ddvr_forward_adjoint_l1 (fu != NULL):
+// target/output/workspace validation, workspace zeroing, the adjoint (or fused)
+// launch, TF-slot reduction and the cell-gradient fold.
+static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, TfArgs& T,
+                       Geometry& G, size_t tbl, int32_t n_views, const float* image,
+                       const float* depth, const float* seed, uint32_t mask, float* d_volume,
+                       double* d_tf, double* d_camera, double* d_dt, void* workspace,
+                       int64_t workspace_bytes, void* stream, const FusedArgs* fu,
+                       int32_t flags) {
   int rc;
-  if ((rc = make_vol(vol, V)) || (rc = make_tf(tf, T, tbl)) || (rc = make_geo(cams, n_views, p, G)))
-    return rc;
+  if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER))
+    return set_error(DDVR_INVALID_PARAMETER, "unknown params.flags bits 0x%x", flags);
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
-  if (!seed) return set_error(DDVR_INVALID_INPUT, "seed pointer is NULL");
-  if (!image && !depth) return set_error(DDVR_INVALID_INPUT, "image and optical depth are NULL");
   if ((mask & DDVR_TARGET_VOLUME) && !d_volume)
     return set_error(DDVR_INVALID_INPUT, "d_volume is NULL but the volume target is set");
   if ((mask & DDVR_TARGET_TF) && !d_tf)
@@ -606,7 +603,7 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
     T.slots = reinterpret_cast<float*>(static_cast<char*>(workspace) + ws_cells);
     T.nslot = tf_nslot(T.slot_floats);
   }
-  if (ws_need > 0) {
+  if (ws_need > 0 && !(flags & DDVR_FLAG_WS_CONTINUE)) {
     cudaError_t e = cudaMemsetAsync(workspace, 0, (size_t)ws_need, st);
     if (e != cudaSuccess)
       return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
@@ -614,9 +611,10 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
   auto launch = mask <= 3 ? launch_adjoint_g0 : mask <= 7 ? launch_adjoint_g1
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;
   const int n_kernels = launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed,
-                               d_volume, d_cells, d_tf, d_camera, d_dt);
-  if ((rc = check_launch("dvr_adjoint_kernel"))) return rc;
+                               d_volume, d_cells, d_tf, d_camera, d_dt, fu);
+  if ((rc = check_launch(fu ? "dvr_adjoint_kernel (fused)" : "dvr_adjoint_kernel"))) return rc;
   g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
+  if (flags & DDVR_FLAG_WS_DEFER) return DDVR_OK;   // a later call of this step folds
   if (ws_tf > 0) {
     const int nout = T.count * T.stride;
     tf_slots_reduce_kernel<<<(nout + 31) / 32, 256, 0, st>>>(T.slots, T.nslot, T.slot_floats,
@@ -630,6 +628,52 @@ int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* c
     return check_launch("fold_cells_kernel");
   }
   return DDVR_OK;
+}
+
+int ddvr_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                 int32_t n_views, const ddvr_params* p, const float* image, const float* depth,
+                 const float* seed, uint32_t mask, float* d_volume, double* d_tf,
+                 double* d_camera, double* d_dt, void* workspace, int64_t workspace_bytes,
+                 void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  TfArgs T;
+  Geometry G;
+  size_t tbl;
+  int rc;
+  if ((rc = make_vol(vol, V)) || (rc = make_tf(tf, T, tbl)) || (rc = make_geo(cams, n_views, p, G)))
+    return rc;
+  if (mask == 0 || (mask & ~15u))
+    return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
+  if (!seed) return set_error(DDVR_INVALID_INPUT, "seed pointer is NULL");
+  if (!image && !depth) return set_error(DDVR_INVALID_INPUT, "image and optical depth are NULL");
+  return run_adjoint(vol, tf, V, T, G, tbl, n_views, image, depth, seed, mask, d_volume, d_tf,
+                     d_camera, d_dt, workspace, workspace_bytes, stream, nullptr, p->flags);
+}
+
+int ddvr_forward_adjoint_l1(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
+                            int32_t n_views, const ddvr_params* p, const float* refs,
+                            double count, uint32_t mask, float* image_out, float* depth_out,
+                            double* loss_out, float* d_volume, double* d_tf, double* d_camera,
+                            double* d_dt, void* workspace, int64_t workspace_bytes,
+                            void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  TfArgs T;
+  Geometry G;
+  size_t tbl;
+  int rc;
+  if ((rc = make_vol(vol, V)) || (rc = make_tf(tf, T, tbl)) || (rc = make_geo(cams, n_views, p, G)))
+    return rc;
+  if (!V.cells)
+    return set_error(DDVR_UNSUPPORTED, "the fused step needs cell records (ddvr_pack_cells)");
+  if (G.tape) return set_error(DDVR_UNSUPPORTED, "the fused step has no stored (tape) mode");
+  if (!refs) return set_error(DDVR_INVALID_INPUT, "reference image pointer is NULL");
+  if (!loss_out) return set_error(DDVR_INVALID_INPUT, "loss pointer is NULL");
+  if (!(count > 0.0)) return set_error(DDVR_INVALID_PARAMETER, "element count must be positive");
+  FusedArgs fu{refs, (float)(1.0 / count), 1.0 / count, loss_out, image_out, depth_out};
+  return run_adjoint(vol, tf, V, T, G, tbl, n_views, nullptr, nullptr, nullptr, mask, d_volume,
+                     d_tf, d_camera, d_dt, workspace, workspace_bytes, stream, &fu, p->flags);
 }
 
 int ddvr_forward_grad(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,

@@ -128,11 +128,23 @@ void launch_forward_color(bool early, bool tape, dim3 grid, cudaStream_t st, con
 void launch_adjoint_color(dim3 grid, cudaStream_t st, const VolArgs& V, const Geometry& G,
                           const float* image, const float* depth, const float* seed,
                           float* d_color);
+// Fused step (ddvr_forward_adjoint_l1): each thread marches its ray forward,
+// forms the L1 seed sign(image - ref) / count (objectives.py:38-54) and its
+// loss term in registers, then walks back with the exact fp64 optical depth.
+struct FusedArgs {
+  const float* __restrict__ refs;   // (V, rows, W, 4) reference images
+  float inv_count;                  // 1 / global element count (fp32 seed)
+  double inv_count_d;
+  double* loss;                     // += sum |image - ref| / count
+  float* image_out;                 // optional (V, rows, W, 4)
+  float* depth_out;                 // optional (V, rows, W)
+};
+
 #define DDVR_ADJ_LAUNCHER(NAME)                                                              \
   int NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
             const VolArgs& V, const TfArgs& T, const Geometry& G, const float* image,       \
             const float* depth, const float* seed, float* dv, float* dcells, double* dtf,   \
-            double* dcam, double* ddt)
+            double* dcam, double* ddt, const FusedArgs* fu)
 DDVR_ADJ_LAUNCHER(launch_adjoint_g0);   // masks 1-3   (camera / stepsize)
 DDVR_ADJ_LAUNCHER(launch_adjoint_g1);   // masks 4-7   (tf [+ camera / stepsize])
 DDVR_ADJ_LAUNCHER(launch_adjoint_g2);   // masks 8-11  (volume [+ camera / stepsize])
@@ -923,6 +935,37 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   depth = S;
 }
 
+// The march of one ray with the variant the CTA's TF selects (kind, emission,
+// segment mode) and the warp's inside flag.  ABS_ONLY: only the emission-free
+// texel variants are compiled (the absorption-only kernels).
+template <bool EARLY, bool CELLS, bool TAPE, bool ABS_ONLY>
+__device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& TFA, float dt32,
+                                               const Ray& r, float* __restrict__ tape,
+                                               bool warp_inside, bool emit, int mode,
+                                               float4& rgba, double& S) {
+#define DDVR_MARCH(SEG, INS, EM) \
+  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM, kTfTexture>(V, TFA, dt32, r, tape, rgba, S)
+#define DDVR_MARCH_SEG(INS, EM)                  \
+  if (mode == kSegP3) DDVR_MARCH(kSegP3, INS, EM); \
+  else if (mode == kSegP7) DDVR_MARCH(kSegP7, INS, EM); \
+  else DDVR_MARCH(kSegGen, INS, EM);
+  if (ABS_ONLY) {
+    if (warp_inside) { DDVR_MARCH_SEG(true, false) } else { DDVR_MARCH_SEG(false, false) }
+  } else if (TFA.kind == kTfPiecewise) {
+    march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfPiecewise>(V, TFA, dt32, r, tape,
+                                                                       rgba, S);
+  } else if (TFA.kind == kTfGaussian) {
+    march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfGaussian>(V, TFA, dt32, r, tape,
+                                                                      rgba, S);
+  } else if (warp_inside) {
+    if (emit) { DDVR_MARCH_SEG(true, true) } else { DDVR_MARCH_SEG(true, false) }
+  } else {
+    if (emit) { DDVR_MARCH_SEG(false, true) } else { DDVR_MARCH_SEG(false, false) }
+  }
+#undef DDVR_MARCH_SEG
+#undef DDVR_MARCH
+}
+
 #ifndef DDVR_FWD_MINB
 #define DDVR_FWD_MINB 5
 #endif
@@ -972,25 +1015,8 @@ __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forwar
   float* tape = TAPE ? G.tape + pix * G.tape_stride : nullptr;
   float4 rgba;
   double S;
-#define DDVR_MARCH(SEG, INS, EM) \
-  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM, kTfTexture>(V, TFA, G.dt32, r, tape, rgba, S)
-#define DDVR_MARCH_SEG(INS, EM)                  \
-  if (mode == kSegP3) DDVR_MARCH(kSegP3, INS, EM); \
-  else if (mode == kSegP7) DDVR_MARCH(kSegP7, INS, EM); \
-  else DDVR_MARCH(kSegGen, INS, EM);
-  if (TFA.kind == kTfPiecewise) {
-    march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfPiecewise>(V, TFA, G.dt32, r, tape,
-                                                                       rgba, S);
-  } else if (TFA.kind == kTfGaussian) {
-    march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfGaussian>(V, TFA, G.dt32, r, tape,
-                                                                      rgba, S);
-  } else if (warp_inside) {
-    if (emit) { DDVR_MARCH_SEG(true, true) } else { DDVR_MARCH_SEG(true, false) }
-  } else {
-    if (emit) { DDVR_MARCH_SEG(false, true) } else { DDVR_MARCH_SEG(false, false) }
-  }
-#undef DDVR_MARCH_SEG
-#undef DDVR_MARCH
+  march_dispatch<EARLY, CELLS, TAPE, false>(V, TFA, G.dt32, r, tape, warp_inside, emit, mode,
+                                             rgba, S);
   reinterpret_cast<float4*>(image)[pix] = rgba;
   if (depth) depth[pix] = (float)S;
 }
@@ -1276,12 +1302,14 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
 // host for masks without the TF target.  The TF class is known only on the
 // device (CTA prologue), so each role's CTAs return at once when the class
 // belongs to the other role -- no host synchronisation.
-template <unsigned MASK, bool CELLS, int ROLE>
+// FUSED: the forward march and the L1 seed run in the same thread first
+// (FusedArgs); image / depth / seed are then unused.
+template <unsigned MASK, bool CELLS, int ROLE, bool FUSED>
 __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
     const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
     float* __restrict__ d_cells, double* __restrict__ d_tf, double* __restrict__ d_camera,
-    double* __restrict__ d_dt) {
+    double* __restrict__ d_dt, FusedArgs Fu) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
   constexpr bool kStep = MASK & DDVR_TARGET_STEPSIZE;
   constexpr bool kTf = MASK & DDVR_TARGET_TF;
@@ -1322,16 +1350,37 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   double S = 0.0;   // optical depth after the current sample (T = exp(-S))
   float4 sd = make_float4(0, 0, 0, 0);
   const float* tape = nullptr;
+  size_t pix = 0;
   if (valid) {
     setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
-    const size_t pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
-    if (G.tape) tape = G.tape + pix * G.tape_stride;
-    sd = reinterpret_cast<const float4*>(seed)[pix];
-    // the forward's exact optical depth; without it, S = -ln(1 - alpha)
-    S = depth ? (double)depth[pix]
-              : -log1p(-(double)reinterpret_cast<const float4*>(image)[pix].w);
+    pix = ((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
+    if (!FUSED) {
+      if (G.tape) tape = G.tape + pix * G.tape_stride;
+      sd = reinterpret_cast<const float4*>(seed)[pix];
+      // the forward's exact optical depth; without it, S = -ln(1 - alpha)
+      S = depth ? (double)depth[pix]
+                : -log1p(-(double)reinterpret_cast<const float4*>(image)[pix].w);
+    }
   }
   const bool warp_inside = CELLS && __all_sync(0xffffffffu, r.all_inside);
+  if (FUSED) {   // forward march (renderer.py:306-357) + L1 seed (objectives.py:38-54)
+    double loss_part = 0.0;
+    if (valid) {
+      float4 rgba;
+      march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
+                                                     s_info[1] != 0u, mode, rgba, S);
+      const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[pix];
+      const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
+                  dw = rgba.w - ref.w;
+      auto sgn = [&](float v) { return v > 0.f ? Fu.inv_count : (v < 0.f ? -Fu.inv_count : 0.f); };
+      sd = make_float4(sgn(dx), sgn(dy), sgn(dz), sgn(dw));
+      loss_part = fabs((double)dx) + fabs((double)dy) + fabs((double)dz) + fabs((double)dw);
+      if (Fu.image_out) reinterpret_cast<float4*>(Fu.image_out)[pix] = rgba;
+      if (Fu.depth_out) Fu.depth_out[pix] = (float)S;
+    }
+    loss_part = warp_sum(loss_part);
+    if ((threadIdx.x & 31) == 0 && loss_part != 0.0) atomicAdd(Fu.loss, loss_part * Fu.inv_count_d);
+  }
 
   AdjState st;
   st.run_cell = kNoRun; st.run_base = 0; st.run_ox = 0; st.run_oy = 0; st.run_oz = 0;

@@ -74,11 +74,17 @@ class ShardedStep:
     density (X,Y,Z) fp32, texels (R,4) fp32 on this rank's GPU (replicated);
     refs: (V_local, H, W, 4) fp32 reference images of the local views;
     lonlat: (V_local, 2) poses; ``total_elements`` = 4*H*W*V_global.
+
+    With cell records (the default layout) the forward, the L1 seed and the
+    adjoint run as one fused kernel per ray (ddvr_forward_adjoint_l1);
+    ``fused=False`` keeps the three separate launches (ddvr_forward,
+    ddvr_l1_loss, ddvr_adjoint).  ``keep_images``: also write the rendered
+    images / optical depth of the fused step into ``img`` / ``depth``.
     """
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
-                 group=None, layout="cells"):
+                 group=None, layout="cells", fused=True, keep_images=False, chunks=4):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
@@ -103,12 +109,19 @@ class ShardedStep:
                       if layout == "cells" else None)
         self.workspace = R.workspace_for(density, self.mask, self.cells, texels)
         self._copy_stream = None
+        self.fused = fused and self.cells is not None
+        self.keep_images = keep_images
+        # view chunks of the fused step when the refs come from the host: chunk k
+        # waits only for its own refs, so the copy of the rest overlaps compute
+        n = max(1, min(chunks, V))
+        edges = [round(k * V / n) for k in range(n + 1)]
+        self._chunks = [slice(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
 
-    def _stage_refs(self, refs_host):
+    def _stage_refs(self, refs_host, chunks):
         """Start the host->device copy of this step's reference images on a side
-        stream; return the event the loss kernel waits on.  The refs are first
-        needed by the L1 seed, after the forward march, so the copy overlaps
-        the pack and forward kernels."""
+        stream, one piece per view chunk; return the events the loss waits on.
+        The refs are first needed by the L1 seed, after the forward march of
+        the chunk, so the copy overlaps the pack and the compute."""
         if refs_host is None:
             return None
         if tuple(refs_host.shape) != tuple(self.refs.shape):
@@ -117,11 +130,14 @@ class ShardedStep:
             self._copy_stream = torch.cuda.Stream(self.refs.device)
         main = torch.cuda.current_stream(self.refs.device)
         self._copy_stream.wait_stream(main)          # the previous step's loss read self.refs
+        events = []
         with torch.cuda.stream(self._copy_stream):
-            self.refs.copy_(refs_host, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(self._copy_stream)
-        return done
+            for sl in chunks:
+                self.refs[sl].copy_(refs_host[sl], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(self._copy_stream)
+                events.append(done)
+        return events
 
     def run(self, hook=None, refs_host=None) -> FlatGrads:
         """One step; ``hook(name)`` (optional) is called at "post_forward",
@@ -130,7 +146,8 @@ class ShardedStep:
         to the device on a side stream, overlapped with the forward."""
         import ctypes
         hook = hook or (lambda name: None)
-        refs_ready = self._stage_refs(refs_host)
+        chunks = self._chunks if (self.fused and refs_host is not None) else [slice(None)]
+        refs_ready = self._stage_refs(refs_host, chunks)
         f = self.flat
         f.buf.zero_()
         self.d_tf64.zero_()
@@ -138,7 +155,30 @@ class ShardedStep:
         self.d_camera.zero_()
         self.loss64.zero_()
         V = self.cams.shape[0]
-        if V:
+        if V and self.fused:
+            R.pack_cells(self.density, self.cells)
+            hook("post_forward")
+            hook("pre_adjoint")
+            main = torch.cuda.current_stream(self.refs.device)
+            want = lambda bit, t: t if self.mask & bit else None  # noqa: E731
+            for k, sl in enumerate(chunks):
+                if refs_ready is not None:
+                    main.wait_event(refs_ready[k])
+                # one workspace for the whole step: zeroed by the first chunk,
+                # folded into the gradients by the last
+                last = k == len(chunks) - 1
+                R.forward_adjoint_l1(
+                    self.density, self.texels, self.cams[sl], self.dt, self.rig, self.refs[sl],
+                    self.count, self.mask, cells=self.cells, loss=self.loss64,
+                    d_volume=want(N.TARGET_VOLUME, f.d_volume), d_tf=want(N.TARGET_TF, self.d_tf64),
+                    d_camera=want(N.TARGET_CAMERA, self.d_camera[sl]),
+                    d_dt=want(N.TARGET_STEPSIZE, self.d_dt64), workspace=self.workspace,
+                    image_out=self.img[sl] if self.keep_images else None,
+                    depth_out=self.depth[sl] if self.keep_images else None,
+                    ws_continue=k > 0 and self.workspace is not None,
+                    ws_defer=not last and self.workspace is not None)
+            hook("post_adjoint")
+        elif V:
             if self.cells is not None:
                 R.pack_cells(self.density, self.cells)
             vol, tf, prm = R._descs(self.density, self.texels, self.rig, self.dt, False,
@@ -150,7 +190,7 @@ class ShardedStep:
                                      st))
             hook("post_forward")
             if refs_ready is not None:
-                torch.cuda.current_stream(self.refs.device).wait_event(refs_ready)
+                torch.cuda.current_stream(self.refs.device).wait_event(refs_ready[0])
             N.check(lib.ddvr_l1_loss(self.img.data_ptr(), self.refs.data_ptr(), self.img.numel(),
                                      self.count, self.seed.data_ptr(), self.loss64.data_ptr(), st))
             want = lambda bit, t: t.data_ptr() if self.mask & bit else None  # noqa: E731

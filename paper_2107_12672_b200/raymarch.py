@@ -251,6 +251,45 @@ def workspace_for(density, mask: int, cells=None, texels=None):
     return torch.empty((need + 3) // 4, dtype=torch.float32, device=density.device)
 
 
+def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: float, mask: int,
+                       *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
+                       workspace=None, image_out=None, depth_out=None, ws_continue=False,
+                       ws_defer=False):
+    """One fused step over these views: forward march, L1 seed sign(image - ref)/count
+    and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
+    device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
+    One step split over several calls (view chunks) shares ``workspace``: every
+    call but the first passes ws_continue, every call but the last ws_defer."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    if cells is None:
+        raise InvalidParameterError("the fused step needs cell records (pack_cells)")
+    vol, tf, prm = _descs(density, texels, rig, dt, False, cells)
+    V = cams.shape[0]
+    shape = (V, rig.band_rows, rig.width, 4)
+    _require(refs, "reference images", torch.float32)
+    if tuple(refs.shape) != shape:
+        raise InvalidInputError(f"refs shape {tuple(refs.shape)} does not match image {shape}")
+    _require(loss, "loss", torch.float64)
+    for buf, name, dt_ in ((d_volume, "d_volume", torch.float32), (d_tf, "d_tf", torch.float64),
+                           (d_camera, "d_camera", torch.float64), (d_dt, "d_dt", torch.float64),
+                           (image_out, "image_out", torch.float32),
+                           (depth_out, "depth_out", torch.float32)):
+        if buf is not None:
+            _require(buf, name, dt_)
+    if workspace is None:
+        if ws_continue or ws_defer:
+            raise InvalidParameterError("a step split over calls needs a shared workspace")
+        workspace = workspace_for(density, mask, cells, texels)
+    prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    ws_bytes = workspace.numel() * 4 if workspace is not None else 0
+    N.check(N.lib().ddvr_forward_adjoint_l1(
+        ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V, ctypes.byref(prm),
+        refs.data_ptr(), float(count), mask, ptr(image_out), ptr(depth_out), loss.data_ptr(),
+        ptr(d_volume), ptr(d_tf), ptr(d_camera), ptr(d_dt), ptr(workspace), ws_bytes,
+        _stream_ptr()))
+
+
 def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask: int, *,
             d_volume=None, d_tf=None, d_camera=None, d_dt=None, cells=None, workspace=None,
             tape=None, tape_stride=0):

@@ -32,7 +32,8 @@ def lib():
 
 def test_header_declares_the_boundary():
     names = _declared()
-    assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_adjoint_workspace_bytes",
+    assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
+                            "ddvr_adjoint_workspace_bytes",
                             "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
                             "ddvr_forward_color", "ddvr_adjoint_color",
                             "ddvr_l1_loss",
@@ -147,6 +148,17 @@ def test_adjoint_with_cells_requires_workspace(lib):
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 8, 16, None, None, None, None, 0, None)
     assert rc == 2 and "workspace" in lib.ddvr_last_error().decode()
+
+
+def test_fused_step_validation(lib):
+    vol, tf, prm = _descs()
+    loss = ctypes.c_double(0)
+    call = lambda v: lib.ddvr_forward_adjoint_l1(  # noqa: E731
+        ctypes.byref(v), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16, 8.0, 8, None, None,
+        ctypes.addressof(loss), 16, None, None, None, None, 0, None)
+    assert call(vol) == 3 and "cell records" in lib.ddvr_last_error().decode()
+    vol.cells = 32
+    assert call(vol) == 2 and "workspace" in lib.ddvr_last_error().decode()
 
 
 def test_zero_views_is_a_no_op(lib):

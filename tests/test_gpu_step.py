@@ -19,7 +19,7 @@ from test_distributed import _rank_grads, _scene
 pytestmark = pytest.mark.gpu
 
 
-def _step(cuda, layout, targets=("volume", "tf", "stepsize")):
+def _step(cuda, layout, targets=("volume", "tf", "stepsize"), **kw):
     import torch
     from paper_2107_12672_b200 import raymarch as R
     from paper_2107_12672_b200.distributed import ShardedStep
@@ -29,13 +29,15 @@ def _step(cuda, layout, targets=("volume", "tf", "stepsize")):
     ll = torch.tensor([[v.lon_deg, v.lat_deg] for v in views], dtype=torch.float64, device=cuda)
     rf = torch.from_numpy(np.stack(refs).astype(np.float32)).to(cuda)
     step = ShardedStep(vol, tx, ll, rf, dt, R.Rig(6, 5), targets=targets, radius=2.3,
-                       layout=layout)
+                       layout=layout, **kw)
     return step, rf
 
 
-@pytest.mark.parametrize("layout", ["cells", "voxels"])
-def test_step_matches_oracle(cuda, layout):
-    step, _ = _step(cuda, layout)
+@pytest.mark.parametrize("layout,fused", [("cells", True), ("cells", False), ("voxels", False)])
+def test_step_matches_oracle(cuda, layout, fused):
+    """fused: ddvr_forward_adjoint_l1 (one kernel per ray); else forward + l1 + adjoint."""
+    step, _ = _step(cuda, layout, fused=fused)
+    assert step.fused == fused
     f = step.run()
     ref = _rank_grads(0, 1)
     assert abs(float(f.loss) - float(ref.loss)) <= 1e-5 * abs(float(ref.loss))
@@ -94,3 +96,18 @@ def test_step_camera_gradients_stay_per_view(cuda):
     assert got.shape == (len(views), 2)
     assert rel_l2(got, np.stack(want)) <= 1e-4
     assert float(f.d_stepsize) != 0.0
+
+
+def test_fused_step_images_and_chunks(cuda):
+    """keep_images: the fused step's images equal forward(); host-staged refs in
+    chunks give the single-launch result."""
+    from paper_2107_12672_b200 import raymarch as R
+    step, rf = _step(cuda, "cells", keep_images=True, chunks=3)
+    f1 = step.run().buf.clone()
+    img, depth = R.forward(step.density, step.texels, step.cams, step.dt, step.rig,
+                           cells=step.cells)
+    assert rel_l2(step.img.double().cpu().numpy(), img.double().cpu().numpy()) <= 1e-6
+    assert rel_l2(step.depth.double().cpu().numpy(), depth.double().cpu().numpy()) <= 1e-6
+    host = rf.cpu().pin_memory()
+    f2 = step.run(refs_host=host).buf.clone()      # 3 chunks, each waits for its refs
+    assert rel_l2(f2.double().cpu().numpy(), f1.double().cpu().numpy()) <= 1e-6
