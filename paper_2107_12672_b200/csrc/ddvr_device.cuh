@@ -396,40 +396,15 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
       : "r"((int)pred), "l"(p));
 }
 
-// predicated shared loads for the held texel pair (same idea as ld256_if)
-__device__ __forceinline__ void lds64_if(bool pred, const void* p, float2& q) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.v2.f32 {%0,%1}, [%3];\n\t}"
-      : "+f"(q.x), "+f"(q.y)
-      : "r"((int)pred), "r"(a));
-}
-
-__device__ __forceinline__ void lds128_if(bool pred, const void* p, float4& q) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
-      "@q ld.shared.v4.f32 {%0,%1,%2,%3}, [%5];\n\t}"
-      : "+f"(q.x), "+f"(q.y), "+f"(q.z), "+f"(q.w)
-      : "r"((int)pred), "r"(a));
-}
-
 #ifndef DDVR_HOLD_CELL
 #define DDVR_HOLD_CELL 1
 #endif
-#ifndef DDVR_PIPE
-#define DDVR_PIPE 0   // measured: +0.6% at C4 (4 CTAs/SM vs 5), -2.9% at 128^3
-#endif
 
-#ifndef DDVR_ABS_UNROLL
-#define DDVR_ABS_UNROLL 1
-#endif
 #ifndef DDVR_ABS_MINB
 #define DDVR_ABS_MINB 5
 #endif
 #ifndef DDVR_ABS_WALK
 #define DDVR_ABS_WALK 1
-#endif
-#ifndef DDVR_HOLD_TEX
-#define DDVR_HOLD_TEX 0   // measured: no gain (shared lookups are not the binding wavefronts)
 #endif
 
 // predicated 128-bit vector red: no branch around it (the cell-run flush of
@@ -660,34 +635,6 @@ __device__ __forceinline__ float4 gauss_eval(const TfArgs& T, float d, float4& s
 constexpr int kTfTexture = DDVR_TF_TEXTURE, kTfPiecewise = DDVR_TF_PIECEWISE,
               kTfGaussian = DDVR_TF_GAUSSIAN;
 
-// The texel pair of the last sample, per lane: consecutive samples of a ray
-// mostly fall on the same texel interval, so the shared table is re-read only
-// by lanes whose interval changed (predicated loads, no branch).  Arithmetic
-// is exactly tf_eval / tf_eval_tau's.
-template <bool EMIT>
-struct TexHold {
-  int i = INT_MIN;
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), dl = make_float4(0.f, 0.f, 0.f, 0.f);  // EMIT
-  float2 q = make_float2(0.f, 0.f);                                                 // tau only
-
-  __device__ __forceinline__ float4 sample(const TfArgs& T, float d, int& i0, float& w,
-                                           float4& slope, bool want_slope) {
-    i0 = texel_coord(T, d, w);
-    const bool ld = i0 != i;
-    i = i0;
-    if (EMIT) {
-      lds128_if(ld, g_smem + 2 * i0 + 2, a);
-      lds128_if(ld, g_smem + 2 * i0 + 3, dl);
-      if (want_slope)
-        slope = make_float4(dl.x * T.fR, dl.y * T.fR, dl.z * T.fR, dl.w * T.fR);
-      return make_float4(__fmaf_rn(w, dl.x, a.x), __fmaf_rn(w, dl.y, a.y),
-                         __fmaf_rn(w, dl.z, a.z), __fmaf_rn(w, dl.w, a.w));
-    }
-    lds64_if(ld, tau_table(T) + i0 + 1, q);
-    if (want_slope) slope = make_float4(0.f, 0.f, 0.f, q.y * T.fR);
-    return make_float4(0.f, 0.f, 0.f, __fmaf_rn(w, q.y, q.x));
-  }
-};
 
 // (rgb, tau) of density d and its slope, for TF kind KIND; i0/w identify the
 // texel or knot interval (texture, piecewise).  EMIT=false: emission-free
@@ -848,8 +795,6 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   double S = 0.0;
   long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
   constexpr bool kHoldCell = CELLS && DDVR_HOLD_CELL;
-  constexpr bool kHoldTex = KIND == kTfTexture && DDVR_HOLD_TEX;
-  TexHold<EMIT> tex;
   // Emission-free TF (rgb = 0) without tape or early stop: the compositing
   // A += (1 - A) a_i (renderer.py:350-355) is exactly A = 1 - prod(1 - a_i)
   // = -expm1(-S), S = sum of the segment optical depths min(dt tau, -ln EPS)
@@ -861,8 +806,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     const float d = clamp_density(INSIDE || c.inside, interp(c, k).rho);
     int i0; float w;
     float4 slope;
-    const float4 s = kHoldTex ? tex.sample(TF, d, i0, w, slope, false)
-                              : tf_sample<KIND, EMIT>(TF, d, i0, w, slope, false);
+    const float4 s = tf_sample<KIND, EMIT>(TF, d, i0, w, slope, false);
     if (kAbs) {   // segment optical depth only (the EPS clamp of field.py:587-600)
       const float x = __fmul_rn(dt32, fmaxf(s.w, 0.f));
       S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
@@ -879,40 +823,6 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     T = __fmul_rn(T, g.ome);
     S += (double)g.od;
   };
-  if (kHoldCell && DDVR_PIPE) {
-    // Software-pipelined march: two record buffers, the gather of sample i+1
-    // is in flight while sample i composites (the kernel is bound by gather
-    // latency: ~70% of warp time in long-scoreboard stalls, ncu).  Each
-    // buffer keeps its record when its next cell is unchanged.
-    float va[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float vb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    int ha = INT_MIN, hb = INT_MIN;
-    Cell ca, cb;
-    const bool ins = INSIDE || r.all_inside;
-    locate<CELLS>(V, gx, gy, gz, ins, ca);
-    ld256_if(r.n > 0, V.cell0 + 8 * (long long)ca.cell, va);
-    ha = ca.cell;
-#pragma unroll 1
-    for (int i = 0; i < r.n; i += 2) {
-      const bool more = i + 1 < r.n;
-      locate<CELLS>(V, gx + r.gs[0], gy + r.gs[1], gz + r.gs[2], ins, cb);
-      ld256_if(more && cb.cell != hb, V.cell0 + 8 * (long long)cb.cell, vb);
-      hb = more ? cb.cell : hb;
-      if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
-      composite(ca, va, i);
-      gx += 2 * r.gs[0]; gy += 2 * r.gs[1]; gz += 2 * r.gs[2];
-      locate<CELLS>(V, gx, gy, gz, ins, ca);
-      const bool next = i + 2 < r.n;
-      ld256_if(next && ca.cell != ha, V.cell0 + 8 * (long long)ca.cell, va);
-      ha = next ? ca.cell : ha;
-      if (!more || (EARLY && A > kAlphaStop)) break;
-      composite(cb, vb, i + 1);
-    }
-    if (kAbs) A = (float)(-expm1(-S));
-    rgba = make_float4(c0, c1, c2, A);
-    depth = S;
-    return;
-  }
   float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int held = INT_MIN;
   // (the emitting variants spill at 48 registers when unrolled)
@@ -1125,12 +1035,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
 
   constexpr bool kHoldCell = CELLS && DDVR_HOLD_CELL;
-  constexpr bool kHoldTex = KIND == kTfTexture && DDVR_HOLD_TEX;
   float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int held = INT_MIN;
-  TexHold<EMIT> tex;
-  constexpr int kUnroll = kAbs ? DDVR_ABS_UNROLL : 1;   // (the full walk spills when unrolled)
-#pragma unroll (kUnroll)
+#pragma unroll 1   // (unrolled, the walks spill at their register budgets)
   for (int i = r.n - 1; i >= 0; --i) {
     Cell c;
     locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
@@ -1156,8 +1063,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       dq = q.y;
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
-      s = kHoldTex ? tex.sample(TF, d, i0, w, slope, want)
-                   : tf_sample<KIND, EMIT>(TF, d, i0, w, slope, want);
+      s = tf_sample<KIND, EMIT>(TF, d, i0, w, slope, want);
     }
     const Segment g = segment<SEG>(s.w, dt32);
 
