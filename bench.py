@@ -270,7 +270,8 @@ def run_own(args, cfg):
     ll = torch.tensor([poses[i] for i in mine], dtype=torch.float64, device=dev).reshape(-1, 2)
     rig = R.Rig(cfg.image, cfg.image)
     cams = R.camera_array(ll, cfg.radius, (0.0, 0.0, 0.0), cfg.fov)
-    refs, _ = R.forward(truth, tex, cams, cfg.dt, rig, with_depth=False)
+    refs, _ = R.forward(truth, tex, cams, cfg.dt, rig, with_depth=False,
+                        cells=R.pack_cells(truth) if args.layout == "cells" else None)
     g = torch.Generator(device=dev).manual_seed(7)
     est = (0.85 * truth + 0.1 * torch.rand(truth.shape, generator=g, device=dev)).contiguous()
     total_elems = 4 * cfg.image * cfg.image * len(poses)
