@@ -1026,6 +1026,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   constexpr bool kAbs = !EMIT && !kTf && !TAPE && KIND == kTfTexture && DDVR_ABS_WALK;
   const float abs_c = kAbs ? sd.w * (float)exp(-S) : 0.f;   // seed_a * T_n
   const float abs_k = abs_c * dt32 * TF.fR;                   // d_hat per unit texel delta
+  // emitting texel TF without the TF target: the slope is only needed dotted
+  // with the output adjoint, so the raw delta is kept and R applied once
+  constexpr bool kEmitTex = EMIT && !kTf && KIND == kTfTexture;
 
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
@@ -1054,9 +1057,17 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     int i0; float w;
     float4 slope, s;
     float dq = 0.f;   // kAbs: the raw texel delta (the slope is dq * R)
+    float4 dl4 = make_float4(0.f, 0.f, 0.f, 0.f);   // kEmitTex: the raw texel delta
     // (emission-free tables never serve the tf target: rgb and its slope are 0)
     const bool want = kDhat || (kTf && KIND != kTfTexture);
-    if (kAbs) {
+    if (kEmitTex) {   // tf_eval with the raw delta kept (d_hat below folds R once)
+      i0 = texel_coord(TF, d, w);
+      const float4 a = g_smem[2 * i0 + 2];
+      dl4 = g_smem[2 * i0 + 3];
+      s = make_float4(__fmaf_rn(w, dl4.x, a.x), __fmaf_rn(w, dl4.y, a.y),
+                      __fmaf_rn(w, dl4.z, a.z), __fmaf_rn(w, dl4.w, a.w));
+      slope = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (kAbs) {
       i0 = texel_coord(TF, d, w);
       const float2 q = tau_table(TF)[i0 + 1];
       s = make_float4(0.f, 0.f, 0.f, __fmaf_rn(w, q.y, q.x));
@@ -1130,9 +1141,13 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
-      const float d_hat = kAbs ? ((s.w < 0.f || g.a_clamped) ? 0.f : dq * abs_k)
-                          : EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
-                                 : slope.w * tau_hat;
+      // (kEmitTex: slope . (aT sd_rgb, tau_hat) = R (aT (delta_rgb . sd_rgb) + delta_tau tau_hat))
+      const float d_hat =
+          kAbs ? ((s.w < 0.f || g.a_clamped) ? 0.f : dq * abs_k)
+          : kEmitTex ? TF.fR * __fmaf_rn(aT, dl4.x * sd.x + dl4.y * sd.y + dl4.z * sd.z,
+                                         dl4.w * tau_hat)
+          : EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
+                 : slope.w * tau_hat;
       const bool live = inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol && CELLS) {   // renderer.py:607-608, accumulated per cell run
         // The run accumulates the 8 moments sum dh * phi(u), phi = {1, ux, uy,
