@@ -277,7 +277,7 @@ def run_own(args, cfg):
     total_elems = 4 * cfg.image * cfg.image * len(poses)
     step = ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                        total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
-                       layout=args.layout, fused=not args.unfused)
+                       layout=args.layout, fused=False if args.unfused else "auto")
     # density targets run the whole optimisation iteration (prior + Adam + projection)
     runner = TomographyIteration(step, lr=0.02, lam=0.5) if "volume" in cfg.targets else step
     _, n_steps, _ = R.ray_setup(cams, cfg.dt, rig, dims=tuple(truth.shape))

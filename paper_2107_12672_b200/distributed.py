@@ -78,13 +78,16 @@ class ShardedStep:
     With cell records (the default layout) the forward, the L1 seed and the
     adjoint run as one fused kernel per ray (ddvr_forward_adjoint_l1);
     ``fused=False`` keeps the three separate launches (ddvr_forward,
-    ddvr_l1_loss, ddvr_adjoint).  ``keep_images``: also write the rendered
+    ddvr_l1_loss, ddvr_adjoint).  ``fused="auto"`` (default) fuses unless the
+    camera or stepsize target is on: their walks carry fp64 sums (~100
+    registers), which would hold the fused forward phase to 2 CTAs/SM where
+    the separate forward runs 5 (C3: 58 vs 65 G samples/s).  ``keep_images``: also write the rendered
     images / optical depth of the fused step into ``img`` / ``depth``.
     """
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
-                 group=None, layout="cells", fused=True, keep_images=False, chunks=4):
+                 group=None, layout="cells", fused="auto", keep_images=False, chunks=4):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
@@ -109,7 +112,9 @@ class ShardedStep:
                       if layout == "cells" else None)
         self.workspace = R.workspace_for(density, self.mask, self.cells, texels)
         self._copy_stream = None
-        self.fused = fused and self.cells is not None
+        if fused == "auto":
+            fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
+        self.fused = bool(fused) and self.cells is not None
         self.keep_images = keep_images
         # view chunks of the fused step when the refs come from the host: chunk k
         # waits only for its own refs, so the copy of the rest overlaps compute

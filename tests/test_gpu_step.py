@@ -49,7 +49,7 @@ def test_step_matches_oracle(cuda, layout, fused):
 
 def test_host_staged_refs_are_identical(cuda):
     """refs_host: the copy runs on a side stream and the loss kernel waits for it."""
-    step, rf = _step(cuda, "cells")
+    step, rf = _step(cuda, "cells", fused=True)
     a = step.run().buf.clone()
     host = rf.cpu().pin_memory()
     rf.zero_()                        # the step must use the staged copy, not stale data
@@ -80,10 +80,13 @@ def test_tomography_iterations_reduce_the_loss(cuda):
     assert float(est.min()) >= 0.0 and float(est.max()) <= 1.0   # projection (optim.py:78-89)
 
 
-def test_step_camera_gradients_stay_per_view(cuda):
-    """C3-style targets: d/d(lon, lat) per view (field.py:11), kept by the owning rank."""
+@pytest.mark.parametrize("fused", ["auto", True])
+def test_step_camera_gradients_stay_per_view(cuda, fused):
+    """C3-style targets: d/d(lon, lat) per view (field.py:11), kept by the owning rank
+    ("auto" runs the separate kernels for these targets)."""
     from oracle import dvr_oracle as O
-    step, _ = _step(cuda, "cells", targets=("camera", "stepsize"))
+    step, _ = _step(cuda, "cells", targets=("camera", "stepsize"), fused=fused)
+    assert step.fused == (fused is True)
     f = step.run()
     grid, tex, views, refs, dt = _scene()
     count = sum(r.size for r in refs)
@@ -102,7 +105,7 @@ def test_fused_step_images_and_chunks(cuda):
     """keep_images: the fused step's images equal forward(); host-staged refs in
     chunks give the single-launch result."""
     from paper_2107_12672_b200 import raymarch as R
-    step, rf = _step(cuda, "cells", keep_images=True, chunks=3)
+    step, rf = _step(cuda, "cells", keep_images=True, chunks=3, fused=True)
     f1 = step.run().buf.clone()
     img, depth = R.forward(step.density, step.texels, step.cams, step.dt, step.rig,
                            cells=step.cells)
