@@ -180,6 +180,10 @@ int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
   const long long nvox = (long long)vol->dims[0] * vol->dims[1] * vol->dims[2];
   if (nvox > 0x7fffffffLL)
     return set_error(DDVR_UNSUPPORTED, "volume has more than 2^31 voxels");
+  // cell indices are int32 (relative to cell (0,0,0)): the padded grid must fit
+  if (vol->cells && (long long)(vol->dims[0] + 1) * (vol->dims[1] + 1) * (vol->dims[2] + 1) >
+                        0x7fffffffLL)
+    return set_error(DDVR_UNSUPPORTED, "cell-record grid has more than 2^31 cells");
   if (need_data && !vol->data) return set_error(DDVR_INVALID_INPUT, "volume data pointer is NULL");
   if (vol->cells && ((uintptr_t)vol->cells & 31) != 0)
     return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");

@@ -161,6 +161,21 @@ def test_fused_step_validation(lib):
     assert call(vol) == 2 and "workspace" in lib.ddvr_last_error().decode()
 
 
+def test_index_range_limits(lib):
+    """int32 voxel and cell indices: larger grids are refused, not wrapped (validation
+    runs before the zero-view early return)."""
+    vol, tf, prm = _descs(dims=(1300, 1300, 1300))
+    assert lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), 16, 0, ctypes.byref(prm), 16,
+                            None, None) == 3
+    vol, tf, prm = _descs(dims=(1289, 1289, 1290))          # < 2^31 voxels, > 2^31 cells
+    assert lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), 16, 0, ctypes.byref(prm), 16,
+                            None, None) == 0                  # voxel layout: accepted
+    vol.cells = 32
+    assert lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), 16, 0, ctypes.byref(prm), 16,
+                            None, None) == 3
+    assert "2^31 cells" in lib.ddvr_last_error().decode()
+
+
 def test_zero_views_is_a_no_op(lib):
     vol, tf, prm = _descs()
     assert lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), None, 0, ctypes.byref(prm), 16,
