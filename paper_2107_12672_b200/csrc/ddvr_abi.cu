@@ -615,7 +615,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   auto launch = mask <= 3 ? launch_adjoint_g0 : mask <= 7 ? launch_adjoint_g1
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;
   const int n_kernels = launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed,
-                               d_volume, d_cells, d_tf, d_camera, d_dt, fu);
+                               d_volume, d_cells, d_camera, d_dt, fu);
   if ((rc = check_launch(fu ? "dvr_adjoint_kernel (fused)" : "dvr_adjoint_kernel"))) return rc;
   g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
   if (flags & DDVR_FLAG_WS_DEFER) return DDVR_OK;   // a later call of this step folds

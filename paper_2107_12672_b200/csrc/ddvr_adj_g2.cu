@@ -6,15 +6,15 @@ namespace ddvr_impl {
 template <unsigned M, bool CELLS, bool FUSED>
 static int adj2(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
                 const Geometry& G, const float* image, const float* depth, const float* seed,
-                float* dv, float* dcells, double* dtf, double* dcam, double* ddt,
+                float* dv, float* dcells, double* dcam, double* ddt,
                 const FusedArgs& fu) {
   auto k = dvr_adjoint_kernel<M, CELLS, 0, FUSED>;
   set_smem(k, smem);
-  k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt, fu);
+  k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dcam, ddt, fu);
   if constexpr (CELLS && !(M & DDVR_TARGET_TF)) {   // the absorption-only walk
     auto k1 = dvr_adjoint_kernel<M, CELLS, 1, FUSED>;
     set_smem(k1, smem);
-    k1<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt, fu);
+    k1<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dcam, ddt, fu);
     return 2;
   }
   return 1;
@@ -24,19 +24,19 @@ static int adj2(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const
 template <unsigned M, bool CELLS>
 static int adj(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
                const Geometry& G, const float* image, const float* depth, const float* seed,
-               float* dv, float* dcells, double* dtf, double* dcam, double* ddt,
+               float* dv, float* dcells, double* dcam, double* ddt,
                const FusedArgs* fu) {
   if (fu) {
     if constexpr (CELLS)
-      return adj2<M, true, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf,
-                                 dcam, ddt, *fu);
+      return adj2<M, true, true>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dcam,
+                                 ddt, *fu);
     return 0;
   }
-  return adj2<M, CELLS, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf,
-                               dcam, ddt, FusedArgs{});
+  return adj2<M, CELLS, false>(grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dcam,
+                               ddt, FusedArgs{});
 }
 
-#define DDVR_ADJ_ARGS grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dtf, dcam, ddt, fu
+#define DDVR_ADJ_ARGS grid, smem, st, V, T, G, image, depth, seed, dv, dcells, dcam, ddt, fu
 DDVR_ADJ_LAUNCHER(launch_adjoint_g2) {
   switch (mask) {
     case 8:

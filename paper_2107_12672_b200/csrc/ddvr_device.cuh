@@ -143,8 +143,8 @@ struct FusedArgs {
 #define DDVR_ADJ_LAUNCHER(NAME)                                                              \
   int NAME(unsigned mask, bool cells, dim3 grid, size_t smem, cudaStream_t st,             \
             const VolArgs& V, const TfArgs& T, const Geometry& G, const float* image,       \
-            const float* depth, const float* seed, float* dv, float* dcells, double* dtf,   \
-            double* dcam, double* ddt, const FusedArgs* fu)
+            const float* depth, const float* seed, float* dv, float* dcells, double* dcam,  \
+            double* ddt, const FusedArgs* fu)
 DDVR_ADJ_LAUNCHER(launch_adjoint_g0);   // masks 1-3   (camera / stepsize)
 DDVR_ADJ_LAUNCHER(launch_adjoint_g1);   // masks 4-7   (tf [+ camera / stepsize])
 DDVR_ADJ_LAUNCHER(launch_adjoint_g2);   // masks 8-11  (volume [+ camera / stepsize])
@@ -1229,8 +1229,8 @@ template <unsigned MASK, bool CELLS, int ROLE, bool FUSED>
 __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
     const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
-    float* __restrict__ d_cells, double* __restrict__ d_tf, double* __restrict__ d_camera,
-    double* __restrict__ d_dt, FusedArgs Fu) {
+    float* __restrict__ d_cells, double* __restrict__ d_camera, double* __restrict__ d_dt,
+    FusedArgs Fu) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
   constexpr bool kStep = MASK & DDVR_TARGET_STEPSIZE;
   constexpr bool kTf = MASK & DDVR_TARGET_TF;
