@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--views", type=int, default=0,
                    help="profiling aid: use only the first N views (not a bench result)")
     p.add_argument("--layout", default="cells", choices=["cells", "voxels"])
+    p.add_argument("--graph", action="store_true",
+                   help="replay each timed iteration from a captured CUDA graph (1 GPU)")
     p.add_argument("--unfused", action="store_true",
                    help="separate forward / L1 / adjoint launches instead of the fused step")
     return p.parse_args()
@@ -279,7 +281,9 @@ def run_own(args, cfg):
                        total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
                        layout=args.layout, fused=False if args.unfused else "auto")
     # density targets run the whole optimisation iteration (prior + Adam + projection)
-    runner = TomographyIteration(step, lr=0.02, lam=0.5) if "volume" in cfg.targets else step
+    graphed = args.graph and world == 1 and "volume" in cfg.targets
+    runner = (TomographyIteration(step, lr=0.02, lam=0.5, graph=graphed)
+              if "volume" in cfg.targets else step)
     _, n_steps, _ = R.ray_setup(cams, cfg.dt, rig, dims=tuple(truth.shape))
     local_samples = int(n_steps.to(torch.int64).sum().item())
     local_rays = n_steps.numel()
@@ -295,12 +299,18 @@ def run_own(args, cfg):
 
     # per-kernel events on the launching stream: step start, forward end,
     # adjoint start, adjoint end, step end
-    def timed_step():
+    def timed_step(r=None):
+        r = r or runner
         st = torch.cuda.current_stream()
         e = {k: torch.cuda.Event(enable_timing=True)
              for k in ("start", "post_forward", "pre_adjoint", "post_adjoint", "end")}
         e["start"].record(st)
-        runner.run(hook=lambda k: e[k].record(st))
+        if graphed and r is runner:        # one replay: no per-kernel events inside
+            runner.run()
+            for k in ("post_forward", "pre_adjoint", "post_adjoint"):
+                e[k].record(st)
+        else:
+            r.run(hook=lambda k: e[k].record(st))
         e["end"].record(st)
         return e
 
@@ -321,6 +331,17 @@ def run_own(args, cfg):
             fwd_ms.append(e["start"].elapsed_time(e["post_forward"]))
             adj_ms.append(e["pre_adjoint"].elapsed_time(e["post_adjoint"]))
     launches = N.launch_count() - launches0
+    if graphed:   # replays launch the captured kernels; the breakdown comes from eager steps
+        launches = runner.graph_launches * args.steps
+        eager = TomographyIteration(step, lr=0.02, lam=0.5)
+        fwd_ms, adj_ms = [], []
+        for _ in range(max(2, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e = timed_step(eager)
+            torch.cuda.synchronize()
+            fwd_ms.append(e["start"].elapsed_time(e["post_forward"]))
+            adj_ms.append(e["pre_adjoint"].elapsed_time(e["post_adjoint"]))
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -342,7 +363,11 @@ def run_own(args, cfg):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         est.copy_(host_vol, non_blocking=True)
-        runner.run(refs_host=host_refs)      # refs H2D overlaps pack + forward
+        if graphed:   # the graph reads step.refs: copy first, then replay
+            refs.copy_(host_refs, non_blocking=True)
+            runner.run()
+        else:
+            runner.run(refs_host=host_refs)  # refs H2D overlaps pack + forward
         f = step.flat
         # the step's result: the updated density (optimiser steps) or its gradient
         host_grad.copy_((est if runner is not step else f.d_volume).reshape(-1),
@@ -422,6 +447,9 @@ def run_own(args, cfg):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        line["config"]["step"] = (("fused forward+L1+adjoint" if getattr(step, "fused", False)
+                                   else "forward, L1, adjoint") +
+                                  (", CUDA-graph replay" if graphed else ""))
         if world == 1 and not args.no_cpu_baseline:
             sps, rps, cores, desc = cpu_sample(cfg, args.cpu_seconds)
             line["cpu_baseline"] = {"value": sps, "unit": "samples/s", "cores": cores,

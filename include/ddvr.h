@@ -242,6 +242,14 @@ typedef struct {
 int ddvr_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
                    const ddvr_adam* cfg, int32_t* nonfinite, void* stream);
 
+/* The same update with the step counter on the device, for CUDA-graph replay:
+ * state (device, 4 int32, zeroed before the first step) holds t; each call
+ * advances it (unless the update is skipped for a non-finite gradient) and
+ * derives the bias corrections on the device.  cfg->step is ignored. */
+int ddvr_adam_step_device(float* params, const float* grads, float* m, float* v, int64_t n,
+                          const ddvr_adam* cfg, int32_t* state, int32_t* nonfinite,
+                          void* stream);
+
 /* upsample_volume (optim.py:92-129): dst (2X,2Y,2Z) from src (X,Y,Z). */
 int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, void* stream);
 

@@ -38,7 +38,8 @@ EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1", "ddvr_adj
             "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
             "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_ray_setup",
             "ddvr_prior_volume",
-            "ddvr_prior_tf", "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_volume_from_raw",
+            "ddvr_prior_tf", "ddvr_adam_step", "ddvr_adam_step_device",
+            "ddvr_upsample_volume", "ddvr_volume_from_raw",
             "ddvr_volume_to_raw", "ddvr_image_to_ppm", "ddvr_last_error",
             "ddvr_abi_version", "ddvr_launch_count")
 
@@ -121,6 +122,9 @@ def _bind(lib):
     lib.ddvr_prior_tf.restype = ctypes.c_int
     lib.ddvr_adam_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(DdvrAdam), vp, vp]
     lib.ddvr_adam_step.restype = ctypes.c_int
+    lib.ddvr_adam_step_device.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(DdvrAdam), vp, vp,
+                                          vp]
+    lib.ddvr_adam_step_device.restype = ctypes.c_int
     lib.ddvr_upsample_volume.argtypes = [vp, i3, vp, vp]
     lib.ddvr_upsample_volume.restype = ctypes.c_int
     lib.ddvr_volume_from_raw.argtypes = [vp, i3, P(ctypes.c_double), vp, vp]

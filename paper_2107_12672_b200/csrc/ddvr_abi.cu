@@ -351,8 +351,13 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p,
                                                  const float* __restrict__ g,
                                                  float* __restrict__ m, float* __restrict__ v,
                                                  long long n, ddvr_adam a, float bc1, float bc2,
-                                                 const int* __restrict__ flag) {
+                                                 const int* __restrict__ flag,
+                                                 const int32_t* __restrict__ state) {
   if (flag && *flag) return;
+  if (state) {   // device step counter: bias corrections from adam_prep_kernel
+    bc1 = __int_as_float(state[1]);
+    bc2 = __int_as_float(state[2]);
+  }
   const long long stride = (long long)gridDim.x * blockDim.x;
   const float b1 = (float)a.beta1, b2 = (float)a.beta2, lr = (float)a.lr, eps = (float)a.eps;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -366,6 +371,18 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p,
     pi = last ? fminf(fmaxf(pi, a.lo), a.hi) : fminf(fmaxf(pi, a.lo_other), a.hi_other);
     p[i] = pi;
   }
+}
+
+// Device-side Adam step counter (ddvr_adam_step_device): t = state[0] + 1 and the
+// bias corrections 1 - beta^t (fp64, rounded once), unless the update is skipped
+// for a non-finite gradient -- so a captured CUDA graph replays correct steps.
+__global__ void adam_prep_kernel(int32_t* __restrict__ state, double beta1, double beta2,
+                                 const int* __restrict__ flag) {
+  if (threadIdx.x != 0 || (flag && *flag)) return;
+  const int t = state[0] + 1;
+  state[0] = t;
+  state[1] = __float_as_int((float)(1.0 - pow(beta1, (double)t)));
+  state[2] = __float_as_int((float)(1.0 - pow(beta2, (double)t)));
 }
 
 // upsample_volume (optim.py:92-129): fine node j at coarse coordinate (j - 0.5)/2,
@@ -812,7 +829,32 @@ int ddvr_adam_step(float* params, const float* grads, float* m, float* v, int64_
   }
   const float bc1 = (float)(1.0 - pow(cfg->beta1, (double)cfg->step));
   const float bc2 = (float)(1.0 - pow(cfg->beta2, (double)cfg->step));
-  adam_kernel<<<grid_blocks(n), 256, 0, st>>>(params, grads, m, v, n, *cfg, bc1, bc2, nonfinite);
+  adam_kernel<<<grid_blocks(n), 256, 0, st>>>(params, grads, m, v, n, *cfg, bc1, bc2, nonfinite,
+                                               nullptr);
+  return check_launch("adam_kernel");
+}
+
+int ddvr_adam_step_device(float* params, const float* grads, float* m, float* v, int64_t n,
+                          const ddvr_adam* cfg, int32_t* state, int32_t* nonfinite,
+                          void* stream) {
+  g_err[0] = 0;
+  if (!cfg) return set_error(DDVR_INVALID_PARAMETER, "adam config is NULL");
+  if (!(cfg->lr > 0.0)) return set_error(DDVR_INVALID_PARAMETER, "learning rate must be positive");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative parameter count");
+  if (!state) return set_error(DDVR_INVALID_INPUT, "adam state pointer is NULL");
+  if (n == 0) return DDVR_OK;
+  if (!params || !grads || !m || !v)
+    return set_error(DDVR_INVALID_INPUT, "parameter, gradient or moment pointer is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (nonfinite) {
+    finite_check_kernel<<<grid_blocks(n), 256, 0, st>>>(grads, n, nonfinite);
+    if ((rc = check_launch("finite_check_kernel"))) return rc;
+  }
+  adam_prep_kernel<<<1, 32, 0, st>>>(state, cfg->beta1, cfg->beta2, nonfinite);
+  if ((rc = check_launch("adam_prep_kernel"))) return rc;
+  adam_kernel<<<grid_blocks(n), 256, 0, st>>>(params, grads, m, v, n, *cfg, 1.f, 1.f, nonfinite,
+                                               state);
   return check_launch("adam_kernel");
 }
 

@@ -229,14 +229,47 @@ class TomographyIteration:
     """
 
     def __init__(self, step: ShardedStep, *, lr: float = 0.02, lam: float = 0.5,
-                 check_finite: bool = False):
+                 check_finite: bool = False, graph: bool = False):
         from .optim import AdamState
         self.step = step
         self.lam = lam
-        self.adam = AdamState(lr=lr)
         self.check_finite = check_finite
+        # graph: after two eager warm-up iterations one iteration is captured in a
+        # CUDA graph and replayed (launch-bound small problems); single process
+        # only, Adam's step counter lives on the device
+        self.graph = graph
+        self.adam = AdamState(lr=lr, device_step=graph)
+        self._g = None
+        self._out = None
+        self._eager = 0
+        self.graph_launches = 0      # libddvr kernels in the captured graph
+        if graph and dist.is_available() and dist.is_initialized() and \
+                dist.get_world_size(step.group) > 1:
+            raise ValueError("graph capture of the step is single-process only")
 
     def run(self, hook=None, refs_host=None):
+        """One iteration -> (loss (1,) f64, prior (1,) f64) on device.  With ``graph``
+        the hook and refs_host are not available (the graph replays fixed work)."""
+        if not self.graph:
+            return self._iterate(hook, refs_host)
+        if hook is not None or refs_host is not None:
+            raise ValueError("a graphed iteration takes no hook or refs_host")
+        if self._g is None and self._eager < 2:
+            self._eager += 1
+            return self._iterate(None, None)
+        if self._g is None:
+            side = torch.cuda.Stream(self.step.density.device)
+            side.wait_stream(torch.cuda.current_stream(self.step.density.device))
+            self._g = torch.cuda.CUDAGraph()
+            n0 = N.launch_count()
+            with torch.cuda.graph(self._g, stream=side):
+                self._out = self._iterate(None, None)
+            self.graph_launches = N.launch_count() - n0
+            torch.cuda.current_stream(self.step.density.device).wait_stream(side)
+        self._g.replay()
+        return self._out
+
+    def _iterate(self, hook, refs_host):
         from .optim import prior_volume
         f = self.step.run(hook=hook, refs_host=refs_host)
         density = self.step.density

@@ -67,12 +67,18 @@ class AdamState:
     m: torch.Tensor | None = None
     v: torch.Tensor | None = None
     flag: torch.Tensor | None = field(default=None, repr=False)
+    # device_step: the step counter lives on the device (ddvr_adam_step_device), so
+    # the update can be captured in a CUDA graph and replayed; no host sync
+    device_step: bool = False
+    state: torch.Tensor | None = field(default=None, repr=False)
 
     def update(self, params: torch.Tensor, grads: torch.Tensor, project: str | None = None,
                tau_max: float = TAU_MAX_DEFAULT, check_finite: bool = True) -> None:
         """One in-place Adam step + projection (``volume``: [0,1]; ``tf``: rgb >= 0,
         tau in [0, tau_max]; None: unconstrained).  Raises NumericalAbortError
-        (and leaves the parameters untouched) on a non-finite gradient."""
+        (and leaves the parameters untouched) on a non-finite gradient; with
+        ``device_step`` the update is still skipped on the device but nothing is
+        raised (no host synchronisation)."""
         _require(params, "params", torch.float32)
         _require(grads, "grads", torch.float32)
         if params.shape != grads.shape:
@@ -93,6 +99,15 @@ class AdamState:
         a = N.DdvrAdam(self.lr, self.beta1, self.beta2, self.eps, self.step + 1, *cfg)
         if check_finite:
             self.flag.zero_()
+        if self.device_step:
+            if self.state is None:
+                self.state = torch.zeros(4, dtype=torch.int32, device=params.device)
+                self.state[0] = self.step
+            N.check(N.lib().ddvr_adam_step_device(
+                params.data_ptr(), grads.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                params.numel(), ctypes.byref(a), self.state.data_ptr(),
+                self.flag.data_ptr() if check_finite else None, _stream_ptr()))
+            return
         N.check(N.lib().ddvr_adam_step(params.data_ptr(), grads.data_ptr(), self.m.data_ptr(),
                                        self.v.data_ptr(), params.numel(), ctypes.byref(a),
                                        self.flag.data_ptr() if check_finite else None,

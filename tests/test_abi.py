@@ -38,7 +38,8 @@ def test_header_declares_the_boundary():
                             "ddvr_forward_color", "ddvr_adjoint_color",
                             "ddvr_l1_loss",
                             "ddvr_ray_setup", "ddvr_prior_volume", "ddvr_prior_tf",
-                            "ddvr_adam_step", "ddvr_upsample_volume", "ddvr_volume_from_raw",
+                            "ddvr_adam_step", "ddvr_adam_step_device",
+                            "ddvr_upsample_volume", "ddvr_volume_from_raw",
                             "ddvr_volume_to_raw", "ddvr_image_to_ppm", "ddvr_last_error",
                             "ddvr_abi_version", "ddvr_launch_count"])
 

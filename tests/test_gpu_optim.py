@@ -53,6 +53,25 @@ def test_adam_trajectory_and_projection(cuda):
     np.testing.assert_allclose(t.cpu().numpy(), g["proj_tf"], rtol=1e-6, atol=1e-6)
 
 
+def test_adam_device_step_counter(cuda):
+    """ddvr_adam_step_device (graph-safe): the same trajectory as the reference's
+    adam_step; a skipped (non-finite) update does not advance the counter."""
+    import torch
+    from paper_2107_12672_b200 import optim as P
+    g = golden("optim")
+    p = _t(g["volume"], cuda)
+    st = P.AdamState(lr=float(g["adam_lr"]), device_step=True)
+    for k in range(3):
+        st.update(p, _t(g["adam_grads"][k], cuda), project=None, check_finite=False)
+        assert rel_max(p.cpu().numpy(), g["adam_traj"][k]) <= 1e-5
+    assert int(st.state[0]) == 3
+    before = p.clone()
+    bad = _t(g["adam_grads"][0], cuda)
+    bad.view(-1)[0] = float("nan")
+    st.update(p, bad, project=None, check_finite=True)       # skipped on the device
+    assert torch.equal(p, before) and int(st.state[0]) == 3
+
+
 def test_adam_rejects_non_finite_gradients(cuda):
     import torch
     from paper_2107_12672_b200 import optim as P

@@ -114,3 +114,20 @@ def test_fused_step_images_and_chunks(cuda):
     host = rf.cpu().pin_memory()
     f2 = step.run(refs_host=host).buf.clone()      # 3 chunks, each waits for its refs
     assert rel_l2(f2.double().cpu().numpy(), f1.double().cpu().numpy()) <= 1e-6
+
+
+def test_graphed_iterations_follow_the_eager_trajectory(cuda):
+    """TomographyIteration(graph=True): two eager warm-ups, then one captured CUDA
+    graph replayed per iteration (device-side Adam counter)."""
+    import torch
+    from paper_2107_12672_b200.distributed import TomographyIteration
+    vols = []
+    for graph in (False, True):
+        step, _ = _step(cuda, "cells", targets=("volume",))
+        it = TomographyIteration(step, lr=0.05, lam=0.1, graph=graph)
+        losses = [float(it.run()[0]) for _ in range(6)]
+        vols.append(step.density.clone())
+        assert losses[-1] < losses[0]
+    assert rel_l2(vols[1].double().cpu().numpy(), vols[0].double().cpu().numpy()) <= 1e-5
+    with pytest.raises(ValueError):
+        it.run(refs_host=torch.zeros(1))
