@@ -199,6 +199,16 @@ int64_t ddvr_cells_bytes(const int32_t dims[3]);
  * ddvr_cells_bytes bytes).  Call again whenever the density changes. */
 int ddvr_pack_cells(const ddvr_volume* vol, float* cells_out, void* stream);
 
+/* opacity_entropy (objectives.py:95-126) of n_images (device) (n_pixels, 4)
+ * float images: out (device, double, n_images x 4) receives [H, S, S+, T] per
+ * image (normalised Shannon entropy of the alpha channel, alpha sum, positive
+ * alpha sum, sum a log2 a); seed_out (device, nullable, same shape as the
+ * images) the seed dH/dalpha in the alpha channel (rgb 0), non-finite values
+ * mapped to +-1e6 and clipped like the reference.  Degenerate (S <= 0 or
+ * n_pixels < 2): H = 0, zero seed. */
+int ddvr_opacity_entropy(const float* images, int64_t n_pixels, int32_t n_images, double* out,
+                         float* seed_out, void* stream);
+
 /* Fused L1 loss + seed (objectives.py:38-54) over n floats: seed_out[i] =
  * sign(x-y)/count (sign(0)=0) and loss_out[0] += sum|x-y|/count (double).
  * count is the normaliser (total element count over all views/ranks). */

@@ -282,6 +282,32 @@ def optim_cases():
          proj_tf_in=tex * 40.0, proj_tf=proj_tf, up_src=small, up=up)
 
 
+def entropy_cases():
+    """opacity_entropy (objectives.py:95-126) on fp32-representable alpha channels,
+    incl. the acceptance contract's images (test_acceptance.py:135-163) and edges."""
+    from voldiff import objectives as vo
+    rng = np.random.default_rng(13)
+    imgs = {}
+    u = np.zeros((8, 8, 4)); u[..., 3] = f32(0.42); imgs["uniform"] = u
+    o = np.zeros((8, 8, 4)); o[3, 5, 3] = f32(0.9); imgs["onehot"] = o
+    r = np.zeros((16, 12, 4)); r[..., 3] = f32(rng.uniform(0.01, 1.0, (16, 12)))
+    r[..., :3] = f32(rng.uniform(0, 1, (16, 12, 3))); imgs["random"] = r
+    z = r.copy(); z[2:5, 3:9, 3] = 0.0; imgs["zeros"] = z      # p = 0: the +1e6 seed
+    imgs["scaled"] = np.where(np.arange(4) == 3, r * np.float32(123.4), r).astype(np.float64)
+    imgs["scaled"][..., 3] = f32(imgs["scaled"][..., 3])
+    imgs["empty"] = np.zeros((5, 7, 4))                       # degenerate
+    imgs["single"] = np.full((1, 1, 4), 0.5)                  # n < 2: degenerate
+    n = r.copy(); n[0, 0, 3] = -0.25; imgs["negative"] = n    # a < 0: excluded from F
+    out = {}
+    for k, im in imgs.items():
+        h, seed, deg = vo.opacity_entropy(im)
+        out[f"{k}_image"] = im
+        out[f"{k}_h"] = np.float64(h)
+        out[f"{k}_seed"] = seed
+        out[f"{k}_degenerate"] = np.bool_(deg)
+    save("entropy", **out)
+
+
 def io_cases():
     """Files written by the reference's fileio (fileio.py:27-127) + fibonacci_views poses."""
     import json
@@ -318,7 +344,10 @@ def io_cases():
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad", "color", "io"]
+    which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad", "color", "io",
+                             "entropy"]
+    if "entropy" in which:
+        entropy_cases()
     if "io" in which:
         io_cases()
     if "color" in which:

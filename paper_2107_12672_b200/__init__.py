@@ -34,6 +34,7 @@ from .voldiff_api import (
     blend_invert,
     fibonacci_views,
     l1_loss,
+    opacity_entropy,
     render,
     render_adjoint,
     render_colorvol,
@@ -61,7 +62,7 @@ __all__ = [
     "MissingMetadataError", "NumericalAbortError", "UnsupportedConfigurationError",
     "VoldiffError", "EPS_ALPHA", "EPS_POLE_DEG", "DensityVolume", "GradientSet", "ImageRGBA",
     "RenderConfig", "SphericalCamera", "TransferFunction", "blend", "blend_adjoint",
-    "blend_invert", "l1_loss", "render", "render_adjoint", "render_forward_grad",
+    "blend_invert", "l1_loss", "opacity_entropy", "render", "render_adjoint", "render_forward_grad",
     "ColorVolume", "render_colorvol", "render_colorvol_adjoint", "fibonacci_views", "fileio",
     "DiffDVR",
     "Rig", "adjoint", "camera_array", "forward", "forward_grad", "l1_loss_seed", "pack_cells",

@@ -34,9 +34,9 @@ TF_TEXTURE = 0
 TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
-EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1", "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes",
-            "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
-            "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_ray_setup",
+EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
+            "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
+            "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_ray_setup",
             "ddvr_prior_volume",
             "ddvr_prior_tf", "ddvr_adam_step", "ddvr_adam_step_device",
             "ddvr_upsample_volume", "ddvr_volume_from_raw",
@@ -112,6 +112,8 @@ def _bind(lib):
     lib.ddvr_pack_cells.restype = ctypes.c_int
     lib.ddvr_l1_loss.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_double, vp, vp, vp]
     lib.ddvr_l1_loss.restype = ctypes.c_int
+    lib.ddvr_opacity_entropy.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]
+    lib.ddvr_opacity_entropy.restype = ctypes.c_int
     lib.ddvr_ray_setup.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp, vp,
                                    vp]
     lib.ddvr_ray_setup.restype = ctypes.c_int

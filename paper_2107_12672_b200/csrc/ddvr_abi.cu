@@ -158,6 +158,59 @@ __global__ void __launch_bounds__(256) l1_loss_kernel(const float* __restrict__ 
   }
 }
 
+// opacity_entropy (objectives.py:95-126), per image v of n pixels:
+// S = sum a, S+ = sum_{a>0} a, T = sum_{a>0} a log2 a (fp64, alpha channel);
+// with p = a / S, F = sum_{p>0} p log2 p = T / S - log2(S) S+ / S, H = -F / log2 n.
+__global__ void __launch_bounds__(256) entropy_sums_kernel(const float4* __restrict__ img,
+                                                          int64_t n, double* __restrict__ out) {
+  __shared__ double part[8][3];
+  const float4* im = img + (size_t)blockIdx.y * n;
+  double s = 0.0, sp = 0.0, t = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = (double)im[i].w;
+    s += a;
+    if (a > 0.0) { sp += a; t += a * log2(a); }
+  }
+  s = warp_sum(s); sp = warp_sum(sp); t = warp_sum(t);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { part[w][0] = s; part[w][1] = sp; part[w][2] = t; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double acc = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) acc += part[k][threadIdx.x];
+    atomicAdd(out + 4 * blockIdx.y + 1 + threadIdx.x, acc);
+  }
+}
+
+// H per image and the alpha-channel seed dH/da_k = -(log2 p_k - F) / (S log2 n),
+// non-finite -> +-1e6 and clipped to [-1e6, 1e6] (objectives.py:118-125); rgb seed 0.
+// The degenerate case (S <= 0 or n < 2) gives H = 0 and a zero seed.
+__global__ void __launch_bounds__(256) entropy_seed_kernel(const float4* __restrict__ img,
+                                                          int64_t n, double* __restrict__ out,
+                                                          float4* __restrict__ seed) {
+  const int v = blockIdx.y;
+  const double S = out[4 * v + 1], Sp = out[4 * v + 2], T = out[4 * v + 3];
+  const bool degenerate = !(S > 0.0) || n < 2;
+  const double log_n = log2((double)n);
+  const double F = degenerate ? 0.0 : T / S - log2(S) * Sp / S;
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[4 * v] = degenerate ? 0.0 : -F / log_n;
+  if (!seed) return;
+  const float4* im = img + (size_t)v * n;
+  float4* sd = seed + (size_t)v * n;
+  constexpr double kBound = 1e6;   // _ENTROPY_GRAD_BOUND, objectives.py:20
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double g = 0.0;
+    if (!degenerate) {
+      const double p = (double)im[i].w / S;
+      // log2 of p <= 0 is -inf or nan: both map to +1e6 in the reference
+      g = p > 0.0 ? fmin(fmax(-(log2(p) - F) / (S * log_n), -kBound), kBound) : kBound;
+    }
+    sd[i] = make_float4(0.f, 0.f, 0.f, (float)g);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host-side validation and launch
 // ---------------------------------------------------------------------------
@@ -766,6 +819,31 @@ int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float*
   l1_loss_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n, (float)(1.0 / count),
                                                            1.0 / count, seed_out, loss_out);
   return check_launch("l1_loss_kernel");
+}
+
+int ddvr_opacity_entropy(const float* images, int64_t n_pixels, int32_t n_images, double* out,
+                         float* seed_out, void* stream) {
+  g_err[0] = 0;
+  if (n_pixels < 0 || n_images < 0)
+    return set_error(DDVR_INVALID_PARAMETER, "negative image count or size");
+  if (n_images == 0) return DDVR_OK;
+  if (!images || !out) return set_error(DDVR_INVALID_INPUT, "image or output pointer is NULL");
+  if (n_images > 65535) return set_error(DDVR_UNSUPPORTED, "more than 65535 images per call");
+  if ((reinterpret_cast<uintptr_t>(images) | reinterpret_cast<uintptr_t>(seed_out)) & 15)
+    return set_error(DDVR_INVALID_INPUT, "images and seed must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * 4 * (size_t)n_images, st);
+  if (e != cudaSuccess) return set_error(DDVR_CUDA_ERROR, "entropy memset: %s", cudaGetErrorString(e));
+  const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_pixels + 255) / 256, 148));
+  const auto* im = reinterpret_cast<const float4*>(images);
+  int rc;
+  if (n_pixels > 0) {
+    entropy_sums_kernel<<<dim3(bx, n_images), 256, 0, st>>>(im, n_pixels, out);
+    if ((rc = check_launch("entropy_sums_kernel"))) return rc;
+  }
+  entropy_seed_kernel<<<dim3(bx, n_images), 256, 0, st>>>(im, n_pixels, out,
+                                                          reinterpret_cast<float4*>(seed_out));
+  return check_launch("entropy_seed_kernel");
 }
 
 int ddvr_ray_setup(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_views,

@@ -337,6 +337,22 @@ def l1_loss_seed(images: torch.Tensor, refs: torch.Tensor, count: float | None =
     return loss, seed
 
 
+def opacity_entropy(images: torch.Tensor, with_seed: bool = True):
+    """Per image of an (..., H, W, 4) float32 batch: (H (V,) f64, seed like images or None,
+    degenerate (V,) bool) of the normalised alpha entropy (objectives.py:95-126)."""
+    _require(images, "images", torch.float32)
+    if images.dim() < 3 or images.shape[-1] != 4:
+        raise InvalidInputError("images must have shape (..., H, W, 4)")
+    v = images.reshape(-1, images.shape[-3] * images.shape[-2], 4)
+    out = torch.empty(v.shape[0], 4, dtype=torch.float64, device=images.device)
+    seed = torch.empty_like(images) if with_seed else None
+    N.check(N.lib().ddvr_opacity_entropy(v.data_ptr(), v.shape[1], v.shape[0], out.data_ptr(),
+                                         seed.data_ptr() if seed is not None else None,
+                                         _stream_ptr()))
+    degenerate = (out[:, 1] <= 0) | (v.shape[1] < 2)
+    return out[:, 0], seed, degenerate
+
+
 def ray_setup(cams, dt: float, rig: Rig, dims=(2, 2, 2)):
     """(tn_tf (V,rows,W,2) f64, n_steps (V,rows,W) i32, flags i32) for parity tests."""
     _require(cams, "cameras", torch.float64, ndim=2)

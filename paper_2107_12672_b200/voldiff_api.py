@@ -485,6 +485,19 @@ def render_adjoint(volume, tf, cam, cfg, seed, *, threads: int = 1, image=None) 
     return out
 
 
+def opacity_entropy(image):
+    """(H, seed (H,W,4) float64 with only alpha populated, degenerate) of the
+    normalised Shannon entropy of the alpha channel (objectives.py:95-126)."""
+    data = image.data if isinstance(image, ImageRGBA) or hasattr(image, "alpha") \
+        else np.asarray(image, np.float64)
+    data = np.asarray(data, np.float64)
+    if data.ndim != 3 or data.shape[2] != 4:
+        raise InvalidInputError("image data must have shape (H, W, 4)")
+    t = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).to(_device())
+    h, seed, degenerate = R.opacity_entropy(t[None])
+    return float(h[0]), seed[0].to(torch.float64).cpu().numpy(), bool(degenerate[0])
+
+
 def l1_loss(images, refs):
     """(mean |x - y|, [sign(x - y)/count]) over all images (objectives.py:38-54)."""
     if len(images) != len(refs):
