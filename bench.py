@@ -342,6 +342,22 @@ def run_own(args, cfg):
             torch.cuda.synchronize()
             fwd_ms.append(e["start"].elapsed_time(e["post_forward"]))
             adj_ms.append(e["pre_adjoint"].elapsed_time(e["post_adjoint"]))
+    # gather roofline: the same rays and held record gathers, one FADD
+    # per sample (ddvr_gather_probe), timed like the kernels
+    probe_ms = None
+    if step.cells is not None:
+        R.pack_cells(step.density, step.cells)
+        pm = []
+        for _ in range(3):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            R.gather_probe(step.density, step.cams, cfg.dt, rig, step.cells, hold=True)
+            b.record()
+            torch.cuda.synchronize()
+            pm.append(a.elapsed_time(b))
+        probe_ms = float(np.median(pm))
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -447,6 +463,17 @@ def run_own(args, cfg):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if probe_ms:
+            probe_rate = local_samples / (probe_ms / 1e3)
+            gr = {"probe": "ddvr_gather_probe: the same rays, fixed-point stepping and held "
+                           "256-bit record gathers, one FADD per sample (6 CTAs/SM)",
+                  "samples_per_s": probe_rate * world, "probe_ms": probe_ms}
+            if fused:   # the fused kernel gathers along every ray twice (forward + walk)
+                gr["fused_frac"] = 2 * local_samples / adj_s / probe_rate
+            else:
+                gr["forward_frac"] = local_samples / fwd_s / probe_rate
+                gr["adjoint_frac"] = local_samples / adj_s / probe_rate
+            line["gather_roofline"] = gr
         line["config"]["step"] = (("fused forward+L1+adjoint" if getattr(step, "fused", False)
                                    else "forward, L1, adjoint") +
                                   (", CUDA-graph replay" if graphed else ""))

@@ -199,6 +199,14 @@ int64_t ddvr_cells_bytes(const int32_t dims[3]);
  * ddvr_cells_bytes bytes).  Call again whenever the density changes. */
 int ddvr_pack_cells(const ddvr_volume* vol, float* cells_out, void* stream);
 
+/* Gather-roofline microbenchmark: the march's rays, stepping and
+ * 256-bit cell-record gathers (hold != 0: reloaded only on a cell change, as
+ * the march does; 0: one per sample) with one FADD per sample instead of the
+ * shading.  out (device) (V, rows, W) float per-ray checksums.  Needs
+ * vol->cells; vol->data may be NULL. */
+int ddvr_gather_probe(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_views,
+                      const ddvr_params* p, int32_t hold, float* out, void* stream);
+
 /* opacity_entropy (objectives.py:95-126) of n_images (device) (n_pixels, 4)
  * float images: out (device, double, n_images x 4) receives [H, S, S+, T] per
  * image (normalised Shannon entropy of the alpha channel, alpha sum, positive

@@ -36,7 +36,8 @@ TF_GAUSSIAN = 2
 
 EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
             "ddvr_adjoint_workspace_bytes", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
-            "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_ray_setup",
+            "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
+            "ddvr_ray_setup",
             "ddvr_prior_volume",
             "ddvr_prior_tf", "ddvr_adam_step", "ddvr_adam_step_device",
             "ddvr_upsample_volume", "ddvr_volume_from_raw",
@@ -114,6 +115,9 @@ def _bind(lib):
     lib.ddvr_l1_loss.restype = ctypes.c_int
     lib.ddvr_opacity_entropy.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]
     lib.ddvr_opacity_entropy.restype = ctypes.c_int
+    lib.ddvr_gather_probe.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams),
+                                      ctypes.c_int32, vp, vp]
+    lib.ddvr_gather_probe.restype = ctypes.c_int
     lib.ddvr_ray_setup.argtypes = [P(DdvrVolume), vp, ctypes.c_int32, P(DdvrParams), vp, vp, vp,
                                    vp]
     lib.ddvr_ray_setup.restype = ctypes.c_int

@@ -821,6 +821,20 @@ int ddvr_l1_loss(const float* x, const float* y, int64_t n, double count, float*
   return check_launch("l1_loss_kernel");
 }
 
+int ddvr_gather_probe(const ddvr_volume* vol, const ddvr_camera* cams, int32_t n_views,
+                      const ddvr_params* p, int32_t hold, float* out, void* stream) {
+  g_err[0] = 0;
+  VolArgs V;
+  Geometry G;
+  int rc;
+  if ((rc = make_vol(vol, V, false)) || (rc = make_geo(cams, n_views, p, G))) return rc;
+  if (!V.cells) return set_error(DDVR_INVALID_INPUT, "the gather probe needs cell records");
+  if (!out) return set_error(DDVR_INVALID_INPUT, "output pointer is NULL");
+  if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
+  launch_gather_probe(hold != 0, grid_of(G, n_views), (cudaStream_t)stream, V, G, out);
+  return check_launch("gather_probe_kernel");
+}
+
 int ddvr_opacity_entropy(const float* images, int64_t n_pixels, int32_t n_images, double* out,
                          float* seed_out, void* stream) {
   g_err[0] = 0;

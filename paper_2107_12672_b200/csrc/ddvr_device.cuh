@@ -120,6 +120,8 @@ struct Geometry {
 void launch_forward(bool early, bool cells, bool tape, dim3 grid, size_t smem, cudaStream_t st,
                     const VolArgs& V, const TfArgs& T, const Geometry& G, float* image,
                     float* depth);
+void launch_gather_probe(bool hold, dim3 grid, cudaStream_t st, const VolArgs& V,
+                         const Geometry& G, float* out);
 void launch_forward_grad(int n_params, bool cells, dim3 grid, size_t smem, cudaStream_t st,
                          const VolArgs& V, const TfArgs& T, const Geometry& G, float* image,
                          float* jac);

@@ -337,6 +337,20 @@ def l1_loss_seed(images: torch.Tensor, refs: torch.Tensor, count: float | None =
     return loss, seed
 
 
+def gather_probe(density, cams, dt: float, rig: Rig, cells, hold: bool = True):
+    """Per-ray checksums of the gather-roofline microbenchmark (ddvr_gather_probe):
+    the march's record gathers with one FADD per sample instead of the shading."""
+    _require(cams, "cameras", torch.float64, ndim=2)
+    tex = torch.zeros(1, 4, dtype=torch.float32, device=density.device)
+    vol, _, prm = _descs(density, tex, rig, dt, False, cells)
+    out = torch.empty(cams.shape[0], rig.band_rows, rig.width, dtype=torch.float32,
+                      device=density.device)
+    N.check(N.lib().ddvr_gather_probe(ctypes.byref(vol), cams.data_ptr(), cams.shape[0],
+                                      ctypes.byref(prm), int(hold), out.data_ptr(),
+                                      _stream_ptr()))
+    return out
+
+
 def opacity_entropy(images: torch.Tensor, with_seed: bool = True):
     """Per image of an (..., H, W, 4) float32 batch: (H (V,) f64, seed like images or None,
     degenerate (V,) bool) of the normalised alpha entropy (objectives.py:95-126)."""

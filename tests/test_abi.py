@@ -36,7 +36,7 @@ def test_header_declares_the_boundary():
                             "ddvr_adjoint_workspace_bytes",
                             "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
                             "ddvr_forward_color", "ddvr_adjoint_color",
-                            "ddvr_l1_loss", "ddvr_opacity_entropy",
+                            "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
                             "ddvr_ray_setup", "ddvr_prior_volume", "ddvr_prior_tf",
                             "ddvr_adam_step", "ddvr_adam_step_device",
                             "ddvr_upsample_volume", "ddvr_volume_from_raw",

@@ -348,3 +348,18 @@ def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt):
             ref = np.asarray(out["d_" + k], np.float64)
             got = d[k].double().cpu().numpy().reshape(ref.shape)
             assert rel_l2(got, ref) <= 1e-4, (tau_scale, k, rel_l2(got, ref))
+
+
+def test_gather_probe_checksums(cuda):
+    """ddvr_gather_probe (the gather-roofline microbenchmark): the held and the
+    per-sample gathers read the same records, so the per-ray checksums agree."""
+    torch = _t()
+    from paper_2107_12672_b200 import raymarch as R
+    rng = np.random.default_rng(3)
+    dens = torch.from_numpy(rng.uniform(0, 1, (20, 18, 16)).astype(np.float32)).to(cuda)
+    cams = R.camera_array(torch.tensor([[20.0, 10.0], [200.0, -40.0]], dtype=torch.float64,
+                                       device=cuda), 2.0, (0.0, 0.0, 0.0), 30.0)
+    cells = R.pack_cells(dens)
+    a = R.gather_probe(dens, cams, 0.01, R.Rig(24, 20), cells, hold=True)
+    b = R.gather_probe(dens, cams, 0.01, R.Rig(24, 20), cells, hold=False)
+    assert torch.equal(a, b) and float(a.abs().sum()) > 0
