@@ -131,3 +131,31 @@ def test_graphed_iterations_follow_the_eager_trajectory(cuda):
     assert rel_l2(vols[1].double().cpu().numpy(), vols[0].double().cpu().numpy()) <= 1e-5
     with pytest.raises(ValueError):
         it.run(refs_host=torch.zeros(1))
+
+
+@pytest.mark.parametrize("kind", ["piecewise", "gaussian"])
+def test_fused_step_analytic_tfs(cuda, kind):
+    """The fused kernel's forward dispatch and walk for the (K,5) piecewise-linear
+    and (G,6) Gaussian TFs equal the separate launches (volume + tf targets)."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    grid, _, views, refs, dt = _scene()
+    rng = np.random.default_rng(8)
+    if kind == "piecewise":
+        pos = np.sort(np.concatenate([[0.0, 1.0], rng.uniform(0.05, 0.95, 5)]))
+        tf = np.column_stack([pos, rng.uniform(0.1, 1.0, (7, 3)), rng.uniform(0.2, 2.5, 7)])
+    else:
+        tf = np.column_stack([rng.uniform(0.2, 0.8, 4), rng.uniform(0.05, 0.3, 4),
+                              rng.uniform(0.1, 1.0, (4, 3)), rng.uniform(0.5, 3.0, 4)])
+    vol = torch.from_numpy(grid.values.astype(np.float32)).to(cuda)
+    tx = torch.from_numpy(tf.astype(np.float32)).to(cuda)
+    ll = torch.tensor([[v.lon_deg, v.lat_deg] for v in views], dtype=torch.float64, device=cuda)
+    rf = torch.from_numpy(np.stack(refs).astype(np.float32)).to(cuda)
+    bufs = []
+    for fused in (True, False):
+        step = ShardedStep(vol, tx, ll, rf, dt, R.Rig(6, 5), targets=("volume", "tf"),
+                           radius=2.3, fused=fused)
+        assert step.fused == fused
+        bufs.append(step.run().buf.double().cpu().numpy())
+    assert rel_l2(bufs[0], bufs[1]) <= 1e-5
