@@ -1,0 +1,92 @@
+// Experiment (not product code): does a 2x2x2-bricked cell-record layout make the
+// march's gathers faster?  Same rays / stepping / held gathers as ddvr_gather_probe,
+// records either z-linear (the product layout) or in 2x2x2 bricks (256 B, one
+// L2::256B fetch = a brick).  Built and run by brick_probe.py.
+#include "ddvr_device.cuh"
+
+namespace {
+using namespace ddvr_impl;
+
+// brick index of padded cell (a, b, c) = (i+1, j+1, k+1)
+__device__ __forceinline__ long long brick_index(int a, int b, int c, int NBY, int NBZ) {
+  const long long br = ((long long)(a >> 1) * NBY + (b >> 1)) * NBZ + (c >> 1);
+  return br * 8 + ((a & 1) | ((b & 1) << 1) | ((c & 1) << 2));
+}
+
+__global__ void rebrick_kernel(const float* __restrict__ lin, int CX, int CY, int CZ, int NBY,
+                               int NBZ, float* __restrict__ out) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (long long)CX * CY * CZ) return;
+  const int c = (int)(id % CZ), b = (int)((id / CZ) % CY), a = (int)(id / ((long long)CY * CZ));
+  const long long o = brick_index(a, b, c, NBY, NBZ);
+  const float4* s = reinterpret_cast<const float4*>(lin + 8 * id);
+  float4* d = reinterpret_cast<float4*>(out + 8 * o);
+  d[0] = s[0];
+  d[1] = s[1];
+}
+
+template <bool BRICK>
+__global__ void __launch_bounds__(kThreads, 6) probe_kernel(VolArgs V, Geometry G,
+                                                             const float* __restrict__ rec,
+                                                             int NBY, int NBZ,
+                                                             float* __restrict__ out) {
+  __shared__ Frame F;
+  const int view = blockIdx.z;
+  if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
+  __syncthreads();
+  int px, py;
+  pixel_of(G, px, py);
+  if (px >= G.W || py >= G.row1) return;
+  Ray r;
+  setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
+  long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  long long held = -1;
+  float acc = 0.f;
+  for (int i = 0; i < r.n; ++i) {
+    const int a = (int)(gx >> 32) + 1, b = (int)(gy >> 32) + 1, c = (int)(gz >> 32) + 1;
+    gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
+    const long long idx = BRICK ? brick_index(a, b, c, NBY, NBZ)
+                                : ((long long)a * V.CY + b) * V.CZ + c;
+    ld256_if(idx != held, rec + 8 * idx, v);
+    held = idx;
+    acc += v[0];
+  }
+  out[((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px] = acc;
+}
+
+}  // namespace
+
+extern "C" int brick_run(const ddvr_volume* vol, const ddvr_camera* cams, int n_views,
+                         const ddvr_params* p, int brick, const float* lin, float* bricks,
+                         float* out, int rebrick, void* stream) {
+  VolArgs V;
+  Geometry G;
+  // minimal copies of make_vol / make_geo for the probe (fields the march reads)
+  V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
+  V.YZ = V.Y * V.Z; V.CY = V.Y + 1; V.CZ = V.Z + 1;
+  V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
+  for (int k = 0; k < 3; ++k) {
+    V.lo[k] = (long long)llrint((-0.5 - 1e-6) * kFix);
+    V.hi[k] = (long long)llrint(((double)vol->dims[k] - 0.5 + 1e-6) * kFix);
+    V.top[k] = (long long)(vol->dims[k] - 1) << 32;
+    V.bmin[k] = vol->box_min[k];
+    V.bmax[k] = vol->box_max[k];
+    V.scale[k] = (double)vol->dims[k] / (vol->box_max[k] - vol->box_min[k]);
+  }
+  G.cams = cams;
+  G.dt = p->dt;
+  G.dt32 = (float)p->dt;
+  G.W = p->width; G.H = p->height; G.row0 = 0; G.row1 = p->height;
+  const int CX = V.X + 1, NBY = (V.CY + 1) / 2, NBZ = (V.CZ + 1) / 2;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rebrick) {
+    const long long n = (long long)CX * V.CY * V.CZ;
+    rebrick_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lin, CX, V.CY, V.CZ, NBY, NBZ,
+                                                                bricks);
+  }
+  const dim3 grid((G.W + kTile - 1) / kTile, (G.H + kTile - 1) / kTile, n_views);
+  if (brick) probe_kernel<true><<<grid, kThreads, 0, st>>>(V, G, bricks, NBY, NBZ, out);
+  else probe_kernel<false><<<grid, kThreads, 0, st>>>(V, G, lin, NBY, NBZ, out);
+  return (int)cudaGetLastError();
+}
