@@ -55,7 +55,98 @@ __global__ void __launch_bounds__(kThreads, 6) probe_kernel(VolArgs V, Geometry 
   out[((size_t)view * (G.row1 - G.row0) + (py - G.row0)) * G.W + px] = acc;
 }
 
+// persistent variant: CTAs on SM s take consecutive tiles of SM s's contiguous
+// range (x fastest, then y, then view) from a per-SM counter, so co-resident
+// CTAs march adjacent beams
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 6) probe_sm_kernel(VolArgs V, Geometry G,
+                                                                const float* __restrict__ rec,
+                                                                int tiles_x, int tiles_y,
+                                                                int n_tiles, int n_sm,
+                                                                unsigned* __restrict__ ctr,
+                                                                float* __restrict__ out) {
+  __shared__ Frame F;
+  __shared__ int s_tile;
+  __shared__ int s_view;
+  if (threadIdx.x == 0) s_view = -1;
+  const unsigned sm = smid() % n_sm;
+  // view-synchronous: within every view, SM s owns a contiguous strip of tiles;
+  // its CTAs walk the views in order, so all SMs stay on about the same view
+  const int per_view = tiles_x * tiles_y, n_views = n_tiles / per_view;
+  const int strip = (per_view + n_sm - 1) / n_sm;
+  const int s0 = min(per_view, (int)sm * strip), s1 = min(per_view, s0 + strip);
+  const int len = s1 - s0, t0 = 0, t1 = len * n_views;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int k = (int)atomicAdd(&ctr[sm], 1u);
+      s_tile = (len > 0 && k < t1) ? (k / len) * per_view + s0 + k % len : n_tiles;
+    }
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= n_tiles) break;
+    const int view = tile / (tiles_x * tiles_y);
+    const int ty = (tile / tiles_x) % tiles_y, tx = tile % tiles_x;
+    if (threadIdx.x == 0) {
+      if (s_view != view || t0 < 0) make_frame(G.cams[view], G.W, G.H, F);
+      s_view = view;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+    if (px < G.W && py < G.H) {
+      Ray r;
+      setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
+      long long gx = r.g0[0], gy = r.g0[1], gz = r.g0[2];
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      long long held = -1;
+      float acc = 0.f;
+      for (int i = 0; i < r.n; ++i) {
+        const int a = (int)(gx >> 32) + 1, b = (int)(gy >> 32) + 1, c = (int)(gz >> 32) + 1;
+        gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
+        const long long idx = ((long long)a * V.CY + b) * V.CZ + c;
+        ld256_if(idx != held, rec + 8 * idx, v);
+        held = idx;
+        acc += v[0];
+      }
+      out[((size_t)view * G.H + py) * G.W + px] = acc;
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" int sm_run(const ddvr_volume* vol, const ddvr_camera* cams, int n_views,
+                      const ddvr_params* p, const float* lin, unsigned* ctr, float* out,
+                      int ctas_per_sm, void* stream) {
+  VolArgs V;
+  Geometry G;
+  V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
+  V.YZ = V.Y * V.Z; V.CY = V.Y + 1; V.CZ = V.Z + 1;
+  V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
+  for (int k = 0; k < 3; ++k) {
+    V.lo[k] = (long long)llrint((-0.5 - 1e-6) * kFix);
+    V.hi[k] = (long long)llrint(((double)vol->dims[k] - 0.5 + 1e-6) * kFix);
+    V.top[k] = (long long)(vol->dims[k] - 1) << 32;
+    V.bmin[k] = vol->box_min[k];
+    V.bmax[k] = vol->box_max[k];
+    V.scale[k] = (double)vol->dims[k] / (vol->box_max[k] - vol->box_min[k]);
+  }
+  G.cams = cams; G.dt = p->dt; G.dt32 = (float)p->dt;
+  G.W = p->width; G.H = p->height; G.row0 = 0; G.row1 = p->height;
+  const int tx = (G.W + kTile - 1) / kTile, ty = (G.H + kTile - 1) / kTile;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(ctr, 0, 148 * sizeof(unsigned), st);
+  probe_sm_kernel<<<148 * ctas_per_sm, kThreads, 0, st>>>(V, G, lin, tx, ty, tx * ty * n_views,
+                                                           148, ctr, out);
+  return (int)cudaGetLastError();
+}
 
 extern "C" int brick_run(const ddvr_volume* vol, const ddvr_camera* cams, int n_views,
                          const ddvr_params* p, int brick, const float* lin, float* bricks,

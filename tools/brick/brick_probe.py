@@ -53,3 +53,17 @@ for mode in (0, 1, 0, 1):
     ref = ref if ref is not None else s
     print(f"{'bricked' if mode else 'linear '} {a.elapsed_time(b):7.2f} ms  checksum {s:.6e} "
           f"({'same' if abs(s - ref) <= 1e-6 * abs(ref) else 'DIFFERENT'})")
+
+ctr = torch.zeros(148, dtype=torch.int32, device=dev)
+for cps in (6, 12, 6, 12):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    lib.sm_run(ctypes.byref(v), ctypes.c_void_p(cams.data_ptr()), 64, ctypes.byref(prm),
+               ctypes.c_void_p(cells.data_ptr()), ctypes.c_void_p(ctr.data_ptr()),
+               ctypes.c_void_p(out.data_ptr()), cps, ctypes.c_void_p(st))
+    b.record()
+    torch.cuda.synchronize()
+    s = float(out.double().sum())
+    print(f"sm-local persistent ({cps} CTAs/SM launched) {a.elapsed_time(b):7.2f} ms  checksum {s:.6e} "
+          f"({'same' if abs(s - ref) <= 1e-6 * abs(ref) else 'DIFFERENT'})")
