@@ -179,7 +179,6 @@ def config_cases():
 
 
 def count_cases():
-    from oracle import dvr_oracle as O
     out = {}
     for name, c in CONFIGS.items():
         vol = vd.DensityVolume(np.zeros((2, 2, 2)))
