@@ -159,3 +159,22 @@ def test_fused_step_analytic_tfs(cuda, kind):
         assert step.fused == fused
         bufs.append(step.run().buf.double().cpu().numpy())
     assert rel_l2(bufs[0], bufs[1]) <= 1e-5
+
+
+def test_fused_step_row_band(cuda):
+    """A row band (renderer.py:491 tiles) through the fused kernel equals the
+    separate launches on the same band."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    grid, tex, views, refs, dt = _scene()
+    vol = torch.from_numpy(grid.values.astype(np.float32)).to(cuda)
+    tx = torch.from_numpy(tex.astype(np.float32)).to(cuda)
+    ll = torch.tensor([[v.lon_deg, v.lat_deg] for v in views], dtype=torch.float64, device=cuda)
+    rf = torch.from_numpy(np.stack(refs).astype(np.float32)[:, 1:4]).to(cuda).contiguous()
+    bufs = []
+    for fused in (True, False):
+        step = ShardedStep(vol, tx, ll, rf, dt, R.Rig(6, 5, rows=(1, 4)),
+                           targets=("volume", "tf", "stepsize"), radius=2.3, fused=fused)
+        bufs.append(step.run().buf.double().cpu().numpy())
+    assert rel_l2(bufs[0], bufs[1]) <= 1e-5
