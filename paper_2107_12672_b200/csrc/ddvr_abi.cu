@@ -963,7 +963,7 @@ int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, vo
 static int swap_xz(const float* src, int A, int B, int C, const double* range, float* dst,
                    void* stream) {
   const dim3 grid((C + kSwapTile - 1) / kSwapTile, (A + kSwapTile - 1) / kSwapTile,
-                  B < 65535 ? B : 65535);
+                  std::max(1, std::min(65535, (B + 3) / 4)));   // 4 slices per CTA
   if ((long long)grid.y > 65535) return set_error(DDVR_UNSUPPORTED, "volume axis too large");
   if (range) {
     swap_xz_kernel<true><<<grid, dim3(kSwapTile, 8), 0, (cudaStream_t)stream>>>(

@@ -6,7 +6,8 @@
 // [0,1] clamp, 0 outside the box), then the same Beer-Lambert compositing as
 // the density path.  The adjoint walks back with the same exact optical-depth
 // inversion and scatters w8 (inside-masked) x the out4 adjoint into the 8
-// corner voxels (renderer.py:611-613) with 128-bit vector reds.
+// corner voxels (renderer.py:611-613), accumulated per cell run and flushed
+// with 128-bit vector reds.
 #include "ddvr_device.cuh"
 
 namespace {
@@ -90,6 +91,22 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_color_kernel(
                    : -log1p(-(double)reinterpret_cast<const float4*>(image)[pix].w);
   const float dt32 = G.dt32;
   float a_hat = sd.w;
+  // per cell run: the 8 corner float4 gradients accumulate in registers and are
+  // flushed with 8 vector reds when the ray leaves the cell (~1 sample in 3 at
+  // dt = 0.2 voxel) instead of on every sample
+  float4 acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int run_base = INT_MIN, run_ox = 0, run_oy = 0, run_oz = 0;
+  auto flush = [&]() {
+    float* base = d_color + 4 * (size_t)run_base;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float* q = base + ((k & 1) ? 4 * run_ox : 0) + ((k & 2) ? 4 * run_oy : 0) +
+                 ((k & 4) ? 4 * run_oz : 0);
+      red128(q, acc[k].x, acc[k].y, acc[k].z, acc[k].w);
+    }
+  };
   long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
   long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
   long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
@@ -114,19 +131,26 @@ __global__ void __launch_bounds__(kThreads) dvr_adjoint_color_kernel(
     const float tau_hat = s.w < 0.f ? 0.f : dt32 * g.e * a_raw_hat;
     const float4 o4 = make_float4(aT * sd.x, aT * sd.y, aT * sd.z, tau_hat);
     if (c.inside) {   // renderer.py:611-613: w8 (inside-masked) x out4_hat per corner
+      if (c.base != run_base) {
+        if (run_base != INT_MIN) flush();
+        run_base = c.base; run_ox = c.ox; run_oy = c.oy; run_oz = c.oz;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       const float ex = 1.f - c.fx, ey = 1.f - c.fy, ez = 1.f - c.fz;
       const float wz[2] = {ez, c.fz}, wy[2] = {ey, c.fy}, wx[2] = {ex, c.fx};
-      float* base = d_color + 4 * (size_t)c.base;
-      const int off[3] = {4 * c.ox, 4 * c.oy, 4 * c.oz};
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float wk = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
-        float* q = base + ((k & 1) ? off[0] : 0) + ((k & 2) ? off[1] : 0) + ((k & 4) ? off[2] : 0);
-        red128(q, wk * o4.x, wk * o4.y, wk * o4.z, wk * o4.w);
+        acc[k].x = __fmaf_rn(wk, o4.x, acc[k].x);
+        acc[k].y = __fmaf_rn(wk, o4.y, acc[k].y);
+        acc[k].z = __fmaf_rn(wk, o4.z, acc[k].z);
+        acc[k].w = __fmaf_rn(wk, o4.w, acc[k].w);
       }
     }
     gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
   }
+  if (run_base != INT_MIN) flush();
 }
 
 }  // namespace
