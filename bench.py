@@ -367,7 +367,15 @@ def run_own(args, cfg):
     host_vol.copy_(est.cpu())
     host_refs = torch.empty(refs.shape, dtype=torch.float32, pin_memory=True)
     host_refs.copy_(refs.cpu())
-    host_grad = torch.empty(est.numel(), dtype=torch.float32, pin_memory=True)
+    # the step's result: the updated density after an optimiser step (volume
+    # targets), else the gradients it computes (tf / stepsize flat tail, camera)
+    if runner is not step:
+        result = est.reshape(-1)
+    else:
+        tail = step.flat.buf[step.flat.d_volume.numel():]
+        result = torch.cat([tail, step.d_camera.reshape(-1).float()]) \
+            if step.mask & 1 else tail
+    host_grad = torch.empty(result.numel(), dtype=torch.float32, pin_memory=True)
     host_loss = torch.empty(1, dtype=torch.float32, pin_memory=True)
     e2e_ms = []
     for i in range(args.warmup + args.steps):
@@ -384,9 +392,11 @@ def run_own(args, cfg):
         else:
             runner.run(refs_host=host_refs)  # refs H2D overlaps pack + forward
         f = step.flat
-        # the step's result: the updated density (optimiser steps) or its gradient
-        host_grad.copy_((est if runner is not step else f.d_volume).reshape(-1),
-                        non_blocking=True)
+        if runner is step:
+            tail = f.buf[f.d_volume.numel():]
+            result = torch.cat([tail, step.d_camera.reshape(-1).float()]) \
+                if step.mask & 1 else tail
+        host_grad.copy_(result, non_blocking=True)
         host_loss.copy_(f.loss, non_blocking=True)
         b.record(st)
         torch.cuda.synchronize()
