@@ -120,7 +120,136 @@ __global__ void __launch_bounds__(kThreads, 6) probe_sm_kernel(VolArgs V, Geomet
   }
 }
 
+// smem-staged probe: CTA of SW x SH rays marches in windows of K steps; each
+// window's cell bounding box (over all rays' segment endpoints) is loaded into
+// shared memory cooperatively, then every sample reads its record from smem.
+// Windows whose box exceeds CAP records fall back to held global gathers.
+constexpr int SW = 16, SH = 8, SNT = SW * SH, CAP = 1536;
+
+__device__ __forceinline__ void box_reduce(int lo[3], int hi[3], int* s_red) {
+  // warp reductions, then across the CTA's warps through shared memory
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+    hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) { s_red[w * 6 + a] = lo[a]; s_red[w * 6 + 3 + a] = hi[a]; }
+  __syncthreads();
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = s_red[a]; hi[a] = s_red[3 + a];
+    for (int k = 1; k < SNT / 32; ++k) {
+      lo[a] = min(lo[a], s_red[k * 6 + a]);
+      hi[a] = max(hi[a], s_red[k * 6 + 3 + a]);
+    }
+  }
+  __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(SNT) probe_staged_kernel(VolArgs V, Geometry G,
+                                                           const float* __restrict__ rec,
+                                                           float* __restrict__ out,
+                                                           unsigned* __restrict__ stats) {
+  extern __shared__ float4 s_rec[];   // CAP records x 2 float4
+  __shared__ Frame F;
+  __shared__ int s_red[6 * (SNT / 32)];
+  __shared__ int s_nmax;
+  const int view = blockIdx.z;
+  if (threadIdx.x == 0) { make_frame(G.cams[view], G.W, G.H, F); s_nmax = 0; }
+  __syncthreads();
+  const int px = blockIdx.x * SW + (threadIdx.x % SW), py = blockIdx.y * SH + threadIdx.x / SW;
+  const bool valid = px < G.W && py < G.H;
+  Ray r;
+  r.n = 0;
+  if (valid) setup_ray(F, V, G.dt, G.W, G.H, px, py, r);
+  atomicMax(&s_nmax, r.n);
+  __syncthreads();
+  const int nmax = s_nmax;
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  long long held = -1;
+  float acc = 0.f;
+  unsigned fallbacks = 0;
+  for (int i0 = 0; i0 < nmax; i0 += K) {
+    const int i1 = min(i0 + K, r.n);   // this ray's samples [i0, i1)
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    if (i1 > i0) {
+      for (int a = 0; a < 3; ++a) {
+        const int c0 = (int)((r.g0[a] + (long long)i0 * r.gs[a]) >> 32) + 1;
+        const int c1 = (int)((r.g0[a] + (long long)(i1 - 1) * r.gs[a]) >> 32) + 1;
+        lo[a] = min(c0, c1); hi[a] = max(c0, c1);
+      }
+    }
+    box_reduce(lo, hi, s_red);
+    if (lo[0] > hi[0]) continue;   // no ray has samples in this window
+    const int bx = hi[0] - lo[0] + 1, by = hi[1] - lo[1] + 1, bz = hi[2] - lo[2] + 1;
+    const bool staged = bx * by * bz <= CAP;
+    if (staged) {
+      for (int t = threadIdx.x; t < bx * by * bz; t += SNT) {
+        const int lz = t % bz, ly = (t / bz) % by, lx = t / (bz * by);
+        const float4* m = reinterpret_cast<const float4*>(
+            rec + 8 * (((long long)(lo[0] + lx) * V.CY + lo[1] + ly) * V.CZ + lo[2] + lz));
+        s_rec[2 * t] = m[0];
+        s_rec[2 * t + 1] = m[1];
+      }
+    } else {
+      ++fallbacks;
+    }
+    __syncthreads();
+    for (int i = i0; i < i1; ++i) {
+      const int a = (int)((r.g0[0] + (long long)i * r.gs[0]) >> 32) + 1;
+      const int b = (int)((r.g0[1] + (long long)i * r.gs[1]) >> 32) + 1;
+      const int c = (int)((r.g0[2] + (long long)i * r.gs[2]) >> 32) + 1;
+      if (staged) {
+        const int l = ((a - lo[0]) * by + (b - lo[1])) * bz + (c - lo[2]);
+        acc += s_rec[2 * l].x;
+      } else {
+        const long long idx = ((long long)a * V.CY + b) * V.CZ + c;
+        ld256_if(idx != held, rec + 8 * idx, v);
+        held = idx;
+        acc += v[0];
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) out[((size_t)view * G.H + py) * G.W + px] = acc;
+  if (threadIdx.x == 0 && stats) atomicAdd(stats, fallbacks);
+}
+
 }  // namespace
+
+extern "C" int staged_run(const ddvr_volume* vol, const ddvr_camera* cams, int n_views,
+                          const ddvr_params* p, const float* lin, float* out, unsigned* stats,
+                          int K, void* stream) {
+  VolArgs V;
+  Geometry G;
+  V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
+  V.YZ = V.Y * V.Z; V.CY = V.Y + 1; V.CZ = V.Z + 1;
+  V.X1 = V.X - 1; V.Y1 = V.Y - 1; V.Z1 = V.Z - 1;
+  for (int k = 0; k < 3; ++k) {
+    V.lo[k] = (long long)llrint((-0.5 - 1e-6) * kFix);
+    V.hi[k] = (long long)llrint(((double)vol->dims[k] - 0.5 + 1e-6) * kFix);
+    V.top[k] = (long long)(vol->dims[k] - 1) << 32;
+    V.bmin[k] = vol->box_min[k];
+    V.bmax[k] = vol->box_max[k];
+    V.scale[k] = (double)vol->dims[k] / (vol->box_max[k] - vol->box_min[k]);
+  }
+  G.cams = cams; G.dt = p->dt; G.dt32 = (float)p->dt;
+  G.W = p->width; G.H = p->height; G.row0 = 0; G.row1 = p->height;
+  const dim3 grid((G.W + SW - 1) / SW, (G.H + SH - 1) / SH, n_views);
+  const size_t sm = CAP * 2 * sizeof(float4);
+  cudaStream_t st = (cudaStream_t)stream;
+#define RUNK(KK)                                                                        \
+  if (K == KK) {                                                                        \
+    cudaFuncSetAttribute(probe_staged_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)sm);                                                      \
+    probe_staged_kernel<KK><<<grid, SNT, sm, st>>>(V, G, lin, out, stats);               \
+  }
+  RUNK(8) RUNK(16) RUNK(32)
+#undef RUNK
+  return (int)cudaGetLastError();
+}
 
 extern "C" int sm_run(const ddvr_volume* vol, const ddvr_camera* cams, int n_views,
                       const ddvr_params* p, const float* lin, unsigned* ctr, float* out,

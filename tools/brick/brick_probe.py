@@ -67,3 +67,18 @@ for cps in (6, 12, 6, 12):
     s = float(out.double().sum())
     print(f"sm-local persistent ({cps} CTAs/SM launched) {a.elapsed_time(b):7.2f} ms  checksum {s:.6e} "
           f"({'same' if abs(s - ref) <= 1e-6 * abs(ref) else 'DIFFERENT'})")
+
+stats = torch.zeros(1, dtype=torch.int32, device=dev)
+for K in (8, 16, 32, 8, 16, 32):
+    stats.zero_()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    lib.staged_run(ctypes.byref(v), ctypes.c_void_p(cams.data_ptr()), 64, ctypes.byref(prm),
+                   ctypes.c_void_p(cells.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                   ctypes.c_void_p(stats.data_ptr()), K, ctypes.c_void_p(st))
+    b.record()
+    torch.cuda.synchronize()
+    s = float(out.double().sum())
+    print(f"smem-staged K={K:2d} {a.elapsed_time(b):7.2f} ms  fallback windows {int(stats[0])}  "
+          f"checksum {s:.6e} ({'same' if abs(s - ref) <= 1e-6 * abs(ref) else 'DIFFERENT'})")
