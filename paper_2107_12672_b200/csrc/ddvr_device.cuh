@@ -402,6 +402,9 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #define DDVR_HOLD_CELL 1
 #endif
 
+#ifndef DDVR_AFF_WALK
+#define DDVR_AFF_WALK 0   // measured: the affine walk variants spill at 48 registers
+#endif
 #ifndef DDVR_ABS_MINB
 #define DDVR_ABS_MINB 5
 #endif
@@ -721,7 +724,9 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
 // shared TF table as (texel k, texel k+1 - texel k) pairs: the lerp is then 4
 // FFMA and the slope (field.py:576) needs no subtraction.  Returns (to every
 // thread, after the barrier the caller issues) the segment mode of the CTA.
-// s_info[0]: largest tau texel (bits), s_info[1]: 1 if any rgb texel is non-zero
+// s_info[0]: largest tau texel (bits), s_info[1]: 1 if any rgb texel is non-zero,
+// s_info[2]: 1 if the tau column is NOT affine in the texel index, s_info[3..4]:
+// the affine tau = a + b k (float bits; texel tables only, see tau_affine)
 __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
   if (tf.kind == kTfPiecewise) {
     const int K = tf.count;
@@ -736,8 +741,8 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
                                   __fsub_rn(b[3], a[3]) * inv, __fsub_rn(b[4], a[4]) * inv);
       pos[i] = a[0];
     }
-    if (threadIdx.x == 0) { s_info[0] = 0x7f800000u; s_info[1] = 1u; }   // general segment mode
-    return;
+    if (threadIdx.x == 0) { s_info[0] = 0x7f800000u; s_info[1] = 1u; s_info[2] = 1u; }
+    return;   // (general segment mode, no texel-table specialisations)
   }
   if (tf.kind == kTfGaussian) {
     const int G = tf.count;
@@ -747,13 +752,19 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
       g_smem[j] = make_float4(a[2], a[3], a[4], a[5]);
       g_smem[G + j] = make_float4(a[0], 1.4426950408889634f / (2.f * s2), 1.f / s2, a[1]);
     }
-    if (threadIdx.x == 0) { s_info[0] = 0x7f800000u; s_info[1] = 1u; }
+    if (threadIdx.x == 0) { s_info[0] = 0x7f800000u; s_info[1] = 1u; s_info[2] = 1u; }
     return;
   }
   const float4* src = reinterpret_cast<const float4*>(tf.params);
   float2* tau = reinterpret_cast<float2*>(g_smem) + (6 * tf.count + 4);
   float mx = 0.f;
-  bool rgb = false;
+  bool rgb = false, bent = false;
+  // affine tau column (e.g. the absorption ramp of tasks.py:348-356): tau_k =
+  // a + b k to within a few fp32 ulps of the end texels' magnitude
+  const float aff_a = src[0].w;
+  const float aff_b = tf.count > 1 ? __fdiv_rn(__fsub_rn(src[tf.count - 1].w, aff_a), tf.fR1) : 0.f;
+  const double aff_tol = 5e-7 * fmax(fmax(fabs((double)aff_a), fabs((double)src[tf.count - 1].w)),
+                                     1e-30);
   for (int e = threadIdx.x; e <= tf.count; e += blockDim.x) {   // guard entries 0 and R
     const float4 a = src[min(max(e - 1, 0), tf.count - 1)];
     const float4 b = src[min(e, tf.count - 1)];
@@ -763,10 +774,29 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
     tau[e] = make_float2(a.w, __fsub_rn(b.w, a.w));
     mx = fmaxf(mx, a.w);   // interpolated tau never exceeds the largest texel
     rgb |= a.x != 0.f || a.y != 0.f || a.z != 0.f;
+    const int k = min(max(e - 1, 0), tf.count - 1);
+    bent |= fabs((double)a.w - ((double)aff_a + (double)aff_b * k)) > aff_tol;
   }
   // non-negative floats order like their bit patterns
   if (mx > 0.f) atomicMax(&s_info[0], __float_as_uint(mx));
   if (rgb) atomicOr(&s_info[1], 1u);
+  if (bent) atomicOr(&s_info[2], 1u);
+  if (threadIdx.x == 0) {
+    s_info[3] = __float_as_uint(aff_a);
+    s_info[4] = __float_as_uint(aff_b);
+  }
+}
+
+// tau of an affine texel column at density d: the table lerp of field.py:540-549
+// with clamp-to-edge is a + b clamp(t, 0, R-1), t = d R - 1/2; its slope is b
+// for t in [0, R-1) and 0 in the clamp bands (the guard texels' zero deltas)
+__device__ __forceinline__ float tau_affine(const TfArgs& T, float d, float a, float b) {
+  const float t = __fmaf_rn(d, T.fR, -0.5f);
+  return __fmaf_rn(b, fminf(fmaxf(t, 0.f), T.fR1), a);
+}
+__device__ __forceinline__ float slope_affine(const TfArgs& T, float d, float b) {
+  const float t = __fmaf_rn(d, T.fR, -0.5f);
+  return (t >= 0.f && t < T.fR1) ? b : 0.f;
 }
 
 __device__ __forceinline__ int seg_mode(float dt32, unsigned maxtau_bits) {
@@ -786,10 +816,11 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 
 // The march of one ray.  INSIDE: every lane of the warp has all_inside (the
 // per-sample inside test and clamps are compiled out); SEG: segment mode.
-template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT, int KIND>
+template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT, int KIND,
+          bool AFF = false>
 __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
-                                          double& depth) {
+                                          double& depth, float aff_a = 0.f, float aff_b = 0.f) {
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
   // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355).
   // S, the ray's optical depth (T = exp(-S)), is summed in fp64 for the adjoint.
@@ -806,6 +837,11 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   auto composite = [&](const Cell& c, const float* k, int i) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     const float d = clamp_density(INSIDE || c.inside, interp(c, k).rho);
+    if (kAbs && AFF) {   // affine tau column: no table lookup
+      const float x = __fmul_rn(dt32, fmaxf(tau_affine(TF, d, aff_a, aff_b), 0.f));
+      S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
+      return;
+    }
     int i0; float w;
     float4 slope;
     const float4 s = tf_sample<KIND, EMIT>(TF, d, i0, w, slope, false);
@@ -854,14 +890,26 @@ template <bool EARLY, bool CELLS, bool TAPE, bool ABS_ONLY>
 __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& TFA, float dt32,
                                                const Ray& r, float* __restrict__ tape,
                                                bool warp_inside, bool emit, int mode,
-                                               float4& rgba, double& S) {
+                                               float4& rgba, double& S, const unsigned* info) {
+  // the affine-tau variant serves emission-free texel TFs without tape / early stop
+  const bool aff = !EARLY && !TAPE && !emit && info[2] == 0u;
+  const float aa = __uint_as_float(info[3]), ab = __uint_as_float(info[4]);
 #define DDVR_MARCH(SEG, INS, EM) \
   march_ray<EARLY, CELLS, TAPE, SEG, INS, EM, kTfTexture>(V, TFA, dt32, r, tape, rgba, S)
 #define DDVR_MARCH_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_MARCH(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_MARCH(kSegP7, INS, EM); \
   else DDVR_MARCH(kSegGen, INS, EM);
-  if (ABS_ONLY) {
+#define DDVR_MARCH_AFF(SEG, INS) \
+  march_ray<EARLY, CELLS, TAPE, SEG, INS, false, kTfTexture, true>(V, TFA, dt32, r, tape, rgba, \
+                                                                    S, aa, ab)
+#define DDVR_MARCH_SEG_AFF(INS)                  \
+  if (mode == kSegP3) DDVR_MARCH_AFF(kSegP3, INS); \
+  else if (mode == kSegP7) DDVR_MARCH_AFF(kSegP7, INS); \
+  else DDVR_MARCH_AFF(kSegGen, INS);
+  if ((ABS_ONLY || (TFA.kind == kTfTexture && !emit)) && aff && !EARLY && !TAPE) {
+    if (warp_inside) { DDVR_MARCH_SEG_AFF(true) } else { DDVR_MARCH_SEG_AFF(false) }
+  } else if (ABS_ONLY) {
     if (warp_inside) { DDVR_MARCH_SEG(true, false) } else { DDVR_MARCH_SEG(false, false) }
   } else if (TFA.kind == kTfPiecewise) {
     march_ray<EARLY, CELLS, TAPE, kSegGen, false, true, kTfPiecewise>(V, TFA, dt32, r, tape,
@@ -874,6 +922,8 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
   } else {
     if (emit) { DDVR_MARCH_SEG(false, true) } else { DDVR_MARCH_SEG(false, false) }
   }
+#undef DDVR_MARCH_SEG_AFF
+#undef DDVR_MARCH_AFF
 #undef DDVR_MARCH_SEG
 #undef DDVR_MARCH
 }
@@ -903,9 +953,9 @@ __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forwar
                                                              float* __restrict__ image,
                                                              float* __restrict__ depth) {
   __shared__ Frame F;
-  __shared__ unsigned s_info[2];
+  __shared__ unsigned s_info[5];
   const int view = blockIdx.z;
-  if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
+  if (threadIdx.x < 5) s_info[threadIdx.x] = 0u;
   __syncthreads();
   load_tf(TFA, s_info);
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
@@ -928,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forwar
   float4 rgba;
   double S;
   march_dispatch<EARLY, CELLS, TAPE, false>(V, TFA, G.dt32, r, tape, warp_inside, emit, mode,
-                                             rgba, S);
+                                             rgba, S, s_info);
   reinterpret_cast<float4*>(image)[pix] = rgba;
   if (depth) depth[pix] = (float)S;
 }
@@ -1004,12 +1054,14 @@ struct AdjState {
 };
 
 // The backward walk of one ray (renderer.py:547-626).
-template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND, bool TAPE>
+template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND, bool TAPE,
+          bool AFF = false>
 __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                             const Ray& r, double S, float4 sd,
                                             const float* __restrict__ tape, float* tf_slot,
                                             float* __restrict__ d_volume,
-                                            float* __restrict__ d_cells, AdjState& st) {
+                                            float* __restrict__ d_cells, AdjState& st,
+                                            float aff_a = 0.f, float aff_b = 0.f) {
   constexpr bool kCam = MASK & DDVR_TARGET_CAMERA;
   constexpr bool kStep = MASK & DDVR_TARGET_STEPSIZE;
   constexpr bool kTf = MASK & DDVR_TARGET_TF;
@@ -1068,6 +1120,11 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       dl4 = g_smem[2 * i0 + 3];
       s = make_float4(__fmaf_rn(w, dl4.x, a.x), __fmaf_rn(w, dl4.y, a.y),
                       __fmaf_rn(w, dl4.z, a.z), __fmaf_rn(w, dl4.w, a.w));
+      slope = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (kAbs && AFF) {   // affine tau column: no table lookup
+      i0 = 0; w = 0.f;
+      s = make_float4(0.f, 0.f, 0.f, tau_affine(TF, d, aff_a, aff_b));
+      dq = slope_affine(TF, d, aff_b);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (kAbs) {
       i0 = texel_coord(TF, d, w);
@@ -1241,14 +1298,14 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 
   __shared__ Frame F;
   __shared__ double s_red[kWarps][3];
-  __shared__ unsigned s_info[2];
+  __shared__ unsigned s_info[5];
   // this CTA's TF-gradient slot in the workspace
   float* tf_slot = kTf ? TFA.slots + (size_t)TFA.slot_floats *
                                          ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
                                            (size_t)blockIdx.z)) % TFA.nslot)
                        : nullptr;
   const int view = blockIdx.z;
-  if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
+  if (threadIdx.x < 5) s_info[threadIdx.x] = 0u;
   __syncthreads();
   load_tf(TFA, s_info);
   __syncthreads();
@@ -1291,7 +1348,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     if (valid) {
       float4 rgba;
       march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
-                                                     s_info[1] != 0u, mode, rgba, S);
+                                                     s_info[1] != 0u, mode, rgba, S, s_info);
       const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[pix];
       const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
                   dw = rgba.w - ref.w;
@@ -1327,7 +1384,17 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 #define DDVR_WALK_GEN(KIND, TP)                                                           \
   adjoint_ray<MASK, CELLS, kSegGen, false, true, KIND, TP>(V, TFA, G.dt32, r, S, sd, tape, \
                                                            tf_slot, d_volume, d_cells, st)
-  if (ROLE == 1) {
+#define DDVR_WALK_AFF(SEG, INS)                                                            \
+  adjoint_ray<MASK, CELLS, SEG, INS, false, kTfTexture, false, true>(                       \
+      V, TFA, G.dt32, r, S, sd, tape, tf_slot, d_volume, d_cells, st,                       \
+      __uint_as_float(s_info[3]), __uint_as_float(s_info[4]))
+#define DDVR_WALK_SEG_AFF(INS)                  \
+  if (mode == kSegP3) DDVR_WALK_AFF(kSegP3, INS); \
+  else if (mode == kSegP7) DDVR_WALK_AFF(kSegP7, INS); \
+  else DDVR_WALK_AFF(kSegGen, INS);
+  if (ROLE == 1 && DDVR_AFF_WALK && s_info[2] == 0u) {   // affine tau column (the ramp)
+    if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
+  } else if (ROLE == 1) {
     if (warp_inside) { DDVR_WALK_SEG(true, false) } else { DDVR_WALK_SEG(false, false) }
   } else if (G.tape) {
     if (TFA.kind == kTfPiecewise) DDVR_WALK_GEN(kTfPiecewise, true);
@@ -1344,6 +1411,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     if (emit) { DDVR_WALK_SEG(false, true) }
     else if (!kTf) { DDVR_WALK_SEG(false, kTf) }
   }
+#undef DDVR_WALK_SEG_AFF
+#undef DDVR_WALK_AFF
 #undef DDVR_WALK_SEG
 #undef DDVR_WALK_GEN
 #undef DDVR_WALK

@@ -19,9 +19,9 @@ __global__ void __launch_bounds__(kThreads) dvr_forward_grad_kernel(VolArgs V, T
                                                                   float* __restrict__ image,
                                                                   float* __restrict__ jac) {
   __shared__ Frame F;
-  __shared__ unsigned s_info[2];
+  __shared__ unsigned s_info[5];
   const int view = blockIdx.z;
-  if (threadIdx.x < 2) s_info[threadIdx.x] = 0u;
+  if (threadIdx.x < 5) s_info[threadIdx.x] = 0u;
   __syncthreads();
   load_tf(TFA, s_info);
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
