@@ -311,12 +311,16 @@ def test_cell_records_are_the_trilinear_polynomial(cuda):
                     assert got[1] == got[4] == got[5] == got[7] == 0.0
 
 
-@pytest.mark.parametrize("tau_scale,dt", [(3.0, 0.02), (60.0, 0.02), (4000.0, 0.05)])
-def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt):
+@pytest.mark.parametrize("tau_scale,dt,shape", [(3.0, 0.02, "ramp"), (60.0, 0.02, "ramp"),
+                                                (4000.0, 0.05, "ramp"), (3.0, 0.02, "bent"),
+                                                (60.0, 0.02, "bent")])
+def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt, shape):
     """Emission-free TF, volume + camera + stepsize targets: the adjoint's
     closed-form absorption walk (tau_hat = dt seed_a T_n per ray) against the
     oracle's inversion walk.  The three scales select the degree-3, degree-7
-    and general opacity modes; the last has clamped segments (a > 1 - EPS)."""
+    and general opacity modes; the last has clamped segments (a > 1 - EPS).
+    "ramp" is affine in the texel index (the march evaluates it without the
+    table), "bent" (tau ~ k^2) is not (the table path)."""
     torch = _t()
     from oracle import dvr_oracle as O
     from paper_2107_12672_b200 import raymarch as R
@@ -324,6 +328,8 @@ def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt):
     rng = np.random.default_rng(11)
     vol = rng.uniform(0.0, 1.0, (9, 8, 7)).astype(np.float32)
     tex = absorption_ramp_texels(32, tau_scale).astype(np.float32)
+    if shape == "bent":
+        tex[:, 3] = (tau_scale * (np.arange(32) / 31.0) ** 2).astype(np.float32)
     view = O.View(47.0, -18.0, 2.0, fov_y_deg=40.0, width=11, height=9)
     seed = rng.normal(size=(9, 11, 4)).astype(np.float32)
     targets = ["volume", "camera", "stepsize"]
