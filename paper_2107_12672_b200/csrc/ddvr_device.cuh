@@ -403,7 +403,7 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #endif
 
 #ifndef DDVR_AFF_WALK
-#define DDVR_AFF_WALK 0   // measured: the affine walk variants spill at 48 registers
+#define DDVR_AFF_WALK 1
 #endif
 #ifndef DDVR_ABS_MINB
 #define DDVR_ABS_MINB 5
@@ -1079,7 +1079,8 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   // inversion walk (and closer to it in fp32 than the walked chain).
   constexpr bool kAbs = !EMIT && !kTf && !TAPE && KIND == kTfTexture && DDVR_ABS_WALK;
   const float abs_c = kAbs ? sd.w * (float)exp(-S) : 0.f;   // seed_a * T_n
-  const float abs_k = abs_c * dt32 * TF.fR;                   // d_hat per unit texel delta
+  // d_hat per unit texel delta (AFF: the affine column's slope b folded in)
+  const float abs_k = abs_c * dt32 * TF.fR * (AFF ? aff_b : 1.f);
   // emitting texel TF without the TF target: the slope is only needed dotted
   // with the output adjoint, so the raw delta is kept and R applied once
   constexpr bool kEmitTex = EMIT && !kTf && KIND == kTfTexture;
@@ -1121,10 +1122,15 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       s = make_float4(__fmaf_rn(w, dl4.x, a.x), __fmaf_rn(w, dl4.y, a.y),
                       __fmaf_rn(w, dl4.z, a.z), __fmaf_rn(w, dl4.w, a.w));
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else if (kAbs && AFF) {   // affine tau column: no table lookup
+    } else if (kAbs && AFF) {
+      // non-negative affine tau column in a polynomial segment mode, no
+      // stepsize target (dispatch guarantees it): tau >= 0, no EPS clamp, and
+      // the slope is b for t in [0, R-1), 0 in the clamp bands -- only the
+      // band test is left per sample (b is folded into abs_k)
       i0 = 0; w = 0.f;
-      s = make_float4(0.f, 0.f, 0.f, tau_affine(TF, d, aff_a, aff_b));
-      dq = slope_affine(TF, d, aff_b);
+      const float t = __fmaf_rn(d, TF.fR, -0.5f);
+      dq = (t >= 0.f && t < TF.fR1) ? 1.f : 0.f;
+      s = make_float4(0.f, 0.f, 0.f, 0.f);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (kAbs) {
       i0 = texel_coord(TF, d, w);
@@ -1390,9 +1396,14 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
       __uint_as_float(s_info[3]), __uint_as_float(s_info[4]))
 #define DDVR_WALK_SEG_AFF(INS)                  \
   if (mode == kSegP3) DDVR_WALK_AFF(kSegP3, INS); \
-  else if (mode == kSegP7) DDVR_WALK_AFF(kSegP7, INS); \
-  else DDVR_WALK_AFF(kSegGen, INS);
-  if (ROLE == 1 && DDVR_AFF_WALK && s_info[2] == 0u) {   // affine tau column (the ramp)
+  else DDVR_WALK_AFF(kSegP7, INS);
+  // affine, non-negative tau column (the ramp), polynomial segment modes, no
+  // stepsize target: the table-free walk
+  const bool aff_walk = DDVR_AFF_WALK && !(MASK & DDVR_TARGET_STEPSIZE) && s_info[2] == 0u &&
+                        mode != kSegGen && __uint_as_float(s_info[3]) >= 0.f &&
+                        __fmaf_rn(__uint_as_float(s_info[4]), TFA.fR1,
+                                  __uint_as_float(s_info[3])) >= 0.f;
+  if (ROLE == 1 && aff_walk) {
     if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
   } else if (ROLE == 1) {
     if (warp_inside) { DDVR_WALK_SEG(true, false) } else { DDVR_WALK_SEG(false, false) }
