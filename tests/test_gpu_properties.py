@@ -314,13 +314,15 @@ def test_cell_records_are_the_trilinear_polynomial(cuda):
 @pytest.mark.parametrize("tau_scale,dt,shape", [(3.0, 0.02, "ramp"), (60.0, 0.02, "ramp"),
                                                 (4000.0, 0.05, "ramp"), (3.0, 0.02, "bent"),
                                                 (60.0, 0.02, "bent")])
-def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt, shape):
+@pytest.mark.parametrize("with_step", [True, False])
+def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt, shape, with_step):
     """Emission-free TF, volume + camera + stepsize targets: the adjoint's
     closed-form absorption walk (tau_hat = dt seed_a T_n per ray) against the
     oracle's inversion walk.  The three scales select the degree-3, degree-7
     and general opacity modes; the last has clamped segments (a > 1 - EPS).
     "ramp" is affine in the texel index (the march evaluates it without the
-    table), "bent" (tau ~ k^2) is not (the table path)."""
+    table), "bent" (tau ~ k^2) is not (the table path); without the stepsize
+    target a ramp in a polynomial mode takes the table-free walk."""
     torch = _t()
     from oracle import dvr_oracle as O
     from paper_2107_12672_b200 import raymarch as R
@@ -332,7 +334,7 @@ def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt, shape):
         tex[:, 3] = (tau_scale * (np.arange(32) / 31.0) ** 2).astype(np.float32)
     view = O.View(47.0, -18.0, 2.0, fov_y_deg=40.0, width=11, height=9)
     seed = rng.normal(size=(9, 11, 4)).astype(np.float32)
-    targets = ["volume", "camera", "stepsize"]
+    targets = ["volume", "camera", "stepsize"] if with_step else ["volume", "camera"]
     (img_o,), (out,) = _oracle(vol, tex, [view], dt, [seed.astype(np.float64)], targets)
     if tau_scale > 1000:   # the case must exercise the EPS clamp
         assert img_o[..., 3].max() > 1 - 2e-6
@@ -348,8 +350,9 @@ def test_absorption_only_walk_matches_oracle(cuda, tau_scale, dt, shape):
              "camera": torch.zeros(1, 2, dtype=torch.float64, device=cuda),
              "stepsize": torch.zeros(1, dtype=torch.float64, device=cuda)}
         R.adjoint(dens, tx, cams, dt, rig, img, depth,
-                  torch.from_numpy(seed).to(cuda)[None].contiguous(), 11, d_volume=d["volume"],
-                  d_camera=d["camera"], d_dt=d["stepsize"], cells=cells)
+                  torch.from_numpy(seed).to(cuda)[None].contiguous(), 11 if with_step else 9,
+                  d_volume=d["volume"], d_camera=d["camera"],
+                  d_dt=d["stepsize"] if with_step else None, cells=cells)
         for k in targets:
             ref = np.asarray(out["d_" + k], np.float64)
             got = d[k].double().cpu().numpy().reshape(ref.shape)
