@@ -402,6 +402,9 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #define DDVR_HOLD_CELL 1
 #endif
 
+#ifndef DDVR_EARLY_WALK
+#define DDVR_EARLY_WALK 1
+#endif
 #ifndef DDVR_AFF_WALK
 #define DDVR_AFF_WALK 1
 #endif
@@ -834,9 +837,11 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // the march sums anyway (fp64) -- so only S is carried per sample.
   constexpr bool kAbs = !EMIT && !TAPE && !EARLY && KIND == kTfTexture && DDVR_ABS_WALK;
   // one compositing step on a located sample and its record
-  auto composite = [&](const Cell& c, const float* k, int i) {
+  auto density = [&](const Cell& c, const float* k) {
+    return clamp_density(INSIDE || c.inside, interp(c, k).rho);
+  };
+  auto shade = [&](float d, int i) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
-    const float d = clamp_density(INSIDE || c.inside, interp(c, k).rho);
     if (kAbs && AFF) {   // affine tau column: no table lookup
       const float x = __fmul_rn(dt32, fmaxf(tau_affine(TF, d, aff_a, aff_b), 0.f));
       S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
@@ -863,20 +868,37 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   };
   float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int held = INT_MIN;
-  // (the emitting variants spill at 48 registers when unrolled)
-#pragma unroll (kAbs ? 4 : 1)
-  for (int i = 0; i < r.n; ++i) {
-    if (EARLY && A > kAlphaStop) break;        // renderer.py:331-335
+  if (kHoldCell) {
+    // The record of sample i+1 is requested as soon as sample i's interpolant
+    // has consumed the registers (a later load may overwrite registers an
+    // earlier instruction has read), so the gather overlaps sample i's TF,
+    // opacity and compositing -- no extra registers.
+    const bool ins = INSIDE || r.all_inside;
     Cell c;
-    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
-    gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
-    if (kHoldCell) {
-      ld256_if(c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
+    locate<CELLS>(V, gx, gy, gz, ins, c);
+    ld256_if(r.n > 0, V.cell0 + 8 * (long long)c.cell, v);
+    held = c.cell;
+    // (the emitting variants spill at 48 registers when unrolled)
+#pragma unroll (kAbs ? 4 : 1)
+    for (int i = 0; i < r.n; ++i) {
+      if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
+      const float d = density(c, v);
+      gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
+      locate<CELLS>(V, gx, gy, gz, ins, c);
+      const bool more = i + 1 < r.n;
+      ld256_if(more && c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
       held = c.cell;
-    } else {
-      fetch8<CELLS>(V, c, v);
+      shade(d, i);
     }
-    composite(c, v, i);
+  } else {
+    for (int i = 0; i < r.n; ++i) {
+      if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
+      Cell c;
+      locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
+      gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
+      fetch8<CELLS>(V, c, v);
+      shade(density(c, v), i);
+    }
   }
   if (kAbs) A = (float)(-expm1(-S));
   rgba = make_float4(c0, c1, c2, A);
@@ -1093,19 +1115,38 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
 
   constexpr bool kHoldCell = CELLS && DDVR_HOLD_CELL;
+  // early issue (as in the march): the next sample's record is requested as
+  // soon as this sample's interpolant has read the registers.  Not for the
+  // camera / stepsize walks, whose spatial derivative reads the record later.
+  constexpr bool kEarly = kHoldCell && !kPos && DDVR_EARLY_WALK;
   float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int held = INT_MIN;
+  Cell cnext;
+  if (kEarly) {
+    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, cnext);
+    ld256_if(r.n > 0, V.cell0 + 8 * (long long)cnext.cell, v);
+    held = cnext.cell;
+  }
 #pragma unroll 1   // (unrolled, the walks spill at their register budgets)
   for (int i = r.n - 1; i >= 0; --i) {
     Cell c;
-    locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
-    if (kHoldCell) {
-      ld256_if(c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
-      held = c.cell;
+    if (kEarly) {
+      c = cnext;
     } else {
-      fetch8<CELLS>(V, c, v);
+      locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
+      if (kHoldCell) {
+        ld256_if(c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
+        held = c.cell;
+      } else {
+        fetch8<CELLS>(V, c, v);
+      }
     }
     const Interp ip = interp(c, v);
+    if (kEarly) {   // v consumed: the record of sample i-1 is now in flight
+      locate<CELLS>(V, gx - r.gs[0], gy - r.gs[1], gz - r.gs[2], INSIDE || r.all_inside, cnext);
+      ld256_if(i > 0 && cnext.cell != held, V.cell0 + 8 * (long long)cnext.cell, v);
+      held = cnext.cell;
+    }
     const float raw = ip.rho;
     const bool inside = INSIDE || c.inside;
     const float d = clamp_density(inside, raw);

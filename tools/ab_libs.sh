@@ -1,10 +1,10 @@
 #!/bin/bash
 # A/B the experiment builds in paper_2107_12672_b200/_variants on one GPU:
-#   tools/ab_libs.sh <config> [steps]   -> gpurun_out/ab_<config>.jsonl
-cfg=${1:-C4}; steps=${2:-4}
+#   tools/ab_libs.sh <config> [steps] [extra bench flags, e.g. --unfused]   -> gpurun_out/ab_<config>.jsonl
+cfg=${1:-C4}; steps=${2:-4}; extra=${3:-}
 out=gpurun_out/ab_${cfg}.jsonl; : > $out
 for lib in paper_2107_12672_b200/libddvr.so paper_2107_12672_b200/_variants/*.so; do
-  line=$(DDVR_LIB=$PWD/$lib timeout 600 python bench.py --config $cfg --steps $steps --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1)
+  line=$(DDVR_LIB=$PWD/$lib timeout 600 python bench.py --config $cfg --steps $steps --warmup 3 --no-cpu-baseline $extra 2>/dev/null | tail -1)
   echo "{\"lib\": \"$(basename $lib)\", \"bench\": $line}" >> $out
 done
 python - "$out" <<'PY'
@@ -12,5 +12,6 @@ import json, sys
 for l in open(sys.argv[1]):
     d = json.loads(l); b = d["bench"]
     k = b.get("kernels", {})
-    print(f'{d["lib"]:24s} {b["value"]/1e9:8.2f} G/s  {b["ms_per_step"]:8.2f} ms  ', "fwd %.2f adj %.2f" % (k["forward"]["ms"], k["adjoint"]["ms"]))
+    ks = " ".join(f"{n} {v['ms']:.2f}" for n, v in k.items() if isinstance(v, dict) and "ms" in v)
+    print(f'{d["lib"]:24s} {b["value"]/1e9:8.2f} G/s  {b["ms_per_step"]:8.2f} ms  ', ks)
 PY
