@@ -13,6 +13,12 @@
  *                        (_adjoint_scene :655-685, _adjoint_tile :491-652)
  *   ddvr_ray_setup    <- voldiff.renderer._ray_setup/_step_counts  renderer.py:182-214, 360-368
  *   ddvr_l1_loss      <- voldiff.objectives.l1_loss            objectives.py:38-54
+ *   ddvr_field_sample <- voldiff.field.trilinear_sample / trilinear_gradients
+ *                                                              field.py:279-349, 379-517
+ *   ddvr_tf_lookup    <- voldiff.field.tf_sample / tf_gradients field.py:525-579
+ *   ddvr_opacity      <- voldiff.field.opacity_from_density   field.py:587-600
+ *   ddvr_camera_rays  <- voldiff.field.camera_from_sphere / camera_gradients
+ *                                                              field.py:186-271
  *   ddvr_last_error   <- the message of the raised voldiff error (errors.py:4-33)
  *
  * Conventions
@@ -40,7 +46,7 @@
 extern "C" {
 #endif
 
-#define DDVR_ABI_VERSION 2
+#define DDVR_ABI_VERSION 3
 
 typedef enum {
   DDVR_OK = 0,
@@ -270,6 +276,54 @@ int ddvr_adam_step_device(float* params, const float* grads, float* m, float* v,
 
 /* upsample_volume (optim.py:92-129): dst (2X,2Y,2Z) from src (X,Y,Z). */
 int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, void* stream);
+
+/* project_params (optim.py:70-89) alone: element i clamped to [lo, hi] when
+ * stride <= 1 or i % stride == stride-1, else to [lo_other, hi_other]; only
+ * cfg->stride / lo / hi / lo_other / hi_other are read. */
+int ddvr_project(float* params, int64_t n, const ddvr_adam* cfg, void* stream);
+
+/* gd_step (optim.py:33-42): params -= lr * grads; a non-finite gradient sets
+ * *nonfinite (device, caller-zeroed, nullable) and skips the update. */
+int ddvr_gd_step(float* params, const float* grads, int64_t n, double lr, int32_t* nonfinite,
+                 void* stream);
+
+/* ---- point-wise field functions, fp64 ---
+ * The march evaluates these inline; these entry points expose them over
+ * caller-given points with the reference's operation order and separately
+ * rounded arithmetic: trilinear_* and tf_* agree with the reference bit for
+ * bit, the transcendental ones (camera, opacity) to libm's last ulp.  All
+ * arrays are (device) doubles; every output is nullable. */
+
+/* trilinear_sample / trilinear_gradients (field.py:279-349, 379-517) of the
+ * (X,Y,Z) z-fastest double grid `values` on [box_min, box_max] at n points
+ * (n, 3): value_out (n) = density clamped to [0, 1], 0 outside the box;
+ * spatial_out (n, 3) world-space gradient, weights_out (n, 8) corner
+ * sensitivities (both zeroed outside the box and where the clamp is active),
+ * corners_out (n, 8) int64 flat corner indices (C order, field.py:311-324). */
+int ddvr_field_sample(const double* values, const int32_t dims[3], const double box_min[3],
+                      const double box_max[3], const double* points, int64_t n,
+                      double* value_out, double* spatial_out, double* weights_out,
+                      int64_t* corners_out, void* stream);
+
+/* tf_sample / tf_gradients (field.py:525-579) of the texel TF (R, 4) at n
+ * densities: out4 (n, 4) (rgb, tau); slope4 (n, 4) zero in the clamp-to-edge
+ * regions; weights2 (n, 2) texel weights; idx2 (n, 2) int64 texel indices. */
+int ddvr_tf_lookup(const double* texels, int32_t resolution, const double* density, int64_t n,
+                   double* out4, double* slope4, double* weights2, int64_t* idx2, void* stream);
+
+/* opacity_from_density (field.py:587-600): alpha = 1 - exp(-dt tau) clamped to
+ * 1 - 1e-6, dalpha = dt exp(-dt tau) (0 where clamped), n segments. */
+int ddvr_opacity(const double* tau, int64_t n, double dt, double* alpha, double* dalpha,
+                 void* stream);
+
+/* camera_from_sphere / camera_gradients (field.py:186-271) of one camera (host
+ * struct) for an image width x height at n pixel coordinates u (column), v
+ * (row), in [0, width) x [0, height): origin (n, 3), dir (n, 3) unit;
+ * j_origin, j_dir (n, 3, 2) Jacobians w.r.t. (lon, lat) per degree, evaluated
+ * with the reference's dual-number formulas (autodiff.py:39-141). */
+int ddvr_camera_rays(const ddvr_camera* cam, int32_t width, int32_t height, const double* u,
+                     const double* v, int64_t n, double* origin, double* dir, double* j_origin,
+                     double* j_dir, void* stream);
 
 /* ---- wire / disk formats (fileio.py:27-127) ------------------------------ */
 

@@ -341,10 +341,76 @@ def io_cases():
          fib=np.array([[c.lon_deg, c.lat_deg] for c in views]))
 
 
+def field_cases():
+    """The point-wise field functions (field.py:186-600): trilinear_sample /
+    trilinear_gradients on a grid with values outside [0, 1] (both clamps), points
+    inside, outside, on faces and exactly on the tolerance band; tf_sample /
+    tf_gradients at R = 1, 2, 8 incl. densities outside [0, 1] and on texel
+    centres; opacity_from_density incl. the 1 - EPS_ALPHA clamp; camera_from_sphere /
+    camera_gradients for three cameras at integer and fractional pixels."""
+    from voldiff import field as vfld
+    rng = np.random.default_rng(21)
+    out = {}
+    for name, dims, bmin, bmax in (("a", (6, 5, 7), [-0.5, -0.5, -0.5], [0.5, 0.5, 0.5]),
+                                   ("b", (4, 1, 3), [-1.0, 0.25, -2.0], [1.5, 0.75, 1.0])):
+        vals = f32(rng.uniform(-0.3, 1.3, dims))
+        vol = vd.DensityVolume(vals, bmin, bmax)
+        bmin, bmax = np.array(bmin), np.array(bmax)
+        ext = bmax - bmin
+        pts = bmin + rng.uniform(-0.1, 1.1, (400, 3)) * ext
+        faces = bmin + rng.uniform(0, 1, (60, 3)) * ext
+        ax = rng.integers(0, 3, 60)
+        side = rng.integers(0, 2, 60)
+        faces[np.arange(60), ax] = np.where(side, bmax[ax], bmin[ax])
+        band = faces.copy()            # just inside / outside the 1e-9 tolerance
+        band[np.arange(60), ax] += np.where(side, 1, -1) * np.where(
+            np.arange(60) % 2, 0.5e-9, 2e-9) * ext[ax]
+        centres = bmin + (np.stack(np.meshgrid(*[np.arange(d) for d in dims], indexing="ij"),
+                                   -1).reshape(-1, 3)[:50] + 0.5) * ext / np.array(dims)
+        p = np.concatenate([pts, faces, band, centres])
+        out[f"vol_{name}"] = vals
+        out[f"box_{name}"] = np.stack([bmin, bmax])
+        out[f"pts_{name}"] = p
+        out[f"value_{name}"] = vd.trilinear_sample(vol, p)
+        sp, w, c = vd.trilinear_gradients(vol, p)
+        out[f"spatial_{name}"], out[f"weights_{name}"], out[f"corners_{name}"] = sp, w, c
+    for R in (1, 2, 8):
+        tf = vd.TransferFunction(f32(rng.uniform(-0.5, 3.0, (R, 4))))
+        d = np.concatenate([rng.uniform(-0.2, 1.2, 300), (np.arange(R) + 0.5) / R,
+                            [0.0, 1.0, -0.0, 0.5 / R, 1 - 0.5 / R]])
+        out[f"tf{R}"] = tf.texels
+        out[f"d{R}"] = d
+        out[f"tfs{R}"] = vd.tf_sample(tf, d)
+        sl, tw, ti = vd.tf_gradients(tf, d)
+        out[f"slope{R}"], out[f"tw{R}"], out[f"ti{R}"] = sl, tw, ti
+    tau = np.concatenate([rng.uniform(-1.0, 50.0, 300), [0.0, 1e6, 13.815510557964274]])
+    for k, dt in enumerate((0.05, 1.0)):
+        a, dadt = vd.opacity_from_density(tau, dt)
+        out[f"alpha{k}"], out[f"dalpha{k}"], out[f"odt{k}"] = a, dadt, np.float64(dt)
+    out["tau"] = tau
+    cams = [vd.SphericalCamera(30.0, 20.0, 2.0, fov_y_deg=30.0, width=9, height=7),
+            vd.SphericalCamera(-117.5, -61.25, 3.5, (0.1, -0.2, 0.3), 47.0, 16, 16),
+            vd.SphericalCamera(400.0, 89.5, 1.25, fov_y_deg=8.0, width=5, height=11)]
+    for k, cam in enumerate(cams):
+        u = np.concatenate([np.repeat(np.arange(cam.width), cam.height),
+                            rng.uniform(0, cam.width, 20)])
+        v = np.concatenate([np.tile(np.arange(cam.height), cam.width),
+                            rng.uniform(0, cam.height, 20)])
+        o, dd = vfld.camera_from_sphere(cam, u, v)
+        jo, jd = vfld.camera_gradients(cam, u, v)
+        out[f"cam{k}"] = np.array([cam.lon_deg, cam.lat_deg, cam.radius, *cam.center,
+                                   cam.fov_y_deg, cam.width, cam.height])
+        out[f"u{k}"], out[f"v{k}"] = u, v
+        out[f"origin{k}"], out[f"dir{k}"], out[f"jo{k}"], out[f"jd{k}"] = o, dd, jo, jd
+    save("fields", **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["kat", "rand", "config", "count", "optim", "fwdgrad", "color", "io",
-                             "entropy"]
+                             "entropy", "fields"]
+    if "fields" in which:
+        field_cases()
     if "entropy" in which:
         entropy_cases()
     if "io" in which:

@@ -32,14 +32,28 @@ from .voldiff_api import (
     blend,
     blend_adjoint,
     blend_invert,
+    OptimState,
+    adam_step,
+    camera_from_sphere,
+    camera_gradients,
     fibonacci_views,
+    gd_step,
     l1_loss,
     opacity_entropy,
+    opacity_from_density,
+    project_params,
     render,
     render_adjoint,
     render_colorvol,
     render_colorvol_adjoint,
     render_forward_grad,
+    smoothness_prior_tf,
+    smoothness_prior_volume,
+    tf_gradients,
+    tf_sample,
+    trilinear_gradients,
+    trilinear_sample,
+    upsample_volume,
 )
 from .raymarch import (
     DiffDVR,
@@ -68,4 +82,8 @@ __all__ = [
     "Rig", "adjoint", "camera_array", "forward", "forward_grad", "l1_loss_seed", "pack_cells",
     "render_views", "CONFIGS",
     "absorption_ramp_texels", "fibonacci_poses", "phantom", "preset_texels",
+    "trilinear_sample", "trilinear_gradients", "tf_sample", "tf_gradients",
+    "opacity_from_density", "camera_from_sphere", "camera_gradients",
+    "smoothness_prior_tf", "smoothness_prior_volume", "OptimState", "gd_step", "adam_step",
+    "project_params", "upsample_volume",
 ]

@@ -19,7 +19,7 @@ from .errors import (
 
 LIB_PATH = os.environ.get("DDVR_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                       "libddvr.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 TARGET_CAMERA = 1
 TARGET_STEPSIZE = 2
@@ -40,7 +40,8 @@ EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
             "ddvr_ray_setup",
             "ddvr_prior_volume",
             "ddvr_prior_tf", "ddvr_adam_step", "ddvr_adam_step_device",
-            "ddvr_upsample_volume", "ddvr_volume_from_raw",
+            "ddvr_upsample_volume", "ddvr_project", "ddvr_gd_step", "ddvr_field_sample",
+            "ddvr_tf_lookup", "ddvr_opacity", "ddvr_camera_rays", "ddvr_volume_from_raw",
             "ddvr_volume_to_raw", "ddvr_image_to_ppm", "ddvr_last_error",
             "ddvr_abi_version", "ddvr_launch_count")
 
@@ -133,6 +134,20 @@ def _bind(lib):
     lib.ddvr_adam_step_device.restype = ctypes.c_int
     lib.ddvr_upsample_volume.argtypes = [vp, i3, vp, vp]
     lib.ddvr_upsample_volume.restype = ctypes.c_int
+    lib.ddvr_project.argtypes = [vp, ctypes.c_int64, P(DdvrAdam), vp]
+    lib.ddvr_project.restype = ctypes.c_int
+    lib.ddvr_gd_step.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_double, vp, vp]
+    lib.ddvr_gd_step.restype = ctypes.c_int
+    d3 = P(ctypes.c_double)
+    lib.ddvr_field_sample.argtypes = [vp, i3, d3, d3, vp, ctypes.c_int64, vp, vp, vp, vp, vp]
+    lib.ddvr_field_sample.restype = ctypes.c_int
+    lib.ddvr_tf_lookup.argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int64, vp, vp, vp, vp, vp]
+    lib.ddvr_tf_lookup.restype = ctypes.c_int
+    lib.ddvr_opacity.argtypes = [vp, ctypes.c_int64, ctypes.c_double, vp, vp, vp]
+    lib.ddvr_opacity.restype = ctypes.c_int
+    lib.ddvr_camera_rays.argtypes = [d3, ctypes.c_int32, ctypes.c_int32, vp, vp, ctypes.c_int64,
+                                     vp, vp, vp, vp, vp]
+    lib.ddvr_camera_rays.restype = ctypes.c_int
     lib.ddvr_volume_from_raw.argtypes = [vp, i3, P(ctypes.c_double), vp, vp]
     lib.ddvr_volume_from_raw.restype = ctypes.c_int
     lib.ddvr_volume_to_raw.argtypes = [vp, i3, vp, vp]

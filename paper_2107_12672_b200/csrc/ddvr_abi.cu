@@ -426,6 +426,26 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p,
   }
 }
 
+// project_params (optim.py:70-89) and gd_step (optim.py:33-42)
+__global__ void __launch_bounds__(256) project_kernel(float* __restrict__ p, long long n,
+                                                    ddvr_adam a) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool last = a.stride <= 1 || (int)(i % a.stride) == a.stride - 1;
+    const float pi = p[i];
+    p[i] = last ? fminf(fmaxf(pi, a.lo), a.hi) : fminf(fmaxf(pi, a.lo_other), a.hi_other);
+  }
+}
+
+__global__ void __launch_bounds__(256) gd_kernel(float* __restrict__ p,
+                                               const float* __restrict__ g, long long n,
+                                               float lr, const int* __restrict__ flag) {
+  if (flag && *flag) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    p[i] -= lr * g[i];
+}
+
 // Device-side Adam step counter (ddvr_adam_step_device): t = state[0] + 1 and the
 // bias corrections 1 - beta^t (fp64, rounded once), unless the update is skipped
 // for a non-finite gradient -- so a captured CUDA graph replays correct steps.
@@ -948,6 +968,95 @@ int ddvr_adam_step_device(float* params, const float* grads, float* m, float* v,
   adam_kernel<<<grid_blocks(n), 256, 0, st>>>(params, grads, m, v, n, *cfg, 1.f, 1.f, nonfinite,
                                                state);
   return check_launch("adam_kernel");
+}
+
+int ddvr_project(float* params, int64_t n, const ddvr_adam* cfg, void* stream) {
+  g_err[0] = 0;
+  if (!cfg) return set_error(DDVR_INVALID_PARAMETER, "projection config is NULL");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative parameter count");
+  if (n == 0) return DDVR_OK;
+  if (!params) return set_error(DDVR_INVALID_INPUT, "parameter pointer is NULL");
+  project_kernel<<<grid_blocks(n), 256, 0, (cudaStream_t)stream>>>(params, n, *cfg);
+  return check_launch("project_kernel");
+}
+
+int ddvr_gd_step(float* params, const float* grads, int64_t n, double lr, int32_t* nonfinite,
+                 void* stream) {
+  g_err[0] = 0;
+  if (!(lr > 0.0)) return set_error(DDVR_INVALID_PARAMETER, "learning rate must be positive");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative parameter count");
+  if (n == 0) return DDVR_OK;
+  if (!params || !grads) return set_error(DDVR_INVALID_INPUT, "parameter or gradient pointer is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (nonfinite) {
+    finite_check_kernel<<<grid_blocks(n), 256, 0, st>>>(grads, n, nonfinite);
+    if ((rc = check_launch("finite_check_kernel"))) return rc;
+  }
+  gd_kernel<<<grid_blocks(n), 256, 0, st>>>(params, grads, n, (float)lr, nonfinite);
+  return check_launch("gd_kernel");
+}
+
+int ddvr_field_sample(const double* values, const int32_t dims[3], const double box_min[3],
+                      const double box_max[3], const double* points, int64_t n,
+                      double* value_out, double* spatial_out, double* weights_out,
+                      int64_t* corners_out, void* stream) {
+  g_err[0] = 0;
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+    return set_error(DDVR_INVALID_PARAMETER, "volume values must be a non-empty 3D array");
+  if (!box_min || !box_max) return set_error(DDVR_INVALID_PARAMETER, "box is NULL");
+  for (int a = 0; a < 3; ++a)
+    if (!(box_max[a] > box_min[a]))
+      return set_error(DDVR_INVALID_PARAMETER, "box_max must exceed box_min on every axis");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative point count");
+  if (n == 0) return DDVR_OK;
+  if (!values || !points) return set_error(DDVR_INVALID_INPUT, "values or points pointer is NULL");
+  const int d[3] = {dims[0], dims[1], dims[2]};
+  launch_field_sample(values, d, box_min, box_max, points, n, value_out, spatial_out,
+                      weights_out, reinterpret_cast<long long*>(corners_out),
+                      (cudaStream_t)stream);
+  return check_launch("field_sample_kernel");
+}
+
+int ddvr_tf_lookup(const double* texels, int32_t resolution, const double* density, int64_t n,
+                   double* out4, double* slope4, double* weights2, int64_t* idx2, void* stream) {
+  g_err[0] = 0;
+  if (resolution < 1) return set_error(DDVR_INVALID_PARAMETER, "transfer function needs >= 1 texel");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative sample count");
+  if (n == 0) return DDVR_OK;
+  if (!texels || !density) return set_error(DDVR_INVALID_INPUT, "texels or density pointer is NULL");
+  launch_tf_lookup(texels, resolution, density, n, out4, slope4, weights2,
+                   reinterpret_cast<long long*>(idx2), (cudaStream_t)stream);
+  return check_launch("tf_lookup_kernel");
+}
+
+int ddvr_opacity(const double* tau, int64_t n, double dt, double* alpha, double* dalpha,
+                 void* stream) {
+  g_err[0] = 0;
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative sample count");
+  if (n == 0) return DDVR_OK;
+  if (!tau) return set_error(DDVR_INVALID_INPUT, "tau pointer is NULL");
+  launch_opacity(tau, n, dt, alpha, dalpha, (cudaStream_t)stream);
+  return check_launch("opacity_kernel");
+}
+
+int ddvr_camera_rays(const ddvr_camera* cam, int32_t width, int32_t height, const double* u,
+                     const double* v, int64_t n, double* origin, double* dir, double* j_origin,
+                     double* j_dir, void* stream) {
+  g_err[0] = 0;
+  if (!cam) return set_error(DDVR_INVALID_PARAMETER, "camera is NULL");
+  if (width < 1 || height < 1) return set_error(DDVR_INVALID_PARAMETER, "image size must be >= 1");
+  if (!(cam->radius > 0.0)) return set_error(DDVR_INVALID_PARAMETER, "camera radius must be positive");
+  if (!(cam->fov_y_deg > 0.0 && cam->fov_y_deg < 180.0))
+    return set_error(DDVR_INVALID_PARAMETER, "fov_y_deg must lie in (0, 180)");
+  if (!(fabs(cam->lat_deg) < 90.0 - 1e-3))
+    return set_error(DDVR_INVALID_PARAMETER, "latitude too close to a pole");
+  if (n < 0) return set_error(DDVR_INVALID_PARAMETER, "negative pixel count");
+  if (n == 0) return DDVR_OK;
+  if (!u || !v) return set_error(DDVR_INVALID_INPUT, "pixel coordinate pointer is NULL");
+  launch_camera_rays(*cam, width, height, u, v, n, origin, dir, j_origin, j_dir,
+                     (cudaStream_t)stream);
+  return check_launch("camera_rays_kernel");
 }
 
 int ddvr_upsample_volume(const float* src, const int32_t dims[3], float* dst, void* stream) {

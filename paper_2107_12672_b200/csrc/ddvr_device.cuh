@@ -130,6 +130,17 @@ void launch_forward_color(bool early, bool tape, dim3 grid, cudaStream_t st, con
 void launch_adjoint_color(dim3 grid, cudaStream_t st, const VolArgs& V, const Geometry& G,
                           const float* image, const float* depth, const float* seed,
                           float* d_color);
+// point-wise field functions in fp64 (ddvr_fields.cu)
+void launch_field_sample(const double* values, const int dims[3], const double bmin[3],
+                         const double bmax[3], const double* pts, long long n, double* value,
+                         double* spatial, double* weights, long long* corners, cudaStream_t st);
+void launch_tf_lookup(const double* texels, int R, const double* d, long long n, double* out4,
+                      double* slope4, double* weights2, long long* idx2, cudaStream_t st);
+void launch_opacity(const double* tau, long long n, double dt, double* alpha, double* dalpha,
+                    cudaStream_t st);
+void launch_camera_rays(const ddvr_camera& cam, int W, int H, const double* u, const double* v,
+                        long long n, double* origin, double* dir, double* j_origin,
+                        double* j_dir, cudaStream_t st);
 // Fused step (ddvr_forward_adjoint_l1): each thread marches its ray forward,
 // forms the L1 seed sign(image - ref) / count (objectives.py:38-54) and its
 // loss term in registers, then walks back with the exact fp64 optical depth.

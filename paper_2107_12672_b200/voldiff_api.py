@@ -15,6 +15,7 @@ renderer.py:243-247).  There is no CPU fallback.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -524,3 +525,260 @@ def l1_loss(images, refs):
         seeds.append(st.to(torch.float64).cpu().numpy().reshape(x.shape))
     return float(loss.item()), seeds
 
+
+
+# ---------------------------------------------------------------------------
+# point-wise field functions (field.py:186-600; SURVEY 8a rows a1, a4-a6, a9,
+# a10): fp64 device kernels with the reference's operation order
+# ---------------------------------------------------------------------------
+
+
+def _dev64(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def _box(a):
+    return (ctypes.c_double * 3)(*np.asarray(a, np.float64).reshape(3))
+
+
+def _field_call(volume, points, spatial: bool):
+    values = np.asarray(volume.values, np.float64)
+    if values.ndim != 3:
+        raise InvalidParameterError("volume values must be a non-empty 3D array")
+    pts = np.asarray(points, dtype=np.float64)
+    if pts.shape[-1:] != (3,):
+        raise InvalidInputError("points must have a trailing axis of 3")
+    shape = pts.shape[:-1]
+    n = int(np.prod(shape, dtype=np.int64))
+    dev = _device()
+    vt, pt = _dev64(values, dev), _dev64(pts.reshape(n, 3), dev)
+    val = torch.empty(n, dtype=torch.float64, device=dev)
+    sp = torch.empty(n, 3, dtype=torch.float64, device=dev) if spatial else None
+    w = torch.empty(n, 8, dtype=torch.float64, device=dev) if spatial else None
+    c = torch.empty(n, 8, dtype=torch.int64, device=dev) if spatial else None
+    N.check(N.lib().ddvr_field_sample(
+        vt.data_ptr(), (ctypes.c_int32 * 3)(*values.shape), _box(volume.box_min),
+        _box(volume.box_max), pt.data_ptr(), n, val.data_ptr(),
+        sp.data_ptr() if spatial else None, w.data_ptr() if spatial else None,
+        c.data_ptr() if spatial else None, R._stream_ptr()))
+    if not spatial:
+        return val.cpu().numpy().reshape(shape)
+    return (sp.cpu().numpy().reshape(shape + (3,)), w.cpu().numpy().reshape(shape + (8,)),
+            c.cpu().numpy().reshape(shape + (8,)))
+
+
+def trilinear_sample(volume, points) -> np.ndarray:
+    """Density at world points, 0 outside the box, clamped to [0, 1] (field.py:352-358)."""
+    return _field_call(volume, points, spatial=False)
+
+
+def trilinear_gradients(volume, points):
+    """(spatial (...,3), weights (...,8), corner_indices (...,8)) (field.py:503-517)."""
+    return _field_call(volume, points, spatial=True)
+
+
+def _tf_call(tf, d, grads: bool):
+    tex = np.asarray(tf.texels, np.float64)
+    if tex.ndim != 2 or tex.shape[1] != 4:
+        raise InvalidParameterError("transfer function must have shape (R, 4), R >= 1")
+    d = np.asarray(d, dtype=np.float64)
+    shape = d.shape
+    n = int(d.size)
+    dev = _device()
+    tt, dt_ = _dev64(tex, dev), _dev64(d.reshape(n), dev)
+    out = torch.empty(n, 4, dtype=torch.float64, device=dev) if not grads else None
+    sl = torch.empty(n, 4, dtype=torch.float64, device=dev) if grads else None
+    w = torch.empty(n, 2, dtype=torch.float64, device=dev) if grads else None
+    ix = torch.empty(n, 2, dtype=torch.int64, device=dev) if grads else None
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    N.check(N.lib().ddvr_tf_lookup(tt.data_ptr(), tex.shape[0], dt_.data_ptr(), n, ptr(out),
+                                   ptr(sl), ptr(w), ptr(ix), R._stream_ptr()))
+    if not grads:
+        return out.cpu().numpy().reshape(shape + (4,))
+    return (sl.cpu().numpy().reshape(shape + (4,)), w.cpu().numpy().reshape(shape + (2,)),
+            ix.cpu().numpy().reshape(shape + (2,)))
+
+
+def tf_sample(tf, d) -> np.ndarray:
+    """(rgb emission, tau) (..., 4) for densities d, clamp-to-edge (field.py:552-555)."""
+    return _tf_call(tf, d, grads=False)
+
+
+def tf_gradients(tf, d):
+    """(slope (...,4), weights (...,2), texel_indices (...,2)) (field.py:558-579)."""
+    return _tf_call(tf, d, grads=True)
+
+
+def opacity_from_density(tau, dt):
+    """(alpha, dalpha/dtau) of one segment, alpha <= 1 - EPS_ALPHA (field.py:587-600)."""
+    tau = np.asarray(tau, dtype=np.float64)
+    shape, n = tau.shape, int(tau.size)
+    dev = _device()
+    tt = _dev64(tau.reshape(n), dev)
+    a = torch.empty(n, dtype=torch.float64, device=dev)
+    da_ = torch.empty(n, dtype=torch.float64, device=dev)
+    N.check(N.lib().ddvr_opacity(tt.data_ptr(), n, float(dt), a.data_ptr(), da_.data_ptr(),
+                                 R._stream_ptr()))
+    return a.cpu().numpy().reshape(shape), da_.cpu().numpy().reshape(shape)
+
+
+def _camera_call(cam, u, v, jac: bool):
+    u = np.asarray(u, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    W, H = int(cam.width), int(cam.height)
+    if np.any(u < 0) or np.any(u >= W) or np.any(v < 0) or np.any(v >= H):   # field.py:231-236
+        raise InvalidParameterError("pixel coordinates outside image bounds")
+    u, v = np.broadcast_arrays(u, v)
+    shape, n = u.shape, int(u.size)
+    c = (ctypes.c_double * N.CAMERA_DOUBLES)(
+        float(cam.lon_deg), float(cam.lat_deg), float(cam.radius),
+        *np.asarray(cam.center, np.float64).reshape(3), float(cam.fov_y_deg), 0.0)
+    dev = _device()
+    ut, vt = _dev64(u.reshape(n), dev), _dev64(v.reshape(n), dev)
+    o = torch.empty(n, 3, dtype=torch.float64, device=dev)
+    d = torch.empty(n, 3, dtype=torch.float64, device=dev)
+    jo = torch.empty(n, 3, 2, dtype=torch.float64, device=dev) if jac else None
+    jd = torch.empty(n, 3, 2, dtype=torch.float64, device=dev) if jac else None
+    N.check(N.lib().ddvr_camera_rays(c, W, H, ut.data_ptr(), vt.data_ptr(), n, o.data_ptr(),
+                                     d.data_ptr(), jo.data_ptr() if jac else None,
+                                     jd.data_ptr() if jac else None, R._stream_ptr()))
+    if jac:
+        return jo.cpu().numpy().reshape(shape + (3, 2)), jd.cpu().numpy().reshape(shape + (3, 2))
+    return o.cpu().numpy().reshape(shape + (3,)), d.cpu().numpy().reshape(shape + (3,))
+
+
+def camera_from_sphere(cam, u, v):
+    """(origin, unit direction) through the centre of pixel (u, v) (field.py:239-250)."""
+    return _camera_call(cam, u, v, jac=False)
+
+
+def camera_gradients(cam, u, v):
+    """(j_origin, j_direction) (..., 3, 2) w.r.t. (lon, lat) per degree (field.py:253-271)."""
+    return _camera_call(cam, u, v, jac=True)
+
+
+# ---------------------------------------------------------------------------
+# the steps either side of the path (SURVEY 8f rank 1): objectives.py:57-92,
+# optim.py:16-129 under the reference's names, on the libddvr kernels of optim.py
+# (fp32 parameters, fp64 reductions)
+# ---------------------------------------------------------------------------
+
+TAU_MAX_DEFAULT = 100.0   # optim.py:12
+
+
+def smoothness_prior_tf(tf):
+    """(mean squared adjacent-texel difference, gradient (R,4)) (objectives.py:57-69)."""
+    from . import optim as P
+    tex = np.asarray(tf.texels if hasattr(tf, "texels") else tf, np.float64)
+    if tex.shape[0] < 2:
+        return 0.0, np.zeros_like(tex)
+    dev = _device()
+    g = torch.zeros(tex.shape, dtype=torch.float64, device=dev)
+    val = P.prior_tf(torch.from_numpy(tex.astype(np.float32)).to(dev), 1.0, g)
+    return float(val.item()), g.cpu().numpy()
+
+
+def smoothness_prior_volume(volume):
+    """(mean squared forward difference, gradient (X,Y,Z)) (objectives.py:72-92)."""
+    from . import optim as P
+    v = np.asarray(volume.values if hasattr(volume, "values") else volume, np.float64)
+    if v.ndim != 3:
+        raise InvalidParameterError("volume values must be a non-empty 3D array")
+    dev = _device()
+    vt = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(dev)
+    g = torch.zeros_like(vt)
+    val = P.prior_volume(vt, 1.0, g)
+    return float(val.item()), g.to(torch.float64).cpu().numpy()
+
+
+@dataclass
+class OptimState:
+    """Adam moment accumulators for one parameter vector (optim.py:15-25)."""
+
+    lr: float
+    m: np.ndarray | None = None
+    v: np.ndarray | None = None
+    step: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+def _params_pair(params, grads):
+    p = np.asarray(params, dtype=np.float64)
+    g = np.asarray(grads, dtype=np.float64)
+    if p.shape != g.shape:
+        raise InvalidParameterError("parameter/gradient shape mismatch")
+    dev = _device()
+    return (p, torch.from_numpy(np.ascontiguousarray(p, np.float32)).to(dev),
+            torch.from_numpy(np.ascontiguousarray(g, np.float32)).to(dev))
+
+
+def gd_step(params, grads, lr: float):
+    """params - lr * grads (optim.py:33-42); NumericalAbortError on non-finite grads."""
+    from .errors import NumericalAbortError
+    p, pt, gt = _params_pair(params, grads)
+    if lr <= 0.0:
+        raise InvalidParameterError("learning rate must be positive")
+    flag = torch.zeros(1, dtype=torch.int32, device=pt.device)
+    N.check(N.lib().ddvr_gd_step(pt.data_ptr(), gt.data_ptr(), pt.numel(), float(lr),
+                                 flag.data_ptr(), R._stream_ptr()))
+    if int(flag.item()):
+        raise NumericalAbortError("non-finite gradients passed to the optimizer")
+    return pt.to(torch.float64).cpu().numpy().reshape(p.shape)
+
+
+def adam_step(state, params, grads):
+    """One Adam update with bias correction; returns ``(new state, params)`` (optim.py:45-67)."""
+    from . import optim as P
+    p, pt, gt = _params_pair(params, grads)
+    st = P.AdamState(lr=float(state.lr), beta1=float(state.beta1), beta2=float(state.beta2),
+                     eps=float(state.eps), step=int(state.step))
+    dev = pt.device
+    st.m = (torch.zeros_like(pt) if state.m is None else
+            torch.from_numpy(np.ascontiguousarray(state.m, np.float32)).to(dev).reshape(pt.shape))
+    st.v = (torch.zeros_like(pt) if state.v is None else
+            torch.from_numpy(np.ascontiguousarray(state.v, np.float32)).to(dev).reshape(pt.shape))
+    st.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    st.update(pt, gt, project=None)
+    new = OptimState(lr=state.lr, m=st.m.to(torch.float64).cpu().numpy().reshape(p.shape),
+                     v=st.v.to(torch.float64).cpu().numpy().reshape(p.shape), step=st.step,
+                     beta1=state.beta1, beta2=state.beta2, eps=state.eps)
+    return new, pt.to(torch.float64).cpu().numpy().reshape(p.shape)
+
+
+def project_params(params, target: str, tau_max: float = TAU_MAX_DEFAULT):
+    """Clamp parameters into their physical range; idempotent (optim.py:70-89)."""
+    p = np.asarray(params, dtype=np.float64)
+    inf = float("inf")
+    if target == "volume":
+        cfg = (1, 0.0, 1.0, 0.0, 1.0)
+    elif target in ("tf", "color"):
+        cfg = (4, 0.0, float(tau_max), 0.0, inf)
+    else:
+        raise InvalidParameterError(f"unknown projection target {target!r}")
+    dev = _device()
+    pt = torch.from_numpy(np.ascontiguousarray(p, np.float32)).to(dev)
+    a = N.DdvrAdam(0.0, 0.0, 0.0, 0.0, 0, *cfg)
+    N.check(N.lib().ddvr_project(pt.data_ptr(), pt.numel(), ctypes.byref(a), R._stream_ptr()))
+    return pt.to(torch.float64).cpu().numpy().reshape(p.shape)
+
+
+def upsample_volume(volume):
+    """Double the grid resolution per axis, world box unchanged (optim.py:114-129)."""
+    from . import optim as P
+    if isinstance(volume, ColorVolume) or (hasattr(volume, "values")
+                                           and np.ndim(volume.values) == 4):
+        vals = np.asarray(volume.values, np.float64)
+        dev = _device()
+        chans = [P.upsample_volume(torch.from_numpy(np.ascontiguousarray(vals[..., c], np.float32))
+                                   .to(dev)) for c in range(vals.shape[3])]
+        up = torch.stack(chans, dim=3).to(torch.float64).cpu().numpy()
+        return ColorVolume(up, np.array(volume.box_min, np.float64),
+                           np.array(volume.box_max, np.float64))
+    if not hasattr(volume, "values"):
+        raise InvalidParameterError("upsample_volume expects a density or color volume")
+    vals = np.asarray(volume.values, np.float64)
+    up = P.upsample_volume(torch.from_numpy(np.ascontiguousarray(vals, np.float32)).to(_device()))
+    return DensityVolume(up.to(torch.float64).cpu().numpy(), np.array(volume.box_min, np.float64),
+                         np.array(volume.box_max, np.float64))

@@ -39,7 +39,9 @@ def test_header_declares_the_boundary():
                             "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
                             "ddvr_ray_setup", "ddvr_prior_volume", "ddvr_prior_tf",
                             "ddvr_adam_step", "ddvr_adam_step_device",
-                            "ddvr_upsample_volume", "ddvr_volume_from_raw",
+                            "ddvr_upsample_volume", "ddvr_project", "ddvr_gd_step",
+                            "ddvr_field_sample", "ddvr_tf_lookup", "ddvr_opacity",
+                            "ddvr_camera_rays", "ddvr_volume_from_raw",
                             "ddvr_volume_to_raw", "ddvr_image_to_ppm", "ddvr_last_error",
                             "ddvr_abi_version", "ddvr_launch_count"])
 
@@ -48,7 +50,8 @@ def test_library_exports_every_declared_symbol(lib):
     handle = ctypes.CDLL(lib._name)
     for name in _declared():
         assert hasattr(handle, name), name
-    assert lib.ddvr_abi_version() == 2
+    from paper_2107_12672_b200 import _native
+    assert lib.ddvr_abi_version() == _native.ABI_VERSION == 3
 
 
 def test_python_binding_matches_header():
@@ -189,3 +192,32 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(N, "LIB_PATH", str(tmp_path / "nope.so"))
     with pytest.raises(N.NativeLibraryError):
         N.lib()
+
+
+def test_field_entry_points_validate_before_launch(lib):
+    """ddvr_field_sample / tf_lookup / opacity / camera_rays / project / gd_step:
+    parameter errors come back as status codes with a message, before any CUDA call."""
+    from paper_2107_12672_b200 import _native as N
+    d3 = lambda *v: (ctypes.c_double * 3)(*v)   # noqa: E731
+    i3 = (ctypes.c_int32 * 3)(4, 4, 4)
+    rc = lib.ddvr_field_sample(None, i3, d3(0, 0, 0), d3(1, 0, 1), None, 5, None, None, None,
+                               None, None)
+    assert rc == 1 and "box" in lib.ddvr_last_error().decode()
+    rc = lib.ddvr_field_sample(None, (ctypes.c_int32 * 3)(0, 4, 4), d3(0, 0, 0), d3(1, 1, 1),
+                               None, 5, None, None, None, None, None)
+    assert rc == 1
+    assert lib.ddvr_field_sample(None, i3, d3(0, 0, 0), d3(1, 1, 1), None, 5, None, None, None,
+                                 None, None) == 2
+    assert lib.ddvr_field_sample(None, i3, d3(0, 0, 0), d3(1, 1, 1), None, 0, None, None, None,
+                                 None, None) == 0
+    assert lib.ddvr_tf_lookup(None, 0, None, 3, None, None, None, None, None) == 1
+    assert lib.ddvr_opacity(None, -1, 0.1, None, None, None) == 1
+    cam = (ctypes.c_double * N.CAMERA_DOUBLES)(0.0, 89.9995, 2.0, 0, 0, 0, 30.0, 0)
+    rc = lib.ddvr_camera_rays(cam, 4, 4, None, None, 1, None, None, None, None, None)
+    assert rc == 1 and "pole" in lib.ddvr_last_error().decode()
+    cam = (ctypes.c_double * N.CAMERA_DOUBLES)(0.0, 10.0, 2.0, 0, 0, 0, 180.0, 0)
+    assert lib.ddvr_camera_rays(cam, 4, 4, None, None, 1, None, None, None, None, None) == 1
+    assert lib.ddvr_gd_step(None, None, 4, 0.0, None, None) == 1
+    assert lib.ddvr_project(None, 4, None, None) == 1
+    a = N.DdvrAdam(0.0, 0.0, 0.0, 0.0, 0, 1, 0.0, 1.0, 0.0, 1.0)
+    assert lib.ddvr_project(None, 4, ctypes.byref(a), None) == 2

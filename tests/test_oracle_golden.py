@@ -147,3 +147,52 @@ def test_oracle_color_volume(key):
     for mode in ("inversion", "stored"):
         got = O.adjoint_color_view(cg, view, dt, g[f"{key}_seed"], stored=(mode == "stored"))
         assert rel_max(got, g[f"{key}_{mode}_d_color"]) <= TOL
+
+
+# --- point-wise field functions (tests/golden/fields.npz, field.py:186-600) ---
+
+
+@pytest.mark.parametrize("name", ["a", "b"])
+def test_oracle_trilinear(name):
+    g = golden("fields")
+    grid = O.Grid(g[f"vol_{name}"], g[f"box_{name}"][0], g[f"box_{name}"][1])
+    pts = g[f"pts_{name}"]
+    d, sp, w, idx = grid.density_and_grads(pts.T)
+    np.testing.assert_array_equal(idx, g[f"corners_{name}"])
+    assert rel_max(d, g[f"value_{name}"]) <= 1e-14
+    assert rel_max(grid.density(pts.T), g[f"value_{name}"]) <= 1e-14
+    assert rel_max(w, g[f"weights_{name}"]) <= 1e-14
+    assert rel_max(sp, g[f"spatial_{name}"]) <= 1e-14
+
+
+@pytest.mark.parametrize("R", [1, 2, 8])
+def test_oracle_tf(R):
+    g = golden("fields")
+    out, slope, (i0, i1), (w0, w1) = O.tf_eval(g[f"tf{R}"], g[f"d{R}"])
+    np.testing.assert_array_equal(out, g[f"tfs{R}"])
+    np.testing.assert_array_equal(slope, g[f"slope{R}"])
+    np.testing.assert_array_equal(np.stack([i0, i1], -1), g[f"ti{R}"])
+    np.testing.assert_array_equal(np.stack([w0, w1], -1), g[f"tw{R}"])
+
+
+def test_oracle_opacity():
+    g = golden("fields")
+    for k in (0, 1):
+        dt = float(g[f"odt{k}"])
+        tau, e, a, clamped = O.segment_opacity(g["tau"], dt)
+        live = g["tau"] >= 0.0          # the oracle folds the renderer's max(tau, 0)
+        np.testing.assert_array_equal(a[live], g[f"alpha{k}"][live])
+        np.testing.assert_array_equal(np.where(clamped, 0.0, dt * e)[live], g[f"dalpha{k}"][live])
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_oracle_camera(k):
+    g = golden("fields")
+    c = g[f"cam{k}"]
+    view = O.View(c[0], c[1], c[2], tuple(c[3:6]), c[6], int(c[7]), int(c[8]))
+    o, d = O.pixel_rays(view, g[f"u{k}"], g[f"v{k}"])
+    np.testing.assert_array_equal(o.T, g[f"origin{k}"])
+    np.testing.assert_array_equal(d.T, g[f"dir{k}"])
+    jo, jd = O.camera_jacobians(view, g[f"u{k}"], g[f"v{k}"])
+    assert rel_max(np.broadcast_to(jo, g[f"jo{k}"].shape), g[f"jo{k}"]) <= 1e-12
+    assert rel_max(np.moveaxis(jd, 0, 1), g[f"jd{k}"]) <= 1e-12
