@@ -437,6 +437,18 @@ __device__ __forceinline__ void red128_if(bool pred, float* p, float a, float b,
       : "memory");
 }
 
+// both halves of a 32-byte moment record under ONE predicate: ptxas turns a
+// predicated red into a branch around it, so one branch instead of two
+__device__ __forceinline__ void red256_if(bool pred, float* p, const float a[8]) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
+      "@q red.global.add.v4.f32 [%1], {%2,%3,%4,%5};\n\t"
+      "@q red.global.add.v4.f32 [%1+16], {%6,%7,%8,%9};\n\t}" ::"r"((int)pred),
+      "l"(p), "f"(a[0]), "f"(a[1]), "f"(a[2]), "f"(a[3]), "f"(a[4]), "f"(a[5]), "f"(a[6]),
+      "f"(a[7])
+      : "memory");
+}
+
 __device__ __forceinline__ void red64(float* p, float a, float b) {
   asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
@@ -1076,7 +1088,6 @@ constexpr int kNoRun = INT_MIN;   // padded cell indices can be negative
 // Per-ray adjoint accumulators that outlive the walk
 struct AdjState {
   int run_cell, run_base, run_ox, run_oy, run_oz;   // volume cell run
-  float* run_q;                                     // its record in the cell workspace
   float acc8[8];
   int tf_run;                                       // TF texel/knot run (i0, i0+1)
   float4 tfa0, tfa1;
@@ -1279,10 +1290,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
         const bool fresh = c.cell != st.run_cell;
         const bool flush = fresh && st.run_cell != kNoRun;
-        float* q = st.run_q;
-        red128_if(flush, q, st.acc8[0], st.acc8[1], st.acc8[2], st.acc8[3]);
-        red128_if(flush, q + 4, st.acc8[4], st.acc8[5], st.acc8[6], st.acc8[7]);
-        st.run_q = fresh ? d_cells + 8 * (long long)c.cell : st.run_q;
+        // (ptxas branches around a predicated red anyway: one branch for both
+        // halves, and the record address is formed only inside it)
+        if (flush) flush_cell<true>(d_volume, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
         const float keep = fresh ? 0.f : 1.f;
         st.acc8[0] = fmaf(st.acc8[0], keep, dh);
         st.acc8[1] = fmaf(st.acc8[1], keep, px);
@@ -1422,7 +1432,6 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 
   AdjState st;
   st.run_cell = kNoRun; st.run_base = 0; st.run_ox = 0; st.run_oy = 0; st.run_oz = 0;
-  st.run_q = d_cells;
 #pragma unroll
   for (int k = 0; k < 8; ++k) st.acc8[k] = 0.f;
   st.tf_run = kNoRun;
