@@ -1189,9 +1189,11 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       // non-negative affine tau column in a polynomial segment mode, no
       // stepsize target (dispatch guarantees it): tau >= 0, no EPS clamp, and
       // the slope is b for t in [0, R-1), 0 in the clamp bands -- only the
-      // band test is left per sample (b is folded into abs_k)
+      // band test is left per sample (b is folded into abs_k).  It is taken on
+      // the raw density: t in [0, R-1) already implies raw in (0, 1), where
+      // d == raw, so it also carries the [0,1] live test of field.py:486-489.
       i0 = 0; w = 0.f;
-      const float t = __fmaf_rn(d, TF.fR, -0.5f);
+      const float t = __fmaf_rn(raw, TF.fR, -0.5f);
       dq = (t >= 0.f && t < TF.fR1) ? 1.f : 0.f;
       s = make_float4(0.f, 0.f, 0.f, 0.f);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1276,7 +1278,8 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
                                          dl4.w * tau_hat)
           : EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
                  : slope.w * tau_hat;
-      const bool live = inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
+      const bool live = (kAbs && AFF) ? inside   // (the band test above covers [0,1])
+                                      : inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol && CELLS) {   // renderer.py:607-608, accumulated per cell run
         // The run accumulates the 8 moments sum dh * phi(u), phi = {1, ux, uy,
         // uz, ux uy, ux uz, uy uz, ux uy uz}, of the polynomial record: the
