@@ -103,6 +103,7 @@ typedef struct {
 
 #define DDVR_FLAG_WS_CONTINUE 1
 #define DDVR_FLAG_WS_DEFER 2
+#define DDVR_FLAG_DETERMINISTIC 4
 
 /* march parameters (RenderConfig, renderer.py:84-106) */
 typedef struct {
@@ -118,7 +119,12 @@ typedef struct {
                                                    step's partial gradients: not zeroed;
                             DDVR_FLAG_WS_DEFER     more calls follow: partial gradients
                                                    stay in the workspace (no fold into
-                                                   d_volume, no reduction into d_tf) */
+                                                   d_volume, no reduction into d_tf)
+                            DDVR_FLAG_DETERMINISTIC  (combinable) camera / stepsize
+                                                   sums per CTA into the workspace,
+                                                   reduced in a fixed order: d_camera
+                                                   and d_dt bitwise reproducible
+                                                   (ddvr_deterministic_bytes) */
   float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
                             forward writes the transmittance before every sample,
                             tape[ray * tape_stride + i]; the adjoint then reads it
@@ -194,6 +200,14 @@ int ddvr_adjoint_color(const ddvr_volume* cv, const ddvr_camera* cams, int32_t n
  * per-CTA TF-gradient slots (tf target). */
 int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf,
                                      uint32_t target_mask);
+
+/* Extra workspace of a DDVR_FLAG_DETERMINISTIC ddvr_adjoint /
+ * ddvr_forward_adjoint_l1 call over n_views views with params p: the caller
+ * passes ddvr_adjoint_workspace_bytes rounded up to 256, plus this.  0 unless
+ * mask has the camera or stepsize target.  (The TF gradient is always reduced
+ * from per-CTA slots in slot order; d_volume and the in-CTA TF sums use fp32
+ * atomics: reproducible to fp32 rounding, not bitwise.) */
+int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:
  * (X+1) * (Y+1) * (Z+1) records of 8 floats -- cells -1 .. dim-1 on every

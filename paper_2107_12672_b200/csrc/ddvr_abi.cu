@@ -321,6 +321,7 @@ int make_geo(const ddvr_camera* cams, int n_views, const ddvr_params* p, Geometr
   G.dt32 = (float)p->dt;
   G.tape = p->tape;
   G.tape_stride = p->tape_stride;
+  G.partials = nullptr;
   if (G.tape && G.tape_stride < 0)
     return set_error(DDVR_INVALID_PARAMETER, "negative tape stride");
   return DDVR_OK;
@@ -574,6 +575,38 @@ __global__ void __launch_bounds__(256) tf_slots_reduce_kernel(const float* __res
   }
 }
 
+// DDVR_FLAG_DETERMINISTIC: the per-CTA camera / stepsize sums (3 doubles per
+// CTA, CTA index = tile + tiles * view) reduced in a fixed order -- each
+// thread strides over the CTAs in index order, then a fixed shared-memory tree
+// -- so d_camera and d_dt are bitwise reproducible.  Blocks [0, cam_blocks)
+// reduce view b's camera pair, the block after them the stepsize total.
+__global__ void __launch_bounds__(256) partials_reduce_kernel(const double* __restrict__ part,
+                                                            int tiles, int n_views,
+                                                            int cam_blocks,
+                                                            double* __restrict__ d_camera,
+                                                            double* __restrict__ d_dt) {
+  __shared__ double s0[256], s1[256];
+  const int b = blockIdx.x, t = threadIdx.x;
+  double a0 = 0.0, a1 = 0.0;
+  if (b < cam_blocks) {
+    const double* q = part + 3 * (size_t)b * tiles;
+    for (int k = t; k < tiles; k += 256) { a0 += q[3 * k]; a1 += q[3 * k + 1]; }
+  } else {
+    const long long n = (long long)tiles * n_views;
+    for (long long k = t; k < n; k += 256) a0 += part[3 * k + 2];
+  }
+  s0[t] = a0; s1[t] = a1;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (t < w) { s0[t] += s0[t + w]; s1[t] += s1[t + w]; }
+    __syncthreads();
+  }
+  if (t == 0) {
+    if (b < cam_blocks) { d_camera[2 * b] += s0[0]; d_camera[2 * b + 1] += s1[0]; }
+    else *d_dt += s0[0];
+  }
+}
+
 int grid_blocks(long long n) {
   long long b = (n + 255) / 256;
   return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -635,6 +668,21 @@ int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf, 
   return ws_cells_bytes(vol, mask) + ws_tf_bytes(tf, mask);
 }
 
+// DDVR_FLAG_DETERMINISTIC partials: after the 256-aligned end of the workspace
+static int64_t det_bytes(int64_t ctas, uint32_t mask) {
+  if (!(mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE))) return 0;
+  return (ctas * 3 * 8 + 255) & ~(int64_t)255;
+}
+
+int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask) {
+  if (!p || n_views < 0 || p->width < 1 || p->height < 1) return 0;
+  const int row1 = p->row1 <= 0 ? p->height : p->row1;
+  const int rows = std::max(0, row1 - p->row0);
+  const int64_t ctas = (int64_t)((p->width + kTile - 1) / kTile) * ((rows + kTile - 1) / kTile) *
+                       n_views;
+  return det_bytes(ctas, mask);
+}
+
 int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
                  int32_t n_views, const ddvr_params* p, float* image_out, float* depth_out,
                  void* stream) {
@@ -665,7 +713,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                        int64_t workspace_bytes, void* stream, const FusedArgs* fu,
                        int32_t flags) {
   int rc;
-  if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER))
+  if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER | DDVR_FLAG_DETERMINISTIC))
     return set_error(DDVR_INVALID_PARAMETER, "unknown params.flags bits 0x%x", flags);
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
@@ -679,17 +727,31 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
     return set_error(DDVR_INVALID_INPUT, "d_dt is NULL but the stepsize target is set");
   const int64_t ws_cells = ws_cells_bytes(vol, mask), ws_tf = ws_tf_bytes(tf, mask);
   const int64_t ws_need = ws_cells + ws_tf;
+  const dim3 grid = grid_of(G, n_views);
+  const int64_t ws_det = (flags & DDVR_FLAG_DETERMINISTIC)
+                             ? det_bytes((int64_t)grid.x * grid.y * grid.z, mask) : 0;
+  const int64_t det_off = (ws_need + 255) & ~(int64_t)255;
   if (ws_need > 0 && (!workspace || workspace_bytes < ws_need))
     return set_error(DDVR_INVALID_INPUT,
                      "this target mask needs a %lld-byte workspace "
                      "(ddvr_adjoint_workspace_bytes)", (long long)ws_need);
+  if (ws_det > 0 && (!workspace || workspace_bytes < det_off + ws_det))
+    return set_error(DDVR_INVALID_INPUT,
+                     "the deterministic mode needs a %lld-byte workspace "
+                     "(ddvr_adjoint_workspace_bytes rounded up to 256 + ddvr_deterministic_bytes)",
+                     (long long)(det_off + ws_det));
   if (workspace && ((uintptr_t)workspace & 31) != 0)
     return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const dim3 grid = grid_of(G, n_views);
   const size_t smem = tbl;
   const bool cells = V.cells != nullptr;
+  if (ws_det > 0) {   // every call reduces its own partials (also under WS_DEFER)
+    G.partials = reinterpret_cast<double*>(static_cast<char*>(workspace) + det_off);
+    cudaError_t e = cudaMemsetAsync(G.partials, 0, (size_t)ws_det, st);
+    if (e != cudaSuccess)
+      return set_error(DDVR_CUDA_ERROR, "partials memset: %s", cudaGetErrorString(e));
+  }
   float* d_cells_all = ws_cells > 0 ? static_cast<float*>(workspace) : nullptr;
   // the kernel indexes cell gradients relative to cell (0,0,0), like V.cell0
   float* d_cells = d_cells_all ? d_cells_all + (V.cell0 - V.cells) : nullptr;
@@ -708,6 +770,14 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                                d_volume, d_cells, d_camera, d_dt, fu);
   if ((rc = check_launch(fu ? "dvr_adjoint_kernel (fused)" : "dvr_adjoint_kernel"))) return rc;
   g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
+  if (ws_det > 0) {
+    const int tiles = (int)(grid.x * grid.y);
+    const int cam_blocks = (mask & DDVR_TARGET_CAMERA) ? n_views : 0;
+    const int blocks = cam_blocks + ((mask & DDVR_TARGET_STEPSIZE) ? 1 : 0);
+    partials_reduce_kernel<<<blocks, 256, 0, st>>>(G.partials, tiles, n_views, cam_blocks,
+                                                   d_camera, d_dt);
+    if ((rc = check_launch("partials_reduce_kernel"))) return rc;
+  }
   if (flags & DDVR_FLAG_WS_DEFER) return DDVR_OK;   // a later call of this step folds
   if (ws_tf > 0) {
     const int nout = T.count * T.stride;

@@ -113,6 +113,8 @@ struct Geometry {
   float dt32;             // (float)dt: the stepsize of the fp32 march
   float* tape;            // stored memory mode (nullable)
   long long tape_stride;
+  double* partials;       // DDVR_FLAG_DETERMINISTIC: per-CTA camera / stepsize sums
+                          // (3 doubles per CTA) instead of fp64 atomics (nullable)
 };
 
 // Launchers with external linkage: each is defined (with its kernel
@@ -1544,8 +1546,14 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     if (threadIdx.x == 0) {
       double t0 = 0, t1 = 0, t2 = 0;
       for (int k = 0; k < kWarps; ++k) { t0 += s_red[k][0]; t1 += s_red[k][1]; t2 += s_red[k][2]; }
-      if (kCam) { atomicAdd(d_camera + 2 * view, t0); atomicAdd(d_camera + 2 * view + 1, t1); }
-      if (kStep) atomicAdd(d_dt, t2);
+      if (G.partials) {   // deterministic mode: reduced in CTA order afterwards
+        double* q = G.partials + 3 * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
+                                                                (size_t)blockIdx.z));
+        q[0] = t0; q[1] = t1; q[2] = t2;
+      } else {
+        if (kCam) { atomicAdd(d_camera + 2 * view, t0); atomicAdd(d_camera + 2 * view + 1, t1); }
+        if (kStep) atomicAdd(d_dt, t2);
+      }
     }
   }
 }

@@ -18,6 +18,7 @@ runs with ``gloo`` on CPU tensors in the tests and ``nccl`` on the GPUs.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -83,11 +84,14 @@ class ShardedStep:
     registers), which would hold the fused forward phase to 2 CTAs/SM where
     the separate forward runs 5 (C3: 58 vs 65 G samples/s).  ``keep_images``: also write the rendered
     images / optical depth of the fused step into ``img`` / ``depth``.
+    ``deterministic``: camera / stepsize gradients reduced from per-CTA partials in a
+    fixed order (DDVR_FLAG_DETERMINISTIC), bitwise reproducible step to step.
     """
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
-                 group=None, layout="cells", fused="auto", keep_images=False, chunks=4):
+                 group=None, layout="cells", fused="auto", keep_images=False, chunks=4,
+                 deterministic=False):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
@@ -110,7 +114,12 @@ class ShardedStep:
         # cell records (rebuilt from the density every step) + adjoint workspace
         self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
                       if layout == "cells" else None)
-        self.workspace = R.workspace_for(density, self.mask, self.cells, texels)
+        self.deterministic = bool(deterministic)
+        extra = 0
+        if self.deterministic:
+            _, _, prm = R._descs(density, texels, rig, dt, False, self.cells)
+            extra = int(N.lib().ddvr_deterministic_bytes(V, ctypes.byref(prm), self.mask))
+        self.workspace = R.workspace_for(density, self.mask, self.cells, texels, extra)
         self._copy_stream = None
         if fused == "auto":
             fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
@@ -181,13 +190,16 @@ class ShardedStep:
                     image_out=self.img[sl] if self.keep_images else None,
                     depth_out=self.depth[sl] if self.keep_images else None,
                     ws_continue=k > 0 and self.workspace is not None,
-                    ws_defer=not last and self.workspace is not None)
+                    ws_defer=not last and self.workspace is not None,
+                    deterministic=self.deterministic)
             hook("post_adjoint")
         elif V:
             if self.cells is not None:
                 R.pack_cells(self.density, self.cells)
             vol, tf, prm = R._descs(self.density, self.texels, self.rig, self.dt, False,
                                     self.cells)
+            if self.deterministic:
+                prm.flags |= N.FLAG_DETERMINISTIC
             lib = N.lib()
             st = R._stream_ptr()
             N.check(lib.ddvr_forward(ctypes.byref(vol), ctypes.byref(tf), self.cams.data_ptr(), V,

@@ -236,16 +236,19 @@ def adjoint_color(color, cams, dt: float, rig: Rig, image, depth, seed, d_color,
         _stream_ptr()))
 
 
-def workspace_for(density, mask: int, cells=None, texels=None):
+def workspace_for(density, mask: int, cells=None, texels=None, extra: int = 0):
     """Device workspace ddvr_adjoint needs for this layout, TF and mask (or None):
     cell-gradient records (volume target, cell layout) + TF-gradient slots
-    (tf target; needs ``texels`` for the TF shape)."""
+    (tf target; needs ``texels`` for the TF shape), + ``extra`` bytes after the
+    256-aligned end (the deterministic mode's partials, ddvr_deterministic_bytes)."""
     if mask & N.TARGET_TF and texels is None:
         raise InvalidParameterError("the tf target's workspace depends on the TF: pass texels")
     if texels is None:
         texels = torch.zeros(1, 4, dtype=torch.float32, device=density.device)
     vol, tf, _ = _descs(density, texels, Rig(1, 1), 1.0, False, cells)
     need = int(N.lib().ddvr_adjoint_workspace_bytes(ctypes.byref(vol), ctypes.byref(tf), mask))
+    if extra:
+        need = ((need + 255) & ~255) + int(extra)
     if need == 0:
         return None
     return torch.empty((need + 3) // 4, dtype=torch.float32, device=density.device)
@@ -254,12 +257,14 @@ def workspace_for(density, mask: int, cells=None, texels=None):
 def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: float, mask: int,
                        *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
                        workspace=None, image_out=None, depth_out=None, ws_continue=False,
-                       ws_defer=False):
+                       ws_defer=False, deterministic=False):
     """One fused step over these views: forward march, L1 seed sign(image - ref)/count
     and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
     device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
     One step split over several calls (view chunks) shares ``workspace``: every
-    call but the first passes ws_continue, every call but the last ws_defer."""
+    call but the first passes ws_continue, every call but the last ws_defer.
+    ``deterministic``: bitwise reproducible d_camera / d_dt (DDVR_FLAG_DETERMINISTIC);
+    a caller-provided workspace then needs the extra partials bytes too."""
     _require(cams, "cameras", torch.float64, ndim=2)
     if cells is None:
         raise InvalidParameterError("the fused step needs cell records (pack_cells)")
@@ -276,11 +281,14 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
                            (depth_out, "depth_out", torch.float32)):
         if buf is not None:
             _require(buf, name, dt_)
+    extra = int(N.lib().ddvr_deterministic_bytes(V, ctypes.byref(prm), mask)) \
+        if deterministic else 0
     if workspace is None:
         if ws_continue or ws_defer:
             raise InvalidParameterError("a step split over calls needs a shared workspace")
-        workspace = workspace_for(density, mask, cells, texels)
-    prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0)
+        workspace = workspace_for(density, mask, cells, texels, extra)
+    prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0) \
+        | (N.FLAG_DETERMINISTIC if deterministic else 0)
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_forward_adjoint_l1(
@@ -292,8 +300,10 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
 
 def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask: int, *,
             d_volume=None, d_tf=None, d_camera=None, d_dt=None, cells=None, workspace=None,
-            tape=None, tape_stride=0):
-    """Accumulate gradients of sum(seed * image) into the given buffers (+=)."""
+            tape=None, tape_stride=0, deterministic=False):
+    """Accumulate gradients of sum(seed * image) into the given buffers (+=).
+    ``deterministic``: d_camera / d_dt from per-CTA partials reduced in a fixed
+    order (bitwise reproducible; DDVR_FLAG_DETERMINISTIC)."""
     _require(cams, "cameras", torch.float64, ndim=2)
     vol, tf, prm = _descs(density, texels, rig, dt, False, cells)
     _set_tape(prm, tape, tape_stride)
@@ -312,8 +322,12 @@ def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask
                            (d_camera, "d_camera", torch.float64), (d_dt, "d_dt", torch.float64)):
         if buf is not None:
             _require(buf, name, dt_)
+    extra = int(N.lib().ddvr_deterministic_bytes(V, ctypes.byref(prm), mask)) \
+        if deterministic else 0
+    if deterministic:
+        prm.flags |= N.FLAG_DETERMINISTIC
     if workspace is None:
-        workspace = workspace_for(density, mask, cells, texels)
+        workspace = workspace_for(density, mask, cells, texels, extra)
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), cams.data_ptr(), V,

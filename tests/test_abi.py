@@ -33,7 +33,7 @@ def lib():
 def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
-                            "ddvr_adjoint_workspace_bytes",
+                            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes",
                             "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
                             "ddvr_forward_color", "ddvr_adjoint_color",
                             "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
@@ -221,3 +221,24 @@ def test_field_entry_points_validate_before_launch(lib):
     assert lib.ddvr_project(None, 4, None, None) == 1
     a = N.DdvrAdam(0.0, 0.0, 0.0, 0.0, 0, 1, 0.0, 1.0, 0.0, 1.0)
     assert lib.ddvr_project(None, 4, ctypes.byref(a), None) == 2
+
+
+def test_deterministic_mode_workspace(lib):
+    """DDVR_FLAG_DETERMINISTIC: per-CTA camera / stepsize partials (3 doubles per
+    16x16-pixel CTA) after the 256-aligned workspace; refused if it does not fit."""
+    from paper_2107_12672_b200 import _native as N
+    vol, tf, prm = _descs(W=512, H=512)
+    det = lambda v, m: lib.ddvr_deterministic_bytes(v, ctypes.byref(prm), m)  # noqa: E731
+    assert det(64, 1) == 32 * 32 * 64 * 24 and det(64, 2) == det(64, 3) == det(64, 1)
+    assert det(64, 8) == 0 and det(64, 4) == 0
+    prm.row0, prm.row1 = 100, 117                            # a 17-row band: 2 tile rows
+    assert det(1, 1) == (32 * 2 * 24 + 255) // 256 * 256
+    vol, tf, prm = _descs()
+    prm.flags = N.FLAG_DETERMINISTIC
+    rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, 16, 1, None, None, 16, None, None, 0, None)
+    assert rc == 2 and "deterministic" in lib.ddvr_last_error().decode()
+    prm.flags = 8
+    rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, 16, 1, None, None, 16, None, None, 0, None)
+    assert rc == 1 and "flags" in lib.ddvr_last_error().decode()
