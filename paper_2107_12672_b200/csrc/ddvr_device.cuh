@@ -988,7 +988,7 @@ constexpr int adj_min_blocks(unsigned mask, int role, bool cells) {
   return !cells ? 2   // voxel layout: 8 scalar gathers per sample, more live state
          : (role == 1 && mask == DDVR_TARGET_VOLUME) ? DDVR_ABS_MINB
          : mask == DDVR_TARGET_VOLUME ? 4
-         : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? 1 : 3;
+         : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? 2 : 3;
 }
 #ifdef DDVR_ADJ_MINB
 #define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, DDVR_ADJ_MINB)

@@ -9,13 +9,16 @@ cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
        "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-Iinclude", "-Ipaper_2107_12672_b200/csrc", *extra,
        "-c", "-o", "/tmp/regs.o", src]
 err = subprocess.run(cmd, capture_output=True, text=True).stderr
-fn = None
+fn, spill = None, ""
 for line in err.splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
         fn = subprocess.run(["c++filt"], input=m.group(1), capture_output=True, text=True).stdout.strip()
+        spill = ""
+    # ptxas prints a function's stack / spill line before its register count
+    m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
+    if m and (m.group(1) != "0" or m.group(2) != "0"):
+        spill = f"  [spill st {m.group(1)} ld {m.group(2)}]"
     m = re.search(r"Used (\d+) registers", line)
     if m and fn:
-        print(f"{m.group(1):>4} regs  {fn[:110]}")
-    if "spill" in line and not line.strip().endswith("0 bytes spill stores, 0 bytes spill loads"):
-        print("     ", line.strip())
+        print(f"{m.group(1):>4} regs  {fn[:100]}{spill}")
