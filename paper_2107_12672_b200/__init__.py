@@ -39,8 +39,11 @@ from .voldiff_api import (
     fibonacci_views,
     gd_step,
     l1_loss,
+    make_absorption_ramp_tf,
+    make_phantom,
     opacity_entropy,
     opacity_from_density,
+    preset_tf,
     project_params,
     render,
     render_adjoint,
@@ -85,5 +88,5 @@ __all__ = [
     "trilinear_sample", "trilinear_gradients", "tf_sample", "tf_gradients",
     "opacity_from_density", "camera_from_sphere", "camera_gradients",
     "smoothness_prior_tf", "smoothness_prior_volume", "OptimState", "gd_step", "adam_step",
-    "project_params", "upsample_volume",
+    "project_params", "upsample_volume", "make_phantom", "make_absorption_ramp_tf", "preset_tf",
 ]

@@ -782,3 +782,28 @@ def upsample_volume(volume):
     up = P.upsample_volume(torch.from_numpy(np.ascontiguousarray(vals, np.float32)).to(_device()))
     return DensityVolume(up.to(torch.float64).cpu().numpy(), np.array(volume.box_min, np.float64),
                          np.array(volume.box_max, np.float64))
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs of the benchmarks under the reference's names
+# ---------------------------------------------------------------------------
+
+
+def make_phantom(kind: str, dims, seed: int = 0, box_min=(-0.5, -0.5, -0.5),
+                 box_max=(0.5, 0.5, 0.5)) -> DensityVolume:
+    """Stock phantom as a DensityVolume (phantoms.py:26-72); host NumPy, input data only."""
+    from .scenes import phantom
+    return DensityVolume(phantom(kind, dims, seed, box_min, box_max), np.asarray(box_min),
+                         np.asarray(box_max))
+
+
+def make_absorption_ramp_tf(resolution: int = 64, tau_scale: float = 3.0) -> TransferFunction:
+    """Emission-free TF with absorption linear in density (tasks.py:348-356)."""
+    from .scenes import absorption_ramp_texels
+    return TransferFunction(absorption_ramp_texels(resolution, tau_scale))
+
+
+def preset_tf(name: str, resolution: int = 16, tau_scale: float = 4.0) -> TransferFunction:
+    """Stock transfer functions grayscale / warm / gaussian (tasks.py:359-388)."""
+    from .scenes import preset_texels
+    return TransferFunction(preset_texels(name, resolution, tau_scale))
