@@ -81,7 +81,8 @@ GRAD_BAR = {"R2048": 3.5e-4}
 
 
 @pytest.mark.parametrize("case", ["inside_box", "tiny_dt", "big_dt", "R2048", "R2048s",
-                                  "row_band", "one_pixel"])
+                                  "row_band", "one_pixel", "flat_volume", "single_voxel",
+                                  "axis_aligned", "R1"])
 def test_edge_cases_match_oracle(cuda, case):
     torch = _t()
     from oracle import dvr_oracle as O
@@ -90,6 +91,16 @@ def test_edge_cases_match_oracle(cuda, case):
     vol = rng.uniform(0.05, 0.95, (8, 8, 8)).astype(np.float32)
     tex = rng.uniform(0.05, 1.0, (8, 4)).astype(np.float32)
     radius, W, H, dt, rows = 2.2, 9, 7, 0.04, None
+    lon, lat = 33.0, 21.0
+    if case == "flat_volume":     # a size-1 axis: every cell clamps to one voxel layer
+        vol = rng.uniform(0.05, 0.95, (1, 6, 5)).astype(np.float32)
+    elif case == "single_voxel":  # 1x1x1: a constant field inside the box
+        vol = np.full((1, 1, 1), 0.6, np.float32)
+    elif case == "axis_aligned":  # w parallel to two slab pairs (renderer.py:194-197)
+        lon, lat = 0.0, 0.0
+        W = H = 1
+    elif case == "R1":            # one texel: both lookup indices 0, zero slope
+        tex = rng.uniform(0.05, 1.0, (1, 4)).astype(np.float32)
     if case == "inside_box":      # clamped rays: the eye is inside the volume (renderer.py:201)
         radius = 0.3
     elif case == "tiny_dt":       # ~2.6k samples per ray: inversion drift, fixed-point positions
@@ -106,7 +117,7 @@ def test_edge_cases_match_oracle(cuda, case):
         rows = (3, 6)
     elif case == "one_pixel":
         W = H = 1
-    view = O.View(33.0, 21.0, radius, fov_y_deg=35.0, width=W, height=H)
+    view = O.View(lon, lat, radius, fov_y_deg=35.0, width=W, height=H)
     r0, r1 = rows if rows else (0, H)
     seed = rng.normal(size=(r1 - r0, W, 4)).astype(np.float32)
     (img_o,), (out,) = _oracle(vol, tex, [view], dt, [seed.astype(np.float64)],
@@ -114,7 +125,7 @@ def test_edge_cases_match_oracle(cuda, case):
         _band_oracle(vol, tex, view, dt, seed, rows)
     dens = torch.from_numpy(vol).to(cuda)
     tx = torch.from_numpy(tex).to(cuda)
-    cams = R.camera_array(torch.tensor([[33.0, 21.0]], dtype=torch.float64, device=cuda), radius,
+    cams = R.camera_array(torch.tensor([[lon, lat]], dtype=torch.float64, device=cuda), radius,
                           (0.0, 0.0, 0.0), 35.0)
     rig = R.Rig(W, H, rows=rows)
     for cells in (R.pack_cells(dens), None):
