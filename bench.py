@@ -62,6 +62,9 @@ def parse():
                    help="replay each timed iteration from a captured CUDA graph (1 GPU)")
     p.add_argument("--unfused", action="store_true",
                    help="separate forward / L1 / adjoint launches instead of the fused step")
+    p.add_argument("--no-band-tape", action="store_true",
+                   help="fused absorption step without the 1-bit-per-sample band tape "
+                        "(DDVR_FLAG_BAND_TAPE; the walk then re-gathers the cell records)")
     return p.parse_args()
 
 
@@ -278,7 +281,8 @@ def run_own(args, cfg):
     total_elems = 4 * cfg.image * cfg.image * len(poses)
     step = ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                        total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
-                       layout=args.layout, fused=False if args.unfused else "auto")
+                       layout=args.layout, fused=False if args.unfused else "auto",
+                       band_tape=False if args.no_band_tape else "auto")
     # density targets run the whole optimisation iteration (prior + Adam + projection)
     graphed = args.graph and world == 1 and "volume" in cfg.targets
     runner = (TomographyIteration(step, lr=0.02, lam=0.5, graph=graphed)
@@ -477,14 +481,20 @@ def run_own(args, cfg):
             gr = {"probe": "ddvr_gather_probe: the same rays, fixed-point stepping and held "
                            "256-bit record gathers, one FADD per sample (6 CTAs/SM)",
                   "samples_per_s": probe_rate * world, "probe_ms": probe_ms}
-            if fused:   # the fused kernel gathers along every ray twice (forward + walk)
-                gr["fused_frac"] = 2 * local_samples / adj_s / probe_rate
+            if fused:
+                # the fused kernel gathers along every ray twice (forward + walk), or
+                # once with the band tape (the walk reads 1 bit per sample instead)
+                passes = 1 if getattr(step, "band_tape", False) else 2
+                gr["record_gather_passes"] = passes
+                gr["fused_frac"] = passes * local_samples / adj_s / probe_rate
             else:
                 gr["forward_frac"] = local_samples / fwd_s / probe_rate
                 gr["adjoint_frac"] = local_samples / adj_s / probe_rate
             line["gather_roofline"] = gr
         line["config"]["step"] = (("fused forward+L1+adjoint" if getattr(step, "fused", False)
                                    else "forward, L1, adjoint") +
+                                  (", band tape (1 bit/sample, DDVR_FLAG_BAND_TAPE)"
+                                   if getattr(step, "band_tape", False) else "") +
                                   (", CUDA-graph replay" if graphed else ""))
         if world == 1 and not args.no_cpu_baseline:
             sps, rps, cores, desc = cpu_sample(cfg, args.cpu_seconds)

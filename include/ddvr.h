@@ -104,6 +104,7 @@ typedef struct {
 #define DDVR_FLAG_WS_CONTINUE 1
 #define DDVR_FLAG_WS_DEFER 2
 #define DDVR_FLAG_DETERMINISTIC 4
+#define DDVR_FLAG_BAND_TAPE 8
 
 /* march parameters (RenderConfig, renderer.py:84-106) */
 typedef struct {
@@ -124,7 +125,15 @@ typedef struct {
                                                    sums per CTA into the workspace,
                                                    reduced in a fixed order: d_camera
                                                    and d_dt bitwise reproducible
-                                                   (ddvr_deterministic_bytes) */
+                                                   (ddvr_deterministic_bytes)
+                            DDVR_FLAG_BAND_TAPE    (ddvr_forward_adjoint_l1, volume
+                                                   target) the march records 1 bit
+                                                   per sample -- whether the
+                                                   absorption walk's d_hat is nonzero
+                                                   -- and the walk reads it instead of
+                                                   re-gathering the cell records
+                                                   (ddvr_band_tape_bytes); identical
+                                                   gradients, O(samples / 32) words */
   float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
                             forward writes the transmittance before every sample,
                             tape[ray * tape_stride + i]; the adjoint then reads it
@@ -208,6 +217,14 @@ int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf,
  * from per-CTA slots in slot order; d_volume and the in-CTA TF sums use fp32
  * atomics: reproducible to fp32 rounding, not bitwise.) */
 int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask);
+
+/* Extra workspace of a DDVR_FLAG_BAND_TAPE ddvr_forward_adjoint_l1 call: one
+ * bit per sample for every ray, 32-bit words per ray bounded by the box
+ * diagonal / dt.  Placed after the workspace (and the deterministic partials),
+ * each part rounded up to 256 bytes.  Used by the affine absorption walk
+ * (emission-free TF with a non-negative affine tau column, volume target);
+ * other steps ignore it. */
+int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:
  * (X+1) * (Y+1) * (Z+1) records of 8 floats -- cells -1 .. dim-1 on every

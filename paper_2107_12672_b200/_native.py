@@ -31,12 +31,13 @@ TARGET_BITS = {"camera": TARGET_CAMERA, "stepsize": TARGET_STEPSIZE, "tf": TARGE
 FLAG_WS_CONTINUE = 1   # ddvr_params.flags (include/ddvr.h)
 FLAG_WS_DEFER = 2
 FLAG_DETERMINISTIC = 4
+FLAG_BAND_TAPE = 8
 TF_TEXTURE = 0
 TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
 EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
-            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
+            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes", "ddvr_band_tape_bytes", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
             "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
             "ddvr_ray_setup",
             "ddvr_prior_volume",
@@ -111,6 +112,8 @@ def _bind(lib):
     lib.ddvr_adjoint_workspace_bytes.restype = ctypes.c_int64
     lib.ddvr_deterministic_bytes.argtypes = [ctypes.c_int32, P(DdvrParams), ctypes.c_uint32]
     lib.ddvr_deterministic_bytes.restype = ctypes.c_int64
+    lib.ddvr_band_tape_bytes.argtypes = [P(DdvrVolume), ctypes.c_int32, P(DdvrParams)]
+    lib.ddvr_band_tape_bytes.restype = ctypes.c_int64
     lib.ddvr_cells_bytes.argtypes = [P(ctypes.c_int32)]
     lib.ddvr_cells_bytes.restype = ctypes.c_int64
     lib.ddvr_pack_cells.argtypes = [P(DdvrVolume), vp, vp]

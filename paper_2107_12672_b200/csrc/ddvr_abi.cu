@@ -322,6 +322,8 @@ int make_geo(const ddvr_camera* cams, int n_views, const ddvr_params* p, Geometr
   G.tape = p->tape;
   G.tape_stride = p->tape_stride;
   G.partials = nullptr;
+  G.bits = nullptr;
+  G.bits_words = 0;
   if (G.tape && G.tape_stride < 0)
     return set_error(DDVR_INVALID_PARAMETER, "negative tape stride");
   return DDVR_OK;
@@ -674,6 +676,28 @@ static int64_t det_bytes(int64_t ctas, uint32_t mask) {
   return (ctas * 3 * 8 + 255) & ~(int64_t)255;
 }
 
+// DDVR_FLAG_BAND_TAPE: 32-bit words per ray, from an upper bound of any ray's
+// step count: n = ceil(chord / dt - 1e-9) <= diag / dt + 1 (renderer.py:209-214)
+static int band_words(const double bmin[3], const double bmax[3], double dt) {
+  double d2 = 0.0;
+  for (int a = 0; a < 3; ++a) d2 += (bmax[a] - bmin[a]) * (bmax[a] - bmin[a]);
+  const double nmax = std::floor(std::sqrt(d2) / dt) + 3.0;
+  return (int)std::min<double>((nmax + 31.0) / 32.0, 1 << 26);
+}
+
+static int64_t grid_ctas(int32_t n_views, const ddvr_params* p) {
+  const int row1 = p->row1 <= 0 ? p->height : p->row1;
+  const int rows = std::max(0, row1 - p->row0);
+  return (int64_t)((p->width + kTile - 1) / kTile) * ((rows + kTile - 1) / kTile) * n_views;
+}
+
+int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p) {
+  if (!vol || !p || n_views < 0 || p->width < 1 || p->height < 1 || !(p->dt > 0.0)) return 0;
+  const int64_t b = grid_ctas(n_views, p) * kThreads * band_words(vol->box_min, vol->box_max,
+                                                                  p->dt) * 4;
+  return (b + 255) & ~(int64_t)255;
+}
+
 int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask) {
   if (!p || n_views < 0 || p->width < 1 || p->height < 1) return 0;
   const int row1 = p->row1 <= 0 ? p->height : p->row1;
@@ -713,7 +737,8 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                        int64_t workspace_bytes, void* stream, const FusedArgs* fu,
                        int32_t flags) {
   int rc;
-  if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER | DDVR_FLAG_DETERMINISTIC))
+  if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER | DDVR_FLAG_DETERMINISTIC |
+                DDVR_FLAG_BAND_TAPE))
     return set_error(DDVR_INVALID_PARAMETER, "unknown params.flags bits 0x%x", flags);
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
@@ -740,6 +765,20 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                      "the deterministic mode needs a %lld-byte workspace "
                      "(ddvr_adjoint_workspace_bytes rounded up to 256 + ddvr_deterministic_bytes)",
                      (long long)(det_off + ws_det));
+  // band tape: fused volume-only steps only (else the flag is ignored)
+  const bool band = (flags & DDVR_FLAG_BAND_TAPE) && fu && mask == DDVR_TARGET_VOLUME && V.cells;
+  const int64_t tape_off = det_off + ((ws_det + 255) & ~(int64_t)255);
+  const int64_t ws_band = band ? (int64_t)grid.x * grid.y * grid.z * kThreads *
+                                     band_words(V.bmin, V.bmax, G.dt) * 4 : 0;
+  if (ws_band > 0 && (!workspace || workspace_bytes < tape_off + ws_band))
+    return set_error(DDVR_INVALID_INPUT,
+                     "the band tape needs a %lld-byte workspace (ddvr_adjoint_workspace_bytes "
+                     "rounded up to 256 [+ ddvr_deterministic_bytes rounded up to 256] + "
+                     "ddvr_band_tape_bytes)", (long long)(tape_off + ws_band));
+  if (ws_band > 0) {
+    G.bits = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + tape_off);
+    G.bits_words = band_words(V.bmin, V.bmax, G.dt);
+  }
   if (workspace && ((uintptr_t)workspace & 31) != 0)
     return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;

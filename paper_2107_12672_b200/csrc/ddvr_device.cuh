@@ -115,6 +115,9 @@ struct Geometry {
   long long tape_stride;
   double* partials;       // DDVR_FLAG_DETERMINISTIC: per-CTA camera / stepsize sums
                           // (3 doubles per CTA) instead of fp64 atomics (nullable)
+  unsigned* bits;         // DDVR_FLAG_BAND_TAPE: the fused absorption step's band bits,
+                          // bits_words 32-bit words per ray, warp-interleaved (nullable)
+  int bits_words;
 };
 
 // Launchers with external linkage: each is defined (with its kernel
@@ -845,10 +848,11 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 // The march of one ray.  INSIDE: every lane of the warp has all_inside (the
 // per-sample inside test and clamps are compiled out); SEG: segment mode.
 template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT, int KIND,
-          bool AFF = false>
+          bool AFF = false, bool BITS = false>
 __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
-                                          double& depth, float aff_a = 0.f, float aff_b = 0.f) {
+                                          double& depth, float aff_a = 0.f, float aff_b = 0.f,
+                                          unsigned* __restrict__ bits = nullptr) {
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
   // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355).
   // S, the ray's optical depth (T = exp(-S)), is summed in fp64 for the adjoint.
@@ -861,6 +865,15 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // = -expm1(-S), S = sum of the segment optical depths min(dt tau, -ln EPS)
   // the march sums anyway (fp64) -- so only S is carried per sample.
   constexpr bool kAbs = !EMIT && !TAPE && !EARLY && KIND == kTfTexture && DDVR_ABS_WALK;
+  // BITS (band tape): one bit per sample = the clamped density d is in the band
+  // t = d R - 1/2 in [0, R-1).  That equals the affine absorption walk's d_hat
+  // test (adjoint_ray: inside the box and t on the raw density in the band --
+  // outside, or raw outside [0,1], d clamps to 0 or 1 and t leaves the band), so
+  // the walk takes it from the tape instead of re-gathering the record.  Word k
+  // of the ray (samples 32k..32k+31, sample 32k+31 at bit 0; a last partial word
+  // holds its samples in the low bits, the last one at bit 0) sits at bits[32 k]:
+  // lane-interleaved, one 128-byte store per warp and word.
+  unsigned word = 0u;
   // one compositing step on a located sample and its record
   auto density = [&](const Cell& c, const float* k) {
     return clamp_density(INSIDE || c.inside, interp(c, k).rho);
@@ -868,7 +881,13 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   auto shade = [&](float d, int i) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     if (kAbs && AFF) {   // affine tau column: no table lookup
-      const float x = __fmul_rn(dt32, fmaxf(tau_affine(TF, d, aff_a, aff_b), 0.f));
+      const float t = __fmaf_rn(d, TF.fR, -0.5f);
+      if (BITS) {   // band bit, pushed in at the LSB (the walk pops it from there)
+        word = (word << 1) | (t >= 0.f && t < TF.fR1 ? 1u : 0u);
+        if ((i & 31) == 31) { bits[(i >> 5) << 5] = word; word = 0u; }
+      }
+      const float tau = __fmaf_rn(aff_b, fminf(fmaxf(t, 0.f), TF.fR1), aff_a);   // tau_affine
+      const float x = __fmul_rn(dt32, fmaxf(tau, 0.f));
       S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
       return;
     }
@@ -925,6 +944,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       shade(density(c, v), i);
     }
   }
+  if (BITS && (r.n & 31)) bits[(r.n >> 5) << 5] = word;   // the partial last word
   if (kAbs) A = (float)(-expm1(-S));
   rgba = make_float4(c0, c1, c2, A);
   depth = S;
@@ -937,7 +957,8 @@ template <bool EARLY, bool CELLS, bool TAPE, bool ABS_ONLY>
 __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& TFA, float dt32,
                                                const Ray& r, float* __restrict__ tape,
                                                bool warp_inside, bool emit, int mode,
-                                               float4& rgba, double& S, const unsigned* info) {
+                                               float4& rgba, double& S, const unsigned* info,
+                                               unsigned* __restrict__ bits = nullptr) {
   // the affine-tau variant serves emission-free texel TFs without tape / early stop
   const bool aff = !EARLY && !TAPE && !emit && info[2] == 0u;
   const float aa = __uint_as_float(info[3]), ab = __uint_as_float(info[4]);
@@ -954,7 +975,16 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
   if (mode == kSegP3) DDVR_MARCH_AFF(kSegP3, INS); \
   else if (mode == kSegP7) DDVR_MARCH_AFF(kSegP7, INS); \
   else DDVR_MARCH_AFF(kSegGen, INS);
-  if ((ABS_ONLY || (TFA.kind == kTfTexture && !emit)) && aff && !EARLY && !TAPE) {
+#define DDVR_MARCH_BITS(SEG, INS)                                                          \
+  march_ray<EARLY, CELLS, TAPE, SEG, INS, false, kTfTexture, true, true>(V, TFA, dt32, r, tape, \
+                                                                          rgba, S, aa, ab, bits)
+  if (ABS_ONLY && CELLS && !EARLY && !TAPE && bits) {   // (the caller checked the band walk)
+    if (warp_inside) {
+      if (mode == kSegP3) DDVR_MARCH_BITS(kSegP3, true); else DDVR_MARCH_BITS(kSegP7, true);
+    } else {
+      if (mode == kSegP3) DDVR_MARCH_BITS(kSegP3, false); else DDVR_MARCH_BITS(kSegP7, false);
+    }
+  } else if ((ABS_ONLY || (TFA.kind == kTfTexture && !emit)) && aff && !EARLY && !TAPE) {
     if (warp_inside) { DDVR_MARCH_SEG_AFF(true) } else { DDVR_MARCH_SEG_AFF(false) }
   } else if (ABS_ONLY) {
     if (warp_inside) { DDVR_MARCH_SEG(true, false) } else { DDVR_MARCH_SEG(false, false) }
@@ -969,6 +999,7 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
   } else {
     if (emit) { DDVR_MARCH_SEG(false, true) } else { DDVR_MARCH_SEG(false, false) }
   }
+#undef DDVR_MARCH_BITS
 #undef DDVR_MARCH_SEG_AFF
 #undef DDVR_MARCH_AFF
 #undef DDVR_MARCH_SEG
@@ -1350,6 +1381,46 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   }
 }
 
+// The affine absorption walk (volume target) from the forward's band tape
+// (DDVR_FLAG_BAND_TAPE, march_ray<..., BITS>): the d_hat of sample i is abs_k
+// when bit i is set, else 0 -- the test adjoint_ray<..., AFF> evaluates on the
+// re-gathered record -- so the walk needs no record gathers at all: positions,
+// cell fractions, the cell-run moments and their flushes only.  Same moments,
+// same runs, same flush order as the gathering walk.
+template <bool INSIDE>
+__device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, float abs_k,
+                                              const unsigned* __restrict__ bits,
+                                              float* __restrict__ d_cells, AdjState& st) {
+  long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
+  long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
+  long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
+  const unsigned* wp = bits + (((r.n - 1) >> 5) << 5);   // the word of sample n-1
+  unsigned word = 0u;
+#pragma unroll 1
+  for (int i = r.n - 1; i >= 0; --i) {
+    if ((i & 31) == 31 || i == r.n - 1) { word = *wp; wp -= 32; }
+    Cell c;
+    locate<true>(V, gx, gy, gz, INSIDE || r.all_inside, c);
+    const float dh = (word & 1u) ? abs_k : 0.f;   // sample i's bit is the lowest left
+    word >>= 1;
+    const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
+    const bool fresh = c.cell != st.run_cell;
+    const bool flush = fresh && st.run_cell != kNoRun;
+    if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+    const float keep = fresh ? 0.f : 1.f;
+    st.acc8[0] = fmaf(st.acc8[0], keep, dh);
+    st.acc8[1] = fmaf(st.acc8[1], keep, px);
+    st.acc8[2] = fmaf(st.acc8[2], keep, py);
+    st.acc8[3] = fmaf(st.acc8[3], keep, dh * c.uz);
+    st.acc8[4] = fmaf(st.acc8[4], keep, pxy);
+    st.acc8[5] = fmaf(st.acc8[5], keep, px * c.uz);
+    st.acc8[6] = fmaf(st.acc8[6], keep, py * c.uz);
+    st.acc8[7] = fmaf(st.acc8[7], keep, pxy * c.uz);
+    st.run_cell = c.cell;
+    gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
+  }
+}
+
 // ROLE 0: every walk; ROLE 1: the absorption-only walk (emission-free texel
 // TF, no TF target, no tape, cell records), launched next to ROLE 0 by the
 // host for masks without the TF target.  The TF class is known only on the
@@ -1416,12 +1487,26 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     }
   }
   const bool warp_inside = CELLS && __all_sync(0xffffffffu, r.all_inside);
+  // affine, non-negative tau column (the ramp), polynomial segment modes, no
+  // stepsize target: the table-free walk
+  const bool aff_walk = DDVR_AFF_WALK && !(MASK & DDVR_TARGET_STEPSIZE) && s_info[2] == 0u &&
+                        mode != kSegGen && __uint_as_float(s_info[3]) >= 0.f &&
+                        __fmaf_rn(__uint_as_float(s_info[4]), TFA.fR1,
+                                  __uint_as_float(s_info[3])) >= 0.f;
+  // band tape (fused volume-only absorption step): this lane's word 0
+  constexpr bool kBitsKernel = FUSED && ROLE == 1 && CELLS && MASK == DDVR_TARGET_VOLUME;
+  unsigned* bits = nullptr;
+  if (kBitsKernel && G.bits && aff_walk)
+    bits = G.bits + ((size_t)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
+                                                         (size_t)blockIdx.z)) * kWarps +
+                     (threadIdx.x >> 5)) * 32 * (size_t)G.bits_words + (threadIdx.x & 31);
   if (FUSED) {   // forward march (renderer.py:306-357) + L1 seed (objectives.py:38-54)
     double loss_part = 0.0;
     if (valid) {
       float4 rgba;
       march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
-                                                     s_info[1] != 0u, mode, rgba, S, s_info);
+                                                     s_info[1] != 0u, mode, rgba, S, s_info,
+                                                     kBitsKernel ? bits : nullptr);
       const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[pix];
       const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
                   dw = rgba.w - ref.w;
@@ -1463,13 +1548,11 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 #define DDVR_WALK_SEG_AFF(INS)                  \
   if (mode == kSegP3) DDVR_WALK_AFF(kSegP3, INS); \
   else DDVR_WALK_AFF(kSegP7, INS);
-  // affine, non-negative tau column (the ramp), polynomial segment modes, no
-  // stepsize target: the table-free walk
-  const bool aff_walk = DDVR_AFF_WALK && !(MASK & DDVR_TARGET_STEPSIZE) && s_info[2] == 0u &&
-                        mode != kSegGen && __uint_as_float(s_info[3]) >= 0.f &&
-                        __fmaf_rn(__uint_as_float(s_info[4]), TFA.fR1,
-                                  __uint_as_float(s_info[3])) >= 0.f;
-  if (ROLE == 1 && aff_walk) {
+  if (kBitsKernel && bits) {
+    const float abs_k = sd.w * (float)exp(-S) * G.dt32 * TFA.fR * __uint_as_float(s_info[4]);
+    if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, d_cells, st);
+    else abs_bits_walk<false>(V, r, abs_k, bits, d_cells, st);
+  } else if (ROLE == 1 && aff_walk) {
     if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
   } else if (ROLE == 1) {
     if (warp_inside) { DDVR_WALK_SEG(true, false) } else { DDVR_WALK_SEG(false, false) }

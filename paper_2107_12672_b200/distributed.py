@@ -86,12 +86,16 @@ class ShardedStep:
     images / optical depth of the fused step into ``img`` / ``depth``.
     ``deterministic``: camera / stepsize gradients reduced from per-CTA partials in a
     fixed order (DDVR_FLAG_DETERMINISTIC), bitwise reproducible step to step.
+    ``band_tape`` (fused volume-only steps): the march stores one bit per sample
+    for the affine absorption walk, which then re-gathers no cell records
+    (DDVR_FLAG_BAND_TAPE; 4.7 GB at C4).  "auto" uses it when it fits
+    min(8 GiB, a quarter of the free device memory).
     """
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
                  group=None, layout="cells", fused="auto", keep_images=False, chunks=4,
-                 deterministic=False):
+                 deterministic=False, band_tape="auto"):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
@@ -115,15 +119,19 @@ class ShardedStep:
         self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
                       if layout == "cells" else None)
         self.deterministic = bool(deterministic)
-        extra = 0
-        if self.deterministic:
-            _, _, prm = R._descs(density, texels, rig, dt, False, self.cells)
-            extra = int(N.lib().ddvr_deterministic_bytes(V, ctypes.byref(prm), self.mask))
-        self.workspace = R.workspace_for(density, self.mask, self.cells, texels, extra)
-        self._copy_stream = None
         if fused == "auto":
             fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
         self.fused = bool(fused) and self.cells is not None
+        vol, _, prm = R._descs(density, texels, rig, dt, False, self.cells)
+        self.band_tape = bool(band_tape) and self.fused and self.mask == N.TARGET_VOLUME
+        if self.band_tape and band_tape == "auto":   # <= min(8 GiB, a quarter of free HBM)
+            need = int(N.lib().ddvr_band_tape_bytes(ctypes.byref(vol), V, ctypes.byref(prm)))
+            free = torch.cuda.mem_get_info(dev)[0] if dev.type == "cuda" else 0
+            self.band_tape = need <= min(8 << 30, free // 4)
+        extra = R.extra_workspace_bytes(vol, prm, V, self.mask, self.deterministic,
+                                        self.band_tape)
+        self.workspace = R.workspace_for(density, self.mask, self.cells, texels, extra)
+        self._copy_stream = None
         self.keep_images = keep_images
         # view chunks of the fused step when the refs come from the host: chunk k
         # waits only for its own refs, so the copy of the rest overlaps compute
@@ -191,7 +199,7 @@ class ShardedStep:
                     depth_out=self.depth[sl] if self.keep_images else None,
                     ws_continue=k > 0 and self.workspace is not None,
                     ws_defer=not last and self.workspace is not None,
-                    deterministic=self.deterministic)
+                    deterministic=self.deterministic, band_tape=self.band_tape)
             hook("post_adjoint")
         elif V:
             if self.cells is not None:

@@ -254,17 +254,33 @@ def workspace_for(density, mask: int, cells=None, texels=None, extra: int = 0):
     return torch.empty((need + 3) // 4, dtype=torch.float32, device=density.device)
 
 
+def extra_workspace_bytes(vol, prm, n_views: int, mask: int, deterministic=False,
+                          band_tape=False) -> int:
+    """Bytes after the 256-aligned adjoint workspace for the optional modes: the
+    deterministic partials, then (256-aligned) the band tape (include/ddvr.h)."""
+    lib = N.lib()
+    det = int(lib.ddvr_deterministic_bytes(n_views, ctypes.byref(prm), mask)) \
+        if deterministic else 0
+    band = int(lib.ddvr_band_tape_bytes(ctypes.byref(vol), n_views, ctypes.byref(prm))) \
+        if band_tape and mask == N.TARGET_VOLUME else 0
+    if not band:
+        return det
+    return ((det + 255) & ~255) + band
+
+
 def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: float, mask: int,
                        *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
                        workspace=None, image_out=None, depth_out=None, ws_continue=False,
-                       ws_defer=False, deterministic=False):
+                       ws_defer=False, deterministic=False, band_tape=False):
     """One fused step over these views: forward march, L1 seed sign(image - ref)/count
     and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
     device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
     One step split over several calls (view chunks) shares ``workspace``: every
     call but the first passes ws_continue, every call but the last ws_defer.
     ``deterministic``: bitwise reproducible d_camera / d_dt (DDVR_FLAG_DETERMINISTIC);
-    a caller-provided workspace then needs the extra partials bytes too."""
+    ``band_tape``: the march stores 1 bit per sample for the affine absorption walk,
+    which then gathers no records (DDVR_FLAG_BAND_TAPE, volume target).  A
+    caller-provided workspace needs those extra bytes too (extra_workspace_bytes)."""
     _require(cams, "cameras", torch.float64, ndim=2)
     if cells is None:
         raise InvalidParameterError("the fused step needs cell records (pack_cells)")
@@ -281,14 +297,13 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
                            (depth_out, "depth_out", torch.float32)):
         if buf is not None:
             _require(buf, name, dt_)
-    extra = int(N.lib().ddvr_deterministic_bytes(V, ctypes.byref(prm), mask)) \
-        if deterministic else 0
+    extra = extra_workspace_bytes(vol, prm, V, mask, deterministic, band_tape)
     if workspace is None:
         if ws_continue or ws_defer:
             raise InvalidParameterError("a step split over calls needs a shared workspace")
         workspace = workspace_for(density, mask, cells, texels, extra)
     prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0) \
-        | (N.FLAG_DETERMINISTIC if deterministic else 0)
+        | (N.FLAG_DETERMINISTIC if deterministic else 0) | (N.FLAG_BAND_TAPE if band_tape else 0)
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_forward_adjoint_l1(

@@ -33,7 +33,7 @@ def lib():
 def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
-                            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes",
+                            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes", "ddvr_band_tape_bytes",
                             "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
                             "ddvr_forward_color", "ddvr_adjoint_color",
                             "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
@@ -238,7 +238,7 @@ def test_deterministic_mode_workspace(lib):
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 2 and "deterministic" in lib.ddvr_last_error().decode()
-    prm.flags = 8
+    prm.flags = 16
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 1 and "flags" in lib.ddvr_last_error().decode()

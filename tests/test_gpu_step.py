@@ -178,3 +178,85 @@ def test_fused_step_row_band(cuda):
                            targets=("volume", "tf", "stepsize"), radius=2.3, fused=fused)
         bufs.append(step.run().buf.double().cpu().numpy())
     assert rel_l2(bufs[0], bufs[1]) <= 1e-5
+
+
+def _ramp_scene(cuda, n=24, views=6, W=32, H=30, texels=None):
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.scenes import absorption_ramp_texels, fibonacci_poses, phantom
+    truth = torch.from_numpy(phantom("sphere", n, seed=0).astype(np.float32)).to(cuda)
+    tex = torch.from_numpy((absorption_ramp_texels(64, 3.0) if texels is None else texels)
+                           .astype(np.float32)).to(cuda)
+    ll = torch.tensor(fibonacci_poses(views), dtype=torch.float64, device=cuda)
+    rig = R.Rig(W, H)
+    dt = 0.2 / n
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    refs, _ = R.forward(truth, tex, cams, dt, rig)
+    est = (0.8 * truth + 0.1).contiguous()
+    return est, tex, ll, refs, dt, rig
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_band_tape_step_equals_gathering_walk(cuda, chunks):
+    """DDVR_FLAG_BAND_TAPE: the absorption walk from the march's band bits gives the
+    gathering walk's gradient (same runs and moments; atomics order aside) and the
+    oracle's, also when the step is split into view chunks."""
+    import torch
+    from oracle import dvr_oracle as O
+    from paper_2107_12672_b200.distributed import ShardedStep
+    est, tex, ll, refs, dt, rig = _ramp_scene(cuda)
+    out = {}
+    for tape in (False, True):
+        step = ShardedStep(est, tex, ll, refs, dt, rig, band_tape=tape, chunks=chunks)
+        assert step.fused and step.band_tape == tape
+        f = step.run(refs_host=refs.cpu().pin_memory() if chunks > 1 else None)
+        out[tape] = (f.d_volume.double().cpu().numpy(), float(f.loss))
+    assert rel_l2(out[True][0], out[False][0]) <= 1e-6
+    assert abs(out[True][1] - out[False][1]) <= 1e-12 * abs(out[False][1])
+    grid = O.Grid(est.cpu().numpy().astype(np.float64))
+    t64 = tex.cpu().numpy().astype(np.float64)
+    count = refs.numel()
+    want = np.zeros(tuple(est.shape))
+    for k, (lon, lat) in enumerate(ll.cpu().numpy()):
+        v = O.View(lon, lat, 2.0, (0, 0, 0), 30.0, rig.width, rig.height)
+        img = O.render_view(grid, t64, v, dt)
+        seed = np.sign(img - refs[k].cpu().numpy().astype(np.float64)) / count
+        want += O.adjoint_view(grid, t64, v, dt, seed, ["volume"], image=img)["d_volume"]
+    assert rel_l2(out[True][0], want) <= 1e-4
+
+
+def test_band_tape_is_ignored_off_the_affine_walk(cuda):
+    """A non-affine emission-free TF takes the table walk: the tape flag changes
+    nothing (the kernel only uses it on the affine band walk)."""
+    from paper_2107_12672_b200.distributed import ShardedStep
+    rng = np.random.default_rng(2)
+    tex = np.zeros((16, 4))
+    tex[:, 3] = np.sort(rng.uniform(0.0, 4.0, 16))
+    est, tx, ll, refs, dt, rig = _ramp_scene(cuda, texels=tex)
+    g = [ShardedStep(est, tx, ll, refs, dt, rig, band_tape=t).run().d_volume.double().cpu()
+         .numpy() for t in (False, True)]
+    assert rel_l2(g[1], g[0]) <= 1e-6
+
+
+def test_band_tape_auto_and_workspace(cuda):
+    """"auto" turns the tape on when it fits; a too-small workspace is refused."""
+    import ctypes
+    import torch
+    from paper_2107_12672_b200 import _native as N
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    est, tex, ll, refs, dt, rig = _ramp_scene(cuda)
+    assert ShardedStep(est, tex, ll, refs, dt, rig).band_tape
+    assert not ShardedStep(est, tex, ll, refs, dt, rig, targets=("volume", "tf")).band_tape
+    cells = R.pack_cells(est)
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    ws = R.workspace_for(est, 8, cells, tex)           # no room for the tape
+    loss = torch.zeros(1, dtype=torch.float64, device=cuda)
+    from paper_2107_12672_b200.errors import InvalidInputError
+    with pytest.raises(InvalidInputError, match="band tape"):
+        R.forward_adjoint_l1(est, tex, cams, dt, rig, refs, float(refs.numel()), 8, cells=cells,
+                             loss=loss, d_volume=torch.zeros_like(est), workspace=ws,
+                             band_tape=True)
+    vol, _, prm = R._descs(est, tex, rig, dt, False, cells)
+    words = int(N.lib().ddvr_band_tape_bytes(ctypes.byref(vol), 6, ctypes.byref(prm)))
+    assert words > 0 and words % 256 == 0
