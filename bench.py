@@ -427,7 +427,8 @@ def run_own(args, cfg):
             adj_b += FWD_B_PER_SAMPLE
         adj_gbs = adj_bytes / adj_s / 1e9
         fwd_gbs = fwd_bytes / fwd_s / 1e9
-        traffic = ncu_traffic(cfg.name, "fused" if fused else "adjoint")
+        traffic = ncu_traffic(cfg.name, ("fused_tape" if getattr(step, "band_tape", False)
+                                         else "fused") if fused else "adjoint")
         kname = ("dvr_adjoint_kernel<FUSED> (forward + L1 seed + adjoint per ray)" if fused
                  else "dvr_adjoint_kernel")
         ray_b = ADJ_B_PER_RAY + (FWD_B_PER_RAY if fused else 0)
@@ -436,8 +437,8 @@ def run_own(args, cfg):
         if traffic:
             note += (f"; ncu measures {traffic / adj_bytes:.2f}x those bytes of DRAM traffic per "
                      "launch (L1/L2 reuse), so frac > 1 is reuse, not missing work; the "
-                     "limiters are gather latency and L1 wavefronts "
-                     "(profiles/r01_ncu_c4v8_poly.txt)")
+                     "limiters are instruction issue and L1 wavefronts (record gathers, "
+                     "cell-run vector reds): profiles/r01_ncu_c4_full_fused_tape.txt")
         if fused:
             kernels = {
                 "pack_cells": {"ms": fwd_s * 1e3},
