@@ -427,6 +427,9 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #ifndef DDVR_ABS_MINB
 #define DDVR_ABS_MINB 5
 #endif
+#ifndef DDVR_ABS_FUSED_MINB
+#define DDVR_ABS_FUSED_MINB 4
+#endif
 #ifndef DDVR_ABS_WALK
 #define DDVR_ABS_WALK 1
 #endif
@@ -1015,8 +1018,11 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
 // (4 CTAs/SM); the camera/stepsize walks carry fp64 sums (ptxas' choice).
 // The absorption-only kernel (ROLE 1) carries none of the emitting walk's
 // state and is compiled for 5 CTAs/SM.
-constexpr int adj_min_blocks(unsigned mask, int role, bool cells) {
+constexpr int adj_min_blocks(unsigned mask, int role, bool cells, bool fused) {
   return !cells ? 2   // voxel layout: 8 scalar gathers per sample, more live state
+         // the fused absorption step carries the band-tape word and pointer
+         // through the march: 64 registers (4 CTAs/SM) beat 48 with spills
+         : (role == 1 && mask == DDVR_TARGET_VOLUME && fused) ? DDVR_ABS_FUSED_MINB
          : (role == 1 && mask == DDVR_TARGET_VOLUME) ? DDVR_ABS_MINB
          : mask == DDVR_TARGET_VOLUME ? 4
          : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? 2 : 3;
@@ -1024,7 +1030,7 @@ constexpr int adj_min_blocks(unsigned mask, int role, bool cells) {
 #ifdef DDVR_ADJ_MINB
 #define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, DDVR_ADJ_MINB)
 #else
-#define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, adj_min_blocks(MASK, ROLE, CELLS))
+#define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, adj_min_blocks(MASK, ROLE, CELLS, FUSED))
 #endif
 template <bool EARLY, bool CELLS, bool TAPE>
 __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
