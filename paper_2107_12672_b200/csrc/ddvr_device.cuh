@@ -427,6 +427,9 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #ifndef DDVR_ABS_MINB
 #define DDVR_ABS_MINB 5
 #endif
+#ifndef DDVR_BITS_WALK_UNROLL
+#define DDVR_BITS_WALK_UNROLL 4
+#endif
 #ifndef DDVR_ABS_FUSED_MINB
 #define DDVR_ABS_FUSED_MINB 4
 #endif
@@ -1402,7 +1405,8 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
   long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
   const unsigned* wp = bits + (((r.n - 1) >> 5) << 5);   // the word of sample n-1
   unsigned word = 0u;
-#pragma unroll 1
+  constexpr int kUnroll = DDVR_BITS_WALK_UNROLL;   // (pragma arguments are not macro-expanded)
+#pragma unroll kUnroll
   for (int i = r.n - 1; i >= 0; --i) {
     if ((i & 31) == 31 || i == r.n - 1) { word = *wp; wp -= 32; }
     Cell c;
