@@ -427,6 +427,9 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #ifndef DDVR_ABS_MINB
 #define DDVR_ABS_MINB 5
 #endif
+#ifndef DDVR_BITS_MARCH_UNROLL
+#define DDVR_BITS_MARCH_UNROLL 4
+#endif
 #ifndef DDVR_BITS_WALK_UNROLL
 #define DDVR_BITS_WALK_UNROLL 4
 #endif
@@ -929,7 +932,8 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     ld256_if(r.n > 0, V.cell0 + 8 * (long long)c.cell, v);
     held = c.cell;
     // (the emitting variants spill at 48 registers when unrolled)
-#pragma unroll (kAbs ? 4 : 1)
+    constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : 1;
+#pragma unroll kMarchUnroll
     for (int i = 0; i < r.n; ++i) {
       if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
       const float d = density(c, v);
