@@ -770,6 +770,9 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   const int64_t tape_off = det_off + ((ws_det + 255) & ~(int64_t)255);
   const int64_t ws_band = band ? (int64_t)grid.x * grid.y * grid.z * kThreads *
                                      band_words(V.bmin, V.bmax, G.dt) * 4 : 0;
+  if (ws_band > (16ll << 30))
+    return set_error(DDVR_UNSUPPORTED, "band tape of %lld bytes exceeds 16 GiB (2^32 words): "
+                     "split the views into chunks", (long long)ws_band);
   if (ws_band > 0 && (!workspace || workspace_bytes < tape_off + ws_band))
     return set_error(DDVR_INVALID_INPUT,
                      "the band tape needs a %lld-byte workspace (ddvr_adjoint_workspace_bytes "

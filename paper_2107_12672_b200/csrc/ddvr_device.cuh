@@ -861,7 +861,8 @@ template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT, in
 __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
                                           double& depth, float aff_a = 0.f, float aff_b = 0.f,
-                                          unsigned* __restrict__ bits = nullptr) {
+                                          unsigned* __restrict__ bits = nullptr,
+                                          unsigned bits_off = 0u) {
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
   // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355).
   // S, the ray's optical depth (T = exp(-S)), is summed in fp64 for the adjoint.
@@ -893,7 +894,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       const float t = __fmaf_rn(d, TF.fR, -0.5f);
       if (BITS) {   // band bit, pushed in at the LSB (the walk pops it from there)
         word = (word << 1) | (t >= 0.f && t < TF.fR1 ? 1u : 0u);
-        if ((i & 31) == 31) { bits[(i >> 5) << 5] = word; word = 0u; }
+        if ((i & 31) == 31) { bits[bits_off + ((i >> 5) << 5)] = word; word = 0u; }
       }
       const float tau = __fmaf_rn(aff_b, fminf(fmaxf(t, 0.f), TF.fR1), aff_a);   // tau_affine
       const float x = __fmul_rn(dt32, fmaxf(tau, 0.f));
@@ -954,7 +955,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       shade(density(c, v), i);
     }
   }
-  if (BITS && (r.n & 31)) bits[(r.n >> 5) << 5] = word;   // the partial last word
+  if (BITS && (r.n & 31)) bits[bits_off + ((r.n >> 5) << 5)] = word;   // partial last word
   if (kAbs) A = (float)(-expm1(-S));
   rgba = make_float4(c0, c1, c2, A);
   depth = S;
@@ -968,7 +969,8 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
                                                const Ray& r, float* __restrict__ tape,
                                                bool warp_inside, bool emit, int mode,
                                                float4& rgba, double& S, const unsigned* info,
-                                               unsigned* __restrict__ bits = nullptr) {
+                                               unsigned* __restrict__ bits = nullptr,
+                                               unsigned bits_off = 0u) {
   // the affine-tau variant serves emission-free texel TFs without tape / early stop
   const bool aff = !EARLY && !TAPE && !emit && info[2] == 0u;
   const float aa = __uint_as_float(info[3]), ab = __uint_as_float(info[4]);
@@ -987,7 +989,8 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
   else DDVR_MARCH_AFF(kSegGen, INS);
 #define DDVR_MARCH_BITS(SEG, INS)                                                          \
   march_ray<EARLY, CELLS, TAPE, SEG, INS, false, kTfTexture, true, true>(V, TFA, dt32, r, tape, \
-                                                                          rgba, S, aa, ab, bits)
+                                                                          rgba, S, aa, ab, bits, \
+                                                                          bits_off)
   if (ABS_ONLY && CELLS && !EARLY && !TAPE && bits) {   // (the caller checked the band walk)
     if (warp_inside) {
       if (mode == kSegP3) DDVR_MARCH_BITS(kSegP3, true); else DDVR_MARCH_BITS(kSegP7, true);
@@ -1403,16 +1406,18 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
 template <bool INSIDE>
 __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, float abs_k,
                                               const unsigned* __restrict__ bits,
-                                              float* __restrict__ d_cells, AdjState& st) {
+                                              unsigned bits_off, float* __restrict__ d_cells,
+                                              AdjState& st) {
   long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
   long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
   long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
-  const unsigned* wp = bits + (((r.n - 1) >> 5) << 5);   // the word of sample n-1
+  // (a 32-bit word index from the uniform tape base: one register, not a pointer pair)
+  unsigned wi = bits_off + (((r.n - 1) >> 5) << 5);   // the word of sample n-1
   unsigned word = 0u;
   constexpr int kUnroll = DDVR_BITS_WALK_UNROLL;   // (pragma arguments are not macro-expanded)
 #pragma unroll kUnroll
   for (int i = r.n - 1; i >= 0; --i) {
-    if ((i & 31) == 31 || i == r.n - 1) { word = *wp; wp -= 32; }
+    if ((i & 31) == 31 || i == r.n - 1) { word = bits[wi]; wi -= 32; }
     Cell c;
     locate<true>(V, gx, gy, gz, INSIDE || r.all_inside, c);
     const float dh = (word & 1u) ? abs_k : 0.f;   // sample i's bit is the lowest left
@@ -1509,18 +1514,18 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
                                   __uint_as_float(s_info[3])) >= 0.f;
   // band tape (fused volume-only absorption step): this lane's word 0
   constexpr bool kBitsKernel = FUSED && ROLE == 1 && CELLS && MASK == DDVR_TARGET_VOLUME;
-  unsigned* bits = nullptr;
-  if (kBitsKernel && G.bits && aff_walk)
-    bits = G.bits + ((size_t)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
-                                                         (size_t)blockIdx.z)) * kWarps +
-                     (threadIdx.x >> 5)) * 32 * (size_t)G.bits_words + (threadIdx.x & 31);
+  // (the host keeps the tape under 2^32 words: 32-bit word indices)
+  unsigned* bits = kBitsKernel && G.bits && aff_walk ? G.bits : nullptr;
+  const unsigned bits_off =
+      ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * kWarps +
+       (threadIdx.x >> 5)) * 32u * (unsigned)G.bits_words + (threadIdx.x & 31);
   if (FUSED) {   // forward march (renderer.py:306-357) + L1 seed (objectives.py:38-54)
     double loss_part = 0.0;
     if (valid) {
       float4 rgba;
       march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
                                                      s_info[1] != 0u, mode, rgba, S, s_info,
-                                                     kBitsKernel ? bits : nullptr);
+                                                     kBitsKernel ? bits : nullptr, bits_off);
       const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[pix];
       const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
                   dw = rgba.w - ref.w;
@@ -1564,8 +1569,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   else DDVR_WALK_AFF(kSegP7, INS);
   if (kBitsKernel && bits) {
     const float abs_k = sd.w * (float)exp(-S) * G.dt32 * TFA.fR * __uint_as_float(s_info[4]);
-    if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, d_cells, st);
-    else abs_bits_walk<false>(V, r, abs_k, bits, d_cells, st);
+    if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, bits_off, d_cells, st);
+    else abs_bits_walk<false>(V, r, abs_k, bits, bits_off, d_cells, st);
   } else if (ROLE == 1 && aff_walk) {
     if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
   } else if (ROLE == 1) {
