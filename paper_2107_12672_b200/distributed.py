@@ -134,9 +134,15 @@ class ShardedStep:
         self._copy_stream = None
         self.keep_images = keep_images
         # view chunks of the fused step when the refs come from the host: chunk k
-        # waits only for its own refs, so the copy of the rest overlaps compute
+        # waits only for its own refs, so the copy of the rest overlaps compute.
+        # The first chunk is small (1/16 of the views) so the first kernel starts
+        # after a short copy; the rest split evenly.
         n = max(1, min(chunks, V))
-        edges = [round(k * V / n) for k in range(n + 1)]
+        if n > 1 and V >= 2 * n:
+            first = max(1, V // 16)
+            edges = [0] + [first + round(k * (V - first) / (n - 1)) for k in range(n)]
+        else:
+            edges = [round(k * V / n) for k in range(n + 1)]
         self._chunks = [slice(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
 
     def _stage_refs(self, refs_host, chunks):
