@@ -242,3 +242,26 @@ def test_deterministic_mode_workspace(lib):
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 1 and "flags" in lib.ddvr_last_error().decode()
+
+
+def test_band_tape_bytes_and_limits(lib):
+    """ddvr_band_tape_bytes: 32-bit words per ray from the box diagonal / dt, for every
+    pixel of every CTA; a fused call whose tape would pass 2^32 words is refused
+    before any CUDA work, and one without room for the tape asks for it."""
+    import math
+    from paper_2107_12672_b200 import _native as N
+    vol, tf, prm = _descs(dt=0.01, W=512, H=512)
+    words = math.ceil((math.floor(math.sqrt(3.0) / 0.01) + 3) / 32)
+    assert lib.ddvr_band_tape_bytes(ctypes.byref(vol), 64, ctypes.byref(prm)) == \
+        32 * 32 * 64 * 256 * words * 4
+    loss = ctypes.c_double(0)
+    vol.cells = 32
+    call = lambda v, p, nv, ws: lib.ddvr_forward_adjoint_l1(  # noqa: E731
+        ctypes.byref(v), ctypes.byref(tf), 16, nv, ctypes.byref(p), 16, 8.0, 8, None, None,
+        ctypes.addressof(loss), 16, None, None, None, 32, ws, None)
+    prm.flags = N.FLAG_BAND_TAPE
+    big_vol, _, big = _descs(dt=1e-3, W=4096, H=4096)
+    big_vol.cells = 32
+    big.flags = N.FLAG_BAND_TAPE
+    assert call(big_vol, big, 64, 1 << 40) == 3 and "16 GiB" in lib.ddvr_last_error().decode()
+    assert call(vol, prm, 1, 1 << 10) == 2 and "band tape" in lib.ddvr_last_error().decode()
