@@ -264,4 +264,4 @@ def test_band_tape_bytes_and_limits(lib):
     big_vol.cells = 32
     big.flags = N.FLAG_BAND_TAPE
     assert call(big_vol, big, 64, 1 << 40) == 3 and "16 GiB" in lib.ddvr_last_error().decode()
-    assert call(vol, prm, 1, 1 << 10) == 2 and "band tape" in lib.ddvr_last_error().decode()
+    assert call(vol, prm, 1, 1 << 16) == 2 and "band tape" in lib.ddvr_last_error().decode()
