@@ -1341,7 +1341,10 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         const float dh = live ? d_hat : 0.f;
         const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
         const bool fresh = c.cell != st.run_cell;
-        const bool flush = fresh && st.run_cell != kNoRun;
+        // (affine absorption walk: every d_hat of a ray is 0 or abs_k, so a run
+        // whose weight sum acc8[0] is 0 has all moments 0 -- no red)
+        const bool flush = fresh && st.run_cell != kNoRun &&
+                           (!(kAbs && AFF) || st.acc8[0] != 0.f);
         // (ptxas branches around a predicated red anyway: one branch for both
         // halves, and the record address is formed only inside it)
         if (flush) flush_cell<true>(d_volume, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
@@ -1424,7 +1427,8 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
     word >>= 1;
     const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
     const bool fresh = c.cell != st.run_cell;
-    const bool flush = fresh && st.run_cell != kNoRun;
+    // all d_hat of the ray share abs_k's sign: a zero weight sum = an empty run
+    const bool flush = fresh && st.run_cell != kNoRun && st.acc8[0] != 0.f;
     if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
     const float keep = fresh ? 0.f : 1.f;
     st.acc8[0] = fmaf(st.acc8[0], keep, dh);
