@@ -492,6 +492,11 @@ def run_own(args, cfg):
                 gr["forward_frac"] = local_samples / fwd_s / probe_rate
                 gr["adjoint_frac"] = local_samples / adj_s / probe_rate
             line["gather_roofline"] = gr
+        if runner is not step:
+            line["config"]["iterations"] = (
+                "one optimisation run: value times iterations W+1..W+K, e2e the next W+K; "
+                "the estimate changes every iteration (Adam + [0,1] projection), and as its "
+                "empty space grows the walk skips more empty cell runs")
         line["config"]["step"] = (("fused forward+L1+adjoint" if getattr(step, "fused", False)
                                    else "forward, L1, adjoint") +
                                   (", band tape (1 bit/sample, DDVR_FLAG_BAND_TAPE)"
