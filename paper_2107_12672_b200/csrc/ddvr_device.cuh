@@ -1411,36 +1411,42 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
                                               const unsigned* __restrict__ bits,
                                               unsigned bits_off, float* __restrict__ d_cells,
                                               AdjState& st) {
-  long long gx = r.g0[0] + (long long)(r.n - 1) * r.gs[0];
-  long long gy = r.g0[1] + (long long)(r.n - 1) * r.gs[1];
-  long long gz = r.g0[2] + (long long)(r.n - 1) * r.gs[2];
+  // Blocks of 32 samples (one tape word), back to front.  A block whose word is 0
+  // adds nothing and is skipped whole: the open cell run is kept, and the first
+  // sample of a later block in another cell flushes it -- the flush the
+  // per-sample walk does at the first cell change inside the skipped block.
   // (a 32-bit word index from the uniform tape base: one register, not a pointer pair)
-  unsigned wi = bits_off + (((r.n - 1) >> 5) << 5);   // the word of sample n-1
-  unsigned word = 0u;
   constexpr int kUnroll = DDVR_BITS_WALK_UNROLL;   // (pragma arguments are not macro-expanded)
+  for (int blk = (r.n - 1) >> 5; blk >= 0; --blk) {
+    unsigned word = bits[bits_off + ((unsigned)blk << 5)];
+    if (word == 0u) continue;
+    const int i1 = min(r.n - 1, (blk << 5) + 31);   // the block's last sample
+    long long gx = r.g0[0] + (long long)i1 * r.gs[0];
+    long long gy = r.g0[1] + (long long)i1 * r.gs[1];
+    long long gz = r.g0[2] + (long long)i1 * r.gs[2];
 #pragma unroll kUnroll
-  for (int i = r.n - 1; i >= 0; --i) {
-    if ((i & 31) == 31 || i == r.n - 1) { word = bits[wi]; wi -= 32; }
-    Cell c;
-    locate<true>(V, gx, gy, gz, INSIDE || r.all_inside, c);
-    const float dh = (word & 1u) ? abs_k : 0.f;   // sample i's bit is the lowest left
-    word >>= 1;
-    const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
-    const bool fresh = c.cell != st.run_cell;
-    // all d_hat of the ray share abs_k's sign: a zero weight sum = an empty run
-    const bool flush = fresh && st.run_cell != kNoRun && st.acc8[0] != 0.f;
-    if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
-    const float keep = fresh ? 0.f : 1.f;
-    st.acc8[0] = fmaf(st.acc8[0], keep, dh);
-    st.acc8[1] = fmaf(st.acc8[1], keep, px);
-    st.acc8[2] = fmaf(st.acc8[2], keep, py);
-    st.acc8[3] = fmaf(st.acc8[3], keep, dh * c.uz);
-    st.acc8[4] = fmaf(st.acc8[4], keep, pxy);
-    st.acc8[5] = fmaf(st.acc8[5], keep, px * c.uz);
-    st.acc8[6] = fmaf(st.acc8[6], keep, py * c.uz);
-    st.acc8[7] = fmaf(st.acc8[7], keep, pxy * c.uz);
-    st.run_cell = c.cell;
-    gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
+    for (int i = i1; i >= (blk << 5); --i) {
+      Cell c;
+      locate<true>(V, gx, gy, gz, INSIDE || r.all_inside, c);
+      const float dh = (word & 1u) ? abs_k : 0.f;   // sample i's bit is the lowest left
+      word >>= 1;
+      const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
+      const bool fresh = c.cell != st.run_cell;
+      // all d_hat of the ray share abs_k's sign: a zero weight sum = an empty run
+      const bool flush = fresh && st.run_cell != kNoRun && st.acc8[0] != 0.f;
+      if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+      const float keep = fresh ? 0.f : 1.f;
+      st.acc8[0] = fmaf(st.acc8[0], keep, dh);
+      st.acc8[1] = fmaf(st.acc8[1], keep, px);
+      st.acc8[2] = fmaf(st.acc8[2], keep, py);
+      st.acc8[3] = fmaf(st.acc8[3], keep, dh * c.uz);
+      st.acc8[4] = fmaf(st.acc8[4], keep, pxy);
+      st.acc8[5] = fmaf(st.acc8[5], keep, px * c.uz);
+      st.acc8[6] = fmaf(st.acc8[6], keep, py * c.uz);
+      st.acc8[7] = fmaf(st.acc8[7], keep, pxy * c.uz);
+      st.run_cell = c.cell;
+      gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
+    }
   }
 }
 

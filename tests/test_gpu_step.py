@@ -260,3 +260,41 @@ def test_band_tape_auto_and_workspace(cuda):
     vol, _, prm = R._descs(est, tex, rig, dt, False, cells)
     words = int(N.lib().ddvr_band_tape_bytes(ctypes.byref(vol), 6, ctypes.byref(prm)))
     assert words > 0 and words % 256 == 0
+
+
+@pytest.mark.parametrize("n,dt_vox", [(24, 0.2), (40, 0.05)])
+def test_band_tape_skips_empty_blocks_exactly(cuda, n, dt_vox):
+    """An estimate with exactly empty space (the sphere phantom: density 0 outside
+    the ball, so whole 32-sample tape words are 0 and the walk skips them, and
+    empty cell runs skip their flush) gives the gathering walk's gradient and the
+    oracle's."""
+    import torch
+    from oracle import dvr_oracle as O
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    from paper_2107_12672_b200.scenes import absorption_ramp_texels, fibonacci_poses, phantom
+    truth = phantom("sphere", n, seed=0).astype(np.float32)
+    est_np = np.where(truth > 0, np.clip(0.7 * truth + 0.05, 0, 1), 0.0).astype(np.float32)
+    est = torch.from_numpy(est_np).to(cuda)
+    tex = torch.from_numpy(absorption_ramp_texels(64, 3.0).astype(np.float32)).to(cuda)
+    ll = torch.tensor(fibonacci_poses(5), dtype=torch.float64, device=cuda)
+    rig = R.Rig(28, 26)
+    dt = dt_vox / n
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    refs, _ = R.forward(torch.from_numpy(truth).to(cuda), tex, cams, dt, rig)
+    got = {}
+    for tape in (False, True):
+        step = ShardedStep(est, tex, ll, refs, dt, rig, band_tape=tape)
+        assert step.band_tape == tape
+        got[tape] = step.run().d_volume.double().cpu().numpy()
+    assert np.abs(got[True]).max() > 0
+    assert rel_l2(got[True], got[False]) <= 1e-6
+    grid = O.Grid(est_np.astype(np.float64))
+    t64 = tex.cpu().numpy().astype(np.float64)
+    want = np.zeros((n, n, n))
+    for k, (lon, lat) in enumerate(ll.cpu().numpy()):
+        v = O.View(lon, lat, 2.0, (0, 0, 0), 30.0, rig.width, rig.height)
+        img = O.render_view(grid, t64, v, dt)
+        seed = np.sign(img - refs[k].cpu().numpy().astype(np.float64)) / refs.numel()
+        want += O.adjoint_view(grid, t64, v, dt, seed, ["volume"], image=img)["d_volume"]
+    assert rel_l2(got[True], want) <= 1e-4
