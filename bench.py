@@ -62,6 +62,8 @@ def parse():
                    help="replay each timed iteration from a captured CUDA graph (1 GPU)")
     p.add_argument("--unfused", action="store_true",
                    help="separate forward / L1 / adjoint launches instead of the fused step")
+    p.add_argument("--no-empty-skip", action="store_true",
+                   help="band tape without the empty-brick skip of the march")
     p.add_argument("--no-band-tape", action="store_true",
                    help="fused absorption step without the 1-bit-per-sample band tape "
                         "(DDVR_FLAG_BAND_TAPE; the walk then re-gathers the cell records)")
@@ -282,7 +284,8 @@ def run_own(args, cfg):
     step = ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                        total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
                        layout=args.layout, fused=False if args.unfused else "auto",
-                       band_tape=False if args.no_band_tape else "auto")
+                       band_tape=False if args.no_band_tape else "auto",
+                       empty_skip=not args.no_empty_skip)
     # density targets run the whole optimisation iteration (prior + Adam + projection)
     graphed = args.graph and world == 1 and "volume" in cfg.targets
     runner = (TomographyIteration(step, lr=0.02, lam=0.5, graph=graphed)
@@ -496,11 +499,14 @@ def run_own(args, cfg):
             line["config"]["iterations"] = (
                 "one optimisation run: value times iterations W+1..W+K, e2e the next W+K; "
                 "the estimate changes every iteration (Adam + [0,1] projection), and as its "
-                "empty space grows the walk skips more empty cell runs")
+                "empty space grows the march and the walk skip more of it")
         line["config"]["step"] = (("fused forward+L1+adjoint" if getattr(step, "fused", False)
                                    else "forward, L1, adjoint") +
                                   (", band tape (1 bit/sample, DDVR_FLAG_BAND_TAPE)"
                                    if getattr(step, "band_tape", False) else "") +
+                                  (", empty-brick skip in the march"
+                                   if getattr(step, "band_tape", False) and step.empty_skip
+                                   else "") +
                                   (", CUDA-graph replay" if graphed else ""))
         if world == 1 and not args.no_cpu_baseline:
             sps, rps, cores, desc = cpu_sample(cfg, args.cpu_seconds)

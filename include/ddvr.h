@@ -105,6 +105,7 @@ typedef struct {
 #define DDVR_FLAG_WS_DEFER 2
 #define DDVR_FLAG_DETERMINISTIC 4
 #define DDVR_FLAG_BAND_TAPE 8
+#define DDVR_FLAG_NO_EMPTY_SKIP 16
 
 /* march parameters (RenderConfig, renderer.py:84-106) */
 typedef struct {
@@ -133,7 +134,15 @@ typedef struct {
                                                    -- and the walk reads it instead of
                                                    re-gathering the cell records
                                                    (ddvr_band_tape_bytes); identical
-                                                   gradients, O(samples / 32) words */
+                                                   gradients, O(samples / 32) words.
+                                                   With the empty-brick map in the
+                                                   workspace the march also skips
+                                                   32-sample blocks that start in an
+                                                   all-zero 8^3-cell brick whose 26
+                                                   neighbours are all zero (bitwise
+                                                   the same outputs)
+                            DDVR_FLAG_NO_EMPTY_SKIP  with DDVR_FLAG_BAND_TAPE: march
+                                                   every block (no brick map) */
   float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
                             forward writes the transmittance before every sample,
                             tape[ray * tape_stride + i]; the adjoint then reads it
@@ -221,9 +230,11 @@ int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t
 /* Extra workspace of a DDVR_FLAG_BAND_TAPE ddvr_forward_adjoint_l1 call: one
  * bit per sample for every ray, 32-bit words per ray bounded by the box
  * diagonal / dt.  Placed after the workspace (and the deterministic partials),
- * each part rounded up to 256 bytes.  Used by the affine absorption walk
- * (emission-free TF with a non-negative affine tau column, volume target);
- * other steps ignore it. */
+ * each part rounded up to 256 bytes: the tape, then the empty-brick map (2 bytes
+ * per brick of 8^3 cell records, rebuilt from vol->cells by every call; a
+ * workspace that ends before the map runs without the empty-space skip).  Used
+ * by the affine absorption walk (emission-free TF with a non-negative affine tau
+ * column, volume target); other steps ignore it. */
 int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:

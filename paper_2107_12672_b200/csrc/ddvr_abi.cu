@@ -242,6 +242,8 @@ int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
     return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");
   V.data = vol->data;
   V.cells = vol->cells;
+  V.empty = nullptr;   // set by run_adjoint for the fused band-tape step
+  V.NBy = (vol->dims[1] + 8) >> 3; V.NBz = (vol->dims[2] + 8) >> 3;
   V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
   V.YZ = V.Y * V.Z;
   V.CY = V.Y + 1; V.CZ = V.Z + 1;
@@ -676,6 +678,51 @@ static int64_t det_bytes(int64_t ctas, uint32_t mask) {
   return (ctas * 3 * 8 + 255) & ~(int64_t)255;
 }
 
+// Empty-brick map of the fused band-tape step: bricks of 8^3 padded cell records
+// (storage indices [8b, 8b+8) per axis), a byte each for the occupancy and for the
+// dilated map the march reads (VolArgs::empty).
+static int64_t brick_map_bytes(const int32_t dims[3]) {
+  const int64_t nb = (int64_t)((dims[0] + 8) >> 3) * ((dims[1] + 8) >> 3) * ((dims[2] + 8) >> 3);
+  return (2 * nb + 255) & ~(int64_t)255;
+}
+
+// occ[b] = some record of brick b has a nonzero coefficient (one CTA per brick; the
+// records of a z-run of the brick are contiguous 256-byte lines)
+__global__ void __launch_bounds__(256) brick_occupancy_kernel(const float* __restrict__ cells,
+                                                            int CX, int CY, int CZ, int NBy,
+                                                            int NBz,
+                                                            unsigned char* __restrict__ occ) {
+  const int b = blockIdx.x;
+  const int bz = b % NBz, by = (b / NBz) % NBy, bx = b / (NBz * NBy);
+  bool nz = false;
+  for (int r = threadIdx.x; r < 512; r += 256) {
+    const int sx = 8 * bx + (r >> 6), sy = 8 * by + ((r >> 3) & 7), sz = 8 * bz + (r & 7);
+    if (sx < CX && sy < CY && sz < CZ) {
+      const uint4* q = reinterpret_cast<const uint4*>(
+          cells + 8 * (((long long)sx * CY + sy) * CZ + sz));
+      const uint4 a = __ldg(q), c = __ldg(q + 1);
+      nz |= ((a.x | a.y | a.z | a.w | c.x | c.y | c.z | c.w) & 0x7fffffffu) != 0u;
+    }
+  }
+  nz = __syncthreads_or(nz);
+  if (threadIdx.x == 0) occ[b] = nz ? 1 : 0;
+}
+
+// empty[b] = brick b and its (existing) 26 neighbours are unoccupied
+__global__ void __launch_bounds__(256) brick_dilate_kernel(const unsigned char* __restrict__ occ,
+                                                         int NBx, int NBy, int NBz,
+                                                         unsigned char* __restrict__ empty) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= NBx * NBy * NBz) return;
+  const int bz = b % NBz, by = (b / NBz) % NBy, bx = b / (NBz * NBy);
+  unsigned char any = 0;
+  for (int x = max(bx - 1, 0); x <= min(bx + 1, NBx - 1); ++x)
+    for (int y = max(by - 1, 0); y <= min(by + 1, NBy - 1); ++y)
+      for (int z = max(bz - 1, 0); z <= min(bz + 1, NBz - 1); ++z)
+        any |= occ[(x * NBy + y) * NBz + z];
+  empty[b] = any ? 0 : 1;
+}
+
 // DDVR_FLAG_BAND_TAPE: 32-bit words per ray, from an upper bound of any ray's
 // step count: n = ceil(chord / dt - 1e-9) <= diag / dt + 1 (renderer.py:209-214)
 static int band_words(const double bmin[3], const double bmax[3], double dt) {
@@ -693,9 +740,11 @@ static int64_t grid_ctas(int32_t n_views, const ddvr_params* p) {
 
 int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p) {
   if (!vol || !p || n_views < 0 || p->width < 1 || p->height < 1 || !(p->dt > 0.0)) return 0;
+  if (vol->dims[0] < 1 || vol->dims[1] < 1 || vol->dims[2] < 1) return 0;
   const int64_t b = grid_ctas(n_views, p) * kThreads * band_words(vol->box_min, vol->box_max,
                                                                   p->dt) * 4;
-  return (b + 255) & ~(int64_t)255;
+  // the tape, then the empty-brick map (optional: a workspace without it marches every block)
+  return ((b + 255) & ~(int64_t)255) + brick_map_bytes(vol->dims);
 }
 
 int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask) {
@@ -738,7 +787,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                        int32_t flags) {
   int rc;
   if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER | DDVR_FLAG_DETERMINISTIC |
-                DDVR_FLAG_BAND_TAPE))
+                DDVR_FLAG_BAND_TAPE | DDVR_FLAG_NO_EMPTY_SKIP))
     return set_error(DDVR_INVALID_PARAMETER, "unknown params.flags bits 0x%x", flags);
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
@@ -782,6 +831,9 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
     G.bits = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + tape_off);
     G.bits_words = band_words(V.bmin, V.bmax, G.dt);
   }
+  const int64_t map_off = tape_off + ((ws_band + 255) & ~(int64_t)255);
+  const bool brick_map = ws_band > 0 && !(flags & DDVR_FLAG_NO_EMPTY_SKIP) &&
+                         workspace_bytes >= map_off + brick_map_bytes(vol->dims);
   if (workspace && ((uintptr_t)workspace & 31) != 0)
     return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;
@@ -805,6 +857,15 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
     cudaError_t e = cudaMemsetAsync(workspace, 0, (size_t)ws_need, st);
     if (e != cudaSuccess)
       return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
+  }
+  if (brick_map) {   // the march skips 32-sample blocks that start in an empty brick
+    const int NBx = (V.X + 8) >> 3, nb = NBx * V.NBy * V.NBz;
+    unsigned char* occ = static_cast<unsigned char*>(workspace) + map_off;
+    brick_occupancy_kernel<<<nb, 256, 0, st>>>(V.cells, V.X + 1, V.CY, V.CZ, V.NBy, V.NBz, occ);
+    if ((rc = check_launch("brick_occupancy_kernel"))) return rc;
+    brick_dilate_kernel<<<(nb + 255) / 256, 256, 0, st>>>(occ, NBx, V.NBy, V.NBz, occ + nb);
+    if ((rc = check_launch("brick_dilate_kernel"))) return rc;
+    V.empty = occ + nb;
   }
   auto launch = mask <= 3 ? launch_adjoint_g0 : mask <= 7 ? launch_adjoint_g1
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;

@@ -43,6 +43,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 
 #include "ddvr.h"
 
@@ -84,7 +85,21 @@ struct VolArgs {
   long long lo[3], hi[3];  // inside test, fixed-point grid units: [-0.5 - tol, dim - 0.5 + tol]
   long long top[3];        // (dim-1) in fixed point: spatial-gradient liveness (field.py:461-463)
   double bmin[3], bmax[3], scale[3];   // scale = dim / extent
+  // fused band-tape march (DDVR_FLAG_BAND_TAPE, nullable): byte per brick of 8^3 padded
+  // cell records (storage index >> 3 per axis), 1 = the records of the brick and of its
+  // 26 neighbours are all zero, so no sample within 7 cells of it has density
+  const unsigned char* __restrict__ empty;
+  int NBy, NBz;            // bricks along y and z: ceil((dim + 1) / 8)
 };
+
+// The brick of the padded cell record at fixed-point grid position (gx, gy, gz).
+__device__ __forceinline__ bool brick_empty(const VolArgs& V, long long gx, long long gy,
+                                            long long gz) {
+  const int bx = (min(max((int)(gx >> 32), -1), V.X1) + 1) >> 3;
+  const int by = (min(max((int)(gy >> 32), -1), V.Y1) + 1) >> 3;
+  const int bz = (min(max((int)(gz >> 32), -1), V.Z1) + 1) >> 3;
+  return __ldg(V.empty + (bx * V.NBy + by) * V.NBz + bz) != 0;
+}
 
 struct TfArgs {
   const float* __restrict__ params;
@@ -888,13 +903,17 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   auto density = [&](const Cell& c, const float* k) {
     return clamp_density(INSIDE || c.inside, interp(c, k).rho);
   };
-  auto shade = [&](float d, int i) {
+  // kStore: the word is stored at its last sample here (else by the caller's block loop)
+  auto shade = [&](float d, int i, auto kStore) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     if (kAbs && AFF) {   // affine tau column: no table lookup
       const float t = __fmaf_rn(d, TF.fR, -0.5f);
       if (BITS) {   // band bit, pushed in at the LSB (the walk pops it from there)
         word = (word << 1) | (t >= 0.f && t < TF.fR1 ? 1u : 0u);
-        if ((i & 31) == 31) { bits[bits_off + ((i >> 5) << 5)] = word; word = 0u; }
+        if (decltype(kStore)::value && (i & 31) == 31) {
+          bits[bits_off + ((i >> 5) << 5)] = word;
+          word = 0u;
+        }
       }
       const float tau = __fmaf_rn(aff_b, fminf(fmaxf(t, 0.f), TF.fR1), aff_a);   // tau_affine
       const float x = __fmul_rn(dt32, fmaxf(tau, 0.f));
@@ -934,16 +953,51 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     held = c.cell;
     // (the emitting variants spill at 48 registers when unrolled)
     constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : 1;
-#pragma unroll kMarchUnroll
-    for (int i = 0; i < r.n; ++i) {
-      if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
+    auto step = [&](int i, auto kStore) {
       const float d = density(c, v);
       gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
       locate<CELLS>(V, gx, gy, gz, ins, c);
       const bool more = i + 1 < r.n;
       ld256_if(more && c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
       held = c.cell;
-      shade(d, i);
+      shade(d, i, kStore);
+    };
+    // Empty-space skip (band tape): a block of 32 samples (one tape word) that starts in
+    // an empty brick stays within 7 cells of it when 31 |step| < 7 cells per axis, so every
+    // sample reads an all-zero record: d = 0, band bit 0 and -- when tau(0) = aff_a <= 0 --
+    // an optical depth of exactly 0.  The block's word is stored as 0 and the march moves
+    // on 32 steps: the same S, image and tape as marching it.
+    constexpr long long kSkipStep = (7LL << 32) / 31;
+    const bool skip = BITS && V.empty != nullptr && aff_a <= 0.f &&
+                      llabs(r.gs[0]) < kSkipStep && llabs(r.gs[1]) < kSkipStep &&
+                      llabs(r.gs[2]) < kSkipStep;
+    if (BITS && skip) {
+      for (int i0 = 0; i0 < r.n; i0 += 32) {
+        if (brick_empty(V, gx, gy, gz)) {
+          if (i0 + 32 <= r.n) bits[bits_off + i0] = 0u;   // word i0/32 (a last partial
+          gx += 32 * r.gs[0]; gy += 32 * r.gs[1]; gz += 32 * r.gs[2];   // word: after the loop)
+          if (i0 + 32 < r.n) {
+            locate<CELLS>(V, gx, gy, gz, ins, c);
+            ld256(V.cell0 + 8 * (long long)c.cell, v);
+            held = c.cell;
+          }
+          continue;
+        }
+        if (i0 + 32 <= r.n) {   // a whole word: fixed trip count, one store after it
+#pragma unroll kMarchUnroll
+          for (int j = 0; j < 32; ++j) step(i0 + j, std::false_type{});
+          bits[bits_off + i0] = word;
+          word = 0u;
+        } else {                // the last partial word (stored after the march)
+          for (int i = i0; i < r.n; ++i) step(i, std::false_type{});
+        }
+      }
+    } else {
+#pragma unroll kMarchUnroll
+      for (int i = 0; i < r.n; ++i) {
+        if (EARLY && A > kAlphaStop) break;      // renderer.py:331-335
+        step(i, std::true_type{});
+      }
     }
   } else {
     for (int i = 0; i < r.n; ++i) {
@@ -952,7 +1006,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
       gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
       fetch8<CELLS>(V, c, v);
-      shade(density(c, v), i);
+      shade(density(c, v), i, std::true_type{});
     }
   }
   if (BITS && (r.n & 31)) bits[bits_off + ((r.n >> 5) << 5)] = word;   // partial last word

@@ -89,13 +89,15 @@ class ShardedStep:
     ``band_tape`` (fused volume-only steps): the march stores one bit per sample
     for the affine absorption walk, which then re-gathers no cell records
     (DDVR_FLAG_BAND_TAPE; 4.7 GB at C4).  "auto" uses it when it fits
-    min(8 GiB, a quarter of the free device memory).
+    min(8 GiB, a quarter of the free device memory).  ``empty_skip`` (band tape):
+    the march skips 32-sample blocks in all-zero 8^3-cell bricks (bitwise the same
+    step; False marches every block, DDVR_FLAG_NO_EMPTY_SKIP).
     """
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
                  group=None, layout="cells", fused="auto", keep_images=False, chunks=4,
-                 deterministic=False, band_tape="auto"):
+                 deterministic=False, band_tape="auto", empty_skip=True):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
@@ -119,6 +121,7 @@ class ShardedStep:
         self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
                       if layout == "cells" else None)
         self.deterministic = bool(deterministic)
+        self.empty_skip = bool(empty_skip)
         if fused == "auto":
             fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
         self.fused = bool(fused) and self.cells is not None
@@ -205,7 +208,8 @@ class ShardedStep:
                     depth_out=self.depth[sl] if self.keep_images else None,
                     ws_continue=k > 0 and self.workspace is not None,
                     ws_defer=not last and self.workspace is not None,
-                    deterministic=self.deterministic, band_tape=self.band_tape)
+                    deterministic=self.deterministic, band_tape=self.band_tape,
+                    empty_skip=self.empty_skip)
             hook("post_adjoint")
         elif V:
             if self.cells is not None:

@@ -271,7 +271,8 @@ def extra_workspace_bytes(vol, prm, n_views: int, mask: int, deterministic=False
 def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: float, mask: int,
                        *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
                        workspace=None, image_out=None, depth_out=None, ws_continue=False,
-                       ws_defer=False, deterministic=False, band_tape=False):
+                       ws_defer=False, deterministic=False, band_tape=False,
+                       empty_skip=True):
     """One fused step over these views: forward march, L1 seed sign(image - ref)/count
     and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
     device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
@@ -279,7 +280,9 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
     call but the first passes ws_continue, every call but the last ws_defer.
     ``deterministic``: bitwise reproducible d_camera / d_dt (DDVR_FLAG_DETERMINISTIC);
     ``band_tape``: the march stores 1 bit per sample for the affine absorption walk,
-    which then gathers no records (DDVR_FLAG_BAND_TAPE, volume target).  A
+    which then gathers no records (DDVR_FLAG_BAND_TAPE, volume target); with it the
+    march skips 32-sample blocks in all-zero bricks unless ``empty_skip`` is False
+    (DDVR_FLAG_NO_EMPTY_SKIP; bitwise the same outputs either way).  A
     caller-provided workspace needs those extra bytes too (extra_workspace_bytes)."""
     _require(cams, "cameras", torch.float64, ndim=2)
     if cells is None:
@@ -303,7 +306,8 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
             raise InvalidParameterError("a step split over calls needs a shared workspace")
         workspace = workspace_for(density, mask, cells, texels, extra)
     prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0) \
-        | (N.FLAG_DETERMINISTIC if deterministic else 0) | (N.FLAG_BAND_TAPE if band_tape else 0)
+        | (N.FLAG_DETERMINISTIC if deterministic else 0) | (N.FLAG_BAND_TAPE if band_tape else 0) \
+        | (0 if empty_skip else N.FLAG_NO_EMPTY_SKIP)
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_forward_adjoint_l1(

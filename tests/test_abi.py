@@ -238,7 +238,7 @@ def test_deterministic_mode_workspace(lib):
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 2 and "deterministic" in lib.ddvr_last_error().decode()
-    prm.flags = 16
+    prm.flags = 32
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 1 and "flags" in lib.ddvr_last_error().decode()
@@ -246,14 +246,14 @@ def test_deterministic_mode_workspace(lib):
 
 def test_band_tape_bytes_and_limits(lib):
     """ddvr_band_tape_bytes: 32-bit words per ray from the box diagonal / dt, for every
-    pixel of every CTA; a fused call whose tape would pass 2^32 words is refused
+    pixel of every CTA, then the empty-brick map; a fused call whose tape would pass 2^32 words is refused
     before any CUDA work, and one without room for the tape asks for it."""
     import math
     from paper_2107_12672_b200 import _native as N
     vol, tf, prm = _descs(dt=0.01, W=512, H=512)
     words = math.ceil((math.floor(math.sqrt(3.0) / 0.01) + 3) / 32)
     assert lib.ddvr_band_tape_bytes(ctypes.byref(vol), 64, ctypes.byref(prm)) == \
-        32 * 32 * 64 * 256 * words * 4
+        32 * 32 * 64 * 256 * words * 4 + 256   # + the empty-brick map (1 brick, 256-aligned)
     loss = ctypes.c_double(0)
     vol.cells = 32
     call = lambda v, p, nv, ws: lib.ddvr_forward_adjoint_l1(  # noqa: E731

@@ -298,3 +298,98 @@ def test_band_tape_skips_empty_blocks_exactly(cuda, n, dt_vox):
         seed = np.sign(img - refs[k].cpu().numpy().astype(np.float64)) / refs.numel()
         want += O.adjoint_view(grid, t64, v, dt, seed, ["volume"], image=img)["d_volume"]
     assert rel_l2(got[True], want) <= 1e-4
+
+
+def _brick_map_np(vol: np.ndarray) -> np.ndarray:
+    """The empty-brick map the fused band-tape step builds (ddvr_abi.cu
+    brick_occupancy_kernel / brick_dilate_kernel), restated: padded cell s (storage
+    index, cell s-1) is occupied when one of its edge-clamped corners is nonzero;
+    brick b = cells [8b, 8b+8) per axis; empty = the brick and its neighbours unoccupied."""
+    nz = np.pad(vol != 0, 1, mode="edge")          # padded[p] = voxel clamp(p-1)
+    cell = np.zeros(tuple(d + 1 for d in vol.shape), bool)
+    for dx in (0, 1):
+        for dy in (0, 1):
+            for dz in (0, 1):
+                cell |= nz[dx:dx + cell.shape[0], dy:dy + cell.shape[1], dz:dz + cell.shape[2]]
+    nb = tuple((d + 8) >> 3 for d in vol.shape)
+    occ = np.zeros(nb, bool)
+    for b in np.ndindex(*nb):
+        occ[b] = cell[8 * b[0]:8 * b[0] + 8, 8 * b[1]:8 * b[1] + 8, 8 * b[2]:8 * b[2] + 8].any()
+    dil = np.pad(occ, 1)
+    empty = np.ones(nb, bool)
+    for dx in range(3):
+        for dy in range(3):
+            for dz in range(3):
+                empty &= ~dil[dx:dx + nb[0], dy:dy + nb[1], dz:dz + nb[2]]
+    return empty
+
+
+@pytest.mark.parametrize("dt_vox", [0.2, 0.11, 0.5])
+def test_band_tape_empty_brick_skip_is_exact(cuda, dt_vox):
+    """The march's empty-space skip (32-sample blocks that start in an empty brick)
+    changes nothing: image and optical depth bitwise, the band tape bitwise, the loss
+    and the density gradient to atomic-order rounding -- against the same call with
+    DDVR_FLAG_NO_EMPTY_SKIP.  The brick map itself equals the numpy restatement and
+    has empty bricks, and the gradient matches the oracle.  dt 0.5 voxel: 31 steps
+    exceed 7 cells, so those rays march every block."""
+    import ctypes
+    import torch
+    from oracle import dvr_oracle as O
+    from paper_2107_12672_b200 import _native as N
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.scenes import absorption_ramp_texels, fibonacci_poses
+    n = 72
+    g = np.stack(np.meshgrid(*[np.arange(n)] * 3, indexing="ij"), -1).astype(np.float64)
+    r = np.linalg.norm(g - np.array([44.0, 34.0, 30.0]), axis=-1)
+    est_np = np.where(r < 14, np.clip(1.0 - r / 16, 0, 1), 0.0).astype(np.float32)
+    truth = np.where(r < 12, 0.8, 0.0).astype(np.float32)
+    est = torch.from_numpy(est_np).to(cuda)
+    tex = torch.from_numpy(absorption_ramp_texels(64, 3.0).astype(np.float32)).to(cuda)
+    ll = torch.tensor(fibonacci_poses(6), dtype=torch.float64, device=cuda)
+    rig = R.Rig(40, 36)
+    dt = dt_vox / n
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    refs, _ = R.forward(torch.from_numpy(truth).to(cuda), tex, cams, dt, rig)
+    cells = R.pack_cells(est)
+    vol, _, prm = R._descs(est, tex, rig, dt, False, cells)
+    band = int(N.lib().ddvr_band_tape_bytes(ctypes.byref(vol), 6, ctypes.byref(prm)))
+    base = int(N.lib().ddvr_adjoint_workspace_bytes(
+        ctypes.byref(vol), ctypes.byref(N.DdvrTf(N.TF_TEXTURE, 64, tex.data_ptr())),
+        N.TARGET_VOLUME))
+    base = (base + 255) & ~255
+    nb = ((n + 8) >> 3) ** 3
+    map_bytes = (2 * nb + 255) & ~255
+    out = {}
+    for skip in (True, False):
+        ws = torch.zeros((base + band) // 4, dtype=torch.float32, device=cuda)
+        img = torch.empty(6, rig.band_rows, rig.width, 4, dtype=torch.float32, device=cuda)
+        depth = torch.empty(6, rig.band_rows, rig.width, dtype=torch.float32, device=cuda)
+        loss = torch.zeros(1, dtype=torch.float64, device=cuda)
+        dv = torch.zeros_like(est)
+        R.forward_adjoint_l1(est, tex, cams, dt, rig, refs, float(refs.numel()), N.TARGET_VOLUME,
+                             cells=cells, loss=loss, d_volume=dv, workspace=ws, image_out=img,
+                             depth_out=depth, band_tape=True, empty_skip=skip)
+        raw = ws.view(torch.uint8).cpu().numpy()
+        out[skip] = dict(img=img.cpu().numpy(), depth=depth.cpu().numpy(), loss=loss.item(),
+                         dv=dv.double().cpu().numpy(), tape=raw[base:base + band - map_bytes],
+                         empty=raw[base + band - map_bytes + nb:base + band - map_bytes + 2 * nb])
+    a, b = out[True], out[False]
+    want_map = _brick_map_np(est_np).ravel()
+    assert want_map.any() and not want_map.all()
+    np.testing.assert_array_equal(a["empty"].astype(bool), want_map)
+    assert not b["empty"].any()      # NO_EMPTY_SKIP builds no map
+    np.testing.assert_array_equal(a["img"], b["img"])
+    np.testing.assert_array_equal(a["depth"], b["depth"])
+    np.testing.assert_array_equal(a["tape"], b["tape"])
+    assert a["loss"] == pytest.approx(b["loss"], rel=1e-12)
+    assert np.abs(a["dv"]).max() > 0
+    assert rel_l2(a["dv"], b["dv"]) <= 1e-6
+    grid = O.Grid(est_np.astype(np.float64))
+    t64 = tex.cpu().numpy().astype(np.float64)
+    want = np.zeros((n, n, n))
+    for k, (lon, lat) in enumerate(ll.cpu().numpy()):
+        v = O.View(lon, lat, 2.0, (0, 0, 0), 30.0, rig.width, rig.height)
+        im = O.render_view(grid, t64, v, dt)
+        seed = np.sign(im - refs[k].cpu().numpy().astype(np.float64)) / refs.numel()
+        want += O.adjoint_view(grid, t64, v, dt, seed, ["volume"], image=im)["d_volume"]
+    assert rel_l2(a["dv"], want) <= 1e-4

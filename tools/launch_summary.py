@@ -17,7 +17,7 @@ for r in rows:
     agg[name][1] += float(r[vi].replace(",", "")) * SCALE[r[ui]]
 tot = sum(t for _, t in agg.values())
 print("ncu --metrics gpu__time_duration.sum --clock-control none -c 400 "
-      "python bench.py --steps 2 --warmup 1 --no-cpu-baseline")
+      "python bench.py --steps 2 --warmup 3 --no-cpu-baseline")
 print("(cold-cache, serialised launches: compare shares with the bench's CUDA-event times)\n")
 for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"{t:10.3f} ms {100 * t / tot:6.2f}%  x{n:3d}  {name}")
