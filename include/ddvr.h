@@ -137,9 +137,8 @@ typedef struct {
                                                    gradients, O(samples / 32) words.
                                                    With the empty-brick map in the
                                                    workspace the march also skips
-                                                   32-sample blocks that start in an
-                                                   all-zero 8^3-cell brick whose 26
-                                                   neighbours are all zero (bitwise
+                                                   32-sample blocks that lie in
+                                                   all-zero 8^3-cell bricks (bitwise
                                                    the same outputs)
                             DDVR_FLAG_NO_EMPTY_SKIP  with DDVR_FLAG_BAND_TAPE: march
                                                    every block (no brick map) */
@@ -230,8 +229,8 @@ int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t
 /* Extra workspace of a DDVR_FLAG_BAND_TAPE ddvr_forward_adjoint_l1 call: one
  * bit per sample for every ray, 32-bit words per ray bounded by the box
  * diagonal / dt.  Placed after the workspace (and the deterministic partials),
- * each part rounded up to 256 bytes: the tape, then the empty-brick map (2 bytes
- * per brick of 8^3 cell records, rebuilt from vol->cells by every call; a
+ * each part rounded up to 256 bytes: the tape, then the brick occupancy maps (2
+ * bytes per brick of 8^3 cell records, rebuilt from vol->cells by every call; a
  * workspace that ends before the map runs without the empty-space skip).  Used
  * by the affine absorption walk (emission-free TF with a non-negative affine tau
  * column, volume target); other steps ignore it. */

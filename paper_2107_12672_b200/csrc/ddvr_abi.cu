@@ -242,7 +242,7 @@ int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
     return set_error(DDVR_INVALID_INPUT, "cell records must be 32-byte aligned");
   V.data = vol->data;
   V.cells = vol->cells;
-  V.empty = nullptr;   // set by run_adjoint for the fused band-tape step
+  V.occ = nullptr;   // set by run_adjoint for the fused band-tape step
   V.NBy = (vol->dims[1] + 8) >> 3; V.NBz = (vol->dims[2] + 8) >> 3;
   V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
   V.YZ = V.Y * V.Z;
@@ -678,9 +678,9 @@ static int64_t det_bytes(int64_t ctas, uint32_t mask) {
   return (ctas * 3 * 8 + 255) & ~(int64_t)255;
 }
 
-// Empty-brick map of the fused band-tape step: bricks of 8^3 padded cell records
-// (storage indices [8b, 8b+8) per axis), a byte each for the occupancy and for the
-// dilated map the march reads (VolArgs::empty).
+// Brick occupancy maps of the fused band-tape step: bricks of 8^3 padded cell records
+// (storage indices [8b, 8b+8) per axis), a byte per brick for the occupancy and for
+// the 2x2x2 window OR the march reads (VolArgs::occ).
 static int64_t brick_map_bytes(const int32_t dims[3]) {
   const int64_t nb = (int64_t)((dims[0] + 8) >> 3) * ((dims[1] + 8) >> 3) * ((dims[2] + 8) >> 3);
   return (2 * nb + 255) & ~(int64_t)255;
@@ -708,19 +708,18 @@ __global__ void __launch_bounds__(256) brick_occupancy_kernel(const float* __res
   if (threadIdx.x == 0) occ[b] = nz ? 1 : 0;
 }
 
-// empty[b] = brick b and its (existing) 26 neighbours are unoccupied
-__global__ void __launch_bounds__(256) brick_dilate_kernel(const unsigned char* __restrict__ occ,
+// win[b] = some brick of the window b .. b+1 (per axis, those that exist) is occupied
+__global__ void __launch_bounds__(256) brick_window_kernel(const unsigned char* __restrict__ occ,
                                                          int NBx, int NBy, int NBz,
-                                                         unsigned char* __restrict__ empty) {
+                                                         unsigned char* __restrict__ win) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= NBx * NBy * NBz) return;
   const int bz = b % NBz, by = (b / NBz) % NBy, bx = b / (NBz * NBy);
   unsigned char any = 0;
-  for (int x = max(bx - 1, 0); x <= min(bx + 1, NBx - 1); ++x)
-    for (int y = max(by - 1, 0); y <= min(by + 1, NBy - 1); ++y)
-      for (int z = max(bz - 1, 0); z <= min(bz + 1, NBz - 1); ++z)
-        any |= occ[(x * NBy + y) * NBz + z];
-  empty[b] = any ? 0 : 1;
+  for (int x = bx; x <= min(bx + 1, NBx - 1); ++x)
+    for (int y = by; y <= min(by + 1, NBy - 1); ++y)
+      for (int z = bz; z <= min(bz + 1, NBz - 1); ++z) any |= occ[(x * NBy + y) * NBz + z];
+  win[b] = any;
 }
 
 // DDVR_FLAG_BAND_TAPE: 32-bit words per ray, from an upper bound of any ray's
@@ -858,14 +857,14 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
     if (e != cudaSuccess)
       return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
   }
-  if (brick_map) {   // the march skips 32-sample blocks that start in an empty brick
+  if (brick_map) {   // the march skips 32-sample blocks that lie in empty bricks
     const int NBx = (V.X + 8) >> 3, nb = NBx * V.NBy * V.NBz;
     unsigned char* occ = static_cast<unsigned char*>(workspace) + map_off;
     brick_occupancy_kernel<<<nb, 256, 0, st>>>(V.cells, V.X + 1, V.CY, V.CZ, V.NBy, V.NBz, occ);
     if ((rc = check_launch("brick_occupancy_kernel"))) return rc;
-    brick_dilate_kernel<<<(nb + 255) / 256, 256, 0, st>>>(occ, NBx, V.NBy, V.NBz, occ + nb);
-    if ((rc = check_launch("brick_dilate_kernel"))) return rc;
-    V.empty = occ + nb;
+    brick_window_kernel<<<(nb + 255) / 256, 256, 0, st>>>(occ, NBx, V.NBy, V.NBz, occ + nb);
+    if ((rc = check_launch("brick_window_kernel"))) return rc;
+    V.occ = occ + nb;
   }
   auto launch = mask <= 3 ? launch_adjoint_g0 : mask <= 7 ? launch_adjoint_g1
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;

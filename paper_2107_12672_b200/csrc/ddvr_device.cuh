@@ -86,19 +86,27 @@ struct VolArgs {
   long long top[3];        // (dim-1) in fixed point: spatial-gradient liveness (field.py:461-463)
   double bmin[3], bmax[3], scale[3];   // scale = dim / extent
   // fused band-tape march (DDVR_FLAG_BAND_TAPE, nullable): byte per brick of 8^3 padded
-  // cell records (storage index >> 3 per axis), 1 = the records of the brick and of its
-  // 26 neighbours are all zero, so no sample within 7 cells of it has density
-  const unsigned char* __restrict__ empty;
+  // cell records (storage index >> 3 per axis), 1 = some record of the 2x2x2 bricks
+  // b .. b+1 (those that exist) is nonzero
+  const unsigned char* __restrict__ occ;
   int NBy, NBz;            // bricks along y and z: ceil((dim + 1) / 8)
 };
 
-// The brick of the padded cell record at fixed-point grid position (gx, gy, gz).
-__device__ __forceinline__ bool brick_empty(const VolArgs& V, long long gx, long long gy,
-                                            long long gz) {
-  const int bx = (min(max((int)(gx >> 32), -1), V.X1) + 1) >> 3;
-  const int by = (min(max((int)(gy >> 32), -1), V.Y1) + 1) >> 3;
-  const int bz = (min(max((int)(gz >> 32), -1), V.Z1) + 1) >> 3;
-  return __ldg(V.empty + (bx * V.NBy + by) * V.NBz + bz) != 0;
+// brick coordinate of the padded cell record at a fixed-point grid coordinate
+__device__ __forceinline__ int brick_of(long long g, int top) {
+  return (min(max((int)(g >> 32), -1), top) + 1) >> 3;
+}
+
+// The 32-sample block from grid position g reads only all-zero records: with fewer
+// than 8 cells per axis between its first and last sample, its cells lie in the start
+// brick and the next one in the direction of travel (back: bit k set = axis k goes
+// down; clamping is monotone), which is the 2x2x2 window at this low corner.
+__device__ __forceinline__ bool block_empty(const VolArgs& V, long long gx, long long gy,
+                                            long long gz, int back) {
+  const int x = max(brick_of(gx, V.X1) - (back & 1), 0);
+  const int y = max(brick_of(gy, V.Y1) - ((back >> 1) & 1), 0);
+  const int z = max(brick_of(gz, V.Z1) - (back >> 2), 0);
+  return __ldg(V.occ + (x * V.NBy + y) * V.NBz + z) == 0;
 }
 
 struct TfArgs {
@@ -962,18 +970,19 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       held = c.cell;
       shade(d, i, kStore);
     };
-    // Empty-space skip (band tape): a block of 32 samples (one tape word) that starts in
-    // an empty brick stays within 7 cells of it when 31 |step| < 7 cells per axis, so every
-    // sample reads an all-zero record: d = 0, band bit 0 and -- when tau(0) = aff_a <= 0 --
-    // an optical depth of exactly 0.  The block's word is stored as 0 and the march moves
-    // on 32 steps: the same S, image and tape as marching it.
-    constexpr long long kSkipStep = (7LL << 32) / 31;
-    const bool skip = BITS && V.empty != nullptr && aff_a <= 0.f &&
+    // Empty-space skip (band tape): when every sample of a block of 32 (one tape word)
+    // lies in unoccupied bricks, each reads an all-zero record: d = 0, band bit 0 and --
+    // when tau(0) = aff_a <= 0 -- an optical depth of exactly 0.  The block's word is
+    // stored as 0 and the march moves on 32 steps: the same S, image and tape as
+    // marching it.
+    constexpr long long kSkipStep = (8LL << 32) / 31;   // 31 steps < 8 cells per axis
+    const bool skip = BITS && V.occ != nullptr && aff_a <= 0.f &&
                       llabs(r.gs[0]) < kSkipStep && llabs(r.gs[1]) < kSkipStep &&
                       llabs(r.gs[2]) < kSkipStep;
+    const int back = (r.gs[0] < 0 ? 1 : 0) | (r.gs[1] < 0 ? 2 : 0) | (r.gs[2] < 0 ? 4 : 0);
     if (BITS && skip) {
       for (int i0 = 0; i0 < r.n; i0 += 32) {
-        if (brick_empty(V, gx, gy, gz)) {
+        if (block_empty(V, gx, gy, gz, back)) {
           if (i0 + 32 <= r.n) bits[bits_off + i0] = 0u;   // word i0/32 (a last partial
           gx += 32 * r.gs[0]; gy += 32 * r.gs[1]; gz += 32 * r.gs[2];   // word: after the loop)
           if (i0 + 32 < r.n) {

@@ -253,7 +253,7 @@ def test_band_tape_bytes_and_limits(lib):
     vol, tf, prm = _descs(dt=0.01, W=512, H=512)
     words = math.ceil((math.floor(math.sqrt(3.0) / 0.01) + 3) / 32)
     assert lib.ddvr_band_tape_bytes(ctypes.byref(vol), 64, ctypes.byref(prm)) == \
-        32 * 32 * 64 * 256 * words * 4 + 256   # + the empty-brick map (1 brick, 256-aligned)
+        32 * 32 * 64 * 256 * words * 4 + 256   # + the brick occupancy maps (1 brick, 256-aligned)
     loss = ctypes.c_double(0)
     vol.cells = 32
     call = lambda v, p, nv, ws: lib.ddvr_forward_adjoint_l1(  # noqa: E731

@@ -301,10 +301,10 @@ def test_band_tape_skips_empty_blocks_exactly(cuda, n, dt_vox):
 
 
 def _brick_map_np(vol: np.ndarray) -> np.ndarray:
-    """The empty-brick map the fused band-tape step builds (ddvr_abi.cu
-    brick_occupancy_kernel / brick_dilate_kernel), restated: padded cell s (storage
-    index, cell s-1) is occupied when one of its edge-clamped corners is nonzero;
-    brick b = cells [8b, 8b+8) per axis; empty = the brick and its neighbours unoccupied."""
+    """The brick occupancy map the fused band-tape step builds (ddvr_abi.cu
+    brick_occupancy_kernel), restated: padded cell s (storage index, cell s-1) is
+    occupied when one of its edge-clamped corners is nonzero; brick b = cells
+    [8b, 8b+8) per axis."""
     nz = np.pad(vol != 0, 1, mode="edge")          # padded[p] = voxel clamp(p-1)
     cell = np.zeros(tuple(d + 1 for d in vol.shape), bool)
     for dx in (0, 1):
@@ -315,23 +315,17 @@ def _brick_map_np(vol: np.ndarray) -> np.ndarray:
     occ = np.zeros(nb, bool)
     for b in np.ndindex(*nb):
         occ[b] = cell[8 * b[0]:8 * b[0] + 8, 8 * b[1]:8 * b[1] + 8, 8 * b[2]:8 * b[2] + 8].any()
-    dil = np.pad(occ, 1)
-    empty = np.ones(nb, bool)
-    for dx in range(3):
-        for dy in range(3):
-            for dz in range(3):
-                empty &= ~dil[dx:dx + nb[0], dy:dy + nb[1], dz:dz + nb[2]]
-    return empty
+    return occ
 
 
 @pytest.mark.parametrize("dt_vox", [0.2, 0.11, 0.5])
 def test_band_tape_empty_brick_skip_is_exact(cuda, dt_vox):
-    """The march's empty-space skip (32-sample blocks that start in an empty brick)
-    changes nothing: image and optical depth bitwise, the band tape bitwise, the loss
-    and the density gradient to atomic-order rounding -- against the same call with
-    DDVR_FLAG_NO_EMPTY_SKIP.  The brick map itself equals the numpy restatement and
-    has empty bricks, and the gradient matches the oracle.  dt 0.5 voxel: 31 steps
-    exceed 7 cells, so those rays march every block."""
+    """The march's empty-space skip (32-sample blocks whose samples all lie in
+    unoccupied bricks) changes nothing: image and optical depth bitwise, the band tape
+    bitwise, the loss and the density gradient to atomic-order rounding -- against the
+    same call with DDVR_FLAG_NO_EMPTY_SKIP.  The occupancy map itself equals the numpy
+    restatement, and the gradient matches the oracle.  dt 0.5 voxel: a block can span
+    more than 8 cells on an axis, so those rays march every block."""
     import ctypes
     import torch
     from oracle import dvr_oracle as O
@@ -372,12 +366,12 @@ def test_band_tape_empty_brick_skip_is_exact(cuda, dt_vox):
         raw = ws.view(torch.uint8).cpu().numpy()
         out[skip] = dict(img=img.cpu().numpy(), depth=depth.cpu().numpy(), loss=loss.item(),
                          dv=dv.double().cpu().numpy(), tape=raw[base:base + band - map_bytes],
-                         empty=raw[base + band - map_bytes + nb:base + band - map_bytes + 2 * nb])
+                         occ=raw[base + band - map_bytes:base + band - map_bytes + nb])
     a, b = out[True], out[False]
     want_map = _brick_map_np(est_np).ravel()
     assert want_map.any() and not want_map.all()
-    np.testing.assert_array_equal(a["empty"].astype(bool), want_map)
-    assert not b["empty"].any()      # NO_EMPTY_SKIP builds no map
+    np.testing.assert_array_equal(a["occ"].astype(bool), want_map)
+    assert not b["occ"].any()        # NO_EMPTY_SKIP builds no map
     np.testing.assert_array_equal(a["img"], b["img"])
     np.testing.assert_array_equal(a["depth"], b["depth"])
     np.testing.assert_array_equal(a["tape"], b["tape"])
