@@ -441,7 +441,7 @@ def run_own(args, cfg):
             note += (f"; ncu measures {traffic / adj_bytes:.2f}x those bytes of DRAM traffic per "
                      "launch (L1/L2 reuse), so frac > 1 is reuse, not missing work; the "
                      "limiters are instruction issue and L1 wavefronts (record gathers, "
-                     "cell-run vector reds): profiles/r01_ncu_c4_full_fused_tape.txt")
+                     "cell-run vector reds): profiles/r01_ncu_c4_full_fused_skip.txt")
         if fused:
             kernels = {
                 "pack_cells": {"ms": fwd_s * 1e3},
