@@ -354,20 +354,25 @@ def test_band_tape_empty_brick_skip_is_exact(cuda, dt_vox):
     nb = ((n + 8) >> 3) ** 3
     map_bytes = (2 * nb + 255) & ~255
     out = {}
-    for skip in (True, False):
-        ws = torch.zeros((base + band) // 4, dtype=torch.float32, device=cuda)
+    for skip in (True, False, "no map"):
+        # "no map": a workspace that ends after the tape (the map is optional)
+        size = base + band - (map_bytes if skip == "no map" else 0)
+        ws = torch.zeros(size // 4, dtype=torch.float32, device=cuda)
         img = torch.empty(6, rig.band_rows, rig.width, 4, dtype=torch.float32, device=cuda)
         depth = torch.empty(6, rig.band_rows, rig.width, dtype=torch.float32, device=cuda)
         loss = torch.zeros(1, dtype=torch.float64, device=cuda)
         dv = torch.zeros_like(est)
         R.forward_adjoint_l1(est, tex, cams, dt, rig, refs, float(refs.numel()), N.TARGET_VOLUME,
                              cells=cells, loss=loss, d_volume=dv, workspace=ws, image_out=img,
-                             depth_out=depth, band_tape=True, empty_skip=skip)
+                             depth_out=depth, band_tape=True, empty_skip=skip is True)
         raw = ws.view(torch.uint8).cpu().numpy()
         out[skip] = dict(img=img.cpu().numpy(), depth=depth.cpu().numpy(), loss=loss.item(),
                          dv=dv.double().cpu().numpy(), tape=raw[base:base + band - map_bytes],
                          occ=raw[base + band - map_bytes:base + band - map_bytes + nb])
     a, b = out[True], out[False]
+    c = out["no map"]
+    np.testing.assert_array_equal(a["img"], c["img"])
+    np.testing.assert_array_equal(a["tape"], c["tape"])
     want_map = _brick_map_np(est_np).ravel()
     assert want_map.any() and not want_map.all()
     np.testing.assert_array_equal(a["occ"].astype(bool), want_map)
