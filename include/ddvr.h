@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define DDVR_ABI_VERSION 3
+#define DDVR_ABI_VERSION 4
 
 typedef enum {
   DDVR_OK = 0,
@@ -147,6 +147,12 @@ typedef struct {
                             tape[ray * tape_stride + i]; the adjoint then reads it
                             instead of inverting.  NULL = inversion mode (default). */
   int64_t tape_stride;   /* >= max step count of any ray of the call */
+  uint64_t* stats;       /* (device, nullable) 4 counters ADDED to by ddvr_forward_adjoint_l1
+                            (measurement only): [0] samples of the call (sum of the
+                            rays' step counts), [1] samples the march stepped over in
+                            empty bricks, [2] samples the band-tape walk stepped over
+                            (all-zero tape words), [3] rays.  Samples marched =
+                            [0] - [1]; samples walked = [0] - [2]. */
 } ddvr_params;
 
 /* Front-to-back march of every view.  image_out (device) (V, rows, W, 4);

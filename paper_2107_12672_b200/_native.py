@@ -19,7 +19,7 @@ from .errors import (
 
 LIB_PATH = os.environ.get("DDVR_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                       "libddvr.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 TARGET_CAMERA = 1
 TARGET_STEPSIZE = 2
@@ -71,7 +71,8 @@ class DdvrParams(ctypes.Structure):
     _fields_ = [("dt", ctypes.c_double), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
                 ("row0", ctypes.c_int32), ("row1", ctypes.c_int32),
                 ("early_stop", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("tape", ctypes.c_void_p), ("tape_stride", ctypes.c_int64)]
+                ("tape", ctypes.c_void_p), ("tape_stride", ctypes.c_int64),
+                ("stats", ctypes.c_void_p)]
 
 
 class DdvrAdam(ctypes.Structure):

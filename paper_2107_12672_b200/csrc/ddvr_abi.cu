@@ -326,6 +326,7 @@ int make_geo(const ddvr_camera* cams, int n_views, const ddvr_params* p, Geometr
   G.partials = nullptr;
   G.bits = nullptr;
   G.bits_words = 0;
+  G.stats = reinterpret_cast<unsigned long long*>(p->stats);
   if (G.tape && G.tape_stride < 0)
     return set_error(DDVR_INVALID_PARAMETER, "negative tape stride");
   return DDVR_OK;

@@ -141,6 +141,8 @@ struct Geometry {
   unsigned* bits;         // DDVR_FLAG_BAND_TAPE: the fused absorption step's band bits,
                           // bits_words 32-bit words per ray, warp-interleaved (nullable)
   int bits_words;
+  unsigned long long* stats;   // ddvr_params.stats (nullable): [samples, march skipped,
+                               // walk skipped, rays], one atomic per warp
 };
 
 // Launchers with external linkage: each is defined (with its kernel
@@ -885,7 +887,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
                                           double& depth, float aff_a = 0.f, float aff_b = 0.f,
                                           unsigned* __restrict__ bits = nullptr,
-                                          unsigned bits_off = 0u) {
+                                          unsigned bits_off = 0u, int* nskip = nullptr) {
   // T (transmittance, accurate as T -> 0) and A (alpha, accurate as A -> 0)
   // are both carried; A += T*a is the reference's A += (1-A)*a (renderer.py:350-355).
   // S, the ray's optical depth (T = exp(-S)), is summed in fp64 for the adjoint.
@@ -983,6 +985,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     if (BITS && skip) {
       for (int i0 = 0; i0 < r.n; i0 += 32) {
         if (block_empty(V, gx, gy, gz, back)) {
+          if (nskip) *nskip += min(32, r.n - i0);
           if (i0 + 32 <= r.n) bits[bits_off + i0] = 0u;   // word i0/32 (a last partial
           gx += 32 * r.gs[0]; gy += 32 * r.gs[1]; gz += 32 * r.gs[2];   // word: after the loop)
           if (i0 + 32 < r.n) {
@@ -1033,7 +1036,7 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
                                                bool warp_inside, bool emit, int mode,
                                                float4& rgba, double& S, const unsigned* info,
                                                unsigned* __restrict__ bits = nullptr,
-                                               unsigned bits_off = 0u) {
+                                               unsigned bits_off = 0u, int* nskip = nullptr) {
   // the affine-tau variant serves emission-free texel TFs without tape / early stop
   const bool aff = !EARLY && !TAPE && !emit && info[2] == 0u;
   const float aa = __uint_as_float(info[3]), ab = __uint_as_float(info[4]);
@@ -1053,7 +1056,7 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
 #define DDVR_MARCH_BITS(SEG, INS)                                                          \
   march_ray<EARLY, CELLS, TAPE, SEG, INS, false, kTfTexture, true, true>(V, TFA, dt32, r, tape, \
                                                                           rgba, S, aa, ab, bits, \
-                                                                          bits_off)
+                                                                          bits_off, nskip)
   if (ABS_ONLY && CELLS && !EARLY && !TAPE && bits) {   // (the caller checked the band walk)
     if (warp_inside) {
       if (mode == kSegP3) DDVR_MARCH_BITS(kSegP3, true); else DDVR_MARCH_BITS(kSegP7, true);
@@ -1473,7 +1476,7 @@ template <bool INSIDE>
 __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, float abs_k,
                                               const unsigned* __restrict__ bits,
                                               unsigned bits_off, float* __restrict__ d_cells,
-                                              AdjState& st) {
+                                              AdjState& st, int* nskip = nullptr) {
   // Blocks of 32 samples (one tape word), back to front.  A block whose word is 0
   // adds nothing and is skipped whole: the open cell run is kept, and the first
   // sample of a later block in another cell flushes it -- the flush the
@@ -1482,7 +1485,10 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
   constexpr int kUnroll = DDVR_BITS_WALK_UNROLL;   // (pragma arguments are not macro-expanded)
   for (int blk = (r.n - 1) >> 5; blk >= 0; --blk) {
     unsigned word = bits[bits_off + ((unsigned)blk << 5)];
-    if (word == 0u) continue;
+    if (word == 0u) {
+      if (nskip) *nskip += min(32, r.n - (blk << 5));
+      continue;
+    }
     const int i1 = min(r.n - 1, (blk << 5) + 31);   // the block's last sample
     long long gx = r.g0[0] + (long long)i1 * r.gs[0];
     long long gy = r.g0[1] + (long long)i1 * r.gs[1];
@@ -1592,13 +1598,15 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   const unsigned bits_off =
       ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * kWarps +
        (threadIdx.x >> 5)) * 32u * (unsigned)G.bits_words + (threadIdx.x & 31);
+  int march_skip = 0, walk_skip = 0;   // measurement counters (G.stats)
   if (FUSED) {   // forward march (renderer.py:306-357) + L1 seed (objectives.py:38-54)
     double loss_part = 0.0;
     if (valid) {
       float4 rgba;
       march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
                                                      s_info[1] != 0u, mode, rgba, S, s_info,
-                                                     kBitsKernel ? bits : nullptr, bits_off);
+                                                     kBitsKernel ? bits : nullptr, bits_off,
+                                                     kBitsKernel ? &march_skip : nullptr);
       const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[pix];
       const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
                   dw = rgba.w - ref.w;
@@ -1642,8 +1650,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   else DDVR_WALK_AFF(kSegP7, INS);
   if (kBitsKernel && bits) {
     const float abs_k = sd.w * (float)exp(-S) * G.dt32 * TFA.fR * __uint_as_float(s_info[4]);
-    if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, bits_off, d_cells, st);
-    else abs_bits_walk<false>(V, r, abs_k, bits, bits_off, d_cells, st);
+    if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
+    else abs_bits_walk<false>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
   } else if (ROLE == 1 && aff_walk) {
     if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
   } else if (ROLE == 1) {
@@ -1669,6 +1677,14 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 #undef DDVR_WALK_GEN
 #undef DDVR_WALK
 
+  if (FUSED && G.stats) {   // measurement only: one atomic per warp and counter
+    const unsigned long long c[4] = {
+        warp_sum((unsigned long long)(valid ? r.n : 0)), warp_sum((unsigned long long)march_skip),
+        warp_sum((unsigned long long)walk_skip), warp_sum((unsigned long long)(valid ? 1 : 0))};
+    if ((threadIdx.x & 31) == 0)
+      for (int k = 0; k < 4; ++k)
+        if (c[k]) atomicAdd(G.stats + k, c[k]);
+  }
   // ---- flush per-ray accumulators ----
   if (kVol && st.run_cell != kNoRun)
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,

@@ -4,13 +4,17 @@ The reference sums per-view gradients in view order on one host
 (``_volume_loss_and_grad``, tasks.py:397-432; TF variant tasks.py:258-270).
 Here views are dealt round-robin to ranks (rank r takes views r, r+N, ...),
 every rank renders and differentiates its own views with the replicated
-volume and TF, and ONE all-reduce(sum) over a flat fp32 buffer
+volume and TF, and the sums are combined by an all-reduce over two flat
+buffers:
 
-    [ d_volume (X*Y*Z) | d_tf (R*4) | d_stepsize (1) | loss (1) ]
+    buf  fp32  [ d_volume (X*Y*Z) ]                      (the large one)
+    tail fp64  [ d_tf (R*4) | d_stepsize (1) | loss (1) ] (a few hundred bytes)
 
-combines them.  The L1 seeds only need the global element count, known
-statically (objectives.py:51-53), so the forward/adjoint need no
-communication at all.  Camera gradients are per view and stay local.
+The tail stays fp64 as the kernels produce it: the reference sums per-view
+gradients in fp64, and the stepsize gradient is cancellation-heavy.  The L1
+seeds only need the global element count, known statically
+(objectives.py:51-53), so the forward/adjoint need no communication at all.
+Camera gradients are per view and stay local.
 
 The packing and the collective are plain torch.distributed, so the same code
 runs with ``gloo`` on CPU tensors in the tests and ``nccl`` on the GPUs.
@@ -37,36 +41,46 @@ def shard_views(n_views: int, rank: int, world: int) -> list[int]:
 
 @dataclass
 class FlatGrads:
-    """One contiguous fp32 buffer holding every all-reduced quantity of a step."""
+    """The all-reduced quantities of a step: ``buf`` fp32 d_volume, ``tail`` fp64
+    [d_tf | d_stepsize | loss] (the kernels accumulate d_tf, d_dt and the loss
+    in fp64 directly into the tail's views)."""
 
     n_vox: int
     n_tf: int
     buf: torch.Tensor
+    tail: torch.Tensor
 
     @classmethod
     def zeros(cls, n_vox: int, n_tf: int, device) -> "FlatGrads":
-        return cls(n_vox, n_tf, torch.zeros(n_vox + n_tf + 2, dtype=torch.float32, device=device))
+        return cls(n_vox, n_tf, torch.zeros(n_vox, dtype=torch.float32, device=device),
+                   torch.zeros(n_tf + 2, dtype=torch.float64, device=device))
 
     @property
     def d_volume(self) -> torch.Tensor:
-        return self.buf[: self.n_vox]
+        return self.buf
 
     @property
     def d_tf(self) -> torch.Tensor:
-        return self.buf[self.n_vox: self.n_vox + self.n_tf]
+        return self.tail[: self.n_tf]
 
     @property
     def d_stepsize(self) -> torch.Tensor:
-        return self.buf[self.n_vox + self.n_tf: self.n_vox + self.n_tf + 1]
+        return self.tail[self.n_tf: self.n_tf + 1]
 
     @property
     def loss(self) -> torch.Tensor:
-        return self.buf[self.n_vox + self.n_tf + 1:]
+        return self.tail[self.n_tf + 1:]
+
+    def zero_(self) -> None:
+        self.buf.zero_()
+        self.tail.zero_()
 
     def allreduce(self, group=None) -> None:
-        """Sum the buffer over all ranks in place (one collective)."""
+        """Sum both buffers over all ranks in place (the fp32 volume gradient and the
+        small fp64 tail; no-op at world size 1)."""
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=group)
+            dist.all_reduce(self.tail, op=dist.ReduceOp.SUM, group=group)
 
 
 class ShardedStep:
@@ -86,6 +100,8 @@ class ShardedStep:
     images / optical depth of the fused step into ``img`` / ``depth``.
     ``deterministic``: camera / stepsize gradients reduced from per-CTA partials in a
     fixed order (DDVR_FLAG_DETERMINISTIC), bitwise reproducible step to step.
+    ``stats`` (fused step, measurement only): (4,) int64 device counters the kernel adds
+    [samples, march-skipped samples, walk-skipped samples, rays] to on every run.
     ``band_tape`` (fused volume-only steps): the march stores one bit per sample
     for the affine absorption walk, which then re-gathers no cell records
     (DDVR_FLAG_BAND_TAPE; 4.7 GB at C4).  "auto" uses it when it fits
@@ -97,8 +113,9 @@ class ShardedStep:
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
                  group=None, layout="cells", fused="auto", keep_images=False, chunks=4,
-                 deterministic=False, band_tape="auto", empty_skip=True):
+                 deterministic=False, band_tape="auto", empty_skip=True, stats=None):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
+        R.validate_cameras(lonlat, radius, fov_y_deg)   # field.py:147-156
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0
         for t in targets:
@@ -111,17 +128,20 @@ class ShardedStep:
         self.img = torch.empty(V, rig.band_rows, rig.width, 4, dtype=torch.float32, device=dev)
         self.seed = torch.empty_like(self.img)
         self.depth = torch.empty(V, rig.band_rows, rig.width, dtype=torch.float32, device=dev)
-        self.d_tf64 = torch.zeros(texels.shape, dtype=torch.float64, device=dev)
-        self.d_dt64 = torch.zeros(1, dtype=torch.float64, device=dev)
+        # the fp64 outputs are views of the all-reduced tail (no cast, no copy)
+        self.d_tf64 = self.flat.d_tf.view(texels.shape)
+        self.d_dt64 = self.flat.d_stepsize
         # camera gradients are per view (d/d(lon, lat) per degree, field.py:11), so
         # they stay with the rank that owns the view: (V_local, 2), not all-reduced
         self.d_camera = torch.zeros(V, 2, dtype=torch.float64, device=dev)
-        self.loss64 = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.loss64 = self.flat.loss
         # cell records (rebuilt from the density every step) + adjoint workspace
         self.cells = (torch.empty(R.cells_numel(density.shape), dtype=torch.float32, device=dev)
                       if layout == "cells" else None)
         self.deterministic = bool(deterministic)
         self.empty_skip = bool(empty_skip)
+        # measurement counters of the fused step (forward_adjoint_l1 ``stats``)
+        self.stats = stats
         if fused == "auto":
             fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
         self.fused = bool(fused) and self.cells is not None
@@ -180,11 +200,8 @@ class ShardedStep:
         chunks = self._chunks if (self.fused and refs_host is not None) else [slice(None)]
         refs_ready = self._stage_refs(refs_host, chunks)
         f = self.flat
-        f.buf.zero_()
-        self.d_tf64.zero_()
-        self.d_dt64.zero_()
+        f.zero_()
         self.d_camera.zero_()
-        self.loss64.zero_()
         V = self.cams.shape[0]
         if V and self.fused:
             R.pack_cells(self.density, self.cells)
@@ -209,7 +226,7 @@ class ShardedStep:
                     ws_continue=k > 0 and self.workspace is not None,
                     ws_defer=not last and self.workspace is not None,
                     deterministic=self.deterministic, band_tape=self.band_tape,
-                    empty_skip=self.empty_skip)
+                    empty_skip=self.empty_skip, stats=self.stats)
             hook("post_adjoint")
         elif V:
             if self.cells is not None:
@@ -242,9 +259,6 @@ class ShardedStep:
                                      self.workspace.numel() * 4 if self.workspace is not None
                                      else 0, st))
             hook("post_adjoint")
-        f.d_tf.copy_(self.d_tf64.reshape(-1))
-        f.d_stepsize.copy_(self.d_dt64)
-        f.loss.copy_(self.loss64)
         f.allreduce(self.group)
         return f
 
@@ -256,14 +270,22 @@ class TomographyIteration:
     volume smoothness prior (objectives.py:72-92, weight ``lam``), one Adam
     update and the [0,1] projection (optim.py:45-89).  Every rank applies the
     same update to its replica after the all-reduce, so replicas stay equal.
+
+    ``check_finite`` (default on, optim.py:28-30): a non-finite gradient skips the
+    update on the device (sticky flag) and raises NumericalAbortError on the host
+    without a per-iteration synchronisation -- the flag is copied to pinned host
+    memory after each iteration and checked at the start of the next ``run`` once
+    that copy has landed, or by ``check()``, which waits for it.
     """
 
     def __init__(self, step: ShardedStep, *, lr: float = 0.02, lam: float = 0.5,
-                 check_finite: bool = False, graph: bool = False):
+                 check_finite: bool = True, graph: bool = False):
         from .optim import AdamState
         self.step = step
         self.lam = lam
         self.check_finite = check_finite
+        self._flag_host = None
+        self._flag_evt = None
         # graph: after two eager warm-up iterations one iteration is captured in a
         # CUDA graph and replayed (launch-bound small problems); single process
         # only, Adam's step counter lives on the device
@@ -280,6 +302,48 @@ class TomographyIteration:
     def run(self, hook=None, refs_host=None):
         """One iteration -> (loss (1,) f64, prior (1,) f64) on device.  With ``graph``
         the hook and refs_host are not available (the graph replays fixed work)."""
+        self._raise_if_flagged(block=False)
+        out = self._run(hook, refs_host)
+        self._post_flag()
+        return out
+
+    def check(self) -> None:
+        """Wait for the last iteration's non-finite flag; raise NumericalAbortError
+        if any iteration so far saw a non-finite gradient."""
+        self._raise_if_flagged(block=True)
+
+    def reset(self, density=None) -> None:
+        """Restore a fixed state (measurement): optionally copy ``density`` into the
+        optimised volume, and zero the Adam moments and step counter."""
+        if density is not None:
+            self.step.density.copy_(density)
+        self.adam.reset()
+
+    def _post_flag(self):
+        if not self.check_finite or self.adam.flag is None:
+            return
+        dev = self.step.density.device
+        if self._flag_host is None:
+            self._flag_host = torch.zeros(1, dtype=torch.int32,
+                                          pin_memory=dev.type == "cuda")
+            self._flag_evt = torch.cuda.Event() if dev.type == "cuda" else None
+        self._flag_host.copy_(self.adam.flag, non_blocking=True)
+        if self._flag_evt is not None:
+            self._flag_evt.record()
+
+    def _raise_if_flagged(self, block):
+        from .errors import NumericalAbortError
+        if self._flag_host is None:
+            return
+        if self._flag_evt is not None:
+            if block:
+                self._flag_evt.synchronize()
+            elif not self._flag_evt.query():
+                return
+        if int(self._flag_host[0]):
+            raise NumericalAbortError("non-finite gradients passed to the optimizer")
+
+    def _run(self, hook, refs_host):
         if not self.graph:
             return self._iterate(hook, refs_host)
         if hook is not None or refs_host is not None:
@@ -305,5 +369,6 @@ class TomographyIteration:
         density = self.step.density
         grad = f.d_volume.view(density.shape)
         prior = prior_volume(density, self.lam, grad)      # grad += lam * d prior
-        self.adam.update(density, grad, project="volume", check_finite=self.check_finite)
+        self.adam.update(density, grad, project="volume",
+                         check_finite="defer" if self.check_finite else False)
         return f.loss, prior

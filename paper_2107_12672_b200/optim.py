@@ -72,13 +72,24 @@ class AdamState:
     device_step: bool = False
     state: torch.Tensor | None = field(default=None, repr=False)
 
+    def reset(self) -> None:
+        """Back to the state before the first update (moments zeroed, t = 0), keeping
+        the buffers (and any CUDA graph that captured them) in place."""
+        self.step = 0
+        for t in (self.m, self.v, self.flag, self.state):
+            if t is not None:
+                t.zero_()
+
     def update(self, params: torch.Tensor, grads: torch.Tensor, project: str | None = None,
-               tau_max: float = TAU_MAX_DEFAULT, check_finite: bool = True) -> None:
+               tau_max: float = TAU_MAX_DEFAULT, check_finite=True) -> None:
         """One in-place Adam step + projection (``volume``: [0,1]; ``tf``: rgb >= 0,
         tau in [0, tau_max]; None: unconstrained).  Raises NumericalAbortError
         (and leaves the parameters untouched) on a non-finite gradient; with
         ``device_step`` the update is still skipped on the device but nothing is
-        raised (no host synchronisation)."""
+        raised (no host synchronisation).  ``check_finite="defer"``: no host
+        synchronisation either; the device flag ``self.flag`` is sticky (never
+        re-zeroed), so once set every later update is skipped too, and the
+        caller raises when it reads the flag (TomographyIteration)."""
         _require(params, "params", torch.float32)
         _require(grads, "grads", torch.float32)
         if params.shape != grads.shape:
@@ -97,7 +108,8 @@ class AdamState:
         else:
             raise InvalidParameterError(f"unknown projection target {project!r}")
         a = N.DdvrAdam(self.lr, self.beta1, self.beta2, self.eps, self.step + 1, *cfg)
-        if check_finite:
+        defer = check_finite == "defer"
+        if check_finite and not defer:
             self.flag.zero_()
         if self.device_step:
             if self.state is None:
@@ -112,7 +124,7 @@ class AdamState:
                                        self.v.data_ptr(), params.numel(), ctypes.byref(a),
                                        self.flag.data_ptr() if check_finite else None,
                                        _stream_ptr()))
-        if check_finite and int(self.flag.item()):
+        if check_finite and not defer and int(self.flag.item()):
             raise NumericalAbortError("non-finite gradients passed to the optimizer")
         self.step += 1
 

@@ -272,7 +272,7 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
                        *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
                        workspace=None, image_out=None, depth_out=None, ws_continue=False,
                        ws_defer=False, deterministic=False, band_tape=False,
-                       empty_skip=True):
+                       empty_skip=True, stats=None):
     """One fused step over these views: forward march, L1 seed sign(image - ref)/count
     and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
     device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
@@ -283,7 +283,9 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
     which then gathers no records (DDVR_FLAG_BAND_TAPE, volume target); with it the
     march skips 32-sample blocks in all-zero bricks unless ``empty_skip`` is False
     (DDVR_FLAG_NO_EMPTY_SKIP; bitwise the same outputs either way).  A
-    caller-provided workspace needs those extra bytes too (extra_workspace_bytes)."""
+    caller-provided workspace needs those extra bytes too (extra_workspace_bytes).
+    ``stats`` (measurement, optional): (4,) int64 device tensor the kernel adds
+    [samples, samples the march skipped, samples the walk skipped, rays] to."""
     _require(cams, "cameras", torch.float64, ndim=2)
     if cells is None:
         raise InvalidParameterError("the fused step needs cell records (pack_cells)")
@@ -308,6 +310,11 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
     prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0) \
         | (N.FLAG_DETERMINISTIC if deterministic else 0) | (N.FLAG_BAND_TAPE if band_tape else 0) \
         | (0 if empty_skip else N.FLAG_NO_EMPTY_SKIP)
+    if stats is not None:
+        _require(stats, "stats", torch.int64)
+        if stats.numel() < 4:
+            raise InvalidInputError("stats needs 4 int64 counters")
+        prm.stats = stats.data_ptr()
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     ws_bytes = workspace.numel() * 4 if workspace is not None else 0
     N.check(N.lib().ddvr_forward_adjoint_l1(
@@ -475,4 +482,7 @@ def render_views(density, texels, lonlat, dt, rig: Rig, *, radius=2.0, center=(0
         raise InvalidParameterError("stepsize must be positive")
     if layout not in ("cells", "voxels"):
         raise InvalidParameterError(f"unknown volume layout {layout!r}")
+    # field.py:147-156: a latitude at the pole degenerates the camera frame (NaN images
+    # and gradients), so it is rejected here like the reference's SphericalCamera does
+    validate_cameras(lonlat, radius, fov_y_deg)
     return DiffDVR.apply(density, texels, lonlat, dt, rig, radius, center, fov_y_deg, layout)

@@ -95,6 +95,24 @@ def test_camera_validation():   # field.py:147-156
     assert vd.SphericalCamera(-30.0, 0.0, 2.0).lon_deg == 330.0
 
 
+@pytest.mark.parametrize("ll,radius,fov", [((0.0, 90.0), 2.0, 30.0), ((0.0, -89.9995), 2.0, 30.0),
+                                           ((0.0, 0.0), 0.0, 30.0), ((0.0, 0.0), 2.0, 180.0)])
+def test_tensor_path_validates_cameras(ll, radius, fov):
+    """render_views / ShardedStep reject the cameras SphericalCamera rejects (field.py:147-156)
+    before any GPU work (a pole latitude would degenerate the frame into NaNs)."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    lonlat = torch.tensor([ll], dtype=torch.float64)
+    vol = torch.zeros(4, 4, 4)
+    tex = torch.zeros(2, 4)
+    with pytest.raises(vd.InvalidParameterError):
+        R.render_views(vol, tex, lonlat, 0.1, R.Rig(4, 4), radius=radius, fov_y_deg=fov)
+    with pytest.raises(vd.InvalidParameterError):
+        ShardedStep(vol, tex, lonlat, torch.zeros(1, 4, 4, 4), 0.1, R.Rig(4, 4), radius=radius,
+                    fov_y_deg=fov)
+
+
 def test_volume_and_tf_validation():
     with pytest.raises(vd.InvalidParameterError):
         vd.DensityVolume(np.zeros((2, 2)))

@@ -39,9 +39,12 @@ def test_flatgrads_views():
     f.d_tf[:] = 2.0
     f.d_stepsize[:] = 3.0
     f.loss[:] = 4.0
-    assert f.buf.shape == (20,)
-    assert f.buf[:10].sum() == 10 and f.buf[10:18].sum() == 16
-    assert f.buf[18] == 3 and f.buf[19] == 4
+    assert f.buf.shape == (10,) and f.buf.dtype == torch.float32
+    assert f.tail.shape == (10,) and f.tail.dtype == torch.float64
+    assert f.buf.sum() == 10 and f.tail[:8].sum() == 16
+    assert f.tail[8] == 3 and f.tail[9] == 4
+    f.zero_()
+    assert f.buf.abs().sum() == 0 and f.tail.abs().sum() == 0
 
 
 def _scene():
@@ -68,7 +71,7 @@ def _rank_grads(rank, world):
         seed = np.sign(img - refs[v]) / count
         g = O.adjoint_view(grid, tex, views[v], dt, seed, ["volume", "tf", "stepsize"], image=img)
         flat.d_volume.add_(torch.from_numpy(g["d_volume"].ravel().astype(np.float32)))
-        flat.d_tf.add_(torch.from_numpy(g["d_tf"].ravel().astype(np.float32)))
+        flat.d_tf.add_(torch.from_numpy(g["d_tf"].ravel()))
         flat.d_stepsize.add_(float(g["d_stepsize"]))
     flat.loss.add_(loss)
     return flat
@@ -82,7 +85,7 @@ def _worker(rank, world, port, out_path):
         flat = _rank_grads(rank, world)
         flat.allreduce()
         if rank == 0:
-            torch.save(flat.buf, out_path)
+            torch.save((flat.buf, flat.tail), out_path)
     finally:
         dist.destroy_process_group()
 
@@ -97,9 +100,11 @@ def test_allreduce_equals_single_process_sum(tmp_path):
     world = 2
     out = str(tmp_path / "buf.pt")
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
-    got = torch.load(out)
-    ref = _rank_grads(0, 1).buf          # one process, every view
-    assert torch.allclose(got, ref, rtol=1e-5, atol=1e-7)
+    got, got_tail = torch.load(out)
+    full = _rank_grads(0, 1)             # one process, every view
+    assert torch.allclose(got, full.buf, rtol=1e-5, atol=1e-7)
+    # the fp64 tail is summed in fp64 (no fp32 round trip)
+    assert torch.allclose(got_tail, full.tail, rtol=1e-12, atol=1e-15)
     # and the shards really split the work: each rank alone is not the total
-    part = _rank_grads(0, world).buf
-    assert not torch.allclose(part, ref)
+    part = _rank_grads(0, world)
+    assert not torch.allclose(part.buf, full.buf)

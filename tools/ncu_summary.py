@@ -1,10 +1,16 @@
 """Summarise an ncu report (.ncu-rep) into the per-kernel numbers DESIGN.md cites.
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--samples N] > profiles/x.txt
+    python tools/ncu_summary.py rep --samples N --kernel dvr_adjoint \
+        --json-out profiles/ncu_r02.json --key C4/fused_tape [--file profiles/x.txt]
 
 --samples: samples processed by each dvr_* launch in the report, to print
-per-sample instruction and wavefront counts.
+per-sample instruction and wavefront counts.  --json-out/--key: merge the
+numbers of the first launch whose name contains --kernel into the JSON file
+bench.py reads for its roofline (achieved = these DRAM bytes / live launch time).
 """
+import json
+import os
 
 from __future__ import annotations
 
@@ -37,6 +43,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("--samples", type=float, default=0.0)
+    ap.add_argument("--json-out")
+    ap.add_argument("--key")
+    ap.add_argument("--kernel", default="dvr_")
+    ap.add_argument("--file", default="", help="the summary file this entry is cited from")
+    ap.add_argument("--state", default="bench.py fixed dense state (iteration 1)")
     args = ap.parse_args()
     out = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"],
                          capture_output=True, text=True, check=True).stdout
@@ -50,6 +61,9 @@ def main():
                 i = head.index(key)
                 vals[key] = r[i]
                 print(f"   {label:26s} {r[i]:>22s} {units[i]}")
+        if args.json_out and args.key and args.kernel in r[head.index("Kernel Name")]:
+            _merge_json(args, vals, units, head, r)
+            args.json_out = None
         if args.samples and "smsp__inst_executed.sum" in vals:
             try:
                 warp_samples = args.samples / 32.0
@@ -57,6 +71,45 @@ def main():
                 print(f"   {'warp-inst / warp-sample':26s} {inst / warp_samples:22.1f}")
             except ValueError:
                 pass
+
+
+def _num(v):
+    return float(str(v).replace(",", ""))
+
+
+def _merge_json(args, vals, units, head, row):
+    """One launch's numbers, normalised to bytes / ms / per-sample, into --json-out."""
+    def unit_scale(key):
+        u = units[head.index(key)]
+        return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(u, 1.0)
+    g = lambda k: _num(vals[k]) * unit_scale(k)  # noqa: E731
+    dur_ms = g("gpu__time_duration.sum")
+    e = {"kernel": row[head.index("Kernel Name")][:120], "state": args.state,
+         "file": args.file, "duration_ms": dur_ms,
+         "dram_bytes": g("dram__bytes_read.sum") + g("dram__bytes_write.sum"),
+         "issue_active_pct": _num(vals["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+         "l1tex_pct": _num(vals["l1tex__throughput.avg.pct_of_peak_sustained_elapsed"]),
+         "l2_pct": _num(vals["lts__throughput.avg.pct_of_peak_sustained_elapsed"]),
+         "dram_pct": _num(vals["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]),
+         "occupancy_pct": _num(vals["sm__warps_active.avg.pct_of_peak_sustained_active"]),
+         "registers": _num(vals["launch__registers_per_thread"])}
+    red = _num(vals.get("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", 0))
+    e["red_requests"] = red
+    e["red_requests_per_s"] = red / (dur_ms / 1e3) if dur_ms else None
+    if args.samples:
+        e["samples"] = args.samples
+        e["warp_inst_per_sample"] = _num(vals["smsp__inst_executed.sum"]) / (args.samples / 32)
+        e["gather_requests_per_sample"] = _num(
+            vals["l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"]) / (args.samples / 32)
+        e["dram_bytes_per_sample"] = e["dram_bytes"] / args.samples
+    d = {}
+    if os.path.exists(args.json_out):
+        with open(args.json_out) as f:
+            d = json.load(f)
+    d[args.key] = e
+    with open(args.json_out, "w") as f:
+        json.dump(d, f, indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
