@@ -83,6 +83,8 @@ def parse(argv=None):
     p.add_argument("--no-band-tape", action="store_true",
                    help="fused absorption step without the 1-bit-per-sample band tape "
                         "(DDVR_FLAG_BAND_TAPE; the walk then re-gathers the cell records)")
+    p.add_argument("--split-walk", action="store_true",
+                   help="band tape: march and walk as two kernels (DDVR_FLAG_SPLIT_WALK)")
     p.add_argument("--dry-run", action="store_true",
                    help="launcher / collective check without kernels (gloo on CPU if no GPU)")
     return p.parse_args(argv)
@@ -429,7 +431,8 @@ def run_own(args, cfg):
         return ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                            total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
                            layout=args.layout, fused=False if args.unfused else "auto",
-                           band_tape=band_tape, empty_skip=not args.no_empty_skip)
+                           band_tape=band_tape, empty_skip=not args.no_empty_skip,
+                           split_walk=args.split_walk)
 
     step = make_step(False if args.no_band_tape else "auto")
     graphed = args.graph and world == 1 and volume_target
@@ -748,6 +751,8 @@ def report(args, cfg, step, runner, world, mine, total_samples, total_rays, loca
                               (", band tape (1 bit/sample, DDVR_FLAG_BAND_TAPE)" if band
                                else "") +
                               (", empty-brick skip in the march" if band and step.empty_skip
+                               else "") +
+                              (", march and walk as two kernels" if band and step.split_walk
                                else "") + (", CUDA-graph replay" if graphed else ""))
     if band:
         from paper_2107_12672_b200 import _native as N

@@ -106,6 +106,7 @@ typedef struct {
 #define DDVR_FLAG_DETERMINISTIC 4
 #define DDVR_FLAG_BAND_TAPE 8
 #define DDVR_FLAG_NO_EMPTY_SKIP 16
+#define DDVR_FLAG_SPLIT_WALK 32
 
 /* march parameters (RenderConfig, renderer.py:84-106) */
 typedef struct {
@@ -141,7 +142,13 @@ typedef struct {
                                                    all-zero 8^3-cell bricks (bitwise
                                                    the same outputs)
                             DDVR_FLAG_NO_EMPTY_SKIP  with DDVR_FLAG_BAND_TAPE: march
-                                                   every block (no brick map) */
+                                                   every block (no brick map)
+                            DDVR_FLAG_SPLIT_WALK   with DDVR_FLAG_BAND_TAPE: march and
+                                                   walk as two kernels (the march
+                                                   hands each ray's walk weight to the
+                                                   walk through the workspace,
+                                                   ddvr_band_tape_bytes); by default
+                                                   one kernel runs both per ray */
   float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
                             forward writes the transmittance before every sample,
                             tape[ray * tape_stride + i]; the adjoint then reads it
@@ -237,7 +244,9 @@ int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t
  * diagonal / dt.  Placed after the workspace (and the deterministic partials),
  * each part rounded up to 256 bytes: the tape, then the brick occupancy maps (2
  * bytes per brick of 8^3 cell records, rebuilt from vol->cells by every call; a
- * workspace that ends before the map runs without the empty-space skip).  Used
+ * workspace that ends before the map runs without the empty-space skip), then a
+ * float per ray (DDVR_FLAG_SPLIT_WALK: the march hands each ray's walk weight to a
+ * separate walk kernel; a workspace that ends before it runs them fused).  Used
  * by the affine absorption walk (emission-free TF with a non-negative affine tau
  * column, volume target); other steps ignore it. */
 int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p);

@@ -17,6 +17,8 @@ Cases (reference call sites in brackets):
 * C1         the full C1 view: image + every target, dense N(0,1) seed
 * C2..C5     row bands of view 0: image band, n_steps, and the config's targets
 * counts     exact per-config sample totals (renderer.py:209-214)
+* C4_step_*, C5_step_*  the fused tomography step at config scale (row bands of a
+             few views): reference images, band images, L1 loss, density gradient
 """
 
 from __future__ import annotations
@@ -176,6 +178,66 @@ def config_cases():
                 out[f"inversion_{t}"] = g
         save(name, **out)
         print(f"  {name}: {time.time() - t0:.1f}s, band samples {int(n.sum())}")
+
+
+# fused-step fixtures at config scale: (views, rows) of each case
+STEP_BANDS = {"C4": ((0, 17), (252, 260)), "C5": ((0,), (508, 516))}
+
+
+def step_cases():
+    """The tomography step the bench times (tasks.py:397-432: render -> l1_loss ->
+    render_adjoint), at the config's full volume and image size on row bands of a few
+    views, computed by the reference: reference images rendered from the truth, the
+    estimate's band images, the L1 loss over the bands (objectives.py:38-54, count =
+    the bands' element count) and the density gradient of that loss.  Estimates:
+    ``dense`` = 0.85 truth + 0.1 U(0,1) (iteration 1 of the bench, no exact zeros) and,
+    for C4, ``sparse`` = the truth's support only (exact zeros outside the object,
+    what the optimisation grows, so the band tape's empty-space skips run)."""
+    rng = np.random.default_rng(99)
+    for name, (views, (r0, r1)) in STEP_BANDS.items():
+        c = CONFIGS[name]
+        truth = c.volume().astype(np.float64)
+        tex = f32(c.texels())
+        ests = {"dense": f32(0.85 * truth + 0.1 * rng.uniform(size=truth.shape))}
+        if name == "C4":
+            ests["sparse"] = f32(np.where(truth > 0, np.clip(0.7 * truth + 0.05, 0, 1), 0.0))
+        T = vd.TransferFunction(tex)
+        poses = c.view_poses()
+        cams = [vd.SphericalCamera(*poses[k], c.radius, fov_y_deg=c.fov, width=c.image,
+                                   height=c.image) for k in views]
+        count = 4 * c.image * (r1 - r0) * len(views)
+        refs = []
+        for cam in cams:
+            u, v = vr._tile_pixels(cam, r0, r1)
+            scene = ("density", vd.DensityVolume(truth), T)
+            o, w, slab = vr._ray_setup(scene, cam, u, v)
+            n = vr._step_counts(slab[0], slab[1], c.dt, slab[4])
+            band, _ = vr._march_fused(scene, o, w, c.dt, slab, n)
+            refs.append(band)
+        for kind, est in ests.items():
+            t0 = time.time()
+            scene = ("density", vd.DensityVolume(est), T)
+            imgs, loss, grad = [], 0.0, np.zeros(est.size)
+            for cam, ref in zip(cams, refs):
+                u, v = vr._tile_pixels(cam, r0, r1)
+                o, w, slab = vr._ray_setup(scene, cam, u, v)
+                n = vr._step_counts(slab[0], slab[1], c.dt, slab[4])
+                band, _ = vr._march_fused(scene, o, w, c.dt, slab, n)
+                loss += float(np.abs(band - ref).sum()) / count     # objectives.py:51-53
+                seed = np.sign(band - ref) / count
+                gs = vr._adjoint_tile(scene, cam, vd.RenderConfig(dt=c.dt, target="volume"),
+                                      seed, (r0, r1), final_rgba=band)
+                grad += np.asarray(gs.d_volume, np.float64).reshape(-1)
+                imgs.append(band.reshape(r1 - r0, c.image, 4))
+            nz = np.flatnonzero(grad)
+            # the estimate is rebuilt by the test from the same generator: store a probe
+            save(f"{name}_step_{kind}", views=np.array(views), rows=np.array([r0, r1]),
+                 texels=tex.astype(np.float32), dt=np.float64(c.dt), count=np.float64(count),
+                 refs=np.stack(refs).reshape(len(views), r1 - r0, c.image, 4).astype(np.float32),
+                 image=np.stack(imgs), loss=np.float64(loss),
+                 est_probe=est.reshape(-1)[:: max(1, est.size // 4096)].copy(),
+                 volume_idx=nz.astype(np.int32), volume_val=grad[nz].astype(np.float32))
+            print(f"  {name} {kind}: {time.time() - t0:.1f}s, loss {loss:.6g}")
 
 
 def count_cases():
@@ -429,3 +491,5 @@ if __name__ == "__main__":
         config_cases()
     if "count" in which:
         count_cases()
+    if "step" in which:
+        step_cases()

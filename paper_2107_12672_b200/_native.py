@@ -33,6 +33,7 @@ FLAG_WS_DEFER = 2
 FLAG_DETERMINISTIC = 4
 FLAG_BAND_TAPE = 8
 FLAG_NO_EMPTY_SKIP = 16
+FLAG_SPLIT_WALK = 32
 TF_TEXTURE = 0
 TF_PIECEWISE = 1
 TF_GAUSSIAN = 2

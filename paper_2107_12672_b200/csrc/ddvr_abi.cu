@@ -327,6 +327,7 @@ int make_geo(const ddvr_camera* cams, int n_views, const ddvr_params* p, Geometr
   G.bits = nullptr;
   G.bits_words = 0;
   G.stats = reinterpret_cast<unsigned long long*>(p->stats);
+  G.ray_k = nullptr;
   if (G.tape && G.tape_stride < 0)
     return set_error(DDVR_INVALID_PARAMETER, "negative tape stride");
   return DDVR_OK;
@@ -732,6 +733,9 @@ static int band_words(const double bmin[3], const double bmax[3], double dt) {
   return (int)std::min<double>((nmax + 31.0) / 32.0, 1 << 26);
 }
 
+// per-ray walk weights of the split band-tape step (one float per thread of the grid)
+static int64_t ray_k_bytes(int64_t ctas) { return (ctas * kThreads * 4 + 255) & ~(int64_t)255; }
+
 static int64_t grid_ctas(int32_t n_views, const ddvr_params* p) {
   const int row1 = p->row1 <= 0 ? p->height : p->row1;
   const int rows = std::max(0, row1 - p->row0);
@@ -743,8 +747,11 @@ int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr
   if (vol->dims[0] < 1 || vol->dims[1] < 1 || vol->dims[2] < 1) return 0;
   const int64_t b = grid_ctas(n_views, p) * kThreads * band_words(vol->box_min, vol->box_max,
                                                                   p->dt) * 4;
-  // the tape, then the empty-brick map (optional: a workspace without it marches every block)
-  return ((b + 255) & ~(int64_t)255) + brick_map_bytes(vol->dims);
+  // the tape, then the empty-brick map (optional: a workspace without it marches every
+  // block), then the per-ray walk weights of the split march / walk kernels (optional:
+  // without them the step runs as one fused kernel)
+  return ((b + 255) & ~(int64_t)255) + brick_map_bytes(vol->dims) +
+         ray_k_bytes(grid_ctas(n_views, p));
 }
 
 int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask) {
@@ -787,7 +794,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                        int32_t flags) {
   int rc;
   if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER | DDVR_FLAG_DETERMINISTIC |
-                DDVR_FLAG_BAND_TAPE | DDVR_FLAG_NO_EMPTY_SKIP))
+                DDVR_FLAG_BAND_TAPE | DDVR_FLAG_NO_EMPTY_SKIP | DDVR_FLAG_SPLIT_WALK))
     return set_error(DDVR_INVALID_PARAMETER, "unknown params.flags bits 0x%x", flags);
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
@@ -834,6 +841,11 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   const int64_t map_off = tape_off + ((ws_band + 255) & ~(int64_t)255);
   const bool brick_map = ws_band > 0 && !(flags & DDVR_FLAG_NO_EMPTY_SKIP) &&
                          workspace_bytes >= map_off + brick_map_bytes(vol->dims);
+  // DDVR_FLAG_SPLIT_WALK: the band-tape step as two kernels (march, walk)
+  const int64_t rayk_off = map_off + brick_map_bytes(vol->dims);
+  if (ws_band > 0 && (flags & DDVR_FLAG_SPLIT_WALK) &&
+      workspace_bytes >= rayk_off + ray_k_bytes((int64_t)grid.x * grid.y * grid.z))
+    G.ray_k = reinterpret_cast<float*>(static_cast<char*>(workspace) + rayk_off);
   if (workspace && ((uintptr_t)workspace & 31) != 0)
     return set_error(DDVR_INVALID_INPUT, "workspace must be 32-byte aligned");
   if (n_views == 0 || G.row1 == G.row0) return DDVR_OK;

@@ -15,6 +15,15 @@ static int adj2(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const
     auto k1 = dvr_adjoint_kernel<M, CELLS, 1, FUSED>;
     set_smem(k1, smem);
     k1<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dcam, ddt, fu);
+    if constexpr (M == DDVR_TARGET_VOLUME && FUSED) {
+      if (G.ray_k) {   // the band-tape step as march + walk kernels (ROLE 1 returns for it)
+        set_smem(dvr_band_march_kernel<0>, smem);
+        dvr_band_march_kernel<0><<<grid, kThreads, smem, st>>>(V, T, G, fu);
+        set_smem(dvr_band_walk_kernel<0>, smem);
+        dvr_band_walk_kernel<0><<<grid, kThreads, smem, st>>>(V, T, G, dcells);
+        return 4;
+      }
+    }
     return 2;
   }
   return 1;

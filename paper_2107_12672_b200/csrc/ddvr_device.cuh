@@ -143,6 +143,8 @@ struct Geometry {
   int bits_words;
   unsigned long long* stats;   // ddvr_params.stats (nullable): [samples, march skipped,
                                // walk skipped, rays], one atomic per warp
+  float* ray_k;           // band-tape step split into march + walk kernels (nullable): the
+                          // march's per-ray walk weight abs_k, (V, rows, W)
 };
 
 // Launchers with external linkage: each is defined (with its kernel
@@ -909,6 +911,9 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // holds its samples in the low bits, the last one at bit 0) sits at bits[32 k]:
   // lane-interleaved, one 128-byte store per warp and word.
   unsigned word = 0u;
+  // BITS: the optical depth of the current 32-sample word in fp32, added to the fp64 S
+  // once per word (32 terms of at most dt*tau_max: ~1e-7 of a word's depth)
+  float Sb = 0.f;
   // one compositing step on a located sample and its record
   auto density = [&](const Cell& c, const float* k) {
     return clamp_density(INSIDE || c.inside, interp(c, k).rho);
@@ -927,7 +932,8 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       }
       const float tau = __fmaf_rn(aff_b, fminf(fmaxf(t, 0.f), TF.fR1), aff_a);   // tau_affine
       const float x = __fmul_rn(dt32, fmaxf(tau, 0.f));
-      S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
+      if (BITS) Sb = __fadd_rn(Sb, SEG == kSegGen ? fminf(x, kNegLnEps) : x);   // per word
+      else S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
       return;
     }
     int i0; float w;
@@ -963,15 +969,17 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     held = c.cell;
     // (the emitting variants spill at 48 registers when unrolled)
     constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : 1;
-    auto step = [&](int i, auto kStore) {
+    // kMore: the next sample exists (known inside whole words but the last)
+    auto step_m = [&](int i, auto kStore, auto kMore) {
       const float d = density(c, v);
       gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
       locate<CELLS>(V, gx, gy, gz, ins, c);
-      const bool more = i + 1 < r.n;
+      const bool more = decltype(kMore)::value || i + 1 < r.n;
       ld256_if(more && c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
       held = c.cell;
       shade(d, i, kStore);
     };
+    auto step = [&](int i, auto kStore) { step_m(i, kStore, std::false_type{}); };
     // Empty-space skip (band tape): when every sample of a block of 32 (one tape word)
     // lies in unoccupied bricks, each reads an all-zero record: d = 0, band bit 0 and --
     // when tau(0) = aff_a <= 0 -- an optical depth of exactly 0.  The block's word is
@@ -982,9 +990,9 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
                       llabs(r.gs[0]) < kSkipStep && llabs(r.gs[1]) < kSkipStep &&
                       llabs(r.gs[2]) < kSkipStep;
     const int back = (r.gs[0] < 0 ? 1 : 0) | (r.gs[1] < 0 ? 2 : 0) | (r.gs[2] < 0 ? 4 : 0);
-    if (BITS && skip) {
+    if (BITS) {   // by tape words (the same arithmetic with and without the skip)
       for (int i0 = 0; i0 < r.n; i0 += 32) {
-        if (block_empty(V, gx, gy, gz, back)) {
+        if (skip && block_empty(V, gx, gy, gz, back)) {
           if (nskip) *nskip += min(32, r.n - i0);
           if (i0 + 32 <= r.n) bits[bits_off + i0] = 0u;   // word i0/32 (a last partial
           gx += 32 * r.gs[0]; gy += 32 * r.gs[1]; gz += 32 * r.gs[2];   // word: after the loop)
@@ -997,12 +1005,15 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
         }
         if (i0 + 32 <= r.n) {   // a whole word: fixed trip count, one store after it
 #pragma unroll kMarchUnroll
-          for (int j = 0; j < 32; ++j) step(i0 + j, std::false_type{});
+          for (int j = 0; j < 31; ++j) step_m(i0 + j, std::false_type{}, std::true_type{});
+          step(i0 + 31, std::false_type{});
           bits[bits_off + i0] = word;
           word = 0u;
         } else {                // the last partial word (stored after the march)
           for (int i = i0; i < r.n; ++i) step(i, std::false_type{});
         }
+        S += (double)Sb;
+        Sb = 0.f;
       }
     } else {
 #pragma unroll kMarchUnroll
@@ -1483,8 +1494,12 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
   // per-sample walk does at the first cell change inside the skipped block.
   // (a 32-bit word index from the uniform tape base: one register, not a pointer pair)
   constexpr int kUnroll = DDVR_BITS_WALK_UNROLL;   // (pragma arguments are not macro-expanded)
-  for (int blk = (r.n - 1) >> 5; blk >= 0; --blk) {
-    unsigned word = bits[bits_off + ((unsigned)blk << 5)];
+  // the tape streams from DRAM: the word of the next block is requested one block ahead
+  int blk = (r.n - 1) >> 5;
+  unsigned next = blk >= 0 ? bits[bits_off + ((unsigned)blk << 5)] : 0u;
+  for (; blk >= 0; --blk) {
+    unsigned word = next;
+    if (blk > 0) next = bits[bits_off + ((unsigned)(blk - 1) << 5)];
     if (word == 0u) {
       if (nskip) *nskip += min(32, r.n - (blk << 5));
       continue;
@@ -1503,7 +1518,11 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
       const bool fresh = c.cell != st.run_cell;
       // all d_hat of the ray share abs_k's sign: a zero weight sum = an empty run
       const bool flush = fresh && st.run_cell != kNoRun && st.acc8[0] != 0.f;
+#ifdef DDVR_WALK_NORED   // measurement variant: the reds replaced by a register sink
+      if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
+#else
       if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+#endif
       const float keep = fresh ? 0.f : 1.f;
       st.acc8[0] = fmaf(st.acc8[0], keep, dh);
       st.acc8[1] = fmaf(st.acc8[1], keep, px);
@@ -1517,6 +1536,124 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
       gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
     }
   }
+}
+
+#ifndef DDVR_RUN_WALK
+#define DDVR_RUN_WALK 1
+#endif
+
+// The affine absorption walk by cell runs (rays inside the box).  Within one cell a
+// ray's centred fractions are affine in the sample index, u_k = u_0 + k d (d = the
+// grid step per sample), so the run's moments sum_k b_k dh phi(u_k) (phi = 1, ux, uy,
+// uz, ux uy, ux uz, uy uz, ux uy uz; b_k the band bits, dh = abs_k) follow in closed
+// form from the power sums P_j = sum_k b_k k^j, j <= 3 -- for a run with every bit
+// set, P_j are those of 0 .. L-1.  Per run: its start position (fixed point, exact),
+// its length (samples until the first cell boundary on any axis: one fp32 quotient
+// per axis; an estimate off by one only moves a sample that sits within ~1e-7 voxel
+// of the boundary onto the neighbouring cell's polynomial, which agrees there), the
+// moments and one flush -- instead of per-sample positions, cell tests and moment
+// updates.  The samples and runs are those of abs_bits_walk (same cells, same
+// gradient up to fp32 rounding); all-zero remainders of tape words are skipped.
+__device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, float abs_k,
+                                              const unsigned* __restrict__ bits,
+                                              unsigned bits_off, float* __restrict__ d_cells,
+                                              int* nskip) {
+  const int n = r.n;
+  if (n <= 0) return;
+  // per-ray constants: the u step per sample, its products, the run-length divisors
+  const float dx = (float)r.gs[0] * kInvFix, dy = (float)r.gs[1] * kInvFix,
+              dz = (float)r.gs[2] * kInvFix;
+  const float dxy = dx * dy, dxz = dx * dz, dyz = dy * dz, dxyz = dxy * dz;
+  // samples left in the cell along an axis: floor(num / |gs|) + 1 with num = 2^32-1-lo
+  // (moving up) or lo (moving down); 1/|gs| = inf on an axis the ray never leaves
+  const float ix = r.gs[0] != 0 ? __frcp_rn((float)llabs(r.gs[0])) : INFINITY;
+  const float iy = r.gs[1] != 0 ? __frcp_rn((float)llabs(r.gs[1])) : INFINITY;
+  const float iz = r.gs[2] != 0 ? __frcp_rn((float)llabs(r.gs[2])) : INFINITY;
+  const unsigned sx = r.gs[0] > 0 ? 0xffffffffu : 0u, sy = r.gs[1] > 0 ? 0xffffffffu : 0u,
+                 sz = r.gs[2] > 0 ? 0xffffffffu : 0u;
+  const int last_word = (n - 1) >> 5;
+  // the tape as a bit stream in sample order: bit j of rw(w) = sample 32 w + j
+  auto rw = [&](int w) -> unsigned {
+    if (w > last_word) return 0u;
+    const unsigned word = bits[bits_off + ((unsigned)w << 5)];
+    return __brev(word) >> (32 - min(32, n - 32 * w));
+  };
+  int wcur = 0;
+  unsigned long long win = (unsigned long long)rw(0) | ((unsigned long long)rw(1) << 32);
+  int i = 0;
+  while (i < n) {
+    const int w = i >> 5;
+    if (w != wcur) {   // next word (one load), or a jump (two)
+      win = w == wcur + 1 ? (win >> 32) | ((unsigned long long)rw(w + 1) << 32)
+                          : (unsigned long long)rw(w) | ((unsigned long long)rw(w + 1) << 32);
+      wcur = w;
+    }
+    if (((unsigned)win >> (i & 31)) == 0u) {   // the rest of this word adds nothing
+      const int to = min(32 * (w + 1), n);
+      if (nskip) *nskip += to - i;
+      i = to;
+      continue;
+    }
+    const long long gx = r.g0[0] + (long long)i * r.gs[0];
+    const long long gy = r.g0[1] + (long long)i * r.gs[1];
+    const long long gz = r.g0[2] + (long long)i * r.gs[2];
+    const unsigned lx = (unsigned)gx, ly = (unsigned)gy, lz = (unsigned)gz;
+    const float Lf = fminf(fminf(__uint2float_rn(lx ^ sx) * ix, __uint2float_rn(ly ^ sy) * iy),
+                           __uint2float_rn(lz ^ sz) * iz);
+    const int L = min((int)fminf(Lf, 31.f) + 1, n - i);   // 1 .. 32
+    const unsigned full = L == 32 ? 0xffffffffu : (1u << L) - 1u;
+    const unsigned m = (unsigned)(win >> (i & 31)) & full;
+    i += L;
+    if (m == 0u) continue;
+    float P0, P1, P2, P3;
+    if (m == full) {   // every sample of the run in the band: sums over 0 .. L-1
+      P0 = (float)L;
+      P1 = 0.5f * P0 * (P0 - 1.f);
+      P2 = P1 * (2.f * P0 - 1.f) * (1.f / 3.f);
+      P3 = P1 * P1;
+    } else {
+      P0 = P1 = P2 = P3 = 0.f;
+      for (unsigned mm = m; mm; mm &= mm - 1u) {
+        const float k = (float)(__ffs(mm) - 1);
+        P0 += 1.f; P1 += k; P2 += k * k; P3 += k * k * k;
+      }
+    }
+    const float q0 = abs_k * P0, q1 = abs_k * P1, q2 = abs_k * P2, q3 = abs_k * P3;
+    const float ux = __fmaf_rn(__uint2float_rn(lx), kInvFix, -0.5f);
+    const float uy = __fmaf_rn(__uint2float_rn(ly), kInvFix, -0.5f);
+    const float uz = __fmaf_rn(__uint2float_rn(lz), kInvFix, -0.5f);
+    const float uxy = ux * uy, uxz = ux * uz, uyz = uy * uz;
+    float a[8];
+    a[0] = q0;
+    a[1] = __fmaf_rn(ux, q0, dx * q1);
+    a[2] = __fmaf_rn(uy, q0, dy * q1);
+    a[3] = __fmaf_rn(uz, q0, dz * q1);
+    a[4] = __fmaf_rn(uxy, q0, __fmaf_rn(__fmaf_rn(ux, dy, uy * dx), q1, dxy * q2));
+    a[5] = __fmaf_rn(uxz, q0, __fmaf_rn(__fmaf_rn(ux, dz, uz * dx), q1, dxz * q2));
+    a[6] = __fmaf_rn(uyz, q0, __fmaf_rn(__fmaf_rn(uy, dz, uz * dy), q1, dyz * q2));
+    const float t1 = __fmaf_rn(uxy, dz, __fmaf_rn(uxz, dy, uyz * dx));
+    const float t2 = __fmaf_rn(ux, dyz, __fmaf_rn(uy, dxz, uz * dxy));
+    a[7] = __fmaf_rn(uxy * uz, q0, __fmaf_rn(t1, q1, __fmaf_rn(t2, q2, dxyz * q3)));
+    const int cell = (((int)(gx >> 32)) * V.CY + (int)(gy >> 32)) * V.CZ + (int)(gz >> 32);
+#ifdef DDVR_WALK_NORED   // measurement variant: no reds (the atomic-free floor)
+    if (a[0] == 12345.f) d_cells[0] = a[7] + (float)cell;
+#else
+    float* q = d_cells + 8 * (long long)cell;
+    red128(q, a[0], a[1], a[2], a[3]);
+    red128(q + 4, a[4], a[5], a[6], a[7]);
+#endif
+  }
+}
+
+// The band-tape class of a fused volume-only step (CTA-uniform: it depends on the TF
+// table and dt only): an emission-free texel TF whose tau column is affine and
+// non-negative, a polynomial segment mode, no tape.  Its walk is abs_bits_walk.
+__device__ __forceinline__ bool band_class(const TfArgs& TFA, const Geometry& G,
+                                           const unsigned* s_info, int mode) {
+  return G.bits != nullptr && DDVR_ABS_WALK && DDVR_AFF_WALK && TFA.kind == kTfTexture &&
+         G.tape == nullptr && s_info[1] == 0u && s_info[2] == 0u && mode != kSegGen &&
+         __uint_as_float(s_info[3]) >= 0.f &&
+         __fmaf_rn(__uint_as_float(s_info[4]), TFA.fR1, __uint_as_float(s_info[3])) >= 0.f;
 }
 
 // ROLE 0: every walk; ROLE 1: the absorption-only walk (emission-free texel
@@ -1556,6 +1693,10 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
                            G.tape == nullptr && s_info[1] == 0u;
     if (ROLE == 0 ? abs_class : !abs_class) return;   // CTA-uniform
   }
+  // the band-tape step split into dvr_band_march_kernel + dvr_band_walk_kernel
+  if (ROLE == 1 && FUSED && MASK == DDVR_TARGET_VOLUME && G.ray_k != nullptr &&
+      band_class(TFA, G, s_info, seg_mode(G.dt32, s_info[0])))
+    return;
   if (threadIdx.x == 0) make_frame(G.cams[view], G.W, G.H, F);
   __syncthreads();
   const int mode = seg_mode(G.dt32, s_info[0]);
@@ -1650,7 +1791,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   else DDVR_WALK_AFF(kSegP7, INS);
   if (kBitsKernel && bits) {
     const float abs_k = sd.w * (float)exp(-S) * G.dt32 * TFA.fR * __uint_as_float(s_info[4]);
-    if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
+    if (warp_inside && DDVR_RUN_WALK) abs_runs_walk(V, r, abs_k, bits, bits_off, d_cells, &walk_skip);
+    else if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
     else abs_bits_walk<false>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
   } else if (ROLE == 1 && aff_walk) {
     if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
@@ -1746,6 +1888,139 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
         if (kStep) atomicAdd(d_dt, t2);
       }
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// The band-tape step as two kernels (G.ray_k set): the march is gather-latency
+// bound and the walk is issue bound, and their union in one thread held the
+// fused kernel to 64 registers (4 CTAs/SM).  Apart they run at their own
+// occupancy; the march hands each ray's walk weight abs_k = seed_a T_n dt R b
+// to the walk through (V, rows, W) floats (4 B per ray).
+// ---------------------------------------------------------------------------
+
+#ifndef DDVR_BAND_MARCH_MINB
+#define DDVR_BAND_MARCH_MINB 4
+#endif
+#ifndef DDVR_BAND_WALK_MINB
+#define DDVR_BAND_WALK_MINB 4
+#endif
+
+// shared prologue of the two kernels: TF table, class test, frame, this lane's ray
+struct BandRay {
+  Ray r;
+  bool valid, warp_inside;
+  size_t pix;
+  unsigned bits_off;
+  int mode;
+};
+
+__device__ __forceinline__ bool band_prologue(const VolArgs& V, const TfArgs& TFA,
+                                              const Geometry& G, Frame& F, unsigned* s_info,
+                                              BandRay& b) {
+  if (threadIdx.x < 5) s_info[threadIdx.x] = 0u;
+  __syncthreads();
+  load_tf(TFA, s_info);
+  __syncthreads();
+  b.mode = seg_mode(G.dt32, s_info[0]);
+  if (!band_class(TFA, G, s_info, b.mode)) return false;   // CTA-uniform
+  if (threadIdx.x == 0) make_frame(G.cams[blockIdx.z], G.W, G.H, F);
+  __syncthreads();
+  int px, py;
+  pixel_of(G, px, py);
+  b.valid = px < G.W && py < G.row1;
+  b.r.n = 0;
+  b.r.all_inside = true;
+  b.pix = 0;
+  if (b.valid) {
+    setup_ray(F, V, G.dt, G.W, G.H, px, py, b.r);
+    b.pix = ((size_t)blockIdx.z * (G.row1 - G.row0) + (py - G.row0)) * G.W + px;
+  }
+  b.warp_inside = __all_sync(0xffffffffu, b.r.all_inside);
+  b.bits_off = ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * kWarps +
+                (threadIdx.x >> 5)) * 32u * (unsigned)G.bits_words + (threadIdx.x & 31);
+  return true;
+}
+
+// forward march (renderer.py:306-357) with the band tape + L1 seed (objectives.py:38-54)
+// and the walk weight of the closed-form absorption adjoint (see adjoint_ray)
+template <int kUnused = 0>   // (a template: instantiated only where launched)
+__global__ void __launch_bounds__(kThreads, DDVR_BAND_MARCH_MINB)
+    dvr_band_march_kernel(VolArgs V, TfArgs TFA, Geometry G, FusedArgs Fu) {
+  __shared__ Frame F;
+  __shared__ unsigned s_info[5];
+  BandRay b;
+  if (!band_prologue(V, TFA, G, F, s_info, b)) return;
+  int march_skip = 0;
+  double loss_part = 0.0;
+  double S = 0.0;
+  if (b.valid) {
+    float4 rgba;
+    const float aa = __uint_as_float(s_info[3]), ab = __uint_as_float(s_info[4]);
+#define DDVR_BAND_MARCH(SEG, INS)                                                            \
+  march_ray<false, true, false, SEG, INS, false, kTfTexture, true, true>(                     \
+      V, TFA, G.dt32, b.r, nullptr, rgba, S, aa, ab, G.bits, b.bits_off, &march_skip)
+    if (b.warp_inside) {
+      if (b.mode == kSegP3) DDVR_BAND_MARCH(kSegP3, true); else DDVR_BAND_MARCH(kSegP7, true);
+    } else {
+      if (b.mode == kSegP3) DDVR_BAND_MARCH(kSegP3, false); else DDVR_BAND_MARCH(kSegP7, false);
+    }
+#undef DDVR_BAND_MARCH
+    const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[b.pix];
+    const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
+                dw = rgba.w - ref.w;
+    const float sw = dw > 0.f ? Fu.inv_count : (dw < 0.f ? -Fu.inv_count : 0.f);
+    loss_part = fabs((double)dx) + fabs((double)dy) + fabs((double)dz) + fabs((double)dw);
+    if (Fu.image_out) reinterpret_cast<float4*>(Fu.image_out)[b.pix] = rgba;
+    if (Fu.depth_out) Fu.depth_out[b.pix] = (float)S;
+    // d_hat per set band bit: seed_a T_n dt R b (the walk of adjoint_ray<..., AFF>)
+    G.ray_k[b.pix] = sw * (float)exp(-S) * G.dt32 * TFA.fR * __uint_as_float(s_info[4]);
+  }
+  loss_part = warp_sum(loss_part);
+  if ((threadIdx.x & 31) == 0 && loss_part != 0.0) atomicAdd(Fu.loss, loss_part * Fu.inv_count_d);
+  if (G.stats) {
+    const unsigned long long c[3] = {warp_sum((unsigned long long)(b.valid ? b.r.n : 0)),
+                                     warp_sum((unsigned long long)march_skip),
+                                     warp_sum((unsigned long long)(b.valid ? 1 : 0))};
+    if ((threadIdx.x & 31) == 0) {
+      if (c[0]) atomicAdd(G.stats + 0, c[0]);
+      if (c[1]) atomicAdd(G.stats + 1, c[1]);
+      if (c[2]) atomicAdd(G.stats + 3, c[2]);
+    }
+  }
+}
+
+// the affine absorption walk from the band tape (abs_bits_walk) + the cell-run flushes
+template <int kUnused = 0>
+__global__ void __launch_bounds__(kThreads, DDVR_BAND_WALK_MINB)
+    dvr_band_walk_kernel(VolArgs V, TfArgs TFA, Geometry G, float* __restrict__ d_cells) {
+  __shared__ Frame F;
+  __shared__ unsigned s_info[5];
+  BandRay b;
+  if (!band_prologue(V, TFA, G, F, s_info, b)) return;
+  AdjState st;
+  st.run_cell = kNoRun;
+  st.tfp0 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) st.acc8[k] = 0.f;
+  int walk_skip = 0;
+  if (b.valid) {
+    const float abs_k = G.ray_k[b.pix];
+    if (b.warp_inside && DDVR_RUN_WALK)
+      abs_runs_walk(V, b.r, abs_k, G.bits, b.bits_off, d_cells, &walk_skip);
+    else if (b.warp_inside)
+      abs_bits_walk<true>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
+    else abs_bits_walk<false>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
+    if (st.run_cell != kNoRun && st.acc8[0] != 0.f)
+      flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+#ifdef DDVR_WALK_NORED
+    if (st.tfp0 == 12345.f) G.ray_k[b.pix] = st.tfp0;
+#endif
+  }
+  if (G.stats) {
+    const unsigned long long c = warp_sum((unsigned long long)walk_skip);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(G.stats + 2, c);
   }
 }
 

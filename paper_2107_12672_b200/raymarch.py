@@ -272,7 +272,7 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
                        *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
                        workspace=None, image_out=None, depth_out=None, ws_continue=False,
                        ws_defer=False, deterministic=False, band_tape=False,
-                       empty_skip=True, stats=None):
+                       empty_skip=True, stats=None, split_walk=False):
     """One fused step over these views: forward march, L1 seed sign(image - ref)/count
     and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
     device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
@@ -284,6 +284,8 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
     march skips 32-sample blocks in all-zero bricks unless ``empty_skip`` is False
     (DDVR_FLAG_NO_EMPTY_SKIP; bitwise the same outputs either way).  A
     caller-provided workspace needs those extra bytes too (extra_workspace_bytes).
+    ``split_walk`` (band tape): march and walk as two kernels (DDVR_FLAG_SPLIT_WALK)
+    instead of one (the same outputs).
     ``stats`` (measurement, optional): (4,) int64 device tensor the kernel adds
     [samples, samples the march skipped, samples the walk skipped, rays] to."""
     _require(cams, "cameras", torch.float64, ndim=2)
@@ -309,7 +311,7 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
         workspace = workspace_for(density, mask, cells, texels, extra)
     prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0) \
         | (N.FLAG_DETERMINISTIC if deterministic else 0) | (N.FLAG_BAND_TAPE if band_tape else 0) \
-        | (0 if empty_skip else N.FLAG_NO_EMPTY_SKIP)
+        | (0 if empty_skip else N.FLAG_NO_EMPTY_SKIP) | (N.FLAG_SPLIT_WALK if split_walk else 0)
     if stats is not None:
         _require(stats, "stats", torch.int64)
         if stats.numel() < 4:

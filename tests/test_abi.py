@@ -51,14 +51,14 @@ def test_library_exports_every_declared_symbol(lib):
     for name in _declared():
         assert hasattr(handle, name), name
     from paper_2107_12672_b200 import _native
-    assert lib.ddvr_abi_version() == _native.ABI_VERSION == 3
+    assert lib.ddvr_abi_version() == _native.ABI_VERSION == 4
 
 
 def test_python_binding_matches_header():
     from paper_2107_12672_b200 import _native
     assert sorted(_native.EXPORTED) == _declared()
     # struct layout: ddvr_params = double + 6 int32 + pointer + int64
-    assert ctypes.sizeof(_native.DdvrParams) == 8 + 6 * 4 + 8 + 8
+    assert ctypes.sizeof(_native.DdvrParams) == 8 + 6 * 4 + 8 + 8 + 8   # ... tape_stride, stats
     assert ctypes.sizeof(_native.DdvrVolume) == 8 + 12 + 4 + 48 + 8
     assert ctypes.sizeof(_native.DdvrTf) == 16
 
@@ -238,7 +238,7 @@ def test_deterministic_mode_workspace(lib):
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 2 and "deterministic" in lib.ddvr_last_error().decode()
-    prm.flags = 32
+    prm.flags = 64   # an unknown bit
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 1 and "flags" in lib.ddvr_last_error().decode()
@@ -246,14 +246,16 @@ def test_deterministic_mode_workspace(lib):
 
 def test_band_tape_bytes_and_limits(lib):
     """ddvr_band_tape_bytes: 32-bit words per ray from the box diagonal / dt, for every
-    pixel of every CTA, then the empty-brick map; a fused call whose tape would pass 2^32 words is refused
+    pixel of every CTA, then the empty-brick map and the per-ray walk weights; a fused call whose tape would pass 2^32 words is refused
     before any CUDA work, and one without room for the tape asks for it."""
     import math
     from paper_2107_12672_b200 import _native as N
     vol, tf, prm = _descs(dt=0.01, W=512, H=512)
     words = math.ceil((math.floor(math.sqrt(3.0) / 0.01) + 3) / 32)
     assert lib.ddvr_band_tape_bytes(ctypes.byref(vol), 64, ctypes.byref(prm)) == \
-        32 * 32 * 64 * 256 * words * 4 + 256   # + the brick occupancy maps (1 brick, 256-aligned)
+        32 * 32 * 64 * 256 * words * 4 + 256 + 32 * 32 * 64 * 256 * 4
+    # + the brick occupancy maps (1 brick, 256-aligned) + a float per ray (the walk weights
+    # the march hands to the separate walk kernel)
     loss = ctypes.c_double(0)
     vol.cells = 32
     call = lambda v, p, nv, ws: lib.ddvr_forward_adjoint_l1(  # noqa: E731

@@ -1,0 +1,107 @@
+"""The benchmarked step at the configs' full sizes against the reference.
+
+tests/golden/{C4,C5}_step_*.npz come from voldiff itself (oracle/gen_golden.py
+step_cases): the tomography loop body of tasks.py:397-432 -- render of the
+estimate, l1_loss against reference images rendered from the truth, render_adjoint
+with that seed -- on row bands of the config's views at the full volume (256^3 /
+512^3) and image (512^2 / 1024^2).  The GPU runs the same bands through
+``ShardedStep`` (ddvr_forward_adjoint_l1), i.e. the kernels bench.py times, with
+the band tape and the empty-space skips on and off:
+
+* ``dense``: 0.85 truth + 0.1 U(0,1), the bench's iteration-1 state (no exact zeros);
+* ``sparse`` (C4): the truth's support only, exact zeros outside the sphere, so the
+  march's empty-brick skip and the walk's zero-word skip run over real empty space.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+
+IMG_TOL = 1e-5
+GRAD_TOL = 1e-4
+# C5's Gaussian texel TF is sharply peaked: perturbing the densities at fp32 rounding
+# level moves the reference's own band gradient by ~1e-4 (tools/fp32_floor_c5.py,
+# profiles/r02_fp32_floor_c5.txt), so its bar is 2.5x that floor.
+GRAD_TOL_C5 = 2.5e-4
+
+
+def _f32(a):
+    return np.asarray(a, np.float64).astype(np.float32).astype(np.float64)
+
+
+def step_estimate(name: str, kind: str) -> np.ndarray:
+    """The estimate of a step fixture: the generator and seed of gen_golden.step_cases
+    (one default_rng(99) stream drawn for C4 then C5)."""
+    from paper_2107_12672_b200.scenes import CONFIGS
+    rng = np.random.default_rng(99)
+    for nm in ("C4", "C5"):
+        truth = CONFIGS[nm].volume().astype(np.float64)
+        u = rng.uniform(size=truth.shape)
+        if nm == name:
+            if kind == "dense":
+                return _f32(0.85 * truth + 0.1 * u)
+            return _f32(np.where(truth > 0, np.clip(0.7 * truth + 0.05, 0, 1), 0.0))
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("case", ["C4_step_dense", "C4_step_sparse"])
+def test_step_estimates_are_reproduced(case):
+    """(CPU) the tests rebuild exactly the estimate the fixture was computed from."""
+    g = golden(case)
+    name, _, kind = case.split("_")
+    est = step_estimate(name, kind)
+    np.testing.assert_array_equal(est.reshape(-1)[:: max(1, est.size // 4096)], g["est_probe"])
+
+
+# (case, band tape, empty skip, split walk)
+MODES = [("C4_step_dense", True, True, False), ("C4_step_dense", False, True, False),
+         ("C4_step_dense", True, True, True),
+         ("C4_step_sparse", True, True, False), ("C4_step_sparse", True, False, False),
+         ("C4_step_sparse", False, True, False), ("C4_step_sparse", True, True, True),
+         ("C5_step_dense", False, True, False)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,tape,skip,split", MODES)
+def test_fused_step_matches_reference_at_config_scale(cuda, case, tape, skip, split):
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    from paper_2107_12672_b200.scenes import CONFIGS
+    g = golden(case)
+    name, _, kind = case.split("_")
+    c = CONFIGS[name]
+    est_np = step_estimate(name, kind)
+    np.testing.assert_array_equal(est_np.reshape(-1)[:: max(1, est_np.size // 4096)],
+                                  g["est_probe"])
+    est = torch.from_numpy(est_np.astype(np.float32)).to(cuda)
+    tex = torch.from_numpy(g["texels"]).to(cuda)
+    poses = c.view_poses()
+    ll = torch.tensor([poses[int(k)] for k in g["views"]], dtype=torch.float64, device=cuda)
+    r0, r1 = (int(r) for r in g["rows"])
+    rig = R.Rig(c.image, c.image, rows=(r0, r1))
+    refs = torch.from_numpy(g["refs"]).to(cuda).contiguous()
+    stats = torch.zeros(4, dtype=torch.int64, device=cuda)
+    step = ShardedStep(est, tex, ll, refs, float(g["dt"]), rig, targets=("volume",),
+                       total_elements=float(g["count"]), radius=c.radius, fov_y_deg=c.fov,
+                       keep_images=True, band_tape=tape, empty_skip=skip, split_walk=split,
+                       stats=stats)
+    assert step.fused and step.band_tape == (tape and name == "C4")
+    f = step.run()
+    img = step.img.double().cpu().numpy()
+    assert rel_l2(img, g["image"]) <= IMG_TOL
+    assert abs(float(f.loss) - float(g["loss"])) <= IMG_TOL * float(g["loss"])
+    want = np.zeros(est_np.size)
+    want[g["volume_idx"]] = g["volume_val"]
+    got = f.d_volume.double().cpu().numpy()
+    err = rel_l2(got, want)
+    assert err <= (GRAD_TOL_C5 if name == "C5" else GRAD_TOL), err
+    s = [int(x) for x in stats.cpu()]
+    _, n, _ = R.ray_setup(step.cams, float(g["dt"]), rig, dims=tuple(est.shape))
+    assert s[0] == int(n.to(torch.int64).sum()) and s[3] == n.numel()
+    if kind == "sparse" and step.band_tape:
+        assert s[2] > 0                        # the walk skipped empty tape words
+        assert (s[1] > 0) == skip              # the march skipped empty bricks

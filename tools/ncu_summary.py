@@ -9,10 +9,11 @@ per-sample instruction and wavefront counts.  --json-out/--key: merge the
 numbers of the first launch whose name contains --kernel into the JSON file
 bench.py reads for its roofline (achieved = these DRAM bytes / live launch time).
 """
-import json
-import os
 
 from __future__ import annotations
+
+import json
+import os
 
 import argparse
 import csv
