@@ -83,7 +83,8 @@ def _merge_json(args, vals, units, head, row):
     def unit_scale(key):
         u = units[head.index(key)]
         return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-                "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(u, 1.0)
+                "nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0,
+                "ms": 1.0, "second": 1e3, "s": 1e3}.get(u, 1.0)
     g = lambda k: _num(vals[k]) * unit_scale(k)  # noqa: E731
     dur_ms = g("gpu__time_duration.sum")
     e = {"kernel": row[head.index("Kernel Name")][:120], "state": args.state,
