@@ -47,6 +47,24 @@
 
 #include "ddvr.h"
 
+// Bounds-checked build (-DDDVR_CHECKED, tests/test_gpu_checked.py): every cell-record
+// gather and cell-gradient flush, every empty-brick lookup, checks its index against
+// the padded record grid and traps with the source line on a violation -- the
+// memory-safety evidence of this path (compute-sanitizer is not available on the pool).
+#ifdef DDVR_CHECKED
+#define DDVR_REQUIRE(cond)                                                                 \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("ddvr check failed: %s (%s:%d) block (%d,%d,%d) thread %d\n", #cond, __FILE__, \
+             __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                   \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define DDVR_REQUIRE(cond) ((void)0)
+#endif
+
+
 namespace ddvr_impl {
 
 
@@ -106,6 +124,7 @@ __device__ __forceinline__ bool block_empty(const VolArgs& V, long long gx, long
   const int x = max(brick_of(gx, V.X1) - (back & 1), 0);
   const int y = max(brick_of(gy, V.Y1) - ((back >> 1) & 1), 0);
   const int z = max(brick_of(gz, V.Z1) - (back >> 2), 0);
+  DDVR_REQUIRE(x >= 0 && y >= 0 && z >= 0 && x <= (V.X1 + 1) >> 3 && y < V.NBy && z < V.NBz);
   return __ldg(V.occ + (x * V.NBy + y) * V.NBz + z) == 0;
 }
 
@@ -500,6 +519,23 @@ __device__ __forceinline__ void red128(float* p, float a, float b, float c, floa
                : "memory");
 }
 
+// a padded cell-record index (relative to cell (0,0,0)) inside the record grid
+__device__ __forceinline__ bool cell_ok(const VolArgs& V, long long cell) {
+  const long long lo = -((long long)V.CY * V.CZ + V.CZ + 1);
+  const long long hi = ((long long)V.X1 * V.CY + V.Y1) * V.CZ + V.Z1;
+  return cell >= lo && cell <= hi;
+}
+
+// the cell-record gathers of the marches and walks (predicated / unconditional)
+__device__ __forceinline__ void gather_if(const VolArgs& V, bool pred, int cell, float v[8]) {
+  DDVR_REQUIRE(!pred || cell_ok(V, cell));
+  ld256_if(pred, V.cell0 + 8 * (long long)cell, v);
+}
+__device__ __forceinline__ void gather(const VolArgs& V, int cell, float v[8]) {
+  DDVR_REQUIRE(cell_ok(V, cell));
+  ld256(V.cell0 + 8 * (long long)cell, v);
+}
+
 // The trilinear interpolant of a cell (field.py:318-349) as a polynomial in
 // the centred fractions u = f - 1/2 in [-1/2, 1/2]:
 //   rho(u) = c0 + cx ux + cy uy + cz uz + cxy ux uy + cxz ux uz + cyz uy uz + cxyz ux uy uz
@@ -536,7 +572,7 @@ __device__ __forceinline__ void corners_to_poly(const float w[8], float c[8]) {
 template <bool CELLS>
 __device__ __forceinline__ void fetch8(const VolArgs& V, const Cell& c, float v[8]) {
   if (CELLS) {
-    ld256(V.cell0 + 8 * (long long)c.cell, v);
+    gather(V, c.cell, v);
   } else {
     const float* p = V.data + c.base;
     float k[8];
@@ -965,7 +1001,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     const bool ins = INSIDE || r.all_inside;
     Cell c;
     locate<CELLS>(V, gx, gy, gz, ins, c);
-    ld256_if(r.n > 0, V.cell0 + 8 * (long long)c.cell, v);
+    gather_if(V, r.n > 0, c.cell, v);
     held = c.cell;
     // (the emitting variants spill at 48 registers when unrolled)
     constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : 1;
@@ -975,7 +1011,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
       gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
       locate<CELLS>(V, gx, gy, gz, ins, c);
       const bool more = decltype(kMore)::value || i + 1 < r.n;
-      ld256_if(more && c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
+      gather_if(V, more && c.cell != held, c.cell, v);
       held = c.cell;
       shade(d, i, kStore);
     };
@@ -998,7 +1034,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
           gx += 32 * r.gs[0]; gy += 32 * r.gs[1]; gz += 32 * r.gs[2];   // word: after the loop)
           if (i0 + 32 < r.n) {
             locate<CELLS>(V, gx, gy, gz, ins, c);
-            ld256(V.cell0 + 8 * (long long)c.cell, v);
+            gather(V, c.cell, v);
             held = c.cell;
           }
           continue;
@@ -1272,7 +1308,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   Cell cnext;
   if (kEarly) {
     locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, cnext);
-    ld256_if(r.n > 0, V.cell0 + 8 * (long long)cnext.cell, v);
+    gather_if(V, r.n > 0, cnext.cell, v);
     held = cnext.cell;
   }
 #pragma unroll 1   // (unrolled, the walks spill at their register budgets)
@@ -1283,7 +1319,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     } else {
       locate<CELLS>(V, gx, gy, gz, INSIDE || r.all_inside, c);
       if (kHoldCell) {
-        ld256_if(c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
+        gather_if(V, c.cell != held, c.cell, v);
         held = c.cell;
       } else {
         fetch8<CELLS>(V, c, v);
@@ -1292,7 +1328,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const Interp ip = interp(c, v);
     if (kEarly) {   // v consumed: the record of sample i-1 is now in flight
       locate<CELLS>(V, gx - r.gs[0], gy - r.gs[1], gz - r.gs[2], INSIDE || r.all_inside, cnext);
-      ld256_if(i > 0 && cnext.cell != held, V.cell0 + 8 * (long long)cnext.cell, v);
+      gather_if(V, i > 0 && cnext.cell != held, cnext.cell, v);
       held = cnext.cell;
     }
     const float raw = ip.rho;
@@ -1424,6 +1460,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
                            (!(kAbs && AFF) || st.acc8[0] != 0.f);
         // (ptxas branches around a predicated red anyway: one branch for both
         // halves, and the record address is formed only inside it)
+        DDVR_REQUIRE(!flush || cell_ok(V, st.run_cell));
         if (flush) flush_cell<true>(d_volume, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
         const float keep = fresh ? 0.f : 1.f;
         st.acc8[0] = fmaf(st.acc8[0], keep, dh);
@@ -1437,6 +1474,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         st.run_cell = c.cell;
       } else if (kVol) {
         if (c.cell != st.run_cell) {
+          DDVR_REQUIRE(st.run_cell == kNoRun || !CELLS || cell_ok(V, st.run_cell));
           if (st.run_cell != kNoRun)
             flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                               st.run_oz, st.acc8);
@@ -1521,6 +1559,7 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
 #ifdef DDVR_WALK_NORED   // measurement variant: the reds replaced by a register sink
       if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
 #else
+      DDVR_REQUIRE(!flush || cell_ok(V, st.run_cell));
       if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
 #endif
       const float keep = fresh ? 0.f : 1.f;
@@ -1638,6 +1677,7 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
 #ifdef DDVR_WALK_NORED   // measurement variant: no reds (the atomic-free floor)
     if (a[0] == 12345.f) d_cells[0] = a[7] + (float)cell;
 #else
+    DDVR_REQUIRE(cell_ok(V, cell));
     float* q = d_cells + 8 * (long long)cell;
     red128(q, a[0], a[1], a[2], a[3]);
     red128(q + 4, a[4], a[5], a[6], a[7]);
@@ -1828,6 +1868,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
         if (c[k]) atomicAdd(G.stats + k, c[k]);
   }
   // ---- flush per-ray accumulators ----
+  DDVR_REQUIRE(!(kVol && CELLS && st.run_cell != kNoRun) || cell_ok(V, st.run_cell));
   if (kVol && st.run_cell != kNoRun)
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                       st.run_oz, st.acc8);
@@ -2012,6 +2053,7 @@ __global__ void __launch_bounds__(kThreads, DDVR_BAND_WALK_MINB)
     else if (b.warp_inside)
       abs_bits_walk<true>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
     else abs_bits_walk<false>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
+    DDVR_REQUIRE(st.run_cell == kNoRun || cell_ok(V, st.run_cell));
     if (st.run_cell != kNoRun && st.acc8[0] != 0.f)
       flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
 #ifdef DDVR_WALK_NORED

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kThreads, 6) gather_probe_kernel(VolArgs V, Ge
     Cell c;
     locate_cells(V, gx, gy, gz, r.all_inside, c);
     gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
-    ld256_if(!HOLD || c.cell != held, V.cell0 + 8 * (long long)c.cell, v);
+    gather_if(V, !HOLD || c.cell != held, c.cell, v);
     held = c.cell;
     acc += v[0];
   }
