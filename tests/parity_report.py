@@ -1,6 +1,6 @@
 """Parity report: measured GPU-vs-reference errors for every golden case (needs a GPU).
 
-    python tests/parity_report.py > profiles/r01_parity.json
+    python tests/parity_report.py > profiles/r02_parity.json
 
 Not a test (pytest does not collect it): it prints the numbers the -m gpu
 parity tests assert against their bars, so DESIGN.md can quote them.
@@ -77,6 +77,32 @@ def main():
                 ref = g[f"inversion_{t}"]
             note(name, f"cells/d_{t}", rel_l2(got[t], ref))
         report["cases"][name]["band_rows"] = [int(r) for r in g["rows"]]
+    # the benchmarked fused step at config scale (test_gpu_step_config.py)
+    from paper_2107_12672_b200.distributed import ShardedStep
+    from test_gpu_step_config import MODES, step_estimate
+    for case, tape, skip, split in MODES:
+        g = golden(case)
+        name, _, kind = case.split("_")
+        c = CONFIGS[name]
+        est = torch.from_numpy(step_estimate(name, kind).astype(np.float32)).to(dev)
+        tex = torch.from_numpy(g["texels"]).to(dev)
+        poses = c.view_poses()
+        ll = torch.tensor([poses[int(k)] for k in g["views"]], dtype=torch.float64, device=dev)
+        r0, r1 = (int(r) for r in g["rows"])
+        rig = R.Rig(c.image, c.image, rows=(r0, r1))
+        step = ShardedStep(est, tex, ll, torch.from_numpy(g["refs"]).to(dev).contiguous(),
+                           float(g["dt"]), rig, total_elements=float(g["count"]),
+                           radius=c.radius, fov_y_deg=c.fov, keep_images=True, band_tape=tape,
+                           empty_skip=skip, split_walk=split)
+        f = step.run()
+        want = np.zeros(est.numel())
+        want[g["volume_idx"]] = g["volume_val"]
+        key = f"{case}/tape={int(step.band_tape)},skip={int(skip)},split={int(split)}"
+        note(key, "step/image", rel_l2(step.img.double().cpu().numpy(), g["image"]))
+        note(key, "step/loss", abs(float(f.loss) - float(g["loss"])) / float(g["loss"]))
+        note(key, "step/d_volume", rel_l2(f.d_volume.double().cpu().numpy(), want))
+        report["cases"][key]["band_rows"] = [r0, r1]
+        report["cases"][key]["views"] = [int(k) for k in g["views"]]
     report["worst"] = worst
     print(json.dumps(report, indent=1, sort_keys=True))
 
