@@ -74,8 +74,9 @@ def parse(argv=None):
     p.add_argument("--views", type=int, default=0,
                    help="profiling aid: use only the first N views (not a bench result)")
     p.add_argument("--layout", default="cells", choices=["cells", "voxels"])
-    p.add_argument("--graph", action="store_true",
-                   help="replay each timed iteration from a captured CUDA graph (1 GPU)")
+    p.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                   help="replay each timed iteration from a captured CUDA graph (1 GPU); "
+                        "auto: on for launch-bound steps (density target, < 1e7 samples)")
     p.add_argument("--unfused", action="store_true",
                    help="separate forward / L1 / adjoint launches instead of the fused step")
     p.add_argument("--no-empty-skip", action="store_true",
@@ -435,7 +436,9 @@ def run_own(args, cfg):
                            split_walk=args.split_walk)
 
     step = make_step(False if args.no_band_tape else "auto")
-    graphed = args.graph and world == 1 and volume_target
+    small = cfg_samples(cfg) is not None and cfg_samples(cfg) < 10 ** 7
+    graphed = (args.graph == "on" or (args.graph == "auto" and small)) and world == 1 \
+        and volume_target and not args.views
     # density targets run the whole optimisation iteration (prior + Adam + projection)
     runner = (TomographyIteration(step, lr=0.02, lam=0.5, graph=graphed) if volume_target
               else step)

@@ -552,11 +552,15 @@ __global__ void __launch_bounds__(256) ppm_kernel(const float4* __restrict__ img
 // d_tf (fp64, the parameter layout count x stride) += sum over the CTA slots
 // (tf_slot layout: rgba rows, then knot positions / (mu, sigma) pairs).
 // 32 outputs x 8 slot lanes per block, reduced through shared memory.
-__global__ void __launch_bounds__(256) tf_slots_reduce_kernel(const float* __restrict__ slots,
-                                                              int nslot, int slot_floats,
-                                                              int kind, int count,
-                                                              double* __restrict__ d_tf) {
-  __shared__ double part[8][33];
+// One output (texel channel, knot position, ...) per lane, 32 lanes of slots per output:
+// slot lane ty sums slots ty, ty + 32, ... with four independent accumulators (slot
+// index mod 4) so the L2 loads overlap, then fixed-order combines -- the same sum for
+// every run (the TF gradient is reproducible bit for bit).
+__global__ void __launch_bounds__(1024) tf_slots_reduce_kernel(const float* __restrict__ slots,
+                                                               int nslot, int slot_floats,
+                                                               int kind, int count,
+                                                               double* __restrict__ d_tf) {
+  __shared__ double part[32][33];
   const int stride = kind == DDVR_TF_TEXTURE ? 4 : kind == DDVR_TF_PIECEWISE ? 5 : 6;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + tx;
@@ -568,15 +572,24 @@ __global__ void __launch_bounds__(256) tf_slots_reduce_kernel(const float* __res
     else if (kind == DDVR_TF_PIECEWISE) pos = c == 0 ? 4 * count + j : 4 * j + c - 1;
     else pos = c < 2 ? 4 * count + 2 * j + c : 4 * j + c - 2;
   }
-  double acc = 0.0;
-  if (k < nout)
-    for (int sl = ty; sl < nslot; sl += 8) acc += (double)slots[(size_t)sl * slot_floats + pos];
-  part[ty][tx] = acc;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (k < nout) {
+    const float* q = slots + pos;
+    int sl = ty;
+    for (; sl + 96 < nslot; sl += 128) {
+      a0 += (double)q[(size_t)sl * slot_floats];
+      a1 += (double)q[(size_t)(sl + 32) * slot_floats];
+      a2 += (double)q[(size_t)(sl + 64) * slot_floats];
+      a3 += (double)q[(size_t)(sl + 96) * slot_floats];
+    }
+    for (; sl < nslot; sl += 32) a0 += (double)q[(size_t)sl * slot_floats];
+  }
+  part[ty][tx] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (ty == 0 && k < nout) {
     double t = 0.0;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) t += part[r][tx];
+    for (int r = 0; r < 32; ++r) t += part[r][tx];
     d_tf[k] += t;
   }
 }
@@ -896,7 +909,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   if (flags & DDVR_FLAG_WS_DEFER) return DDVR_OK;   // a later call of this step folds
   if (ws_tf > 0) {
     const int nout = T.count * T.stride;
-    tf_slots_reduce_kernel<<<(nout + 31) / 32, 256, 0, st>>>(T.slots, T.nslot, T.slot_floats,
+    tf_slots_reduce_kernel<<<(nout + 31) / 32, 1024, 0, st>>>(T.slots, T.nslot, T.slot_floats,
                                                              T.kind, T.count, d_tf);
     if ((rc = check_launch("tf_slots_reduce_kernel"))) return rc;
   }
