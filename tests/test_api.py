@@ -265,3 +265,25 @@ def test_dropin_l1_loss(cuda):   # objectives.py:38-54
     for x, y, s in zip(xs, ys, seeds):
         np.testing.assert_allclose(s, np.sign(x - y) / count, rtol=1e-7)
     assert seeds[0][0, 0, 0] == 0.0
+
+
+@pytest.mark.gpu
+def test_dropin_caches_the_device_volume(cuda):
+    """The per-view call pattern of tasks.py:397-432 (render / render_adjoint for every
+    view with one DensityVolume) uploads and packs the volume once; a new DensityVolume
+    (what each optimiser step builds, tasks.py:473-480) is uploaded again."""
+    from paper_2107_12672_b200 import _native as N
+    g, vol, tf, cam, dt = _scene("rand_500")
+    cfg = vd.RenderConfig(dt=dt, target="volume")
+    first = vd.render(vol, tf, cam, cfg)
+    n0 = N.launch_count()
+    again = vd.render(vol, tf, cam, cfg)
+    vd.render_adjoint(vol, tf, cam, cfg, np.ones(first.data.shape), image=again)
+    n_cached = N.launch_count() - n0           # forward + adjoint (+ fold): no pack
+    np.testing.assert_array_equal(first.data, again.data)
+    vol2 = vd.DensityVolume(vol.values * 0.5, vol.box_min, vol.box_max)
+    n1 = N.launch_count()
+    half = vd.render(vol2, tf, cam, cfg)
+    assert N.launch_count() - n1 == 2          # pack_cells + forward: a new volume
+    assert not np.array_equal(half.data, first.data)
+    assert n_cached <= 4
