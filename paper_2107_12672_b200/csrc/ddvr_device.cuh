@@ -892,14 +892,10 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
 
 // tau of an affine texel column at density d: the table lerp of field.py:540-549
 // with clamp-to-edge is a + b clamp(t, 0, R-1), t = d R - 1/2; its slope is b
-// for t in [0, R-1) and 0 in the clamp bands (the guard texels' zero deltas)
+// for t in [0, R-1] (the live range of field.py:573-576) and 0 in the clamp bands
 __device__ __forceinline__ float tau_affine(const TfArgs& T, float d, float a, float b) {
   const float t = __fmaf_rn(d, T.fR, -0.5f);
   return __fmaf_rn(b, fminf(fmaxf(t, 0.f), T.fR1), a);
-}
-__device__ __forceinline__ float slope_affine(const TfArgs& T, float d, float b) {
-  const float t = __fmaf_rn(d, T.fR, -0.5f);
-  return (t >= 0.f && t < T.fR1) ? b : 0.f;
 }
 
 __device__ __forceinline__ int seg_mode(float dt32, unsigned maxtau_bits) {
@@ -939,7 +935,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // the march sums anyway (fp64) -- so only S is carried per sample.
   constexpr bool kAbs = !EMIT && !TAPE && !EARLY && KIND == kTfTexture && DDVR_ABS_WALK;
   // BITS (band tape): one bit per sample = the clamped density d is in the band
-  // t = d R - 1/2 in [0, R-1).  That equals the affine absorption walk's d_hat
+  // t = d R - 1/2 in [0, R-1] (field.py:573-576).  That equals the affine absorption walk's d_hat
   // test (adjoint_ray: inside the box and t on the raw density in the band --
   // outside, or raw outside [0,1], d clamps to 0 or 1 and t leaves the band), so
   // the walk takes it from the tape instead of re-gathering the record.  Word k
@@ -950,6 +946,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // BITS: the optical depth of the current 32-sample word in fp32, added to the fp64 S
   // once per word (32 terms of at most dt*tau_max: ~1e-7 of a word's depth)
   float Sb = 0.f;
+  const float dt_a = dt32 * aff_a, dt_b = dt32 * aff_b;   // (band march)
   // one compositing step on a located sample and its record
   auto density = [&](const Cell& c, const float* k) {
     return clamp_density(INSIDE || c.inside, interp(c, k).rho);
@@ -957,19 +954,26 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // kStore: the word is stored at its last sample here (else by the caller's block loop)
   auto shade = [&](float d, int i, auto kStore) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
+    if (kAbs && AFF && BITS) {
+      // band march (non-negative affine tau column): band bit = t inside [0, R-1], the
+      // live range of field.py:573-576 (t == its clamp), pushed in at the LSB (the walk
+      // pops it from there); dt*tau = dt*a + dt*b*clamp(t) in one FFMA (tau >= 0 here)
+      const float t = __fmaf_rn(d, TF.fR, -0.5f);
+      const float tc = fminf(fmaxf(t, 0.f), TF.fR1);
+      word = (word << 1) | (tc == t ? 1u : 0u);
+      if (decltype(kStore)::value && (i & 31) == 31) {
+        bits[bits_off + ((i >> 5) << 5)] = word;
+        word = 0u;
+      }
+      const float x = __fmaf_rn(dt_b, tc, dt_a);
+      Sb = __fadd_rn(Sb, SEG == kSegGen ? fminf(x, kNegLnEps) : x);   // per word
+      return;
+    }
     if (kAbs && AFF) {   // affine tau column: no table lookup
       const float t = __fmaf_rn(d, TF.fR, -0.5f);
-      if (BITS) {   // band bit, pushed in at the LSB (the walk pops it from there)
-        word = (word << 1) | (t >= 0.f && t < TF.fR1 ? 1u : 0u);
-        if (decltype(kStore)::value && (i & 31) == 31) {
-          bits[bits_off + ((i >> 5) << 5)] = word;
-          word = 0u;
-        }
-      }
       const float tau = __fmaf_rn(aff_b, fminf(fmaxf(t, 0.f), TF.fR1), aff_a);   // tau_affine
       const float x = __fmul_rn(dt32, fmaxf(tau, 0.f));
-      if (BITS) Sb = __fadd_rn(Sb, SEG == kSegGen ? fminf(x, kNegLnEps) : x);   // per word
-      else S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
+      S += (double)(SEG == kSegGen ? fminf(x, kNegLnEps) : x);
       return;
     }
     int i0; float w;
@@ -1350,13 +1354,13 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     } else if (kAbs && AFF) {
       // non-negative affine tau column in a polynomial segment mode, no
       // stepsize target (dispatch guarantees it): tau >= 0, no EPS clamp, and
-      // the slope is b for t in [0, R-1), 0 in the clamp bands -- only the
-      // band test is left per sample (b is folded into abs_k).  It is taken on
-      // the raw density: t in [0, R-1) already implies raw in (0, 1), where
+      // the slope is b for t in [0, R-1] (field.py:573-576), 0 in the clamp bands --
+      // only the band test is left per sample (b is folded into abs_k).  It is taken
+      // on the raw density: t in [0, R-1] already implies raw in (0, 1), where
       // d == raw, so it also carries the [0,1] live test of field.py:486-489.
       i0 = 0; w = 0.f;
       const float t = __fmaf_rn(raw, TF.fR, -0.5f);
-      dq = (t >= 0.f && t < TF.fR1) ? 1.f : 0.f;
+      dq = (t >= 0.f && t <= TF.fR1) ? 1.f : 0.f;   // live range of field.py:573-576
       s = make_float4(0.f, 0.f, 0.f, 0.f);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (kAbs) {
@@ -1461,7 +1465,11 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         // (ptxas branches around a predicated red anyway: one branch for both
         // halves, and the record address is formed only inside it)
         DDVR_REQUIRE(!flush || cell_ok(V, st.run_cell));
+#ifdef DDVR_WALK_NORED   // measurement variant: the reds replaced by a register sink
+        if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
+#else
         if (flush) flush_cell<true>(d_volume, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+#endif
         const float keep = fresh ? 0.f : 1.f;
         st.acc8[0] = fmaf(st.acc8[0], keep, dh);
         st.acc8[1] = fmaf(st.acc8[1], keep, px);
@@ -1599,10 +1607,13 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
                                               int* nskip) {
   const int n = r.n;
   if (n <= 0) return;
-  // per-ray constants: the u step per sample, its products, the run-length divisors
+  // per-ray constants: the u step per sample and its products, scaled by the walk
+  // weight abs_k (so a run's moments need the power sums unscaled), the run-length
+  // divisors
   const float dx = (float)r.gs[0] * kInvFix, dy = (float)r.gs[1] * kInvFix,
               dz = (float)r.gs[2] * kInvFix;
-  const float dxy = dx * dy, dxz = dx * dz, dyz = dy * dz, dxyz = dxy * dz;
+  const float kx = abs_k * dx, ky = abs_k * dy, kz = abs_k * dz;
+  const float kxy = kx * dy, kxz = kx * dz, kyz = ky * dz, kxyz = kxy * dz;
   // samples left in the cell along an axis: floor(num / |gs|) + 1 with num = 2^32-1-lo
   // (moving up) or lo (moving down); 1/|gs| = inf on an axis the ray never leaves
   const float ix = r.gs[0] != 0 ? __frcp_rn((float)llabs(r.gs[0])) : INFINITY;
@@ -1657,22 +1668,24 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
         P0 += 1.f; P1 += k; P2 += k * k; P3 += k * k * k;
       }
     }
-    const float q0 = abs_k * P0, q1 = abs_k * P1, q2 = abs_k * P2, q3 = abs_k * P3;
+    // sum_k dh phi(u0 + k d) expanded in the power sums (dh = abs_k folded into q0 and
+    // the k* constants)
+    const float q0 = abs_k * P0;
     const float ux = __fmaf_rn(__uint2float_rn(lx), kInvFix, -0.5f);
     const float uy = __fmaf_rn(__uint2float_rn(ly), kInvFix, -0.5f);
     const float uz = __fmaf_rn(__uint2float_rn(lz), kInvFix, -0.5f);
     const float uxy = ux * uy, uxz = ux * uz, uyz = uy * uz;
     float a[8];
     a[0] = q0;
-    a[1] = __fmaf_rn(ux, q0, dx * q1);
-    a[2] = __fmaf_rn(uy, q0, dy * q1);
-    a[3] = __fmaf_rn(uz, q0, dz * q1);
-    a[4] = __fmaf_rn(uxy, q0, __fmaf_rn(__fmaf_rn(ux, dy, uy * dx), q1, dxy * q2));
-    a[5] = __fmaf_rn(uxz, q0, __fmaf_rn(__fmaf_rn(ux, dz, uz * dx), q1, dxz * q2));
-    a[6] = __fmaf_rn(uyz, q0, __fmaf_rn(__fmaf_rn(uy, dz, uz * dy), q1, dyz * q2));
-    const float t1 = __fmaf_rn(uxy, dz, __fmaf_rn(uxz, dy, uyz * dx));
-    const float t2 = __fmaf_rn(ux, dyz, __fmaf_rn(uy, dxz, uz * dxy));
-    a[7] = __fmaf_rn(uxy * uz, q0, __fmaf_rn(t1, q1, __fmaf_rn(t2, q2, dxyz * q3)));
+    a[1] = __fmaf_rn(ux, q0, kx * P1);
+    a[2] = __fmaf_rn(uy, q0, ky * P1);
+    a[3] = __fmaf_rn(uz, q0, kz * P1);
+    a[4] = __fmaf_rn(uxy, q0, __fmaf_rn(__fmaf_rn(ux, ky, uy * kx), P1, kxy * P2));
+    a[5] = __fmaf_rn(uxz, q0, __fmaf_rn(__fmaf_rn(ux, kz, uz * kx), P1, kxz * P2));
+    a[6] = __fmaf_rn(uyz, q0, __fmaf_rn(__fmaf_rn(uy, kz, uz * ky), P1, kyz * P2));
+    const float t1 = __fmaf_rn(uxy, kz, __fmaf_rn(uxz, ky, uyz * kx));
+    const float t2 = __fmaf_rn(ux, kyz, __fmaf_rn(uy, kxz, uz * kxy));
+    a[7] = __fmaf_rn(uxy * uz, q0, __fmaf_rn(t1, P1, __fmaf_rn(t2, P2, kxyz * P3)));
     const int cell = (((int)(gx >> 32)) * V.CY + (int)(gy >> 32)) * V.CZ + (int)(gz >> 32);
 #ifdef DDVR_WALK_NORED   // measurement variant: no reds (the atomic-free floor)
     if (a[0] == 12345.f) d_cells[0] = a[7] + (float)cell;
@@ -1867,6 +1880,9 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
       for (int k = 0; k < 4; ++k)
         if (c[k]) atomicAdd(G.stats + k, c[k]);
   }
+#ifdef DDVR_WALK_NORED
+  if (!kTf && st.tfp0 == 12345.f && d_cells) d_cells[0] = st.tfp0;
+#endif
   // ---- flush per-ray accumulators ----
   DDVR_REQUIRE(!(kVol && CELLS && st.run_cell != kNoRun) || cell_ok(V, st.run_cell));
   if (kVol && st.run_cell != kNoRun)
