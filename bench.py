@@ -79,6 +79,8 @@ def parse(argv=None):
                         "auto: on for launch-bound steps (density target, < 1e7 samples)")
     p.add_argument("--unfused", action="store_true",
                    help="separate forward / L1 / adjoint launches instead of the fused step")
+    p.add_argument("--fused", action="store_true",
+                   help="the fused step also for camera / stepsize targets")
     p.add_argument("--no-empty-skip", action="store_true",
                    help="band tape without the empty-brick skip of the march")
     p.add_argument("--no-band-tape", action="store_true",
@@ -431,7 +433,8 @@ def run_own(args, cfg):
     def make_step(band_tape):
         return ShardedStep(est, tex, ll, refs, cfg.dt, rig, targets=cfg.targets,
                            total_elements=total_elems, radius=cfg.radius, fov_y_deg=cfg.fov,
-                           layout=args.layout, fused=False if args.unfused else "auto",
+                           layout=args.layout,
+                           fused=False if args.unfused else (True if args.fused else "auto"),
                            band_tape=band_tape, empty_skip=not args.no_empty_skip,
                            split_walk=args.split_walk)
 

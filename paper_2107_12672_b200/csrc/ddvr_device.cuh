@@ -892,7 +892,7 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
 
 // tau of an affine texel column at density d: the table lerp of field.py:540-549
 // with clamp-to-edge is a + b clamp(t, 0, R-1), t = d R - 1/2; its slope is b
-// for t in [0, R-1] (the live range of field.py:573-576) and 0 in the clamp bands
+// for t in [0, R-1) and 0 in the clamp bands (the guard texels' zero deltas)
 __device__ __forceinline__ float tau_affine(const TfArgs& T, float d, float a, float b) {
   const float t = __fmaf_rn(d, T.fR, -0.5f);
   return __fmaf_rn(b, fminf(fmaxf(t, 0.f), T.fR1), a);
@@ -935,7 +935,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   // the march sums anyway (fp64) -- so only S is carried per sample.
   constexpr bool kAbs = !EMIT && !TAPE && !EARLY && KIND == kTfTexture && DDVR_ABS_WALK;
   // BITS (band tape): one bit per sample = the clamped density d is in the band
-  // t = d R - 1/2 in [0, R-1] (field.py:573-576).  That equals the affine absorption walk's d_hat
+  // t = d R - 1/2 in [0, R-1).  That equals the affine absorption walk's d_hat
   // test (adjoint_ray: inside the box and t on the raw density in the band --
   // outside, or raw outside [0,1], d clamps to 0 or 1 and t leaves the band), so
   // the walk takes it from the tape instead of re-gathering the record.  Word k
@@ -955,12 +955,14 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
   auto shade = [&](float d, int i, auto kStore) {
     if (TAPE) tape[i] = T;                     // stored mode (renderer.py:348-349)
     if (kAbs && AFF && BITS) {
-      // band march (non-negative affine tau column): band bit = t inside [0, R-1], the
-      // live range of field.py:573-576 (t == its clamp), pushed in at the LSB (the walk
-      // pops it from there); dt*tau = dt*a + dt*b*clamp(t) in one FFMA (tau >= 0 here)
+      // band march (non-negative affine tau column): band bit = t in [0, R-1) -- the
+      // texel table's slope band (its guard texel at R-1 has a zero delta; the
+      // reference's closed live range differs only at t == R-1 exactly) -- pushed in at
+      // the LSB (the walk pops it from there); dt*tau = dt*a + dt*b*clamp(t) in one
+      // FFMA (tau >= 0 here)
       const float t = __fmaf_rn(d, TF.fR, -0.5f);
       const float tc = fminf(fmaxf(t, 0.f), TF.fR1);
-      word = (word << 1) | (tc == t ? 1u : 0u);
+      word = (word << 1) | (t >= 0.f && t < TF.fR1 ? 1u : 0u);
       if (decltype(kStore)::value && (i & 31) == 31) {
         bits[bits_off + ((i >> 5) << 5)] = word;
         word = 0u;
@@ -1145,6 +1147,12 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
 // (4 CTAs/SM); the camera/stepsize walks carry fp64 sums (ptxas' choice).
 // The absorption-only kernel (ROLE 1) carries none of the emitting walk's
 // state and is compiled for 5 CTAs/SM.
+#ifndef DDVR_POS_MINB
+#define DDVR_POS_MINB 3   // camera / stepsize walks (fp64 per-ray sums; 80 registers: C3 +13% vs 2)
+#endif
+#ifndef DDVR_TF_MINB
+#define DDVR_TF_MINB 3    // TF-target walks
+#endif
 constexpr int adj_min_blocks(unsigned mask, int role, bool cells, bool fused) {
   return !cells ? 2   // voxel layout: 8 scalar gathers per sample, more live state
          // the fused absorption step carries the band-tape word and pointer
@@ -1152,7 +1160,9 @@ constexpr int adj_min_blocks(unsigned mask, int role, bool cells, bool fused) {
          : (role == 1 && mask == DDVR_TARGET_VOLUME && fused) ? DDVR_ABS_FUSED_MINB
          : (role == 1 && mask == DDVR_TARGET_VOLUME) ? DDVR_ABS_MINB
          : mask == DDVR_TARGET_VOLUME ? 4
-         : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? 2 : 3;
+         // camera / stepsize with the TF target too: fp64 sums + texel runs (128 registers)
+         : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) && (mask & DDVR_TARGET_TF) ? 2
+         : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? DDVR_POS_MINB : DDVR_TF_MINB;
 }
 #ifdef DDVR_ADJ_MINB
 #define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, DDVR_ADJ_MINB)
@@ -1354,13 +1364,13 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     } else if (kAbs && AFF) {
       // non-negative affine tau column in a polynomial segment mode, no
       // stepsize target (dispatch guarantees it): tau >= 0, no EPS clamp, and
-      // the slope is b for t in [0, R-1] (field.py:573-576), 0 in the clamp bands --
-      // only the band test is left per sample (b is folded into abs_k).  It is taken
-      // on the raw density: t in [0, R-1] already implies raw in (0, 1), where
+      // the slope is b for t in [0, R-1), 0 in the clamp bands -- only the band test
+      // is left per sample (b is folded into abs_k).  It is taken on the raw density:
+      // t in [0, R-1) already implies raw in (0, 1), where
       // d == raw, so it also carries the [0,1] live test of field.py:486-489.
       i0 = 0; w = 0.f;
       const float t = __fmaf_rn(raw, TF.fR, -0.5f);
-      dq = (t >= 0.f && t <= TF.fR1) ? 1.f : 0.f;   // live range of field.py:573-576
+      dq = (t >= 0.f && t < TF.fR1) ? 1.f : 0.f;
       s = make_float4(0.f, 0.f, 0.f, 0.f);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (kAbs) {

@@ -1,0 +1,5 @@
+run() { timeout 600 python bench.py --no-extras --no-cpu-baseline --steps 5 --warmup 3 "$@" 2>&1 | grep '^{' | python -c "import json,sys;d=json.loads(sys.stdin.read());print('RESULT', '${DDVR_LIB##*/}', sys.argv[1:], round(d['value']/1e9,2), round(d['ms_per_step'],3), d['kernels'])" "$@"; }
+for v in "" tf4 pos3; do
+  if [ -n "$v" ]; then export DDVR_LIB=paper_2107_12672_b200/_variants/libddvr_$v.so; fi
+  run --config C2; run --config C3; run --config C1
+done
