@@ -86,6 +86,9 @@ def parse(argv=None):
     p.add_argument("--no-band-tape", action="store_true",
                    help="fused absorption step without the 1-bit-per-sample band tape "
                         "(DDVR_FLAG_BAND_TAPE; the walk then re-gathers the cell records)")
+    p.add_argument("--deterministic", action="store_true",
+                   help="bitwise-reproducible gradients (DDVR_FLAG_DETERMINISTIC: int64 "
+                        "fixed-point cell moments, fixed-order camera / stepsize sums)")
     p.add_argument("--split-walk", action="store_true",
                    help="band tape: march and walk as two kernels (DDVR_FLAG_SPLIT_WALK)")
     p.add_argument("--dry-run", action="store_true",
@@ -436,7 +439,7 @@ def run_own(args, cfg):
                            layout=args.layout,
                            fused=False if args.unfused else (True if args.fused else "auto"),
                            band_tape=band_tape, empty_skip=not args.no_empty_skip,
-                           split_walk=args.split_walk)
+                           split_walk=args.split_walk, deterministic=args.deterministic)
 
     step = make_step(False if args.no_band_tape else "auto")
     small = cfg_samples(cfg) is not None and cfg_samples(cfg) < 10 ** 7
@@ -757,6 +760,8 @@ def report(args, cfg, step, runner, world, mine, total_samples, total_rays, loca
                               (", band tape (1 bit/sample, DDVR_FLAG_BAND_TAPE)" if band
                                else "") +
                               (", empty-brick skip in the march" if band and step.empty_skip
+                               else "") +
+                              (", deterministic (int64 cell moments)" if step.deterministic
                                else "") +
                               (", march and walk as two kernels" if band and step.split_walk
                                else "") + (", CUDA-graph replay" if graphed else ""))

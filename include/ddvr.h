@@ -233,11 +233,18 @@ int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf,
 
 /* Extra workspace of a DDVR_FLAG_DETERMINISTIC ddvr_adjoint /
  * ddvr_forward_adjoint_l1 call over n_views views with params p: the caller
- * passes ddvr_adjoint_workspace_bytes rounded up to 256, plus this.  0 unless
- * mask has the camera or stepsize target.  (The TF gradient is always reduced
- * from per-CTA slots in slot order; d_volume and the in-CTA TF sums use fp32
- * atomics: reproducible to fp32 rounding, not bitwise.) */
-int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask);
+ * passes ddvr_adjoint_workspace_bytes rounded up to 256, plus this.  It holds
+ *   - with the camera or stepsize target: per-CTA partials, reduced in a fixed order
+ *     (d_camera and d_dt bitwise reproducible);
+ *   - with the volume target and cell records: the cell-gradient moments as int64
+ *     fixed point (round(moment * scale), scale = 2^50 / a bound of any one flush
+ *     derived from the TF table and max|seed|): integer adds commute, so d_volume is
+ *     bitwise reproducible for any order of the atomics.  Texel TFs only; for
+ *     ddvr_adjoint one call per step (no WS_CONTINUE / WS_DEFER: the scale comes
+ *     from that call's seed); the fused step's seed is +-1/count in every call.
+ * (The in-CTA TF sums stay fp32 atomics: d_tf is reproducible to rounding.) */
+int64_t ddvr_deterministic_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p,
+                                 uint32_t mask);
 
 /* Extra workspace of a DDVR_FLAG_BAND_TAPE ddvr_forward_adjoint_l1 call: one
  * bit per sample for every ray, 32-bit words per ray bounded by the box

@@ -113,7 +113,8 @@ def _bind(lib):
     lib.ddvr_adjoint_color.restype = ctypes.c_int
     lib.ddvr_adjoint_workspace_bytes.argtypes = [P(DdvrVolume), P(DdvrTf), ctypes.c_uint32]
     lib.ddvr_adjoint_workspace_bytes.restype = ctypes.c_int64
-    lib.ddvr_deterministic_bytes.argtypes = [ctypes.c_int32, P(DdvrParams), ctypes.c_uint32]
+    lib.ddvr_deterministic_bytes.argtypes = [P(DdvrVolume), ctypes.c_int32, P(DdvrParams),
+                                             ctypes.c_uint32]
     lib.ddvr_deterministic_bytes.restype = ctypes.c_int64
     lib.ddvr_band_tape_bytes.argtypes = [P(DdvrVolume), ctypes.c_int32, P(DdvrParams)]
     lib.ddvr_band_tape_bytes.restype = ctypes.c_int64

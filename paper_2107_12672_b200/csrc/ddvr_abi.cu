@@ -77,6 +77,10 @@ __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
                                                        const float* __restrict__ d_cells,
                                                        float* __restrict__ d_volume,
                                                        long long nvox) {
+  // the deterministic mode's int64 fixed-point moments (V.cells64 relative to cell 0)
+  const unsigned long long* c64 =
+      V.cells64 ? V.cells64 - (V.cell0 - V.cells) : nullptr;
+  const double inv = c64 ? 1.0 / __ldg(V.det_scale) : 0.0;
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= nvox) return;
   const int z = (int)(id % V.Z);
@@ -106,8 +110,18 @@ __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
     for (int b = 0; b < cn[1]; ++b)
       for (int c = 0; c < cn[2]; ++c) {
         const size_t cell = ((size_t)ci[0][a] * V.CY + ci[1][b]) * V.CZ + ci[2][c];
-        const float4* m = reinterpret_cast<const float4*>(d_cells + 8 * cell);
-        s += corner_from_moments(m[0], m[1], cb[0][a] | cb[1][b] << 1 | cb[2][c] << 2);
+        const int corner = cb[0][a] | cb[1][b] << 1 | cb[2][c] << 2;
+        if (c64) {
+          const long long* q = reinterpret_cast<const long long*>(c64 + 8 * cell);
+          const float4 m0 = make_float4((float)(q[0] * inv), (float)(q[1] * inv),
+                                        (float)(q[2] * inv), (float)(q[3] * inv));
+          const float4 m1 = make_float4((float)(q[4] * inv), (float)(q[5] * inv),
+                                        (float)(q[6] * inv), (float)(q[7] * inv));
+          s += corner_from_moments(m0, m1, corner);
+        } else {
+          const float4* m = reinterpret_cast<const float4*>(d_cells + 8 * cell);
+          s += corner_from_moments(m[0], m[1], corner);
+        }
       }
   d_volume[id] += s;
 }
@@ -243,6 +257,8 @@ int make_vol(const ddvr_volume* vol, VolArgs& V, bool need_data = true) {
   V.data = vol->data;
   V.cells = vol->cells;
   V.occ = nullptr;   // set by run_adjoint for the fused band-tape step
+  V.cells64 = nullptr;   // set by run_adjoint in the deterministic volume mode
+  V.det_scale = nullptr;
   V.NBy = (vol->dims[1] + 8) >> 3; V.NBz = (vol->dims[2] + 8) >> 3;
   V.X = vol->dims[0]; V.Y = vol->dims[1]; V.Z = vol->dims[2];
   V.YZ = V.Y * V.Z;
@@ -693,6 +709,64 @@ static int64_t det_bytes(int64_t ctas, uint32_t mask) {
   return (ctas * 3 * 8 + 255) & ~(int64_t)255;
 }
 
+// DDVR_FLAG_DETERMINISTIC with the volume target and cell records: a 256-byte header
+// (the fixed-point scale, the seed bound) and the int64 cell-gradient moments (8 per
+// padded cell record), after the partials
+static int64_t det_vol_bytes(const ddvr_volume* vol, uint32_t mask) {
+  if (!vol || !vol->cells || !(mask & DDVR_TARGET_VOLUME)) return 0;
+  return 256 + 2 * ((ddvr_cells_bytes(vol->dims) + 255) & ~(int64_t)255);
+}
+
+// max |seed| over n floats as ordered float bits (non-negative floats order like ints)
+__global__ void __launch_bounds__(256) seed_absmax_kernel(const float* __restrict__ seed,
+                                                        long long n,
+                                                        unsigned* __restrict__ out) {
+  float m = 0.f;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    m = fmaxf(m, fabsf(seed[i]));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// The fixed-point scale of the deterministic cell gradients: 2^50 / C, C a bound of any
+// one flush's moment (a run of at most lmax samples, |phi| <= 1, |d_hat| <= dmax).  From
+// the blend / Beer-Lambert adjoint (renderer.py:583-608) with |seed| <= smax, rgb <= c:
+//   |d_hat| <= R smax (3 max|delta rgb| + dt max|delta tau| (2 + 6 c))
+// (the affine absorption walk's d_hat = seed_a T_n dt R b is the delta-tau term).  Each
+// flush is then < 2^50 and a cell's int64 sum has room for 8192 such flushes; fp32
+// moments keep ~2^-50 of C in the quantisation.
+__global__ void __launch_bounds__(256) det_scale_kernel(const float* __restrict__ texels,
+                                                      int R, double dt, double lmax,
+                                                      double smax_host,
+                                                      double* __restrict__ header) {
+  __shared__ float s_max[3][256];
+  float drgb = 0.f, dtau = 0.f, rgb = 0.f;
+  for (int k = threadIdx.x; k < R; k += blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(texels)[k];
+    const float4 b = reinterpret_cast<const float4*>(texels)[min(k + 1, R - 1)];
+    drgb = fmaxf(drgb, fmaxf(fabsf(b.x - a.x), fmaxf(fabsf(b.y - a.y), fabsf(b.z - a.z))));
+    dtau = fmaxf(dtau, fabsf(b.w - a.w));
+    rgb = fmaxf(rgb, fmaxf(fabsf(a.x), fmaxf(fabsf(a.y), fabsf(a.z))));
+  }
+  s_max[0][threadIdx.x] = drgb; s_max[1][threadIdx.x] = dtau; s_max[2][threadIdx.x] = rgb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < blockDim.x; ++t) {
+      drgb = fmaxf(drgb, s_max[0][t]); dtau = fmaxf(dtau, s_max[1][t]); rgb = fmaxf(rgb, s_max[2][t]);
+    }
+    const double smax = smax_host >= 0.0 ? smax_host
+                        : (double)__uint_as_float(reinterpret_cast<unsigned*>(header + 1)[0]);
+    const double dmax = (double)R * smax * (3.0 * drgb + dt * dtau * (2.0 + 6.0 * rgb));
+    const double c = lmax * dmax;
+    header[0] = c > 0.0 ? 1125899906842624.0 / c : 1.0;   // 2^50 / C
+  }
+}
+
 // Brick occupancy maps of the fused band-tape step: bricks of 8^3 padded cell records
 // (storage indices [8b, 8b+8) per axis), a byte per brick for the occupancy and for
 // the 2x2x2 window OR the march reads (VolArgs::occ).
@@ -767,13 +841,14 @@ int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr
          ray_k_bytes(grid_ctas(n_views, p));
 }
 
-int64_t ddvr_deterministic_bytes(int32_t n_views, const ddvr_params* p, uint32_t mask) {
+int64_t ddvr_deterministic_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p,
+                                 uint32_t mask) {
   if (!p || n_views < 0 || p->width < 1 || p->height < 1) return 0;
   const int row1 = p->row1 <= 0 ? p->height : p->row1;
   const int rows = std::max(0, row1 - p->row0);
   const int64_t ctas = (int64_t)((p->width + kTile - 1) / kTile) * ((rows + kTile - 1) / kTile) *
                        n_views;
-  return det_bytes(ctas, mask);
+  return det_bytes(ctas, mask) + det_vol_bytes(vol, mask);
 }
 
 int ddvr_forward(const ddvr_volume* vol, const ddvr_tf* tf, const ddvr_camera* cams,
@@ -822,9 +897,16 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   const int64_t ws_cells = ws_cells_bytes(vol, mask), ws_tf = ws_tf_bytes(tf, mask);
   const int64_t ws_need = ws_cells + ws_tf;
   const dim3 grid = grid_of(G, n_views);
-  const int64_t ws_det = (flags & DDVR_FLAG_DETERMINISTIC)
-                             ? det_bytes((int64_t)grid.x * grid.y * grid.z, mask) : 0;
+  const int64_t ws_part = (flags & DDVR_FLAG_DETERMINISTIC)
+                              ? det_bytes((int64_t)grid.x * grid.y * grid.z, mask) : 0;
+  const int64_t ws_dvol = (flags & DDVR_FLAG_DETERMINISTIC) ? det_vol_bytes(vol, mask) : 0;
+  const int64_t ws_det = ws_part + ws_dvol;
   const int64_t det_off = (ws_need + 255) & ~(int64_t)255;
+  if (ws_dvol > 0 && T.kind != DDVR_TF_TEXTURE)
+    return set_error(DDVR_UNSUPPORTED, "the deterministic density gradient needs a texel TF");
+  if (ws_dvol > 0 && !fu && (flags & (DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER)))
+    return set_error(DDVR_UNSUPPORTED, "the deterministic density gradient of ddvr_adjoint "
+                     "takes its fixed-point scale from the call's seed: one call per step");
   if (ws_need > 0 && (!workspace || workspace_bytes < ws_need))
     return set_error(DDVR_INVALID_INPUT,
                      "this target mask needs a %lld-byte workspace "
@@ -865,9 +947,35 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   cudaStream_t st = (cudaStream_t)stream;
   const size_t smem = tbl;
   const bool cells = V.cells != nullptr;
-  if (ws_det > 0) {   // every call reduces its own partials (also under WS_DEFER)
+  if (ws_dvol > 0) {   // int64 fixed-point cell gradients (order-independent sums)
+    double* header = reinterpret_cast<double*>(static_cast<char*>(workspace) + det_off + ws_part);
+    unsigned long long* c64 = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(header) + 256);
+    V.cells64 = c64 + (V.cell0 - V.cells);   // relative to cell (0,0,0), like cell0
+    V.det_scale = header;
+    if (!(flags & DDVR_FLAG_WS_CONTINUE)) {   // the first call of the step fixes the scale
+      cudaError_t e = cudaMemsetAsync(header, 0, (size_t)ws_dvol, st);
+      if (e != cudaSuccess)
+        return set_error(DDVR_CUDA_ERROR, "workspace memset: %s", cudaGetErrorString(e));
+      double smax_host = -1.0;
+      if (fu) {
+        smax_host = (double)fu->inv_count;   // the L1 seed is +-1/count
+      } else {
+        const long long n = 4ll * n_views * (G.row1 - G.row0) * G.W;
+        seed_absmax_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0,
+                             st>>>(seed, n, reinterpret_cast<unsigned*>(header + 1));
+        if ((rc = check_launch("seed_absmax_kernel"))) return rc;
+      }
+      // the longest run of samples in one cell: the cell diagonal over the smallest step
+      const double smin = std::min(V.scale[0], std::min(V.scale[1], V.scale[2]));
+      const double lmax = std::ceil(std::sqrt(3.0) / (G.dt * smin)) + 2.0;
+      det_scale_kernel<<<1, 256, 0, st>>>(T.params, T.count, G.dt, lmax, smax_host, header);
+      if ((rc = check_launch("det_scale_kernel"))) return rc;
+    }
+  }
+  if (ws_part > 0) {   // every call reduces its own partials (also under WS_DEFER)
     G.partials = reinterpret_cast<double*>(static_cast<char*>(workspace) + det_off);
-    cudaError_t e = cudaMemsetAsync(G.partials, 0, (size_t)ws_det, st);
+    cudaError_t e = cudaMemsetAsync(G.partials, 0, (size_t)ws_part, st);
     if (e != cudaSuccess)
       return set_error(DDVR_CUDA_ERROR, "partials memset: %s", cudaGetErrorString(e));
   }
@@ -898,7 +1006,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                                d_volume, d_cells, d_camera, d_dt, fu);
   if ((rc = check_launch(fu ? "dvr_adjoint_kernel (fused)" : "dvr_adjoint_kernel"))) return rc;
   g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
-  if (ws_det > 0) {
+  if (ws_part > 0) {
     const int tiles = (int)(grid.x * grid.y);
     const int cam_blocks = (mask & DDVR_TARGET_CAMERA) ? n_views : 0;
     const int blocks = cam_blocks + ((mask & DDVR_TARGET_STEPSIZE) ? 1 : 0);

@@ -108,6 +108,12 @@ struct VolArgs {
   // b .. b+1 (those that exist) is nonzero
   const unsigned char* __restrict__ occ;
   int NBy, NBz;            // bricks along y and z: ceil((dim + 1) / 8)
+  // DDVR_FLAG_DETERMINISTIC with the volume target (nullable): the cell-gradient
+  // moments accumulate as int64 fixed point (round(moment * *det_scale)) at this
+  // address (relative to cell (0,0,0), like cell0) -- integer adds commute, so the
+  // sums and d_volume are the same bits for any order of the atomics
+  unsigned long long* cells64;
+  const double* det_scale;
 };
 
 // brick coordinate of the padded cell record at a fixed-point grid coordinate
@@ -534,6 +540,23 @@ __device__ __forceinline__ void gather_if(const VolArgs& V, bool pred, int cell,
 __device__ __forceinline__ void gather(const VolArgs& V, int cell, float v[8]) {
   DDVR_REQUIRE(cell_ok(V, cell));
   ld256(V.cell0 + 8 * (long long)cell, v);
+}
+
+// One cell run's 8 moments into the cell-gradient workspace: two 128-bit vector reds
+// (fp32), or in the deterministic mode eight int64 fixed-point adds.
+__device__ __forceinline__ void flush_record(const VolArgs& V, float* __restrict__ d_cells,
+                                             int cell, const float a[8]) {
+  if (V.cells64) {
+    const double sc = __ldg(V.det_scale);
+    unsigned long long* q = V.cells64 + 8 * (long long)cell;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      atomicAdd(q + k, (unsigned long long)__double2ll_rn((double)a[k] * sc));
+  } else {
+    float* q = d_cells + 8 * (long long)cell;
+    red128(q, a[0], a[1], a[2], a[3]);
+    red128(q + 4, a[4], a[5], a[6], a[7]);
+  }
 }
 
 // The trilinear interpolant of a cell (field.py:318-349) as a polynomial in
@@ -1150,6 +1173,9 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
 #ifndef DDVR_POS_MINB
 #define DDVR_POS_MINB 3   // camera / stepsize walks (fp64 per-ray sums; 80 registers: C3 +13% vs 2)
 #endif
+#ifndef DDVR_VOL_MINB
+#define DDVR_VOL_MINB 4   // volume-target walks (ROLE 0: the emitting inversion walk)
+#endif
 #ifndef DDVR_TF_MINB
 #define DDVR_TF_MINB 3    // TF-target walks
 #endif
@@ -1159,7 +1185,7 @@ constexpr int adj_min_blocks(unsigned mask, int role, bool cells, bool fused) {
          // through the march: 64 registers (4 CTAs/SM) beat 48 with spills
          : (role == 1 && mask == DDVR_TARGET_VOLUME && fused) ? DDVR_ABS_FUSED_MINB
          : (role == 1 && mask == DDVR_TARGET_VOLUME) ? DDVR_ABS_MINB
-         : mask == DDVR_TARGET_VOLUME ? 4
+         : mask == DDVR_TARGET_VOLUME ? DDVR_VOL_MINB
          // camera / stepsize with the TF target too: fp64 sums + texel runs (128 registers)
          : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) && (mask & DDVR_TARGET_TF) ? 2
          : (mask & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) ? DDVR_POS_MINB : DDVR_TF_MINB;
@@ -1478,7 +1504,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
 #ifdef DDVR_WALK_NORED   // measurement variant: the reds replaced by a register sink
         if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
 #else
-        if (flush) flush_cell<true>(d_volume, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+        if (flush) flush_record(V, d_cells, st.run_cell, st.acc8);
 #endif
         const float keep = fresh ? 0.f : 1.f;
         st.acc8[0] = fmaf(st.acc8[0], keep, dh);
@@ -1578,7 +1604,7 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
       if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
 #else
       DDVR_REQUIRE(!flush || cell_ok(V, st.run_cell));
-      if (flush) flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+      if (flush) flush_record(V, d_cells, st.run_cell, st.acc8);
 #endif
       const float keep = fresh ? 0.f : 1.f;
       st.acc8[0] = fmaf(st.acc8[0], keep, dh);
@@ -1701,9 +1727,7 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
     if (a[0] == 12345.f) d_cells[0] = a[7] + (float)cell;
 #else
     DDVR_REQUIRE(cell_ok(V, cell));
-    float* q = d_cells + 8 * (long long)cell;
-    red128(q, a[0], a[1], a[2], a[3]);
-    red128(q + 4, a[4], a[5], a[6], a[7]);
+    flush_record(V, d_cells, cell, a);
 #endif
   }
 }
@@ -1895,7 +1919,9 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
 #endif
   // ---- flush per-ray accumulators ----
   DDVR_REQUIRE(!(kVol && CELLS && st.run_cell != kNoRun) || cell_ok(V, st.run_cell));
-  if (kVol && st.run_cell != kNoRun)
+  if (kVol && CELLS && st.run_cell != kNoRun)
+    flush_record(V, d_cells, st.run_cell, st.acc8);
+  else if (kVol && st.run_cell != kNoRun)
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                       st.run_oz, st.acc8);
   if (kTf && TFA.kind != kTfGaussian && st.tf_run != kNoRun)
@@ -2080,8 +2106,7 @@ __global__ void __launch_bounds__(kThreads, DDVR_BAND_WALK_MINB)
       abs_bits_walk<true>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
     else abs_bits_walk<false>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
     DDVR_REQUIRE(st.run_cell == kNoRun || cell_ok(V, st.run_cell));
-    if (st.run_cell != kNoRun && st.acc8[0] != 0.f)
-      flush_cell<true>(nullptr, d_cells, st.run_cell, 0, 0, 0, 0, st.acc8);
+    if (st.run_cell != kNoRun && st.acc8[0] != 0.f) flush_record(V, d_cells, st.run_cell, st.acc8);
 #ifdef DDVR_WALK_NORED
     if (st.tfp0 == 12345.f) G.ray_k[b.pix] = st.tfp0;
 #endif

@@ -259,7 +259,7 @@ def extra_workspace_bytes(vol, prm, n_views: int, mask: int, deterministic=False
     """Bytes after the 256-aligned adjoint workspace for the optional modes: the
     deterministic partials, then (256-aligned) the band tape (include/ddvr.h)."""
     lib = N.lib()
-    det = int(lib.ddvr_deterministic_bytes(n_views, ctypes.byref(prm), mask)) \
+    det = int(lib.ddvr_deterministic_bytes(ctypes.byref(vol), n_views, ctypes.byref(prm), mask)) \
         if deterministic else 0
     band = int(lib.ddvr_band_tape_bytes(ctypes.byref(vol), n_views, ctypes.byref(prm))) \
         if band_tape and mask == N.TARGET_VOLUME else 0
@@ -350,7 +350,7 @@ def adjoint(density, texels, cams, dt: float, rig: Rig, image, depth, seed, mask
                            (d_camera, "d_camera", torch.float64), (d_dt, "d_dt", torch.float64)):
         if buf is not None:
             _require(buf, name, dt_)
-    extra = int(N.lib().ddvr_deterministic_bytes(V, ctypes.byref(prm), mask)) \
+    extra = int(N.lib().ddvr_deterministic_bytes(ctypes.byref(vol), V, ctypes.byref(prm), mask)) \
         if deterministic else 0
     if deterministic:
         prm.flags |= N.FLAG_DETERMINISTIC

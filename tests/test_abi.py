@@ -225,14 +225,21 @@ def test_field_entry_points_validate_before_launch(lib):
 
 def test_deterministic_mode_workspace(lib):
     """DDVR_FLAG_DETERMINISTIC: per-CTA camera / stepsize partials (3 doubles per
-    16x16-pixel CTA) after the 256-aligned workspace; refused if it does not fit."""
+    16x16-pixel CTA) after the 256-aligned workspace, then (volume target, cell records)
+    the int64 cell-gradient moments; refused if it does not fit."""
     from paper_2107_12672_b200 import _native as N
     vol, tf, prm = _descs(W=512, H=512)
-    det = lambda v, m: lib.ddvr_deterministic_bytes(v, ctypes.byref(prm), m)  # noqa: E731
+    det = lambda v, m: lib.ddvr_deterministic_bytes(ctypes.byref(vol), v, ctypes.byref(prm),  # noqa
+                                                    m)
     assert det(64, 1) == 32 * 32 * 64 * 24 and det(64, 2) == det(64, 3) == det(64, 1)
-    assert det(64, 8) == 0 and det(64, 4) == 0
+    assert det(64, 8) == 0 and det(64, 4) == 0             # no cell records: no int64 region
     prm.row0, prm.row1 = 100, 117                            # a 17-row band: 2 tile rows
     assert det(1, 1) == (32 * 2 * 24 + 255) // 256 * 256
+    vol.cells = 32                                          # with cell records, the volume
+    cells = (5 * 5 * 5 * 32 + 255) // 256 * 256             # target adds a 256-byte header +
+    assert det(1, 8) == 256 + 2 * cells                     # the int64 moments (8 per record)
+    assert det(1, 9) == det(1, 1) + det(1, 8)
+    vol.cells = None
     vol, tf, prm = _descs()
     prm.flags = N.FLAG_DETERMINISTIC
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,

@@ -94,7 +94,9 @@ def test_fused_chunks_keep_per_view_camera_sums(cuda):
                 import ctypes
                 from paper_2107_12672_b200 import _native as N
                 _, _, prm = R._descs(vol, tex, rig, dt, False, cells)
-                extra = int(N.lib().ddvr_deterministic_bytes(int(cams.shape[0]),
+                vold, _, prm = R._descs(vol, tex, rig, dt, False, cells)
+                extra = int(N.lib().ddvr_deterministic_bytes(ctypes.byref(vold),
+                                                              int(cams.shape[0]),
                                                               ctypes.byref(prm), 3))
                 ws = R.workspace_for(vol, 3, cells, tex, extra)
             R.forward_adjoint_l1(vol, tex, cams[a:b], dt, rig, refs[a:b], count, 3, cells=cells,
@@ -120,3 +122,63 @@ def test_sharded_step_deterministic(cuda, fused):
     cam_a, dt_a = step.d_camera.clone(), a.d_stepsize.clone()
     b = step.run()
     assert bool((step.d_camera == cam_a).all()) and bool((b.d_stepsize == dt_a).all())
+
+
+def _det_scene(cuda, texels, n=28, views=4, W=30, H=26):
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.scenes import fibonacci_poses, phantom
+    truth = torch.from_numpy(phantom("sphere", n, seed=0).astype(np.float32)).to(cuda)
+    tex = torch.from_numpy(texels.astype(np.float32)).to(cuda)
+    ll = torch.tensor(fibonacci_poses(views), dtype=torch.float64, device=cuda)
+    rig = R.Rig(W, H)
+    dt = 0.2 / n
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    refs, _ = R.forward(truth, tex, cams, dt, rig)
+    est = (0.8 * truth + 0.1).contiguous()
+    return est, tex, ll, refs, dt, rig
+
+
+@pytest.mark.parametrize("tf", ["ramp", "warm"])
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_density_gradient_is_bitwise_reproducible(cuda, tf, chunks):
+    """DDVR_FLAG_DETERMINISTIC with the volume target: int64 fixed-point cell moments,
+    so the fused step's d_volume is the same bits on every run (band tape / absorption
+    walk for the ramp, the emitting inversion walk for the warm TF), also when the step
+    is split into view chunks, and equals the fp32-atomic result to rounding."""
+    import torch
+    from paper_2107_12672_b200.distributed import ShardedStep
+    from paper_2107_12672_b200.scenes import absorption_ramp_texels, preset_texels
+    texels = absorption_ramp_texels(32, 3.0) if tf == "ramp" else preset_texels("warm", 16, 6.0)
+    est, tex, ll, refs, dt, rig = _det_scene(cuda, texels)
+    host = refs.cpu().pin_memory() if chunks > 1 else None
+    runs = []
+    for _ in range(3):
+        step = ShardedStep(est, tex, ll, refs, dt, rig, deterministic=True, chunks=chunks)
+        runs.append(step.run(refs_host=host).d_volume.clone())
+    assert float(runs[0].abs().max()) > 0
+    for r in runs[1:]:
+        assert torch.equal(r, runs[0])
+    plain = ShardedStep(est, tex, ll, refs, dt, rig).run().d_volume
+    assert rel_l2(runs[0].double().cpu().numpy(), plain.double().cpu().numpy()) <= 1e-6
+
+
+def test_adjoint_density_gradient_is_bitwise_reproducible(cuda):
+    """ddvr_adjoint (one call, arbitrary seed): the scale comes from max|seed|."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.scenes import preset_texels
+    est, tex, ll, refs, dt, rig = _det_scene(cuda, preset_texels("warm", 16, 6.0))
+    cams = R.camera_array(ll, 2.0, (0.0, 0.0, 0.0), 30.0)
+    cells = R.pack_cells(est)
+    img, depth = R.forward(est, tex, cams, dt, rig, cells=cells)
+    seed = torch.randn(img.shape, generator=torch.Generator(device=cuda).manual_seed(3),
+                       device=cuda)
+    outs = []
+    for det in (True, True, False):
+        dv = torch.zeros_like(est)
+        R.adjoint(est, tex, cams, dt, rig, img, depth, seed, 8, d_volume=dv, cells=cells,
+                  deterministic=det)
+        outs.append(dv)
+    assert torch.equal(outs[0], outs[1])
+    assert rel_l2(outs[0].double().cpu().numpy(), outs[2].double().cpu().numpy()) <= 1e-6
