@@ -237,9 +237,10 @@ int64_t ddvr_adjoint_workspace_bytes(const ddvr_volume* vol, const ddvr_tf* tf,
  *   - with the camera or stepsize target: per-CTA partials, reduced in a fixed order
  *     (d_camera and d_dt bitwise reproducible);
  *   - with the volume target and cell records: the cell-gradient moments as int64
- *     fixed point (round(moment * scale), scale = 2^50 / a bound of any one flush
+ *     fixed point (round(fp32 moment * scale), scale = 2^50 / a bound of any one flush
  *     derived from the TF table and max|seed|): integer adds commute, so d_volume is
- *     bitwise reproducible for any order of the atomics.  Texel TFs only; for
+ *     bitwise reproducible for any order of the atomics.  Texel TFs and the volume
+ *     target alone (mask DDVR_TARGET_VOLUME; other masks are UNSUPPORTED); for
  *     ddvr_adjoint one call per step (no WS_CONTINUE / WS_DEFER: the scale comes
  *     from that call's seed); the fused step's seed is +-1/count in every call.
  * (The in-CTA TF sums stay fp32 atomics: d_tf is reproducible to rounding.) */

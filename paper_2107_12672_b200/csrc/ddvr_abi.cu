@@ -904,6 +904,9 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   const int64_t det_off = (ws_need + 255) & ~(int64_t)255;
   if (ws_dvol > 0 && T.kind != DDVR_TF_TEXTURE)
     return set_error(DDVR_UNSUPPORTED, "the deterministic density gradient needs a texel TF");
+  if (ws_dvol > 0 && mask != DDVR_TARGET_VOLUME)
+    return set_error(DDVR_UNSUPPORTED, "the deterministic density gradient is computed for the "
+                     "volume target alone (mask %u)", mask);
   if (ws_dvol > 0 && !fu && (flags & (DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER)))
     return set_error(DDVR_UNSUPPORTED, "the deterministic density gradient of ddvr_adjoint "
                      "takes its fixed-point scale from the call's seed: one call per step");

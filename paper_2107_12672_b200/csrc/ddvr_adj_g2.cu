@@ -3,24 +3,31 @@
 
 namespace ddvr_impl {
 
-template <unsigned M, bool CELLS, bool FUSED>
+template <unsigned M, bool CELLS, bool FUSED, bool DET = false>
 static int adj2(dim3 grid, size_t smem, cudaStream_t st, const VolArgs& V, const TfArgs& T,
                 const Geometry& G, const float* image, const float* depth, const float* seed,
                 float* dv, float* dcells, double* dcam, double* ddt,
                 const FusedArgs& fu) {
-  auto k = dvr_adjoint_kernel<M, CELLS, 0, FUSED>;
+  // the deterministic density gradient (int64 cell moments) has its own instantiations
+  // for the volume target alone (the flush's conversions would cost registers elsewhere)
+  if constexpr (M == DDVR_TARGET_VOLUME && CELLS && !DET) {
+    if (V.cells64)
+      return adj2<M, CELLS, FUSED, true>(grid, smem, st, V, T, G, image, depth, seed, dv,
+                                         dcells, dcam, ddt, fu);
+  }
+  auto k = dvr_adjoint_kernel<M, CELLS, 0, FUSED, DET>;
   set_smem(k, smem);
   k<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dcam, ddt, fu);
   if constexpr (CELLS && !(M & DDVR_TARGET_TF)) {   // the absorption-only walk
-    auto k1 = dvr_adjoint_kernel<M, CELLS, 1, FUSED>;
+    auto k1 = dvr_adjoint_kernel<M, CELLS, 1, FUSED, DET>;
     set_smem(k1, smem);
     k1<<<grid, kThreads, smem, st>>>(V, T, G, image, depth, seed, dv, dcells, dcam, ddt, fu);
     if constexpr (M == DDVR_TARGET_VOLUME && FUSED) {
       if (G.ray_k) {   // the band-tape step as march + walk kernels (ROLE 1 returns for it)
         set_smem(dvr_band_march_kernel<0>, smem);
         dvr_band_march_kernel<0><<<grid, kThreads, smem, st>>>(V, T, G, fu);
-        set_smem(dvr_band_walk_kernel<0>, smem);
-        dvr_band_walk_kernel<0><<<grid, kThreads, smem, st>>>(V, T, G, dcells);
+        set_smem(dvr_band_walk_kernel<DET>, smem);
+        dvr_band_walk_kernel<DET><<<grid, kThreads, smem, st>>>(V, T, G, dcells);
         return 4;
       }
     }

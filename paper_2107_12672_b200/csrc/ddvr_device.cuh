@@ -544,14 +544,15 @@ __device__ __forceinline__ void gather(const VolArgs& V, int cell, float v[8]) {
 
 // One cell run's 8 moments into the cell-gradient workspace: two 128-bit vector reds
 // (fp32), or in the deterministic mode eight int64 fixed-point adds.
+template <bool DET>
 __device__ __forceinline__ void flush_record(const VolArgs& V, float* __restrict__ d_cells,
                                              int cell, const float a[8]) {
-  if (V.cells64) {
-    const double sc = __ldg(V.det_scale);
+  if (DET) {   // (fp32 product: each contribution keeps fp32's relative precision)
+    const float sc = (float)__ldg(V.det_scale);
     unsigned long long* q = V.cells64 + 8 * (long long)cell;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      atomicAdd(q + k, (unsigned long long)__double2ll_rn((double)a[k] * sc));
+      atomicAdd(q + k, (unsigned long long)__float2ll_rn(a[k] * sc));
   } else {
     float* q = d_cells + 8 * (long long)cell;
     red128(q, a[0], a[1], a[2], a[3]);
@@ -1301,7 +1302,7 @@ struct AdjState {
 
 // The backward walk of one ray (renderer.py:547-626).
 template <unsigned MASK, bool CELLS, int SEG, bool INSIDE, bool EMIT, int KIND, bool TAPE,
-          bool AFF = false>
+          bool AFF = false, bool DET = false>
 __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                             const Ray& r, double S, float4 sd,
                                             const float* __restrict__ tape, float* tf_slot,
@@ -1504,7 +1505,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
 #ifdef DDVR_WALK_NORED   // measurement variant: the reds replaced by a register sink
         if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
 #else
-        if (flush) flush_record(V, d_cells, st.run_cell, st.acc8);
+        if (flush) flush_record<DET>(V, d_cells, st.run_cell, st.acc8);
 #endif
         const float keep = fresh ? 0.f : 1.f;
         st.acc8[0] = fmaf(st.acc8[0], keep, dh);
@@ -1565,7 +1566,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
 // re-gathered record -- so the walk needs no record gathers at all: positions,
 // cell fractions, the cell-run moments and their flushes only.  Same moments,
 // same runs, same flush order as the gathering walk.
-template <bool INSIDE>
+template <bool INSIDE, bool DET = false>
 __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, float abs_k,
                                               const unsigned* __restrict__ bits,
                                               unsigned bits_off, float* __restrict__ d_cells,
@@ -1604,7 +1605,7 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
       if (flush) st.tfp0 += st.acc8[0] + st.acc8[3] + st.acc8[7];
 #else
       DDVR_REQUIRE(!flush || cell_ok(V, st.run_cell));
-      if (flush) flush_record(V, d_cells, st.run_cell, st.acc8);
+      if (flush) flush_record<DET>(V, d_cells, st.run_cell, st.acc8);
 #endif
       const float keep = fresh ? 0.f : 1.f;
       st.acc8[0] = fmaf(st.acc8[0], keep, dh);
@@ -1637,6 +1638,7 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
 // moments and one flush -- instead of per-sample positions, cell tests and moment
 // updates.  The samples and runs are those of abs_bits_walk (same cells, same
 // gradient up to fp32 rounding); all-zero remainders of tape words are skipped.
+template <bool DET = false>
 __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, float abs_k,
                                               const unsigned* __restrict__ bits,
                                               unsigned bits_off, float* __restrict__ d_cells,
@@ -1727,7 +1729,7 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
     if (a[0] == 12345.f) d_cells[0] = a[7] + (float)cell;
 #else
     DDVR_REQUIRE(cell_ok(V, cell));
-    flush_record(V, d_cells, cell, a);
+    flush_record<DET>(V, d_cells, cell, a);
 #endif
   }
 }
@@ -1750,7 +1752,7 @@ __device__ __forceinline__ bool band_class(const TfArgs& TFA, const Geometry& G,
 // belongs to the other role -- no host synchronisation.
 // FUSED: the forward march and the L1 seed run in the same thread first
 // (FusedArgs); image / depth / seed are then unused.
-template <unsigned MASK, bool CELLS, int ROLE, bool FUSED>
+template <unsigned MASK, bool CELLS, int ROLE, bool FUSED, bool DET = false>
 __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
     const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
@@ -1859,18 +1861,18 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   st.s1x = st.s1y = st.s1z = st.s2x = st.s2y = st.s2z = st.dt_bl = st.dt_pos = 0.0;
 
 #define DDVR_WALK(SEG, INS, EM)                                                          \
-  adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture, false>(V, TFA, G.dt32, r, S, sd, tape, \
-                                                            tf_slot, d_volume, d_cells, st)
+  adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture, false, false, DET>(                   \
+      V, TFA, G.dt32, r, S, sd, tape, tf_slot, d_volume, d_cells, st)
 #define DDVR_WALK_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_WALK(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_WALK(kSegP7, INS, EM); \
   else DDVR_WALK(kSegGen, INS, EM);
   // stored mode (tape) and the analytic TFs take the general variant
 #define DDVR_WALK_GEN(KIND, TP)                                                           \
-  adjoint_ray<MASK, CELLS, kSegGen, false, true, KIND, TP>(V, TFA, G.dt32, r, S, sd, tape, \
-                                                           tf_slot, d_volume, d_cells, st)
+  adjoint_ray<MASK, CELLS, kSegGen, false, true, KIND, TP, false, DET>(                    \
+      V, TFA, G.dt32, r, S, sd, tape, tf_slot, d_volume, d_cells, st)
 #define DDVR_WALK_AFF(SEG, INS)                                                            \
-  adjoint_ray<MASK, CELLS, SEG, INS, false, kTfTexture, false, true>(                       \
+  adjoint_ray<MASK, CELLS, SEG, INS, false, kTfTexture, false, true, DET>(                  \
       V, TFA, G.dt32, r, S, sd, tape, tf_slot, d_volume, d_cells, st,                       \
       __uint_as_float(s_info[3]), __uint_as_float(s_info[4]))
 #define DDVR_WALK_SEG_AFF(INS)                  \
@@ -1878,9 +1880,11 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   else DDVR_WALK_AFF(kSegP7, INS);
   if (kBitsKernel && bits) {
     const float abs_k = sd.w * (float)exp(-S) * G.dt32 * TFA.fR * __uint_as_float(s_info[4]);
-    if (warp_inside && DDVR_RUN_WALK) abs_runs_walk(V, r, abs_k, bits, bits_off, d_cells, &walk_skip);
-    else if (warp_inside) abs_bits_walk<true>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
-    else abs_bits_walk<false>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
+    if (warp_inside && DDVR_RUN_WALK)
+      abs_runs_walk<DET>(V, r, abs_k, bits, bits_off, d_cells, &walk_skip);
+    else if (warp_inside)
+      abs_bits_walk<true, DET>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
+    else abs_bits_walk<false, DET>(V, r, abs_k, bits, bits_off, d_cells, st, &walk_skip);
   } else if (ROLE == 1 && aff_walk) {
     if (warp_inside) { DDVR_WALK_SEG_AFF(true) } else { DDVR_WALK_SEG_AFF(false) }
   } else if (ROLE == 1) {
@@ -1920,7 +1924,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   // ---- flush per-ray accumulators ----
   DDVR_REQUIRE(!(kVol && CELLS && st.run_cell != kNoRun) || cell_ok(V, st.run_cell));
   if (kVol && CELLS && st.run_cell != kNoRun)
-    flush_record(V, d_cells, st.run_cell, st.acc8);
+    flush_record<DET>(V, d_cells, st.run_cell, st.acc8);
   else if (kVol && st.run_cell != kNoRun)
     flush_cell<CELLS>(d_volume, d_cells, st.run_cell, st.run_base, st.run_ox, st.run_oy,
                       st.run_oz, st.acc8);
@@ -2085,7 +2089,7 @@ __global__ void __launch_bounds__(kThreads, DDVR_BAND_MARCH_MINB)
 }
 
 // the affine absorption walk from the band tape (abs_bits_walk) + the cell-run flushes
-template <int kUnused = 0>
+template <bool DET = false>
 __global__ void __launch_bounds__(kThreads, DDVR_BAND_WALK_MINB)
     dvr_band_walk_kernel(VolArgs V, TfArgs TFA, Geometry G, float* __restrict__ d_cells) {
   __shared__ Frame F;
@@ -2101,12 +2105,13 @@ __global__ void __launch_bounds__(kThreads, DDVR_BAND_WALK_MINB)
   if (b.valid) {
     const float abs_k = G.ray_k[b.pix];
     if (b.warp_inside && DDVR_RUN_WALK)
-      abs_runs_walk(V, b.r, abs_k, G.bits, b.bits_off, d_cells, &walk_skip);
+      abs_runs_walk<DET>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, &walk_skip);
     else if (b.warp_inside)
-      abs_bits_walk<true>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
-    else abs_bits_walk<false>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
+      abs_bits_walk<true, DET>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
+    else abs_bits_walk<false, DET>(V, b.r, abs_k, G.bits, b.bits_off, d_cells, st, &walk_skip);
     DDVR_REQUIRE(st.run_cell == kNoRun || cell_ok(V, st.run_cell));
-    if (st.run_cell != kNoRun && st.acc8[0] != 0.f) flush_record(V, d_cells, st.run_cell, st.acc8);
+    if (st.run_cell != kNoRun && st.acc8[0] != 0.f)
+      flush_record<DET>(V, d_cells, st.run_cell, st.acc8);
 #ifdef DDVR_WALK_NORED
     if (st.tfp0 == 12345.f) G.ray_k[b.pix] = st.tfp0;
 #endif
