@@ -4,6 +4,7 @@
     python tools/ncu_summary.py rep --samples N --kernel dvr_adjoint \
         --json-out profiles/ncu_r02.json --key C4/fused_tape [--file profiles/x.txt]
 
+The report may also be the raw page saved as CSV (`ncu -i rep --page raw --csv > x.csv`).
 --samples: samples processed by each dvr_* launch in the report, to print
 per-sample instruction and wavefront counts.  --json-out/--key: merge the
 numbers of the first launch whose name contains --kernel into the JSON file
@@ -50,8 +51,12 @@ def main():
     ap.add_argument("--file", default="", help="the summary file this entry is cited from")
     ap.add_argument("--state", default="bench.py fixed dense state (iteration 1)")
     args = ap.parse_args()
-    out = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"],
-                         capture_output=True, text=True, check=True).stdout
+    if args.report.endswith(".csv"):   # a saved `ncu -i rep --page raw --csv` page
+        with open(args.report) as f:
+            out = f.read()
+    else:
+        out = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(out.splitlines()))
     head, units = rows[0], rows[1]
     for r in rows[2:]:
