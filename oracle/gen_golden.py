@@ -19,6 +19,8 @@ Cases (reference call sites in brackets):
 * counts     exact per-config sample totals (renderer.py:209-214)
 * C4_step_*, C5_step_*  the fused tomography step at config scale (row bands of a
              few views): reference images, band images, L1 loss, density gradient
+* C1_step_*, C2_step_*  the fused TF-target steps (C1 full view, C2 bands): loss, d_tf
+             (and C1's d_volume)
 """
 
 from __future__ import annotations
@@ -238,6 +240,62 @@ def step_cases():
                  est_probe=est.reshape(-1)[:: max(1, est.size // 4096)].copy(),
                  volume_idx=nz.astype(np.int32), volume_val=grad[nz].astype(np.float32))
             print(f"  {name} {kind}: {time.time() - t0:.1f}s, loss {loss:.6g}")
+
+
+# the fused TF-target steps (C1: volume + tf, full view; C2: tf, row bands of two views)
+TF_STEP_BANDS = {"C1": ((0,), (0, 128)), "C2": ((0, 5), (120, 136))}
+
+
+def tf_step_cases():
+    """The fused step of the TF-target configs as the bench runs it (ShardedStep:
+    forward -> l1_loss -> render_adjoint per view, tasks.py:258-270 / 397-432) at the
+    configs' full sizes, computed by the reference: references rendered from the truth,
+    the dense estimate 0.85 truth + 0.1 U(0,1) (its own default_rng(77) stream, C1 then
+    C2), the L1 loss over the bands and the gradients of the config's targets."""
+    rng = np.random.default_rng(77)
+    for name, (views, (r0, r1)) in TF_STEP_BANDS.items():
+        t0 = time.time()
+        c = CONFIGS[name]
+        truth = c.volume().astype(np.float64)
+        est = f32(0.85 * truth + 0.1 * rng.uniform(size=truth.shape))
+        tex = f32(c.texels())
+        T = vd.TransferFunction(tex)
+        poses = c.view_poses()
+        cams = [vd.SphericalCamera(*poses[k], c.radius, fov_y_deg=c.fov, width=c.image,
+                                   height=c.image) for k in views]
+        count = 4 * c.image * (r1 - r0) * len(views)
+        refs, imgs, loss = [], [], 0.0
+        grads = {t: None for t in c.targets}
+        for cam in cams:
+            u, v = vr._tile_pixels(cam, r0, r1)
+            scene = ("density", vd.DensityVolume(truth), T)
+            o, w, slab = vr._ray_setup(scene, cam, u, v)
+            n = vr._step_counts(slab[0], slab[1], c.dt, slab[4])
+            ref, _ = vr._march_fused(scene, o, w, c.dt, slab, n)
+            scene = ("density", vd.DensityVolume(est), T)
+            o, w, slab = vr._ray_setup(scene, cam, u, v)
+            band, _ = vr._march_fused(scene, o, w, c.dt, slab, n)
+            loss += float(np.abs(band - ref).sum()) / count
+            seed = np.sign(band - ref) / count
+            for t in c.targets:
+                gs = vr._adjoint_tile(scene, cam, vd.RenderConfig(dt=c.dt, target=t), seed,
+                                      (r0, r1), final_rgba=band)
+                g = np.asarray(grads_of(gs, t), np.float64)
+                grads[t] = g if grads[t] is None else grads[t] + g
+            refs.append(ref)
+            imgs.append(band.reshape(r1 - r0, c.image, 4))
+        out = dict(views=np.array(views), rows=np.array([r0, r1]), texels=tex.astype(np.float32),
+                   dt=np.float64(c.dt), count=np.float64(count),
+                   refs=np.stack(refs).reshape(len(views), r1 - r0, c.image, 4).astype(np.float32),
+                   image=np.stack(imgs), loss=np.float64(loss),
+                   est_probe=est.reshape(-1)[:: max(1, est.size // 4096)].copy(),
+                   d_tf=grads["tf"])
+        if "volume" in grads:
+            nz = np.flatnonzero(grads["volume"])
+            out["volume_idx"] = nz.astype(np.int32)
+            out["volume_val"] = grads["volume"].reshape(-1)[nz].astype(np.float32)
+        save(f"{name}_step_dense", **out)
+        print(f"  {name}: {time.time() - t0:.1f}s, loss {loss:.6g}")
 
 
 def count_cases():
@@ -493,3 +551,5 @@ if __name__ == "__main__":
         count_cases()
     if "step" in which:
         step_cases()
+    if "tfstep" in which:
+        tf_step_cases()

@@ -103,6 +103,31 @@ def main():
         note(key, "step/d_volume", rel_l2(f.d_volume.double().cpu().numpy(), want))
         report["cases"][key]["band_rows"] = [r0, r1]
         report["cases"][key]["views"] = [int(k) for k in g["views"]]
+    for case in ("C1_step_dense", "C2_step_dense"):   # the fused TF-target steps
+        g = golden(case)
+        name = case.split("_")[0]
+        c = CONFIGS[name]
+        est = torch.from_numpy(step_estimate(name, "dense").astype(np.float32)).to(dev)
+        poses = c.view_poses()
+        ll = torch.tensor([poses[int(k)] for k in g["views"]], dtype=torch.float64, device=dev)
+        r0, r1 = (int(r) for r in g["rows"])
+        step = ShardedStep(est, torch.from_numpy(g["texels"]).to(dev), ll,
+                           torch.from_numpy(g["refs"]).to(dev).contiguous(), float(g["dt"]),
+                           R.Rig(c.image, c.image, rows=(r0, r1)), targets=tuple(c.targets),
+                           total_elements=float(g["count"]), radius=c.radius, fov_y_deg=c.fov,
+                           keep_images=True)
+        f = step.run()
+        key = f"{case}/targets={'+'.join(c.targets)}"
+        note(key, "step/image", rel_l2(step.img.double().cpu().numpy(), g["image"]))
+        note(key, "step/loss", abs(float(f.loss) - float(g["loss"])) / float(g["loss"]))
+        note(key, "step/d_tf", rel_l2(f.d_tf.double().cpu().numpy().reshape(-1),
+                                      g["d_tf"].reshape(-1)))
+        if "volume" in c.targets:
+            want = np.zeros(est.numel())
+            want[g["volume_idx"]] = g["volume_val"]
+            note(key, "step/d_volume", rel_l2(f.d_volume.double().cpu().numpy(), want))
+        report["cases"][key]["band_rows"] = [r0, r1]
+        report["cases"][key]["views"] = [int(k) for k in g["views"]]
     report["worst"] = worst
     print(json.dumps(report, indent=1, sort_keys=True))
 

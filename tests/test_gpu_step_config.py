@@ -12,7 +12,11 @@ the band tape and the empty-space skips on and off:
 * ``sparse`` (C4): the truth's support only, exact zeros outside the sphere, so the
   march's empty-brick skip and the walk's zero-word skip run over real empty space.
 
-Bars: image rel-L2 <= 1e-5, loss <= 1e-5 relative, d_volume rel-L2 <= 1e-4.
+tests/golden/{C1,C2}_step_dense.npz (gen_golden.py tf_step_cases) hold the fused
+TF-target steps the same way: C1 (64^3, one full 128^2 view, volume + TF targets) and
+C2 (128^3, 16 rows of two 256^2 views, TF target), with d_tf in fp64.
+
+Bars: image rel-L2 <= 1e-5, loss <= 1e-5 relative, d_volume and d_tf rel-L2 <= 1e-4.
 """
 
 from __future__ import annotations
@@ -34,10 +38,12 @@ def _f32(a):
 
 def step_estimate(name: str, kind: str) -> np.ndarray:
     """The estimate of a step fixture: the generator and seed of gen_golden.step_cases
-    (one default_rng(99) stream drawn for C4 then C5)."""
+    (one default_rng(99) stream drawn for C4 then C5; tf_step_cases: default_rng(77),
+    C1 then C2)."""
     from paper_2107_12672_b200.scenes import CONFIGS
-    rng = np.random.default_rng(99)
-    for nm in ("C4", "C5"):
+    order = ("C1", "C2") if name in ("C1", "C2") else ("C4", "C5")
+    rng = np.random.default_rng(77 if name in ("C1", "C2") else 99)
+    for nm in order:
         truth = CONFIGS[nm].volume().astype(np.float64)
         u = rng.uniform(size=truth.shape)
         if nm == name:
@@ -47,7 +53,8 @@ def step_estimate(name: str, kind: str) -> np.ndarray:
     raise KeyError(name)
 
 
-@pytest.mark.parametrize("case", ["C4_step_dense", "C4_step_sparse"])
+@pytest.mark.parametrize("case", ["C4_step_dense", "C4_step_sparse", "C1_step_dense",
+                                  "C2_step_dense"])
 def test_step_estimates_are_reproduced(case):
     """(CPU) the tests rebuild exactly the estimate the fixture was computed from."""
     g = golden(case)
@@ -105,3 +112,54 @@ def test_fused_step_matches_reference_at_config_scale(cuda, case, tape, skip, sp
     if kind == "sparse" and step.band_tape:
         assert s[2] > 0                        # the walk skipped empty tape words
         assert (s[1] > 0) == skip              # the march skipped empty bricks
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["C1_step_dense", "C2_step_dense"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_tf_step_matches_reference_at_config_scale(cuda, case, graph):
+    """The fused TF-target step (C1: volume + TF, C2: TF) the bench times, eagerly and
+    replayed from a CUDA graph (bench.py's default for C1)."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    from paper_2107_12672_b200.scenes import CONFIGS
+    g = golden(case)
+    name = case.split("_")[0]
+    c = CONFIGS[name]
+    est_np = step_estimate(name, "dense")
+    np.testing.assert_array_equal(est_np.reshape(-1)[:: max(1, est_np.size // 4096)],
+                                  g["est_probe"])
+    est = torch.from_numpy(est_np.astype(np.float32)).to(cuda)
+    tex = torch.from_numpy(g["texels"]).to(cuda)
+    poses = c.view_poses()
+    ll = torch.tensor([poses[int(k)] for k in g["views"]], dtype=torch.float64, device=cuda)
+    r0, r1 = (int(r) for r in g["rows"])
+    rig = R.Rig(c.image, c.image, rows=(r0, r1))
+    refs = torch.from_numpy(g["refs"]).to(cuda).contiguous()
+    targets = tuple(c.targets)
+    step = ShardedStep(est, tex, ll, refs, float(g["dt"]), rig, targets=targets,
+                       total_elements=float(g["count"]), radius=c.radius, fov_y_deg=c.fov,
+                       keep_images=True)
+    assert step.fused
+    if graph:
+        step.run()                              # warm up outside the capture
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            f = step.run()
+        for _ in range(2):                      # every replay zeroes and refills the grads
+            gr.replay()
+        torch.cuda.synchronize()
+    else:
+        f = step.run()
+    img = step.img.double().cpu().numpy()
+    assert rel_l2(img, g["image"]) <= IMG_TOL
+    assert abs(float(f.loss) - float(g["loss"])) <= IMG_TOL * float(g["loss"])
+    err = rel_l2(f.d_tf.double().cpu().numpy().reshape(-1), g["d_tf"].reshape(-1))
+    assert err <= GRAD_TOL, err
+    if "volume" in targets:
+        want = np.zeros(est_np.size)
+        want[g["volume_idx"]] = g["volume_val"]
+        err = rel_l2(f.d_volume.double().cpu().numpy().reshape(-1), want)
+        assert err <= GRAD_TOL, err
