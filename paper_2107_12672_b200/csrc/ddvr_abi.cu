@@ -59,11 +59,12 @@ __global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __res
 // (d rho / d v_b = sum_k L[k][b] phi_k, so g_b = sum_k L[k][b] m_k)
 __device__ __forceinline__ float corner_from_moments(const float4& a, const float4& h, int b) {
   const float sx = (b & 1) ? 1.f : -1.f, sy = (b & 2) ? 1.f : -1.f, sz = (b & 4) ? 1.f : -1.f;
+  // (moment order {1, ux, uy, ux uy, uz, ux uz, uy uz, ux uy uz}, corners_to_poly)
   float g = a.x * 0.125f;
   g = fmaf(0.25f * sx, a.y, g);
   g = fmaf(0.25f * sy, a.z, g);
-  g = fmaf(0.25f * sz, a.w, g);
-  g = fmaf(0.5f * sx * sy, h.x, g);
+  g = fmaf(0.5f * sx * sy, a.w, g);
+  g = fmaf(0.25f * sz, h.x, g);
   g = fmaf(0.5f * sx * sz, h.y, g);
   g = fmaf(0.5f * sy * sz, h.z, g);
   return fmaf(sx * sy * sz, h.w, g);

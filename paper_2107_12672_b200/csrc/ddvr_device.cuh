@@ -374,6 +374,27 @@ __device__ void setup_ray(const Frame& F, const VolArgs& V, double dt, int W, in
 // trilinear density (field.py:279-349, 379-500) in grid coordinates, fp32
 // ---------------------------------------------------------------------------
 
+// packed fp32 pair arithmetic (FFMA2 / FMUL2 on sm_100a; DDVR_F32X2=0 gives the
+// same per-lane IEEE operations as scalar instructions, for A/B measurements)
+#ifndef DDVR_F32X2
+#define DDVR_F32X2 1
+#endif
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+#if DDVR_F32X2
+  return __ffma2_rn(a, b, c);
+#else
+  return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
+#endif
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+#if DDVR_F32X2
+  return __fmul2_rn(a, b);
+#else
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+#endif
+}
+__device__ __forceinline__ float2 bcast(float a) { return make_float2(a, a); }
+
 struct Cell {
   int cell;            // padded cell-record index relative to cell0 (may be negative)
   int base;            // flat voxel index of corner (ix, iy, iz)
@@ -430,8 +451,10 @@ __device__ __forceinline__ void locate_cells(const VolArgs& V, long long gx, lon
     hz = min(max(hz, -1), V.Z1);
   }
   // u = lo * 2^-32 - 1/2 in one FFMA (the fraction itself is not needed)
-  c.ux = __fmaf_rn(__uint2float_rn((unsigned)gx), kInvFix, -0.5f);
-  c.uy = __fmaf_rn(__uint2float_rn((unsigned)gy), kInvFix, -0.5f);
+  const float2 uxy = fma2(make_float2(__uint2float_rn((unsigned)gx), __uint2float_rn((unsigned)gy)),
+                          bcast(kInvFix), bcast(-0.5f));
+  c.ux = uxy.x;
+  c.uy = uxy.y;
   c.uz = __fmaf_rn(__uint2float_rn((unsigned)gz), kInvFix, -0.5f);
   c.fx = c.ux + 0.5f; c.fy = c.uy + 0.5f; c.fz = c.uz + 0.5f;   // unused on this path
   c.cell = (hx * V.CY + hy) * V.CZ + hz;
@@ -562,19 +585,19 @@ __device__ __forceinline__ void flush_record(const VolArgs& V, float* __restrict
 
 // The trilinear interpolant of a cell (field.py:318-349) as a polynomial in
 // the centred fractions u = f - 1/2 in [-1/2, 1/2]:
-//   rho(u) = c0 + cx ux + cy uy + cz uz + cxy ux uy + cxz ux uz + cyz uy uz + cxyz ux uy uz
-// with c = L v for the 8 corner values v (bit 0 = +x, bit 1 = +y, bit 2 = +z,
-// the corner order of field.py:318-322):
-//   c0 = sum v / 8, cx = sum s_x v / 4, cxy = sum s_x s_y v / 2, cxyz = sum s_x s_y s_z v
-// (s = +1 on the + corner, -1 on the - corner).  Records store c in the order
-// {c0, cx, cy, cz, cxy, cxz, cyz, cxyz}: the interpolant is 7 FFMA instead of
-// 7 lerps (14 instructions), and its partial products are the spatial
-// derivative.  Built in fp64 (each coefficient rounded once) from pairwise
+//   rho(u) = sum_b c_b prod_{axes of b} u,   b = bx | by << 1 | bz << 2
+// i.e. c = {c0, cx, cy, cxy, cz, cxz, cyz, cxyz} -- the corner-bit order of
+// field.py:318-322 applied to the monomials -- with c = L v for the 8 corner
+// values v (s = +1 on the + corner, -1 on the - corner):
+//   c0 = sum v / 8, cx = sum s_x v / 4, cxy = sum s_x s_y v / 2, cxyz = sum s_x s_y s_z v.
+// In this order the x-free and x-carrying coefficients of each (y, z) monomial
+// sit in adjacent registers of the 256-bit gather, so the interpolant is two
+// packed FFMA2 (sm_100a: two fp32 FMAs per lane and instruction), an FMUL, two
+// FFMA and the FADD of c0 instead of 7 dependent FFMAs, and its partial products give the
+// spatial derivative.  Built in fp64 (each coefficient rounded once) from pairwise
 // x-sums / x-differences, so a replicated (edge-clamped) axis gives exactly
 // zero coefficients: the clamp-to-edge semantics of the corner form are kept
-// exactly.  With c0 added last (interp) the fp32 interpolant is as accurate
-// as the lerp form (measured rms 2.1e-8 vs 2.1e-8, max 9.5e-8 vs 1.6e-7 on
-// uniform [0,1) corners against fp64).
+// exactly.
 __device__ __forceinline__ void corners_to_poly(const float w[8], float c[8]) {
   double v[8];
 #pragma unroll
@@ -584,13 +607,32 @@ __device__ __forceinline__ void corners_to_poly(const float w[8], float c[8]) {
   c[0] = (float)(((s00 + s10) + (s01 + s11)) * 0.125);
   c[1] = (float)(((d00 + d10) + (d01 + d11)) * 0.25);
   c[2] = (float)(((s10 - s00) + (s11 - s01)) * 0.25);
-  c[3] = (float)(((s01 - s00) + (s11 - s10)) * 0.25);
-  c[4] = (float)(((d10 - d00) + (d11 - d01)) * 0.5);
+  c[3] = (float)(((d10 - d00) + (d11 - d01)) * 0.5);
+  c[4] = (float)(((s01 - s00) + (s11 - s10)) * 0.25);
   c[5] = (float)(((d01 - d00) + (d11 - d10)) * 0.5);
   c[6] = (float)(((s11 - s01) - (s10 - s00)) * 0.5);
   c[7] = (float)((d11 - d01) - (d10 - d00));
 }
 
+// The 8 monomials of a sample, phi = {1, ux, uy, ux uy, uz, ux uz, uy uz, ux uy uz}
+// (the record order), scaled by w: the sample's contribution to a record's moment
+// gradient.  One FMUL and three FMUL2.
+__device__ __forceinline__ void monomials(float w, float ux, float uy, float uz, float2 m[4]) {
+  m[0] = make_float2(w, __fmul_rn(w, ux));
+  m[1] = mul2(bcast(uy), m[0]);
+  m[2] = mul2(bcast(uz), m[0]);
+  m[3] = mul2(bcast(uz), m[1]);
+}
+
+// acc = acc * keep + m over the 8 moments (four FFMA2)
+__device__ __forceinline__ void moments_fma(float acc[8], float keep, const float2 m[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 a = fma2(make_float2(acc[2 * j], acc[2 * j + 1]), bcast(keep), m[j]);
+    acc[2 * j] = a.x;
+    acc[2 * j + 1] = a.y;
+  }
+}
 // polynomial coefficients of the cell (one 256-bit record, or the 8 corner
 // voxels converted in registers for the plain voxel layout)
 template <bool CELLS>
@@ -616,27 +658,31 @@ __device__ __forceinline__ void fetch8(const VolArgs& V, const Cell& c, float v[
 struct Interp {
   float rho;   // unclamped density
   float gx;    // d rho / d ux
-  float t1, t3;
+  float2 q1;   // (cz + uy cyz, cxz + uy cxyz): d rho / d uz = q1.x + ux q1.y
 };
 
 __device__ __forceinline__ Interp interp(const Cell& c, const float k[8]) {
   Interp r;
-  r.t1 = __fmaf_rn(c.uy, k[7], k[5]);               // cxz + uy cxyz
-  const float t2 = __fmaf_rn(c.uy, k[4], k[1]);     // cx + uy cxy
-  r.gx = __fmaf_rn(c.uz, r.t1, t2);
-  r.t3 = __fmaf_rn(c.uy, k[6], k[3]);               // cz + uy cyz
-  // the variation first, the mean c0 last: one rounding at |rho|
-  const float dv = __fmaf_rn(c.ux, r.gx, __fmaf_rn(c.uz, r.t3, __fmul_rn(c.uy, k[2])));
-  r.rho = __fadd_rn(k[0], dv);
+  // lane pairs (x-free, x-carrying): q0 = (uy cy, cx + uy cxy) (the x-free lane
+  // adds uy cy to 0: k[0] = c0 is added last), q1 = (cz + uy cyz, cxz + uy cxyz),
+  // q = q0 + uz q1 = (rho - c0 at ux = 0, d rho / d ux)
+  const float2 q0 = make_float2(__fmul_rn(c.uy, k[2]), __fmaf_rn(c.uy, k[3], k[1]));
+  r.q1 = fma2(bcast(c.uy), make_float2(k[6], k[7]), make_float2(k[4], k[5]));
+  const float2 q = fma2(bcast(c.uz), r.q1, q0);
+  r.gx = q.y;
+  // the variation first, the mean c0 last: one rounding at |rho| (the fp32
+  // interpolant is then as accurate as the lerp form: rms 2.1e-8 against fp64
+  // on uniform [0,1) corners)
+  r.rho = __fadd_rn(k[0], __fmaf_rn(c.ux, q.y, q.x));
   return r;
 }
 
 // d rho / d uy and d rho / d uz (grid units)
 __device__ __forceinline__ float interp_gy(const Cell& c, const float k[8]) {
-  return __fmaf_rn(c.uz, __fmaf_rn(c.ux, k[7], k[6]), __fmaf_rn(c.ux, k[4], k[2]));
+  return __fmaf_rn(c.uz, __fmaf_rn(c.ux, k[7], k[6]), __fmaf_rn(c.ux, k[3], k[2]));
 }
 __device__ __forceinline__ float interp_gz(const Cell& c, const Interp& r) {
-  return __fmaf_rn(c.ux, r.t1, r.t3);
+  return __fmaf_rn(c.ux, r.q1.y, r.q1.x);
 }
 
 // density actually used by the march: 0 outside the box, clamped to [0,1]
@@ -689,6 +735,13 @@ __device__ __forceinline__ float tf_eval_tau(const TfArgs& T, float d, int& i0, 
   return __fmaf_rn(w, q.y, q.x);
 }
 
+// a + w dlt on the four channels (two FFMA2)
+__device__ __forceinline__ float4 lerp_texel(float w, const float4& a, const float4& dlt) {
+  const float2 xy = fma2(bcast(w), make_float2(dlt.x, dlt.y), make_float2(a.x, a.y));
+  const float2 zw = fma2(bcast(w), make_float2(dlt.z, dlt.w), make_float2(a.z, a.w));
+  return make_float4(xy.x, xy.y, zw.x, zw.y);
+}
+
 // texel table: R texels, centre of texel r at (r + 0.5)/R, clamp-to-edge
 // (field.py:540-549); fR, fR1, Rm2 are precomputed on the host (TfArgs)
 __device__ __forceinline__ float4 tf_eval(const TfArgs& T, float d, int& i0, float& w,
@@ -696,10 +749,12 @@ __device__ __forceinline__ float4 tf_eval(const TfArgs& T, float d, int& i0, flo
   i0 = texel_coord(T, d, w);
   const float4 a = g_smem[2 * i0 + 2];
   const float4 dlt = g_smem[2 * i0 + 3];
-  if (want_slope)   // guard entries have dlt = 0: the clamp bands' zero slope
-    slope = make_float4(dlt.x * T.fR, dlt.y * T.fR, dlt.z * T.fR, dlt.w * T.fR);
-  return make_float4(__fmaf_rn(w, dlt.x, a.x), __fmaf_rn(w, dlt.y, a.y),
-                     __fmaf_rn(w, dlt.z, a.z), __fmaf_rn(w, dlt.w, a.w));
+  if (want_slope) {   // guard entries have dlt = 0: the clamp bands' zero slope
+    const float2 sxy = mul2(make_float2(dlt.x, dlt.y), bcast(T.fR));
+    const float2 szw = mul2(make_float2(dlt.z, dlt.w), bcast(T.fR));
+    slope = make_float4(sxy.x, sxy.y, szw.x, szw.y);
+  }
+  return lerp_texel(w, a, dlt);
 }
 
 // Piecewise-linear TF on non-uniform knots, params (K,5) = [pos, r, g, b, tau].
@@ -1013,8 +1068,9 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     const Segment g = segment<SEG>(s.w, dt32);
     const float Ta = __fmul_rn(T, g.a);
     if (EMIT) {
-      c0 = __fmaf_rn(Ta, s.x, c0);
-      c1 = __fmaf_rn(Ta, s.y, c1);
+      const float2 c01 = fma2(bcast(Ta), make_float2(s.x, s.y), make_float2(c0, c1));
+      c0 = c01.x;
+      c1 = c01.y;
       c2 = __fmaf_rn(Ta, s.z, c2);
     }
     A = __fadd_rn(A, Ta);
@@ -1385,8 +1441,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       i0 = texel_coord(TF, d, w);
       const float4 a = g_smem[2 * i0 + 2];
       dl4 = g_smem[2 * i0 + 3];
-      s = make_float4(__fmaf_rn(w, dl4.x, a.x), __fmaf_rn(w, dl4.y, a.y),
-                      __fmaf_rn(w, dl4.z, a.z), __fmaf_rn(w, dl4.w, a.w));
+      s = lerp_texel(w, a, dl4);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (kAbs && AFF) {
       // non-negative affine tau column in a polynomial segment mode, no
@@ -1484,16 +1539,15 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
       const bool live = (kAbs && AFF) ? inside   // (the band test above covers [0,1])
                                       : inside && raw >= 0.f && raw <= 1.f;   // field.py:486-489
       if (kVol && CELLS) {   // renderer.py:607-608, accumulated per cell run
-        // The run accumulates the 8 moments sum dh * phi(u), phi = {1, ux, uy,
-        // uz, ux uy, ux uz, uy uz, ux uy uz}, of the polynomial record: the
-        // record's gradient is exactly these moments (rho is linear in the
-        // coefficients), and fold_cells_kernel maps them back to corner
-        // voxels through L^T.  7 FMUL + 8 FFMA per sample instead of the 8
+        // The run accumulates the 8 moments sum dh * phi(u) (monomials: the
+        // record order) of the polynomial record: the record's gradient is
+        // exactly these moments (rho is linear in the coefficients), and
+        // fold_cells_kernel maps them back to corner voxels through L^T.
+        // One FMUL, three FMUL2 and four FFMA2 per sample instead of the 8
         // corner weights (25 instructions).  Branch-free: the finished run is
         // flushed with predicated vector reds and the accumulators restart by
         // scaling them with 0.
         const float dh = live ? d_hat : 0.f;
-        const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
         const bool fresh = c.cell != st.run_cell;
         // (affine absorption walk: every d_hat of a ray is 0 or abs_k, so a run
         // whose weight sum acc8[0] is 0 has all moments 0 -- no red)
@@ -1507,15 +1561,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
 #else
         if (flush) flush_record<DET>(V, d_cells, st.run_cell, st.acc8);
 #endif
-        const float keep = fresh ? 0.f : 1.f;
-        st.acc8[0] = fmaf(st.acc8[0], keep, dh);
-        st.acc8[1] = fmaf(st.acc8[1], keep, px);
-        st.acc8[2] = fmaf(st.acc8[2], keep, py);
-        st.acc8[3] = fmaf(st.acc8[3], keep, dh * c.uz);
-        st.acc8[4] = fmaf(st.acc8[4], keep, pxy);
-        st.acc8[5] = fmaf(st.acc8[5], keep, px * c.uz);
-        st.acc8[6] = fmaf(st.acc8[6], keep, py * c.uz);
-        st.acc8[7] = fmaf(st.acc8[7], keep, pxy * c.uz);
+        float2 m[4];
+        monomials(dh, c.ux, c.uy, c.uz, m);
+        moments_fma(st.acc8, fresh ? 0.f : 1.f, m);
         st.run_cell = c.cell;
       } else if (kVol) {
         if (c.cell != st.run_cell) {
@@ -1597,7 +1645,6 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
       locate<true>(V, gx, gy, gz, INSIDE || r.all_inside, c);
       const float dh = (word & 1u) ? abs_k : 0.f;   // sample i's bit is the lowest left
       word >>= 1;
-      const float px = dh * c.ux, py = dh * c.uy, pxy = px * c.uy;
       const bool fresh = c.cell != st.run_cell;
       // all d_hat of the ray share abs_k's sign: a zero weight sum = an empty run
       const bool flush = fresh && st.run_cell != kNoRun && st.acc8[0] != 0.f;
@@ -1607,15 +1654,9 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
       DDVR_REQUIRE(!flush || cell_ok(V, st.run_cell));
       if (flush) flush_record<DET>(V, d_cells, st.run_cell, st.acc8);
 #endif
-      const float keep = fresh ? 0.f : 1.f;
-      st.acc8[0] = fmaf(st.acc8[0], keep, dh);
-      st.acc8[1] = fmaf(st.acc8[1], keep, px);
-      st.acc8[2] = fmaf(st.acc8[2], keep, py);
-      st.acc8[3] = fmaf(st.acc8[3], keep, dh * c.uz);
-      st.acc8[4] = fmaf(st.acc8[4], keep, pxy);
-      st.acc8[5] = fmaf(st.acc8[5], keep, px * c.uz);
-      st.acc8[6] = fmaf(st.acc8[6], keep, py * c.uz);
-      st.acc8[7] = fmaf(st.acc8[7], keep, pxy * c.uz);
+      float2 m[4];
+      monomials(dh, c.ux, c.uy, c.uz, m);
+      moments_fma(st.acc8, fresh ? 0.f : 1.f, m);
       st.run_cell = c.cell;
       gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
     }
@@ -1629,7 +1670,7 @@ __device__ __forceinline__ void abs_bits_walk(const VolArgs& V, const Ray& r, fl
 // The affine absorption walk by cell runs (rays inside the box).  Within one cell a
 // ray's centred fractions are affine in the sample index, u_k = u_0 + k d (d = the
 // grid step per sample), so the run's moments sum_k b_k dh phi(u_k) (phi = 1, ux, uy,
-// uz, ux uy, ux uz, uy uz, ux uy uz; b_k the band bits, dh = abs_k) follow in closed
+// ux uy, uz, ux uz, uy uz, ux uy uz; b_k the band bits, dh = abs_k) follow in closed
 // form from the power sums P_j = sum_k b_k k^j, j <= 3 -- for a run with every bit
 // set, P_j are those of 0 .. L-1.  Per run: its start position (fixed point, exact),
 // its length (samples until the first cell boundary on any axis: one fp32 quotient
@@ -1707,7 +1748,7 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
       }
     }
     // sum_k dh phi(u0 + k d) expanded in the power sums (dh = abs_k folded into q0 and
-    // the k* constants)
+    // the k* constants), in the record order {1, ux, uy, ux uy, uz, ux uz, uy uz, ux uy uz}
     const float q0 = abs_k * P0;
     const float ux = __fmaf_rn(__uint2float_rn(lx), kInvFix, -0.5f);
     const float uy = __fmaf_rn(__uint2float_rn(ly), kInvFix, -0.5f);
@@ -1717,8 +1758,8 @@ __device__ __forceinline__ void abs_runs_walk(const VolArgs& V, const Ray& r, fl
     a[0] = q0;
     a[1] = __fmaf_rn(ux, q0, kx * P1);
     a[2] = __fmaf_rn(uy, q0, ky * P1);
-    a[3] = __fmaf_rn(uz, q0, kz * P1);
-    a[4] = __fmaf_rn(uxy, q0, __fmaf_rn(__fmaf_rn(ux, ky, uy * kx), P1, kxy * P2));
+    a[4] = __fmaf_rn(uz, q0, kz * P1);
+    a[3] = __fmaf_rn(uxy, q0, __fmaf_rn(__fmaf_rn(ux, ky, uy * kx), P1, kxy * P2));
     a[5] = __fmaf_rn(uxz, q0, __fmaf_rn(__fmaf_rn(ux, kz, uz * kx), P1, kxz * P2));
     a[6] = __fmaf_rn(uyz, q0, __fmaf_rn(__fmaf_rn(uy, kz, uz * ky), P1, kyz * P2));
     const float t1 = __fmaf_rn(uxy, kz, __fmaf_rn(uxz, ky, uyz * kx));

@@ -282,8 +282,9 @@ def test_analytic_tf_modes_match_oracle(cuda, kind):
 
 def test_cell_records_are_the_trilinear_polynomial(cuda):
     """ddvr_pack_cells: padded, edge-clamped records of the polynomial
-    coefficients {c0, cx, cy, cz, cxy, cxz, cyz, cxyz} in u = f - 1/2; the
-    polynomial equals the reference's lerp form (field.py:318-349)."""
+    coefficients {c0, cx, cy, cxy, cz, cxz, cyz, cxyz} (the monomial of corner
+    bit b = bx | by << 1 | bz << 2 at index b) in u = f - 1/2; the polynomial
+    equals the reference's lerp form (field.py:318-349)."""
     torch = _t()
     from paper_2107_12672_b200 import raymarch as R
     rng = np.random.default_rng(5)
@@ -301,8 +302,8 @@ def test_cell_records_are_the_trilinear_polynomial(cuda):
                                        min(max(k + (b >> 2 & 1), 0), Z - 1)] for b in range(8)])
                 want = np.array([corner.sum() / 8,
                                  (s[:, 0] * corner).sum() / 4, (s[:, 1] * corner).sum() / 4,
-                                 (s[:, 2] * corner).sum() / 4,
                                  (s[:, 0] * s[:, 1] * corner).sum() / 2,
+                                 (s[:, 2] * corner).sum() / 4,
                                  (s[:, 0] * s[:, 2] * corner).sum() / 2,
                                  (s[:, 1] * s[:, 2] * corner).sum() / 2,
                                  (s[:, 0] * s[:, 1] * s[:, 2] * corner).sum()])
@@ -311,7 +312,7 @@ def test_cell_records_are_the_trilinear_polynomial(cuda):
                 for _ in range(3):   # polynomial == x-then-y-then-z lerps
                     f = rng.uniform(0, 1, 3)
                     ux, uy, uz = f - 0.5
-                    poly = (got[0] + got[1] * ux + got[2] * uy + got[3] * uz + got[4] * ux * uy
+                    poly = (got[0] + got[1] * ux + got[2] * uy + got[3] * ux * uy + got[4] * uz
                             + got[5] * ux * uz + got[6] * uy * uz + got[7] * ux * uy * uz)
                     a = [corner[b] + f[0] * (corner[b + 1] - corner[b]) for b in (0, 2, 4, 6)]
                     p0 = a[0] + f[1] * (a[1] - a[0])
@@ -319,7 +320,7 @@ def test_cell_records_are_the_trilinear_polynomial(cuda):
                     assert abs(poly - (p0 + f[2] * (p1 - p0))) < 1e-6
                 # a replicated (clamped) axis has exactly zero odd coefficients
                 if i in (-1, X - 1):
-                    assert got[1] == got[4] == got[5] == got[7] == 0.0
+                    assert got[1] == got[3] == got[5] == got[7] == 0.0
 
 
 @pytest.mark.parametrize("tau_scale,dt,shape", [(3.0, 0.02, "ramp"), (60.0, 0.02, "ramp"),

@@ -33,5 +33,5 @@ for i, (a, text) in enumerate(ins):
     for _, t in ins[j:i + 1]:
         op = re.sub(r"^@!?U?P\w+\s+", "", t).split()[0]
         ops[op.split(".")[0]] += 1
-    keys = ("LDL", "STL", "LDG", "LDS", "MUFU", "RED", "FFMA", "FMUL", "FADD", "IMAD", "IADD3", "I2F", "F2I", "FRND", "DADD", "F2F", "SHF", "LOP3", "ISETP", "FSETP", "SEL", "FSEL", "FMNMX", "BRA")
+    keys = ("LDL", "STL", "LDG", "LDS", "MUFU", "RED", "REDG", "FFMA", "FFMA2", "FMUL", "FMUL2", "FADD", "FADD2", "IMAD", "IADD3", "I2F", "F2I", "FRND", "DADD", "F2F", "SHF", "LOP3", "ISETP", "FSETP", "SEL", "FSEL", "FMNMX", "BRA")
     print(f"loop 0x{tgt:05x}-0x{a:05x}: {n:4d} instr  " + " ".join(f"{k}={ops[k]}" for k in keys if ops[k]))
