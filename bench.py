@@ -91,6 +91,9 @@ def parse(argv=None):
                         "fixed-point cell moments, fixed-order camera / stepsize sums)")
     p.add_argument("--split-walk", action="store_true",
                    help="band tape: march and walk as two kernels (DDVR_FLAG_SPLIT_WALK)")
+    p.add_argument("--ray-split", default="auto", choices=["auto", "1", "2", "4", "8"],
+                   help="fused TF-target steps: threads per ray (DDVR_FLAG_RAY_SPLIT_*; auto "
+                        "splits steps too small to fill the GPU, e.g. C1)")
     p.add_argument("--dry-run", action="store_true",
                    help="launcher / collective check without kernels (gloo on CPU if no GPU)")
     return p.parse_args(argv)
@@ -439,7 +442,9 @@ def run_own(args, cfg):
                            layout=args.layout,
                            fused=False if args.unfused else (True if args.fused else "auto"),
                            band_tape=band_tape, empty_skip=not args.no_empty_skip,
-                           split_walk=args.split_walk, deterministic=args.deterministic)
+                           split_walk=args.split_walk, deterministic=args.deterministic,
+                           ray_split=args.ray_split if args.ray_split == "auto"
+                           else int(args.ray_split))
 
     step = make_step(False if args.no_band_tape else "auto")
     small = cfg_samples(cfg) is not None and cfg_samples(cfg) < 10 ** 7

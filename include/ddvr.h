@@ -107,6 +107,13 @@ typedef struct {
 #define DDVR_FLAG_BAND_TAPE 8
 #define DDVR_FLAG_NO_EMPTY_SKIP 16
 #define DDVR_FLAG_SPLIT_WALK 32
+/* segment-split rays of a fused TF-target step (ddvr_forward_adjoint_l1, masks TF and
+   TF|VOLUME): by default chosen from the ray count (a step too small to fill the GPU
+   with one thread per ray gets 2, 4 or 8 threads per ray); these force it (at most one) */
+#define DDVR_FLAG_RAY_SPLIT_OFF 64
+#define DDVR_FLAG_RAY_SPLIT_2 128
+#define DDVR_FLAG_RAY_SPLIT_4 256
+#define DDVR_FLAG_RAY_SPLIT_8 512
 
 /* march parameters (RenderConfig, renderer.py:84-106) */
 typedef struct {
@@ -148,7 +155,13 @@ typedef struct {
                                                    hands each ray's walk weight to the
                                                    walk through the workspace,
                                                    ddvr_band_tape_bytes); by default
-                                                   one kernel runs both per ray */
+                                                   one kernel runs both per ray
+                            DDVR_FLAG_RAY_SPLIT_OFF / _2 / _4 / _8  (fused step, TF
+                                                   target without camera / stepsize)
+                                                   threads per ray: 1, 2, 4 or 8
+                                                   consecutive lanes march and walk
+                                                   one sample segment each (default:
+                                                   from the ray count) */
   float* tape;           /* (device, nullable) "stored" memory mode (renderer.py:507-513, 576-577):
                             forward writes the transmittance before every sample,
                             tape[ray * tape_stride + i]; the adjoint then reads it
@@ -258,6 +271,12 @@ int64_t ddvr_deterministic_bytes(const ddvr_volume* vol, int32_t n_views, const 
  * by the affine absorption walk (emission-free TF with a non-negative affine tau
  * column, volume target); other steps ignore it. */
 int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p);
+
+/* Threads per ray ddvr_forward_adjoint_l1 uses for this target mask, ray count
+ * (views x band rows x width) and params.flags (DDVR_FLAG_RAY_SPLIT_*): 1 (one thread
+ * per ray) unless the mask is TF or TF|VOLUME and the rays alone would not fill the
+ * GPU, then the smallest of 2, 4, 8 giving ~113 K threads.  Host-side, no GPU work. */
+int32_t ddvr_ray_split(uint32_t mask, int64_t rays, int32_t flags);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:
  * (X+1) * (Y+1) * (Z+1) records of 8 floats -- cells -1 .. dim-1 on every

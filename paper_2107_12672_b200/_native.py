@@ -34,12 +34,13 @@ FLAG_DETERMINISTIC = 4
 FLAG_BAND_TAPE = 8
 FLAG_NO_EMPTY_SKIP = 16
 FLAG_SPLIT_WALK = 32
+FLAG_RAY_SPLIT = {1: 64, 2: 128, 4: 256, 8: 512}   # DDVR_FLAG_RAY_SPLIT_OFF / _2 / _4 / _8
 TF_TEXTURE = 0
 TF_PIECEWISE = 1
 TF_GAUSSIAN = 2
 
 EXPORTED = ("ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
-            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes", "ddvr_band_tape_bytes", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
+            "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes", "ddvr_band_tape_bytes", "ddvr_ray_split", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad", "ddvr_forward_color",
             "ddvr_adjoint_color", "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
             "ddvr_ray_setup",
             "ddvr_prior_volume",
@@ -118,6 +119,8 @@ def _bind(lib):
     lib.ddvr_deterministic_bytes.restype = ctypes.c_int64
     lib.ddvr_band_tape_bytes.argtypes = [P(DdvrVolume), ctypes.c_int32, P(DdvrParams)]
     lib.ddvr_band_tape_bytes.restype = ctypes.c_int64
+    lib.ddvr_ray_split.argtypes = [ctypes.c_uint32, ctypes.c_int64, ctypes.c_int32]
+    lib.ddvr_ray_split.restype = ctypes.c_int32
     lib.ddvr_cells_bytes.argtypes = [P(ctypes.c_int32)]
     lib.ddvr_cells_bytes.restype = ctypes.c_int64
     lib.ddvr_pack_cells.argtypes = [P(DdvrVolume), vp, vp]

@@ -1,6 +1,7 @@
 // ddvr_abi.cu -- the C ABI of include/ddvr.h: validation, launches, small kernels.
 // (Device code: ddvr_device.cuh; kernel instantiations: ddvr_fwd.cu, ddvr_adj_g*.cu.)
 #include <algorithm>
+#include <cstdlib>
 
 #include "ddvr_device.cuh"
 
@@ -30,6 +31,23 @@ int check_launch(const char* what) {
 // cell-record layout: pack (volume -> cells) and fold (cell gradients -> voxels)
 // ---------------------------------------------------------------------------
 
+// (x, y, z) of flat voxel index id (z fastest) with 32-bit division below 2^31 voxels
+__device__ __forceinline__ void vox_coords(long long id, long long n, int Y, int Z, int& x, int& y,
+                                           int& z) {
+  if (n < (1ll << 31)) {
+    const unsigned u = (unsigned)id, yz = (unsigned)Y * (unsigned)Z;
+    x = (int)(u / yz);
+    const unsigned r = u - (unsigned)x * yz;
+    y = (int)(r / (unsigned)Z);
+    z = (int)(r - (unsigned)y * (unsigned)Z);
+  } else {
+    z = (int)(id % Z);
+    const long long xy = id / Z;
+    y = (int)(xy % Y);
+    x = (int)(xy / Y);
+  }
+}
+
 // Padded record of cell (i,j,k), i in [-1, X-1] (storage index i+1): the
 // polynomial coefficients (corners_to_poly) of its 8 edge-clamped corners
 //   v[b] = vol[clamp(i+bx, 0, X-1)][clamp(j+by, 0, Y-1)][clamp(k+bz, 0, Z-1)],
@@ -38,10 +56,9 @@ __global__ void __launch_bounds__(256) pack_cells_kernel(VolArgs V, float* __res
                                                        long long ncells) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= ncells) return;
-  const int k = (int)(id % V.CZ) - 1;
-  const long long ij = id / V.CZ;
-  const int j = (int)(ij % V.CY) - 1;
-  const int i = (int)(ij / V.CY) - 1;
+  int i, j, k;
+  vox_coords(id, ncells, V.CY, V.CZ, i, j, k);
+  --i; --j; --k;
   const int i0 = max(i, 0), j0 = max(j, 0), k0 = max(k, 0);
   const int i1 = min(i + 1, V.X - 1), j1 = min(j + 1, V.Y - 1), k1 = min(k + 1, V.Z - 1);
   const float* p = V.data;
@@ -70,24 +87,10 @@ __device__ __forceinline__ float corner_from_moments(const float4& a, const floa
   return fmaf(sx * sy * sz, h.w, g);
 }
 
-// d_volume[x,y,z] += the gradient of every record corner that pack_cells_kernel
-// filled from voxel (x,y,z) (its exact transpose, padding included); the
-// adjoint leaves each record's moment gradient, mapped back per corner here
-// (one 32-byte sector per contributing record, as the corner form read)
-__global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
-                                                       const float* __restrict__ d_cells,
-                                                       float* __restrict__ d_volume,
-                                                       long long nvox) {
-  // the deterministic mode's int64 fixed-point moments (V.cells64 relative to cell 0)
-  const unsigned long long* c64 =
-      V.cells64 ? V.cells64 - (V.cell0 - V.cells) : nullptr;
-  const double inv = c64 ? 1.0 / __ldg(V.det_scale) : 0.0;
-  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= nvox) return;
-  const int z = (int)(id % V.Z);
-  const long long xy = id / V.Z;
-  const int y = (int)(xy % V.Y);
-  const int x = (int)(xy / V.Y);
+// one voxel of the fold (any position, either moment format)
+__device__ void fold_voxel(const VolArgs& V, const unsigned long long* c64, double inv,
+                           const float* __restrict__ d_cells, float* __restrict__ d_volume,
+                           long long id, int x, int y, int z) {
   // per axis, the (storage cell index, corner bit) pairs whose clamped corner is this voxel
   int ci[3][4], cb[3][4], cn[3];
   const int dims[3] = {V.X, V.Y, V.Z};
@@ -125,6 +128,25 @@ __global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
         }
       }
   d_volume[id] += s;
+}
+
+// d_volume[x,y,z] += the gradient of every record corner that pack_cells_kernel
+// filled from voxel (x,y,z) (its exact transpose, padding included); the
+// adjoint leaves each record's moment gradient, mapped back per corner here
+// (one 32-byte sector per contributing record, as the corner form read)
+__global__ void __launch_bounds__(256) fold_cells_kernel(VolArgs V,
+                                                       const float* __restrict__ d_cells,
+                                                       float* __restrict__ d_volume,
+                                                       long long nvox) {
+  // the deterministic mode's int64 fixed-point moments (V.cells64 relative to cell 0)
+  const unsigned long long* c64 =
+      V.cells64 ? V.cells64 - (V.cell0 - V.cells) : nullptr;
+  const double inv = c64 ? 1.0 / __ldg(V.det_scale) : 0.0;
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nvox) return;
+  int x, y, z;
+  vox_coords(id, nvox, V.Y, V.Z, x, y, z);
+  fold_voxel(V, c64, inv, d_cells, d_volume, id, x, y, z);
 }
 
 // ---------------------------------------------------------------------------
@@ -382,9 +404,8 @@ __global__ void __launch_bounds__(256) prior_volume_kernel(const float* __restri
   double part = 0.0;
   const long long sx = (long long)Y * Z, sy = Z;
   for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += stride) {
-    const int z = (int)(id % Z);
-    const int y = (int)((id / Z) % Y);
-    const int x = (int)(id / sx);
+    int x, y, z;
+    vox_coords(id, n, Y, Z, x, y, z);
     const float c = v[id];
     float g = 0.f;
     if (x + 1 < X) { const float d = v[id + sx] - c; g -= 2.f * d; part += (double)d * d; }
@@ -830,6 +851,32 @@ static int64_t grid_ctas(int32_t n_views, const ddvr_params* p) {
   return (int64_t)((p->width + kTile - 1) / kTile) * ((rows + kTile - 1) / kTile) * n_views;
 }
 
+// Segment-split rays for a fused step with the TF target (masks 4 and 12: no camera /
+// stepsize) whose rays alone would not fill the GPU: the smallest SPLIT in {2, 4, 8} that
+// gives ~113 K threads (148 SMs x 3 CTAs x 256), else 1.  DDVR_SPLIT=1|2|4|8 in the
+// environment overrides it (A/B measurements; 16 only there).
+static int split_of(uint32_t mask, long long rays, int32_t flags) {
+  if (mask != DDVR_TARGET_TF && mask != (DDVR_TARGET_TF | DDVR_TARGET_VOLUME)) return 1;
+  if (flags & DDVR_FLAG_RAY_SPLIT_OFF) return 1;
+  if (flags & DDVR_FLAG_RAY_SPLIT_2) return 2;
+  if (flags & DDVR_FLAG_RAY_SPLIT_4) return 4;
+  if (flags & DDVR_FLAG_RAY_SPLIT_8) return 8;
+  static const int forced = [] {
+    const char* e = std::getenv("DDVR_SPLIT");
+    const int v = e ? std::atoi(e) : 0;
+    return v == 1 || v == 2 || v == 4 || v == 8 || v == 16 ? v : 0;
+  }();
+  if (forced) return forced;
+  constexpr long long kFill = 148ll * 3 * kThreads;
+  int k = 1;
+  while (k < 8 && rays * k < kFill) k *= 2;
+  return k;
+}
+
+int32_t ddvr_ray_split(uint32_t mask, int64_t rays, int32_t flags) {
+  return split_of(mask, rays, flags);
+}
+
 int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p) {
   if (!vol || !p || n_views < 0 || p->width < 1 || p->height < 1 || !(p->dt > 0.0)) return 0;
   if (vol->dims[0] < 1 || vol->dims[1] < 1 || vol->dims[2] < 1) return 0;
@@ -883,8 +930,16 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
                        int32_t flags) {
   int rc;
   if (flags & ~(DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER | DDVR_FLAG_DETERMINISTIC |
-                DDVR_FLAG_BAND_TAPE | DDVR_FLAG_NO_EMPTY_SKIP | DDVR_FLAG_SPLIT_WALK))
+                DDVR_FLAG_BAND_TAPE | DDVR_FLAG_NO_EMPTY_SKIP | DDVR_FLAG_SPLIT_WALK |
+                DDVR_FLAG_RAY_SPLIT_OFF | DDVR_FLAG_RAY_SPLIT_2 | DDVR_FLAG_RAY_SPLIT_4 |
+                DDVR_FLAG_RAY_SPLIT_8))
     return set_error(DDVR_INVALID_PARAMETER, "unknown params.flags bits 0x%x", flags);
+  {
+    const int32_t sf = flags & (DDVR_FLAG_RAY_SPLIT_OFF | DDVR_FLAG_RAY_SPLIT_2 |
+                                DDVR_FLAG_RAY_SPLIT_4 | DDVR_FLAG_RAY_SPLIT_8);
+    if (sf & (sf - 1))
+      return set_error(DDVR_INVALID_PARAMETER, "at most one DDVR_FLAG_RAY_SPLIT_* flag (0x%x)", sf);
+  }
   if (mask == 0 || (mask & ~15u))
     return set_error(DDVR_UNSUPPORTED, "adjoint requires a differentiation target (mask %u)", mask);
   if ((mask & DDVR_TARGET_VOLUME) && !d_volume)
@@ -1006,8 +1061,13 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   }
   auto launch = mask <= 3 ? launch_adjoint_g0 : mask <= 7 ? launch_adjoint_g1
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;
-  const int n_kernels = launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed,
-                               d_volume, d_cells, d_camera, d_dt, fu);
+  const int split = fu && cells ? split_of(mask, (long long)n_views * (G.row1 - G.row0) * G.W, flags)
+                                  : 1;
+  const int n_kernels =
+      split > 1 ? launch_adjoint_split(mask, split, n_views, smem, st, V, T, G, d_volume, d_cells,
+                                       *fu)
+                : launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed, d_volume,
+                         d_cells, d_camera, d_dt, fu);
   if ((rc = check_launch(fu ? "dvr_adjoint_kernel (fused)" : "dvr_adjoint_kernel"))) return rc;
   g_launches.fetch_add(n_kernels - 1, std::memory_order_relaxed);
   if (ws_part > 0) {

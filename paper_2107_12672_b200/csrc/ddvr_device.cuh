@@ -219,6 +219,11 @@ DDVR_ADJ_LAUNCHER(launch_adjoint_g0);   // masks 1-3   (camera / stepsize)
 DDVR_ADJ_LAUNCHER(launch_adjoint_g1);   // masks 4-7   (tf [+ camera / stepsize])
 DDVR_ADJ_LAUNCHER(launch_adjoint_g2);   // masks 8-11  (volume [+ camera / stepsize])
 DDVR_ADJ_LAUNCHER(launch_adjoint_g3);   // masks 12-15 (volume + tf [+ ...])
+// fused TF-target steps (masks 4, 12) with segment-split rays (SPLIT = 2, 4, 8); returns
+// the kernels launched (0: not instantiated)
+int launch_adjoint_split(unsigned mask, int split, int n_views, size_t smem, cudaStream_t st,
+                         const VolArgs& V, const TfArgs& T, const Geometry& G, float* dv,
+                         float* dcells, const FusedArgs& fu);
 
 #ifndef DDVR_CARVEOUT
 #define DDVR_CARVEOUT -1
@@ -1093,7 +1098,9 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : 1;
     // kMore: the next sample exists (known inside whole words but the last)
     auto step_m = [&](int i, auto kStore, auto kMore) {
-      const float d = density(c, v);
+      // (band march of inside rays: the raw interpolant -- the band test and the clamp
+      // of t to [0, R-1] give the same bit and tau as on the [0,1]-clamped density)
+      const float d = (kAbs && AFF && BITS && INSIDE) ? interp(c, v).rho : density(c, v);
       gx += r.gs[0]; gy += r.gs[1]; gz += r.gs[2];
       locate<CELLS>(V, gx, gy, gz, ins, c);
       const bool more = decltype(kMore)::value || i + 1 < r.n;
@@ -1250,7 +1257,12 @@ constexpr int adj_min_blocks(unsigned mask, int role, bool cells, bool fused) {
 #ifdef DDVR_ADJ_MINB
 #define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, DDVR_ADJ_MINB)
 #else
-#define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, adj_min_blocks(MASK, ROLE, CELLS, FUSED))
+// (segment-split steps are small: 2 CTAs/SM, the registers of the unsplit TF walk's spills)
+#ifndef DDVR_SPLIT_MINB
+#define DDVR_SPLIT_MINB 2
+#endif
+#define DDVR_ADJ_BOUNDS \
+  __launch_bounds__(kThreads, SPLIT > 1 ? DDVR_SPLIT_MINB : adj_min_blocks(MASK, ROLE, CELLS, FUSED))
 #endif
 template <bool EARLY, bool CELLS, bool TAPE>
 __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
@@ -1387,6 +1399,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
   // emitting texel TF without the TF target: the slope is only needed dotted
   // with the output adjoint, so the raw delta is kept and R applied once
   constexpr bool kEmitTex = EMIT && !kTf && KIND == kTfTexture;
+  // (kEmitTex: R folded into the rgb seed and into dt for the tau term of d_hat)
+  const float sRx = sd.x * TF.fR, sRy = sd.y * TF.fR, sRz = sd.z * TF.fR;
+  const float dtR = dt32 * TF.fR;
 
   // adjoint state: rgb seed is constant along the walk (renderer.py:540)
   float a_hat = sd.w;
@@ -1529,11 +1544,11 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     }
     if (kDhat) {
       // renderer.py:606 d_hat = slope . out4_hat
-      // (kEmitTex: slope . (aT sd_rgb, tau_hat) = R (aT (delta_rgb . sd_rgb) + delta_tau tau_hat))
+      // (kEmitTex: slope . (aT sd_rgb, tau_hat) = aT (delta_rgb . R sd_rgb) + delta_tau R tau_hat)
       const float d_hat =
           kAbs ? ((s.w < 0.f || g.a_clamped) ? 0.f : dq * abs_k)
-          : kEmitTex ? TF.fR * __fmaf_rn(aT, dl4.x * sd.x + dl4.y * sd.y + dl4.z * sd.z,
-                                         dl4.w * tau_hat)
+          : kEmitTex ? __fmaf_rn(aT, dl4.x * sRx + dl4.y * sRy + dl4.z * sRz,
+                                 dl4.w * (s.w < 0.f ? 0.f : dtR * ea))
           : EMIT ? slope.x * h0 + slope.y * h1 + slope.z * h2 + slope.w * tau_hat
                  : slope.w * tau_hat;
       const bool live = (kAbs && AFF) ? inside   // (the band test above covers [0,1])
@@ -1547,7 +1562,9 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         // corner weights (25 instructions).  Branch-free: the finished run is
         // flushed with predicated vector reds and the accumulators restart by
         // scaling them with 0.
-        const float dh = live ? d_hat : 0.f;
+        // (texel tables: outside the box, or raw outside [0, 1], the clamped density sits
+        // in a clamp band whose guard texel has a zero delta -- d_hat is 0 already)
+        const float dh = (live || kEmitTex) ? d_hat : 0.f;
         const bool fresh = c.cell != st.run_cell;
         // (affine absorption walk: every d_hat of a ray is 0 or abs_k, so a run
         // whose weight sum acc8[0] is 0 has all moments 0 -- no red)
@@ -1793,7 +1810,18 @@ __device__ __forceinline__ bool band_class(const TfArgs& TFA, const Geometry& G,
 // belongs to the other role -- no host synchronisation.
 // FUSED: the forward march and the L1 seed run in the same thread first
 // (FusedArgs); image / depth / seed are then unused.
-template <unsigned MASK, bool CELLS, int ROLE, bool FUSED, bool DET = false>
+// SPLIT > 1 (fused TF-target steps without camera / stepsize, few rays): SPLIT
+// consecutive lanes share one ray, lane k marching and walking the k-th of SPLIT equal
+// sample segments (8-pixel-wide CTA tiles of kThreads/SPLIT rays).  Front-to-back
+// compositing is associative, so the segments' (premultiplied rgb, alpha, depth)
+// compose the ray's image exactly as the serial march (up to fp32 reassociation); the
+// walk of segment k starts from the depth after its last sample (prefix of the
+// segments' depths) and from the blend adjoint a_hat the later segments leave behind,
+// a_hat = T_after sd_a - sd_rgb . C_after (C_after, T_after: the composite of segments
+// k+1.. with T = 1 at their start) -- the value the serial walk reaches there
+// (renderer.py:583-589 unrolled over those samples).  A ray's serial chain is then
+// SPLIT times shorter, for steps too small to fill the GPU with one thread per ray.
+template <unsigned MASK, bool CELLS, int ROLE, bool FUSED, bool DET = false, int SPLIT = 1>
 __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     VolArgs V, TfArgs TFA, Geometry G, const float* __restrict__ image,
     const float* __restrict__ depth, const float* __restrict__ seed, float* __restrict__ d_volume,
@@ -1833,8 +1861,17 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   // the tf target needs the rgb channels even when they are zero
   const bool emit = kTf || s_info[1] != 0u;
 
-  int px, py;
-  pixel_of(G, px, py);
+  static_assert(SPLIT == 1 || (FUSED && !kPos && kThreads % (8 * SPLIT) == 0 && 32 % SPLIT == 0),
+                "segment-split rays: fused steps without camera / stepsize targets");
+  int px, py, seg = 0;
+  if (SPLIT > 1) {   // ray (threadIdx / SPLIT) of an 8 x (kThreads / SPLIT / 8) tile
+    const int rid = threadIdx.x / SPLIT;
+    seg = threadIdx.x % SPLIT;
+    px = blockIdx.x * 8 + (rid & 7);
+    py = G.row0 + blockIdx.y * (kThreads / SPLIT / 8) + (rid >> 3);
+  } else {
+    pixel_of(G, px, py);
+  }
   const bool valid = px < G.W && py < G.row1;
 
   Ray r;
@@ -1856,6 +1893,13 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     }
   }
   const bool warp_inside = CELLS && __all_sync(0xffffffffu, r.all_inside);
+  if (SPLIT > 1 && valid) {   // this lane's segment [i0, i1) of the ray's samples
+    const int i0 = (int)((long long)r.n * seg / SPLIT);
+    const int i1 = (int)((long long)r.n * (seg + 1) / SPLIT);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r.g0[k] += (long long)i0 * r.gs[k];
+    r.n = i1 - i0;
+  }
   // affine, non-negative tau column (the ramp), polynomial segment modes, no
   // stepsize target: the table-free walk
   const bool aff_walk = DDVR_AFF_WALK && !(MASK & DDVR_TARGET_STEPSIZE) && s_info[2] == 0u &&
@@ -1872,20 +1916,63 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   int march_skip = 0, walk_skip = 0;   // measurement counters (G.stats)
   if (FUSED) {   // forward march (renderer.py:306-357) + L1 seed (objectives.py:38-54)
     double loss_part = 0.0;
+    float4 rgba = make_float4(0.f, 0.f, 0.f, 0.f);
     if (valid) {
-      float4 rgba;
       march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
                                                      s_info[1] != 0u, mode, rgba, S, s_info,
                                                      kBitsKernel ? bits : nullptr, bits_off,
                                                      kBitsKernel ? &march_skip : nullptr);
+    }
+    double S_tot = S;
+    float4 after = make_float4(0.f, 0.f, 0.f, 0.f);   // SPLIT: composite of the later segments
+    float T_after = 1.f;
+    if (SPLIT > 1) {   // every lane of the warp: the segment groups exchange by shuffles
+      if (!valid) { rgba = make_float4(0.f, 0.f, 0.f, 0.f); S = 0.0; }
+      const int base = (threadIdx.x & 31) & ~(SPLIT - 1);
+      float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+      float T_front = 1.f;
+      double S_end = 0.0;
+      S_tot = 0.0;
+#pragma unroll
+      for (int j = 0; j < SPLIT; ++j) {
+        const float4 c = make_float4(__shfl_sync(0xffffffffu, rgba.x, base + j),
+                                     __shfl_sync(0xffffffffu, rgba.y, base + j),
+                                     __shfl_sync(0xffffffffu, rgba.z, base + j),
+                                     __shfl_sync(0xffffffffu, rgba.w, base + j));
+        const double Sj = __shfl_sync(0xffffffffu, S, base + j);
+        const float Tj = (float)exp(-Sj);   // the segment's transmittance
+        tot.x = __fmaf_rn(T_front, c.x, tot.x);   // front-to-back over (renderer.py:350-355)
+        tot.y = __fmaf_rn(T_front, c.y, tot.y);
+        tot.z = __fmaf_rn(T_front, c.z, tot.z);
+        tot.w = __fmaf_rn(T_front, c.w, tot.w);
+        T_front *= Tj;
+        S_tot += Sj;
+        if (j <= seg) S_end += Sj;
+        if (j > seg) {
+          after.x = __fmaf_rn(T_after, c.x, after.x);
+          after.y = __fmaf_rn(T_after, c.y, after.y);
+          after.z = __fmaf_rn(T_after, c.z, after.z);
+          T_after *= Tj;
+        }
+      }
+      rgba = tot;
+      S = S_end;   // the walk of this segment starts after its last sample
+    }
+    if (valid) {
       const float4 ref = reinterpret_cast<const float4*>(Fu.refs)[pix];
       const float dx = rgba.x - ref.x, dy = rgba.y - ref.y, dz = rgba.z - ref.z,
                   dw = rgba.w - ref.w;
       auto sgn = [&](float v) { return v > 0.f ? Fu.inv_count : (v < 0.f ? -Fu.inv_count : 0.f); };
       sd = make_float4(sgn(dx), sgn(dy), sgn(dz), sgn(dw));
-      loss_part = fabs((double)dx) + fabs((double)dy) + fabs((double)dz) + fabs((double)dw);
-      if (Fu.image_out) reinterpret_cast<float4*>(Fu.image_out)[pix] = rgba;
-      if (Fu.depth_out) Fu.depth_out[pix] = (float)S;
+      if (seg == 0) {
+        loss_part = fabs((double)dx) + fabs((double)dy) + fabs((double)dz) + fabs((double)dw);
+        if (Fu.image_out) reinterpret_cast<float4*>(Fu.image_out)[pix] = rgba;
+        if (Fu.depth_out) Fu.depth_out[pix] = (float)S_tot;
+      }
+      // SPLIT: the blend adjoint's a_hat after this segment (see the kernel comment);
+      // sd.w only seeds a_hat in the emitting / TF walks
+      if (SPLIT > 1)
+        sd.w = __fmaf_rn(T_after, sd.w, -(sd.x * after.x + sd.y * after.y + sd.z * after.z));
     }
     loss_part = warp_sum(loss_part);
     if ((threadIdx.x & 31) == 0 && loss_part != 0.0) atomicAdd(Fu.loss, loss_part * Fu.inv_count_d);
@@ -1954,7 +2041,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   if (FUSED && G.stats) {   // measurement only: one atomic per warp and counter
     const unsigned long long c[4] = {
         warp_sum((unsigned long long)(valid ? r.n : 0)), warp_sum((unsigned long long)march_skip),
-        warp_sum((unsigned long long)walk_skip), warp_sum((unsigned long long)(valid ? 1 : 0))};
+        warp_sum((unsigned long long)walk_skip),
+        warp_sum((unsigned long long)(valid && seg == 0 ? 1 : 0))};
     if ((threadIdx.x & 31) == 0)
       for (int k = 0; k < 4; ++k)
         if (c[k]) atomicAdd(G.stats + k, c[k]);

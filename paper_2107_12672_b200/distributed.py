@@ -109,13 +109,15 @@ class ShardedStep:
     the march skips 32-sample blocks in all-zero 8^3-cell bricks (bitwise the same
     step; False marches every block, DDVR_FLAG_NO_EMPTY_SKIP).  ``split_walk`` (band
     tape): march and walk as two kernels instead of one (DDVR_FLAG_SPLIT_WALK).
+    ``ray_split`` (fused TF-target steps): threads per ray (1, 2, 4, 8 or "auto",
+    DDVR_FLAG_RAY_SPLIT_*).
     """
 
     def __init__(self, density, texels, lonlat, refs, dt, rig: R.Rig, *, targets=("volume",),
                  total_elements=None, radius=2.0, center=(0.0, 0.0, 0.0), fov_y_deg=30.0,
                  group=None, layout="cells", fused="auto", keep_images=False, chunks=4,
                  deterministic=False, band_tape="auto", empty_skip=True, stats=None,
-                 split_walk=False):
+                 split_walk=False, ray_split="auto"):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
         R.validate_cameras(lonlat, radius, fov_y_deg)   # field.py:147-156
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
@@ -145,6 +147,7 @@ class ShardedStep:
         # measurement counters of the fused step (forward_adjoint_l1 ``stats``)
         self.stats = stats
         self.split_walk = bool(split_walk)
+        self.ray_split = ray_split
         if fused == "auto":
             fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
         self.fused = bool(fused) and self.cells is not None
@@ -229,7 +232,8 @@ class ShardedStep:
                     ws_continue=k > 0 and self.workspace is not None,
                     ws_defer=not last and self.workspace is not None,
                     deterministic=self.deterministic, band_tape=self.band_tape,
-                    empty_skip=self.empty_skip, stats=self.stats, split_walk=self.split_walk)
+                    empty_skip=self.empty_skip, stats=self.stats, split_walk=self.split_walk,
+                    ray_split=self.ray_split)
             hook("post_adjoint")
         elif V:
             if self.cells is not None:

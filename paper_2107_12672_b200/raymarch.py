@@ -272,7 +272,7 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
                        *, cells, loss, d_volume=None, d_tf=None, d_camera=None, d_dt=None,
                        workspace=None, image_out=None, depth_out=None, ws_continue=False,
                        ws_defer=False, deterministic=False, band_tape=False,
-                       empty_skip=True, stats=None, split_walk=False):
+                       empty_skip=True, stats=None, split_walk=False, ray_split="auto"):
     """One fused step over these views: forward march, L1 seed sign(image - ref)/count
     and adjoint walk per ray in one kernel (ddvr_forward_adjoint_l1).  loss (fp64,
     device) += sum |image - ref| / count; gradients accumulate (+=) as in adjoint().
@@ -286,6 +286,9 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
     caller-provided workspace needs those extra bytes too (extra_workspace_bytes).
     ``split_walk`` (band tape): march and walk as two kernels (DDVR_FLAG_SPLIT_WALK)
     instead of one (the same outputs).
+    ``ray_split`` (TF target without camera / stepsize): threads per ray, 1, 2, 4 or 8
+    consecutive lanes marching and walking one sample segment each; "auto" picks it
+    from the ray count (DDVR_FLAG_RAY_SPLIT_*).
     ``stats`` (measurement, optional): (4,) int64 device tensor the kernel adds
     [samples, samples the march skipped, samples the walk skipped, rays] to."""
     _require(cams, "cameras", torch.float64, ndim=2)
@@ -312,6 +315,10 @@ def forward_adjoint_l1(density, texels, cams, dt: float, rig: Rig, refs, count: 
     prm.flags = (N.FLAG_WS_CONTINUE if ws_continue else 0) | (N.FLAG_WS_DEFER if ws_defer else 0) \
         | (N.FLAG_DETERMINISTIC if deterministic else 0) | (N.FLAG_BAND_TAPE if band_tape else 0) \
         | (0 if empty_skip else N.FLAG_NO_EMPTY_SKIP) | (N.FLAG_SPLIT_WALK if split_walk else 0)
+    if ray_split != "auto":
+        if ray_split not in N.FLAG_RAY_SPLIT:
+            raise InvalidParameterError(f"ray_split must be 'auto', 1, 2, 4 or 8, not {ray_split!r}")
+        prm.flags |= N.FLAG_RAY_SPLIT[ray_split]
     if stats is not None:
         _require(stats, "stats", torch.int64)
         if stats.numel() < 4:

@@ -34,7 +34,7 @@ def test_header_declares_the_boundary():
     names = _declared()
     assert names == sorted(["ddvr_forward", "ddvr_adjoint", "ddvr_forward_adjoint_l1",
                             "ddvr_adjoint_workspace_bytes", "ddvr_deterministic_bytes", "ddvr_band_tape_bytes",
-                            "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
+                            "ddvr_ray_split", "ddvr_cells_bytes", "ddvr_pack_cells", "ddvr_forward_grad",
                             "ddvr_forward_color", "ddvr_adjoint_color",
                             "ddvr_l1_loss", "ddvr_opacity_entropy", "ddvr_gather_probe",
                             "ddvr_ray_setup", "ddvr_prior_volume", "ddvr_prior_tf",
@@ -245,10 +245,14 @@ def test_deterministic_mode_workspace(lib):
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 2 and "deterministic" in lib.ddvr_last_error().decode()
-    prm.flags = 64   # an unknown bit
+    prm.flags = 1 << 20   # an unknown bit
     rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
                           None, 16, 1, None, None, 16, None, None, 0, None)
     assert rc == 1 and "flags" in lib.ddvr_last_error().decode()
+    prm.flags = N.FLAG_RAY_SPLIT[2] | N.FLAG_RAY_SPLIT[8]   # two ray splits
+    rc = lib.ddvr_adjoint(ctypes.byref(vol), ctypes.byref(tf), 16, 1, ctypes.byref(prm), 16,
+                          None, 16, 1, None, None, 16, None, None, 0, None)
+    assert rc == 1 and "RAY_SPLIT" in lib.ddvr_last_error().decode()
 
 
 def test_band_tape_bytes_and_limits(lib):
@@ -274,3 +278,21 @@ def test_band_tape_bytes_and_limits(lib):
     big.flags = N.FLAG_BAND_TAPE
     assert call(big_vol, big, 64, 1 << 40) == 3 and "16 GiB" in lib.ddvr_last_error().decode()
     assert call(vol, prm, 1, 1 << 16) == 2 and "band tape" in lib.ddvr_last_error().decode()
+
+
+def test_ray_split_choice(lib):
+    """Segment-split rays (DDVR_FLAG_RAY_SPLIT_*): only fused TF-target masks without
+    camera / stepsize split, by default only when the rays alone would not fill the
+    GPU (C1's 16 K rays: 8 threads per ray; C2's 524 K: 1); the flags force it."""
+    from paper_2107_12672_b200 import _native as N
+    TF, VOL, CAM = N.TARGET_BITS["tf"], N.TARGET_BITS["volume"], N.TARGET_BITS["camera"]
+    split = lib.ddvr_ray_split
+    assert split(TF | VOL, 128 * 128, 0) == 8          # C1
+    assert split(TF, 8 * 256 * 256, 0) == 1            # C2
+    assert split(TF, 40000, 0) == 4 and split(TF, 60000, 0) == 2
+    for mask in (VOL, TF | CAM, VOL | CAM, TF | VOL | CAM):
+        assert split(mask, 100, 0) == 1
+        assert split(mask, 100, N.FLAG_RAY_SPLIT[4]) == 1
+    for k, flag in N.FLAG_RAY_SPLIT.items():
+        assert split(TF | VOL, 128 * 128, flag) == k
+        assert split(TF, 10 ** 8, flag) == k

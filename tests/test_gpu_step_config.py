@@ -116,10 +116,13 @@ def test_fused_step_matches_reference_at_config_scale(cuda, case, tape, skip, sp
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", ["C1_step_dense", "C2_step_dense"])
-@pytest.mark.parametrize("graph", [False, True])
-def test_tf_step_matches_reference_at_config_scale(cuda, case, graph):
+@pytest.mark.parametrize("graph,split", [(False, "auto"), (True, "auto"), (False, 1), (False, 2),
+                                         (False, 4), (False, 8)])
+def test_tf_step_matches_reference_at_config_scale(cuda, case, graph, split):
     """The fused TF-target step (C1: volume + TF, C2: TF) the bench times, eagerly and
-    replayed from a CUDA graph (bench.py's default for C1)."""
+    replayed from a CUDA graph (bench.py's default for C1), with the default and every
+    forced segment split of the rays (DDVR_FLAG_RAY_SPLIT_*: 1, 2, 4, 8 threads per ray;
+    the C1 and C2 bands have few enough rays that "auto" splits them)."""
     import torch
     from paper_2107_12672_b200 import raymarch as R
     from paper_2107_12672_b200.distributed import ShardedStep
@@ -140,7 +143,7 @@ def test_tf_step_matches_reference_at_config_scale(cuda, case, graph):
     targets = tuple(c.targets)
     step = ShardedStep(est, tex, ll, refs, float(g["dt"]), rig, targets=targets,
                        total_elements=float(g["count"]), radius=c.radius, fov_y_deg=c.fov,
-                       keep_images=True)
+                       keep_images=True, ray_split=split)
     assert step.fused
     if graph:
         step.run()                              # warm up outside the capture
