@@ -16,7 +16,7 @@ cap() {  # name, kernel regex, count, bench args...
   timeout 900 ncu $K -k "regex:$k" -c $c -o /tmp/ncu/$n python bench.py "$@" --steps 1 --warmup 1 --no-extras --no-cpu-baseline > gpurun_out/final/ncu_$n.log 2>&1; echo "ncu $n rc=$?"
   ncu -i /tmp/ncu/$n.ncu-rep --page raw --csv > gpurun_out/final/ncu_${n}_raw.csv 2>/dev/null
 }
-cap C4 'int\)1, \(bool\)1, \(bool\)0>' 1
+cap C4 'int\)1, \(bool\)1, \(bool\)0, \(int\)1>' 1
 cap C5 'dvr_adjoint_kernel' 1 --config C5 --views 16
 cap C2 'dvr_adjoint_kernel' 1 --config C2
 cap C3 'dvr_adjoint_kernel|dvr_forward_kernel' 3 --config C3
