@@ -207,7 +207,8 @@ class ShardedStep:
         refs_ready = self._stage_refs(refs_host, chunks)
         f = self.flat
         f.zero_()
-        self.d_camera.zero_()
+        if self.mask & N.TARGET_CAMERA:
+            self.d_camera.zero_()
         V = self.cams.shape[0]
         if V and self.fused:
             R.pack_cells(self.density, self.cells)

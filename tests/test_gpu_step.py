@@ -404,3 +404,51 @@ def test_band_tape_empty_brick_skip_is_exact(cuda, dt_vox):
         seed = np.sign(im - refs[k].cpu().numpy().astype(np.float64)) / refs.numel()
         want += O.adjoint_view(grid, t64, v, dt, seed, ["volume"], image=im)["d_volume"]
     assert rel_l2(a["dv"], want) <= 1e-4
+
+
+@pytest.mark.parametrize("kind", ["texture", "piecewise", "gaussian"])
+@pytest.mark.parametrize("targets", [("tf",), ("volume", "tf")])
+def test_fused_step_ray_split_matches_one_thread_per_ray(cuda, kind, targets):
+    """Segment-split rays (DDVR_FLAG_RAY_SPLIT_2/4/8) against one thread per ray, for
+    every TF kind and both split masks: the composed image, the L1 loss and every
+    gradient agree up to fp32 reassociation (segments shorter than SPLIT included: the
+    scene's rays have 3-40 samples)."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    rng = np.random.default_rng(21)
+    n = 20
+    vol = torch.from_numpy(rng.uniform(0.0, 1.0, (n, n, n)).astype(np.float32)).to(cuda)
+    if kind == "texture":
+        tf = rng.uniform(0.1, 1.0, (16, 4)) * np.array([1, 1, 1, 6.0])
+    elif kind == "piecewise":
+        pos = np.sort(np.concatenate([[0.0, 1.0], rng.uniform(0.05, 0.95, 5)]))
+        tf = np.column_stack([pos, rng.uniform(0.1, 1.0, (7, 3)), rng.uniform(0.2, 6.0, 7)])
+    else:
+        tf = np.column_stack([rng.uniform(0.2, 0.8, 4), rng.uniform(0.05, 0.3, 4),
+                              rng.uniform(0.1, 1.0, (4, 3)), rng.uniform(0.5, 6.0, 4)])
+    tx = torch.from_numpy(tf.astype(np.float32)).to(cuda)
+    ll = torch.tensor([[25.0, 10.0], [200.0, -40.0], [95.0, 65.0]], dtype=torch.float64,
+                      device=cuda)
+    W, H = 21, 19
+    # references at -1 or 2: every seed sign is fixed away from image == ref (an image
+    # change of 1e-7 cannot flip a pixel's seed)
+    refs = torch.from_numpy(rng.choice([-1.0, 2.0], (3, H, W, 4)).astype(np.float32)).to(cuda)
+    out = {}
+    for split in (1, 2, 4, 8):
+        step = ShardedStep(vol, tx, ll, refs, 0.6 / n, R.Rig(W, H), targets=targets,
+                           radius=2.0, keep_images=True, ray_split=split)
+        assert step.fused
+        f = step.run()
+        torch.cuda.synchronize()
+        out[split] = (step.img.double().cpu().numpy(), float(f.loss),
+                      f.d_tf.double().cpu().numpy(), f.d_volume.double().cpu().numpy())
+    img1, loss1, dtf1, dvol1 = out[1]
+    assert np.abs(dtf1).max() > 0
+    for split in (2, 4, 8):
+        img, loss, dtf, dvol = out[split]
+        assert rel_l2(img, img1) <= 1e-6, (split, rel_l2(img, img1))
+        assert abs(loss - loss1) <= 1e-6 * abs(loss1)
+        assert rel_l2(dtf, dtf1) <= 1e-5, (split, rel_l2(dtf, dtf1))
+        if "volume" in targets:
+            assert rel_l2(dvol, dvol1) <= 1e-5, (split, rel_l2(dvol, dvol1))
