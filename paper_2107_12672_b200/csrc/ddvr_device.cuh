@@ -700,8 +700,12 @@ __device__ __forceinline__ float clamp_density(bool inside, float raw) {
 // ---------------------------------------------------------------------------
 
 // Dynamic shared memory of every kernel (R = TF texels; float offsets):
-//   [0, 8(R+1))          the TF as (texel, next texel - texel) float4 pairs with
-//                        guard entries at both ends (see texel_coord)
+//   [0, 8(R+1))          the TF as two planes of R+1 float4 entries with guard
+//                        entries at both ends (see texel_coord): texels [0, R+1),
+//                        then the deltas next texel - texel [R+1, 2R+2) (float4
+//                        index).  One 16-byte load per plane and sample: lanes of a
+//                        warp reading up to 8 consecutive entries hit distinct banks
+//                        (interleaved 32-byte pairs conflicted from 4 on)
 //   [8(R+1), 12R+8)      the per-CTA TF gradient (adjoint, tf target)
 //   [12R+8, 14R+10)      (tau, next tau - tau) float2 pairs: the table of an
 //                        emission-free TF (rgb texels all zero, e.g. the
@@ -717,7 +721,7 @@ extern __shared__ float4 g_smem[];
 // clamp bands (field.py:575-576) are then baked into the table: i = floor(t),
 // w = t - i, no clamps and no live test.  (Only the measure-zero point
 // t = R-1 exactly differs: the reference takes the left interval's slope.)
-// Float offsets: pairs [0, 8(R+1)), TF gradient [8(R+1), 12R+8),
+// Float offsets: texel and delta planes [0, 8(R+1)), TF gradient [8(R+1), 12R+8),
 // tau pairs [12R+8, 14R+10).
 __device__ __forceinline__ const float2* tau_table(const TfArgs& T) {
   return reinterpret_cast<const float2*>(g_smem) + (6 * T.count + 4);
@@ -752,8 +756,8 @@ __device__ __forceinline__ float4 lerp_texel(float w, const float4& a, const flo
 __device__ __forceinline__ float4 tf_eval(const TfArgs& T, float d, int& i0, float& w,
                                           float4& slope, bool want_slope) {
   i0 = texel_coord(T, d, w);
-  const float4 a = g_smem[2 * i0 + 2];
-  const float4 dlt = g_smem[2 * i0 + 3];
+  const float4 a = g_smem[i0 + 1];
+  const float4 dlt = g_smem[T.count + 2 + i0];
   if (want_slope) {   // guard entries have dlt = 0: the clamp bands' zero slope
     const float2 sxy = mul2(make_float2(dlt.x, dlt.y), bcast(T.fR));
     const float2 szw = mul2(make_float2(dlt.z, dlt.w), bcast(T.fR));
@@ -908,7 +912,7 @@ __device__ __forceinline__ Segment segment(float tau_raw, float dt32) {
 // shared prologue: TF table + view frame into shared memory
 // ---------------------------------------------------------------------------
 
-// shared TF table as (texel k, texel k+1 - texel k) pairs: the lerp is then 4
+// shared TF table as (texel k, texel k+1 - texel k) planes: the lerp is then 4
 // FFMA and the slope (field.py:576) needs no subtraction.  Returns (to every
 // thread, after the barrier the caller issues) the segment mode of the CTA.
 // s_info[0]: largest tau texel (bits), s_info[1]: 1 if any rgb texel is non-zero,
@@ -955,8 +959,8 @@ __device__ __forceinline__ void load_tf(const TfArgs& tf, unsigned* s_info) {
   for (int e = threadIdx.x; e <= tf.count; e += blockDim.x) {   // guard entries 0 and R
     const float4 a = src[min(max(e - 1, 0), tf.count - 1)];
     const float4 b = src[min(e, tf.count - 1)];
-    g_smem[2 * e] = a;
-    g_smem[2 * e + 1] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
+    g_smem[e] = a;
+    g_smem[tf.count + 1 + e] = make_float4(__fsub_rn(b.x, a.x), __fsub_rn(b.y, a.y),
                                     __fsub_rn(b.z, a.z), __fsub_rn(b.w, a.w));
     tau[e] = make_float2(a.w, __fsub_rn(b.w, a.w));
     mx = fmaxf(mx, a.w);   // interpolated tau never exceeds the largest texel
@@ -1465,8 +1469,8 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
     const bool want = kDhat || (kTf && KIND != kTfTexture);
     if (kEmitTex) {   // tf_eval with the raw delta kept (d_hat below folds R once)
       i0 = texel_coord(TF, d, w);
-      const float4 a = g_smem[2 * i0 + 2];
-      dl4 = g_smem[2 * i0 + 3];
+      const float4 a = g_smem[i0 + 1];
+      dl4 = g_smem[TF.count + 2 + i0];
       s = lerp_texel(w, a, dl4);
       slope = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (kAbs && AFF) {
