@@ -108,6 +108,9 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+RED_SECTORS_PEAK = 2 * 93.9e9   # profiles/r02_bulk_red_probe.txt, 64 MB, mode 0
+
+
 def ncu_entry(config, kernel):
     """The committed ncu --set full numbers of one kernel launch at the bench's fixed
     state (tools/ncu_summary.py --json-out), or None."""
@@ -708,6 +711,20 @@ def report(args, cfg, step, runner, world, mine, total_samples, total_rays, loca
                                        "red_requests_per_s", "gather_requests_per_sample",
                                        "occupancy_pct", "registers", "duration_ms")
                     if k in nc}})
+        if nc.get("red_sectors") and nc["red_sectors"] / nc["duration_ms"] > 1e9:
+            # the kernel's density / TF gradient reds against the measured red ceiling:
+            # 2 x red.v4 per 32-byte record into an L2-resident array, random records,
+            # 94 G records/s = 188 G sectors/s (tools/probes/bulk_red_probe.cu mode 0,
+            # profiles/r02_bulk_red_probe.txt)
+            sectors = float(nc["red_sectors"]) * (local_samples / nc["samples"]
+                                                  if nc.get("samples") else 1.0)
+            roof["atomics"] = {
+                "bound": "L2 reds", "sectors_per_launch": sectors,
+                "achieved": sectors / adj_s, "peak": RED_SECTORS_PEAK, "unit": "sectors/s",
+                "frac": sectors / adj_s / RED_SECTORS_PEAK,
+                "peak_source": "measured: bulk_red_probe mode 0 (2 x red.v4 per 32-byte "
+                               "record, random records, 64 MB L2-resident array)",
+                "pct_of_l2_red_peak_ncu": nc.get("red_sectors_pct_of_l2_peak")}
     else:
         roof.update({"achieved": model_gbs, "frac": model_gbs / peak, "traffic": None,
                      "traffic_source": "no ncu capture of this kernel at this state: "

@@ -38,6 +38,8 @@ METRICS = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 red sectors"),
+    ("lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed", "L2 red sectors % peak"),
 ]
 
 
@@ -104,6 +106,10 @@ def _merge_json(args, vals, units, head, row):
     red = _num(vals.get("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", 0))
     e["red_requests"] = red
     e["red_requests_per_s"] = red / (dur_ms / 1e3) if dur_ms else None
+    if "lts__t_sectors_srcunit_tex_op_red.sum" in vals:   # 32-byte sectors the L2 reduced
+        e["red_sectors"] = _num(vals["lts__t_sectors_srcunit_tex_op_red.sum"])
+        e["red_sectors_pct_of_l2_peak"] = _num(
+            vals["lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed"])
     if args.samples:
         e["samples"] = args.samples
         e["warp_inst_per_sample"] = _num(vals["smsp__inst_executed.sum"]) / (args.samples / 32)
