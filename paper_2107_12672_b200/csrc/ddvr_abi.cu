@@ -130,6 +130,96 @@ __device__ void fold_voxel(const VolArgs& V, const unsigned long long* c64, doub
   d_volume[id] += s;
 }
 
+// The fold split by position: interior voxels (1 <= coordinate <= dim-2 on every axis)
+// read exactly the 8 records of the 2x2x2 block ending at their own record, corner b from
+// storage (x+1, y+1, z+1) - b, no clamping; the boundary shell takes fold_voxel's
+// clamped pair lists.  Separate index spaces, so no warp mixes the two paths (with one
+// thread per voxel every warp of a 64-voxel row held an edge voxel and ran both).
+__global__ void __launch_bounds__(256) fold_interior_kernel(VolArgs V,
+                                                          const float* __restrict__ d_cells,
+                                                          float* __restrict__ d_volume,
+                                                          long long n) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= n) return;
+  int x, y, z;
+  vox_coords(id, n, V.Y - 2, V.Z - 2, x, y, z);
+  ++x; ++y; ++z;
+  const float* base = d_cells + 8 * (((long long)(x + 1) * V.CY + (y + 1)) * V.CZ + (z + 1));
+  const long long sx = 8ll * V.CY * V.CZ, sy = 8ll * V.CZ;
+  float s = 0.f;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const float4* m = reinterpret_cast<const float4*>(
+        base - ((b & 1) ? sx : 0) - ((b & 2) ? sy : 0) - ((b & 4) ? 8 : 0));
+    s += corner_from_moments(__ldg(m), __ldg(m + 1), b);
+  }
+  d_volume[((long long)x * V.Y + y) * V.Z + z] += s;
+}
+
+// shell voxel k of an X x Y x Z grid (faces x = 0, X-1; then y = 0, Y-1 without them;
+// then z = 0, Z-1 without either): its coordinates
+__device__ __forceinline__ void shell_coords(long long k, int X, int Y, int Z, int& x, int& y,
+                                             int& z) {
+  const long long fx = (long long)Y * Z;                        // one x face
+  const long long fy = (long long)max(X - 2, 0) * Z;            // one y face, x interior
+  const long long fz = (long long)max(X - 2, 0) * max(Y - 2, 0);   // one z face
+  const int nx = X > 1 ? 2 : 1, ny = Y > 1 ? 2 : 1;
+  if (k < nx * fx) {
+    const int f = (int)(k / fx);
+    const long long r = k - f * fx;
+    x = f ? X - 1 : 0; y = (int)(r / Z); z = (int)(r - (long long)y * Z);
+    return;
+  }
+  k -= nx * fx;
+  if (k < ny * fy) {
+    const int f = (int)(k / fy);
+    const long long r = k - f * fy;
+    y = f ? Y - 1 : 0; x = 1 + (int)(r / Z); z = (int)(r - (long long)(x - 1) * Z);
+    return;
+  }
+  k -= ny * fy;
+  const int f = (int)(k / fz);
+  const long long r = k - f * fz;
+  z = f ? Z - 1 : 0; x = 1 + (int)(r / max(Y - 2, 1)); y = 1 + (int)(r - (long long)(x - 1) * max(Y - 2, 1));
+}
+
+// A boundary voxel (dims >= 2 on every axis): per axis the pairs (storage pos, corner 1)
+// and (pos + 1, corner 0) of an interior voxel, plus (pos, 0) on the low face and
+// (pos + 1, 1) on the high face -- the clamped corners of the padded cells (the pair
+// lists fold_voxel builds) as 3 x 3 x 3 predicated terms in registers
+__global__ void __launch_bounds__(256) fold_shell_kernel(VolArgs V,
+                                                       const float* __restrict__ d_cells,
+                                                       float* __restrict__ d_volume,
+                                                       long long n) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int p[3];
+  shell_coords(k, V.X, V.Y, V.Z, p[0], p[1], p[2]);
+  const int dims[3] = {V.X, V.Y, V.Z};
+  int sa[3][3], ba[3][3];
+  bool va[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool lo = p[a] == 0, hi = p[a] == dims[a] - 1;
+    sa[a][0] = p[a];     ba[a][0] = 1; va[a][0] = true;
+    sa[a][1] = p[a] + 1; ba[a][1] = 0; va[a][1] = true;
+    sa[a][2] = lo ? p[a] : p[a] + 1; ba[a][2] = lo ? 0 : 1; va[a][2] = lo || hi;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        if (!(va[0][i] && va[1][j] && va[2][l])) continue;
+        const long long cell = ((long long)sa[0][i] * V.CY + sa[1][j]) * V.CZ + sa[2][l];
+        const float4* m = reinterpret_cast<const float4*>(d_cells + 8 * cell);
+        s += corner_from_moments(__ldg(m), __ldg(m + 1), ba[0][i] | ba[1][j] << 1 | ba[2][l] << 2);
+      }
+  d_volume[((long long)p[0] * V.Y + p[1]) * V.Z + p[2]] += s;
+}
+
 // d_volume[x,y,z] += the gradient of every record corner that pack_cells_kernel
 // filled from voxel (x,y,z) (its exact transpose, padding included); the
 // adjoint leaves each record's moment gradient, mapped back per corner here
@@ -1063,6 +1153,15 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
               : mask <= 11 ? launch_adjoint_g2 : launch_adjoint_g3;
   const int split = fu && cells ? split_of(mask, (long long)n_views * (G.row1 - G.row0) * G.W, flags)
                                   : 1;
+  if (ws_tf > 0 && !(flags & (DDVR_FLAG_WS_CONTINUE | DDVR_FLAG_WS_DEFER))) {
+    // a one-call step uses (and reduces) only as many TF slots as it has CTAs
+    const long long ctas =
+        split > 1 ? (long long)((G.W + 7) / 8) *
+                        ((G.row1 - G.row0 + kThreads / split / 8 - 1) / (kThreads / split / 8)) *
+                        n_views
+                  : (long long)grid.x * grid.y * grid.z;
+    T.nslot = (int)std::min<long long>(T.nslot, ctas);
+  }
   const int n_kernels =
       split > 1 ? launch_adjoint_split(mask, split, n_views, smem, st, V, T, G, d_volume, d_cells,
                                        *fu)
@@ -1087,6 +1186,15 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   }
   if (d_cells) {
     const long long nvox = (long long)V.X * V.Y * V.Z;
+    if (!V.cells64 && V.X >= 3 && V.Y >= 3 && V.Z >= 3) {   // interior + boundary shell
+      const long long nin = (long long)(V.X - 2) * (V.Y - 2) * (V.Z - 2), nsh = nvox - nin;
+      fold_interior_kernel<<<(unsigned)((nin + 255) / 256), 256, 0, st>>>(V, d_cells_all,
+                                                                         d_volume, nin);
+      if ((rc = check_launch("fold_interior_kernel"))) return rc;
+      fold_shell_kernel<<<(unsigned)((nsh + 255) / 256), 256, 0, st>>>(V, d_cells_all, d_volume,
+                                                                      nsh);
+      return check_launch("fold_shell_kernel");
+    }
     fold_cells_kernel<<<(unsigned)((nvox + 255) / 256), 256, 0, st>>>(V, d_cells_all, d_volume,
                                                                      nvox);
     return check_launch("fold_cells_kernel");
