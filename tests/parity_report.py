@@ -103,7 +103,10 @@ def main():
         note(key, "step/d_volume", rel_l2(f.d_volume.double().cpu().numpy(), want))
         report["cases"][key]["band_rows"] = [r0, r1]
         report["cases"][key]["views"] = [int(k) for k in g["views"]]
-    for case in ("C1_step_dense", "C2_step_dense"):   # the fused TF-target steps
+    for case, split in (("C1_step_dense", "auto"), ("C1_step_dense", 1),
+                        ("C2_step_dense", "auto"), ("C2_step_dense", 1)):
+        # the fused TF-target steps, with the default ray split (8 lanes per ray on these
+        # bands) and one thread per ray
         g = golden(case)
         name = case.split("_")[0]
         c = CONFIGS[name]
@@ -115,9 +118,9 @@ def main():
                            torch.from_numpy(g["refs"]).to(dev).contiguous(), float(g["dt"]),
                            R.Rig(c.image, c.image, rows=(r0, r1)), targets=tuple(c.targets),
                            total_elements=float(g["count"]), radius=c.radius, fov_y_deg=c.fov,
-                           keep_images=True)
+                           keep_images=True, ray_split=split)
         f = step.run()
-        key = f"{case}/targets={'+'.join(c.targets)}"
+        key = f"{case}/targets={'+'.join(c.targets)},ray_split={split}"
         note(key, "step/image", rel_l2(step.img.double().cpu().numpy(), g["image"]))
         note(key, "step/loss", abs(float(f.loss) - float(g["loss"])) / float(g["loss"]))
         note(key, "step/d_tf", rel_l2(f.d_tf.double().cpu().numpy().reshape(-1),
