@@ -711,7 +711,7 @@ def report(args, cfg, step, runner, world, mine, total_samples, total_rays, loca
                                        "red_requests_per_s", "gather_requests_per_sample",
                                        "occupancy_pct", "registers", "duration_ms")
                     if k in nc}})
-        if nc.get("red_sectors") and nc["red_sectors"] / nc["duration_ms"] > 1e9:
+        if nc.get("red_sectors") and nc["red_sectors"] / nc["duration_ms"] > 1e6:   # > 1 G/s
             # the kernel's density / TF gradient reds against the measured red ceiling:
             # 2 x red.v4 per 32-byte record into an L2-resident array, random records,
             # 94 G records/s = 188 G sectors/s (tools/probes/bulk_red_probe.cu mode 0,
