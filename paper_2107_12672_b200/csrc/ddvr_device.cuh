@@ -1239,7 +1239,9 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
 // The absorption-only kernel (ROLE 1) carries none of the emitting walk's
 // state and is compiled for 5 CTAs/SM.
 #ifndef DDVR_POS_MINB
-#define DDVR_POS_MINB 3   // camera / stepsize walks (fp64 per-ray sums; 80 registers: C3 +13% vs 2)
+#define DDVR_POS_MINB 4   // camera / stepsize walks (fp64 per-ray sums): 4 CTAs/SM at 64 registers
+                          // (some spills to L1, which runs at 34% here) beat 3 at 80: C3 +2.4%,
+                          // and 3 beat 2 by 13% (profiles/r02_minb3)
 #endif
 #ifndef DDVR_VOL_MINB
 #define DDVR_VOL_MINB 4   // volume-target walks (ROLE 0: the emitting inversion walk)
