@@ -510,6 +510,10 @@ __device__ __forceinline__ void ld256_if(bool pred, const float* p, float v[8]) 
 #ifndef DDVR_BITS_MARCH_UNROLL
 #define DDVR_BITS_MARCH_UNROLL 4
 #endif
+#ifndef DDVR_EMIT_MARCH_UNROLL
+#define DDVR_EMIT_MARCH_UNROLL 2   // the fused kernels' emitting marches (C5 +1.3%; the
+                                   // 48-register forward kernel spills unrolled: C3 -6%)
+#endif
 #ifndef DDVR_BITS_WALK_UNROLL
 #define DDVR_BITS_WALK_UNROLL 4
 #endif
@@ -1004,7 +1008,7 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 // The march of one ray.  INSIDE: every lane of the warp has all_inside (the
 // per-sample inside test and clamps are compiled out); SEG: segment mode.
 template <bool EARLY, bool CELLS, bool TAPE, int SEG, bool INSIDE, bool EMIT, int KIND,
-          bool AFF = false, bool BITS = false>
+          bool AFF = false, bool BITS = false, int EU = 1>
 __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, float dt32,
                                           const Ray& r, float* __restrict__ tape, float4& rgba,
                                           double& depth, float aff_a = 0.f, float aff_b = 0.f,
@@ -1099,7 +1103,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
     gather_if(V, r.n > 0, c.cell, v);
     held = c.cell;
     // (the emitting variants spill at 48 registers when unrolled)
-    constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : 1;
+    constexpr int kMarchUnroll = kAbs ? (BITS ? DDVR_BITS_MARCH_UNROLL : 4) : EU;
     // kMore: the next sample exists (known inside whole words but the last)
     auto step_m = [&](int i, auto kStore, auto kMore) {
       // (band march of inside rays: the raw interpolant -- the band test and the clamp
@@ -1174,7 +1178,7 @@ __device__ __forceinline__ void march_ray(const VolArgs& V, const TfArgs& TF, fl
 // The march of one ray with the variant the CTA's TF selects (kind, emission,
 // segment mode) and the warp's inside flag.  ABS_ONLY: only the emission-free
 // texel variants are compiled (the absorption-only kernels).
-template <bool EARLY, bool CELLS, bool TAPE, bool ABS_ONLY>
+template <bool EARLY, bool CELLS, bool TAPE, bool ABS_ONLY, int EU = 1>
 __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& TFA, float dt32,
                                                const Ray& r, float* __restrict__ tape,
                                                bool warp_inside, bool emit, int mode,
@@ -1185,7 +1189,8 @@ __device__ __forceinline__ void march_dispatch(const VolArgs& V, const TfArgs& T
   const bool aff = !EARLY && !TAPE && !emit && info[2] == 0u;
   const float aa = __uint_as_float(info[3]), ab = __uint_as_float(info[4]);
 #define DDVR_MARCH(SEG, INS, EM) \
-  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM, kTfTexture>(V, TFA, dt32, r, tape, rgba, S)
+  march_ray<EARLY, CELLS, TAPE, SEG, INS, EM, kTfTexture, false, false, EU>(V, TFA, dt32, r, tape, \
+                                                                          rgba, S)
 #define DDVR_MARCH_SEG(INS, EM)                  \
   if (mode == kSegP3) DDVR_MARCH(kSegP3, INS, EM); \
   else if (mode == kSegP7) DDVR_MARCH(kSegP7, INS, EM); \
@@ -1943,10 +1948,9 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     double loss_part = 0.0;
     float4 rgba = make_float4(0.f, 0.f, 0.f, 0.f);
     if (valid) {
-      march_dispatch<false, CELLS, false, ROLE == 1>(V, TFA, G.dt32, r, nullptr, warp_inside,
-                                                     s_info[1] != 0u, mode, rgba, S, s_info,
-                                                     kBitsKernel ? bits : nullptr, bits_off,
-                                                     kBitsKernel ? &march_skip : nullptr);
+      march_dispatch<false, CELLS, false, ROLE == 1, DDVR_EMIT_MARCH_UNROLL>(
+          V, TFA, G.dt32, r, nullptr, warp_inside, s_info[1] != 0u, mode, rgba, S, s_info,
+          kBitsKernel ? bits : nullptr, bits_off, kBitsKernel ? &march_skip : nullptr);
     }
     double S_tot = S;
     float4 after = make_float4(0.f, 0.f, 0.f, 0.f);   // SPLIT: composite of the later segments
