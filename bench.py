@@ -367,7 +367,8 @@ def run_dry(args, cfg):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
-    dist = init_group(world, dev) if world > 1 else None
+    # (under torchrun even one rank forms the process group: the collectives then run)
+    dist = init_group(world, dev) if world > 1 or "WORLD_SIZE" in os.environ else None
     mine = shard_views(cfg.views, rank, world)
     f = FlatGrads.zeros(1024, 16, dev)
     t0 = time.perf_counter()
@@ -417,7 +418,9 @@ def run_own(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = init_group(world, dev) if world > 1 else None
+    # (under torchrun even one rank forms the process group: NCCL init and the
+    # max-over-ranks / all-reduce collectives run)
+    dist = init_group(world, dev) if world > 1 or "WORLD_SIZE" in os.environ else None
     N.lib()
 
     # --- synthetic inputs of the named shape ---

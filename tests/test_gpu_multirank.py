@@ -76,3 +76,29 @@ def test_two_rank_step_equals_single_process(tmp_path):
     v0 = torch.load(tmp_path / "vol0.pt")
     v1 = torch.load(tmp_path / "vol1.pt")
     assert torch.equal(v0, v1)                        # replicas stay identical
+
+
+def test_torchrun_single_rank_runs_nccl(tmp_path):
+    """bench.py under torch.distributed.run with one rank on the GPU: the NCCL process
+    group forms (its INIT log names the communicator: nranks 1) and the bench's
+    collectives -- the sample-count all-reduce and the max-over-ranks step time -- run
+    through NCCL; one JSON line comes out.  (The pool gives one GPU: N > 1 runs the same
+    code with the view sharding the gloo tests cover.)"""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "bench.py"), "--gpus", "1", "--config", "C1", "--steps", "2",
+           "--warmup", "3", "--no-extras", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=dict(os.environ, NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT"))
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    log = p.stdout + p.stderr
+    assert "NCCL INFO" in log, log[-2000:]
+    assert "nranks 1" in log.lower() or "nRanks 1" in log, log[-2000:]
