@@ -119,6 +119,9 @@ class ShardedStep:
                  deterministic=False, band_tape="auto", empty_skip=True, stats=None,
                  split_walk=False, ray_split="auto"):
         self.density, self.texels, self.refs, self.dt, self.rig = density, texels, refs, dt, rig
+        if ray_split != "auto" and ray_split not in N.FLAG_RAY_SPLIT:
+            from .errors import InvalidParameterError
+            raise InvalidParameterError(f"ray_split must be 'auto', 1, 2, 4 or 8, not {ray_split!r}")
         R.validate_cameras(lonlat, radius, fov_y_deg)   # field.py:147-156
         self.cams = R.camera_array(lonlat, radius, center, fov_y_deg)
         self.mask = 0

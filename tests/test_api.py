@@ -113,6 +113,19 @@ def test_tensor_path_validates_cameras(ll, radius, fov):
                     fov_y_deg=fov)
 
 
+@pytest.mark.parametrize("split", [3, 0, 16, "8"])
+def test_step_rejects_unknown_ray_splits(split):
+    """ShardedStep's ray_split is 'auto' or one of DDVR_FLAG_RAY_SPLIT_* (1, 2, 4, 8),
+    checked before any GPU work."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    with pytest.raises(vd.InvalidParameterError):
+        ShardedStep(torch.zeros(4, 4, 4), torch.zeros(2, 4),
+                    torch.tensor([[10.0, 20.0]], dtype=torch.float64), torch.zeros(1, 4, 4, 4),
+                    0.1, R.Rig(4, 4), targets=("tf",), ray_split=split)
+
+
 def test_volume_and_tf_validation():
     with pytest.raises(vd.InvalidParameterError):
         vd.DensityVolume(np.zeros((2, 2)))
