@@ -43,17 +43,26 @@ def shard_views(n_views: int, rank: int, world: int) -> list[int]:
 class FlatGrads:
     """The all-reduced quantities of a step: ``buf`` fp32 d_volume, ``tail`` fp64
     [d_tf | d_stepsize | loss] (the kernels accumulate d_tf, d_dt and the loss
-    in fp64 directly into the tail's views)."""
+    in fp64 directly into the tail's views).  ``zeros`` places both, plus one fp64
+    ``aux`` slot that is not reduced (the iteration's prior value), in one byte
+    buffer ``raw``, so zeroing a step is a single fill (one graph node)."""
 
     n_vox: int
     n_tf: int
     buf: torch.Tensor
     tail: torch.Tensor
+    raw: torch.Tensor | None = None
+    aux: torch.Tensor | None = None
 
     @classmethod
     def zeros(cls, n_vox: int, n_tf: int, device) -> "FlatGrads":
-        return cls(n_vox, n_tf, torch.zeros(n_vox, dtype=torch.float32, device=device),
-                   torch.zeros(n_tf + 2, dtype=torch.float64, device=device))
+        n_tail = n_tf + 2
+        off = (8 * (n_tail + 1) + 255) // 256 * 256          # buf 256-byte aligned
+        raw = torch.zeros(off + 4 * n_vox, dtype=torch.uint8, device=device)
+        tail = raw[: 8 * n_tail].view(torch.float64)
+        aux = raw[8 * n_tail: 8 * (n_tail + 1)].view(torch.float64)
+        buf = raw[off: off + 4 * n_vox].view(torch.float32)
+        return cls(n_vox, n_tf, buf, tail, raw, aux)
 
     @property
     def d_volume(self) -> torch.Tensor:
@@ -72,8 +81,11 @@ class FlatGrads:
         return self.tail[self.n_tf + 1:]
 
     def zero_(self) -> None:
-        self.buf.zero_()
-        self.tail.zero_()
+        if self.raw is not None:
+            self.raw.zero_()
+        else:
+            self.buf.zero_()
+            self.tail.zero_()
 
     def allreduce(self, group=None) -> None:
         """Sum both buffers over all ranks in place (the fp32 volume gradient and the
@@ -379,7 +391,8 @@ class TomographyIteration:
         f = self.step.run(hook=hook, refs_host=refs_host)
         density = self.step.density
         grad = f.d_volume.view(density.shape)
-        prior = prior_volume(density, self.lam, grad)      # grad += lam * d prior
+        # grad += lam * d prior; the value into the step's zeroed aux slot
+        prior = prior_volume(density, self.lam, grad, out=f.aux)
         self.adam.update(density, grad, project="volume",
                          check_finite="defer" if self.check_finite else False)
         return f.loss, prior

@@ -31,10 +31,18 @@ def _dims(values):
     return (ctypes.c_int32 * 3)(*values.shape)
 
 
-def prior_volume(values: torch.Tensor, weight: float = 1.0, grad: torch.Tensor | None = None):
-    """weight * smoothness_prior_volume: returns the value (1,) f64; grad += weight * dP/dv."""
+def prior_volume(values: torch.Tensor, weight: float = 1.0, grad: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None):
+    """weight * smoothness_prior_volume: returns the value (1,) f64; grad += weight * dP/dv.
+    ``out``: a (1,) f64 device tensor the value is ADDED to (the caller zeroes it),
+    instead of a fresh zeroed one."""
     _require(values, "volume", torch.float32, ndim=3)
-    out = torch.zeros(1, dtype=torch.float64, device=values.device)
+    if out is None:
+        out = torch.zeros(1, dtype=torch.float64, device=values.device)
+    else:
+        _require(out, "prior value", torch.float64)
+        if out.numel() != 1:
+            raise InvalidParameterError("the prior value output holds one float64")
     if grad is not None:
         _require(grad, "gradient", torch.float32)
     N.check(N.lib().ddvr_prior_volume(values.data_ptr(), _dims(values), float(weight),

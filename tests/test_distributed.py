@@ -85,7 +85,7 @@ def _worker(rank, world, port, out_path):
         flat = _rank_grads(rank, world)
         flat.allreduce()
         if rank == 0:
-            torch.save((flat.buf, flat.tail), out_path)
+            torch.save((flat.buf.clone(), flat.tail.clone()), out_path)   # (views of one buffer)
     finally:
         dist.destroy_process_group()
 
