@@ -80,7 +80,7 @@ def parse(argv=None):
     p.add_argument("--unfused", action="store_true",
                    help="separate forward / L1 / adjoint launches instead of the fused step")
     p.add_argument("--fused", action="store_true",
-                   help="the fused step also for camera / stepsize targets")
+                   help="the fused step also for camera / stepsize targets with the TF target")
     p.add_argument("--no-empty-skip", action="store_true",
                    help="band tape without the empty-brick skip of the march")
     p.add_argument("--no-band-tape", action="store_true",

@@ -106,9 +106,11 @@ class ShardedStep:
     adjoint run as one fused kernel per ray (ddvr_forward_adjoint_l1);
     ``fused=False`` keeps the three separate launches (ddvr_forward,
     ddvr_l1_loss, ddvr_adjoint).  ``fused="auto"`` (default) fuses unless the
-    camera or stepsize target is on: their walks carry fp64 sums (~100
-    registers), which would hold the fused forward phase to 2 CTAs/SM where
-    the separate forward runs 5 (C3: 58 vs 65 G samples/s).  ``keep_images``: also write the rendered
+    camera or stepsize target comes with the TF target: those walks carry fp64
+    sums and texel runs (~128 registers, 2 CTAs/SM), which would hold the fused
+    forward phase there while the separate forward runs 5 CTAs/SM.  Camera /
+    stepsize alone fuse (64-register walks: C3 82.3 vs 78.6 G samples/s
+    separate).  ``keep_images``: also write the rendered
     images / optical depth of the fused step into ``img`` / ``depth``.
     ``deterministic``: camera / stepsize gradients reduced from per-CTA partials in a
     fixed order (DDVR_FLAG_DETERMINISTIC), bitwise reproducible step to step.
@@ -164,7 +166,8 @@ class ShardedStep:
         self.split_walk = bool(split_walk)
         self.ray_split = ray_split
         if fused == "auto":
-            fused = not self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
+            pos = self.mask & (N.TARGET_CAMERA | N.TARGET_STEPSIZE)
+            fused = not (pos and self.mask & N.TARGET_TF)
         self.fused = bool(fused) and self.cells is not None
         vol, _, prm = R._descs(density, texels, rig, dt, False, self.cells)
         self.band_tape = bool(band_tape) and self.fused and self.mask == N.TARGET_VOLUME
