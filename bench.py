@@ -790,6 +790,14 @@ def report(args, cfg, step, runner, world, mine, total_samples, total_rays, loca
                                else "") +
                               (", march and walk as two kernels" if band and step.split_walk
                                else "") + (", CUDA-graph replay" if graphed else ""))
+    if fused:   # threads per ray of the fused kernel (DDVR_FLAG_RAY_SPLIT_*, ddvr_ray_split)
+        from paper_2107_12672_b200 import _native as N
+        sflags = (0 if step.ray_split == "auto" else N.FLAG_RAY_SPLIT[step.ray_split]) | \
+            (N.FLAG_DETERMINISTIC if step.deterministic else 0)
+        k = int(N.lib().ddvr_ray_split(step.mask, local_rays, sflags))
+        line["config"]["lanes_per_ray"] = k
+        if k > 1:
+            line["config"]["step"] += f", {k} lanes per ray (segment-split rays)"
     if band:
         from paper_2107_12672_b200 import _native as N
         from paper_2107_12672_b200 import raymarch as R

@@ -107,9 +107,9 @@ typedef struct {
 #define DDVR_FLAG_BAND_TAPE 8
 #define DDVR_FLAG_NO_EMPTY_SKIP 16
 #define DDVR_FLAG_SPLIT_WALK 32
-/* segment-split rays of a fused TF-target step (ddvr_forward_adjoint_l1, masks TF and
-   TF|VOLUME): by default chosen from the ray count (a step too small to fill the GPU
-   with one thread per ray gets 2, 4 or 8 threads per ray); these force it (at most one) */
+/* segment-split rays of a fused step (ddvr_forward_adjoint_l1, masks TF, TF|VOLUME and
+   camera / stepsize alone): by default chosen from the ray count (ddvr_ray_split); these
+   force it (at most one) */
 #define DDVR_FLAG_RAY_SPLIT_OFF 64
 #define DDVR_FLAG_RAY_SPLIT_2 128
 #define DDVR_FLAG_RAY_SPLIT_4 256
@@ -273,9 +273,11 @@ int64_t ddvr_deterministic_bytes(const ddvr_volume* vol, int32_t n_views, const 
 int64_t ddvr_band_tape_bytes(const ddvr_volume* vol, int32_t n_views, const ddvr_params* p);
 
 /* Threads per ray ddvr_forward_adjoint_l1 uses for this target mask, ray count
- * (views x band rows x width) and params.flags (DDVR_FLAG_RAY_SPLIT_*): 1 (one thread
- * per ray) unless the mask is TF or TF|VOLUME and the rays alone would not fill the
- * GPU, then the smallest of 2, 4, 8 giving ~113 K threads.  Host-side, no GPU work. */
+ * (views x band rows x width) and params.flags (DDVR_FLAG_RAY_SPLIT_*): for TF or
+ * TF|VOLUME, 1 unless the rays alone would not fill the GPU, then the smallest of 2, 4, 8
+ * giving ~113 K threads; for camera and / or stepsize alone, 2 below ~606 K rays (fewer
+ * than 4 waves of one thread per ray), else 1, never with DDVR_FLAG_DETERMINISTIC (forced:
+ * 2 or 4); other masks 1.  Host-side, no GPU work. */
 int32_t ddvr_ray_split(uint32_t mask, int64_t rays, int32_t flags);
 
 /* Size of the cell-record copy of a dims[0] x dims[1] x dims[2] volume:

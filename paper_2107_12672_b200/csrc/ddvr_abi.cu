@@ -946,6 +946,18 @@ static int64_t grid_ctas(int32_t n_views, const ddvr_params* p) {
 // gives ~113 K threads (148 SMs x 3 CTAs x 256), else 1.  DDVR_SPLIT=1|2|4|8 in the
 // environment overrides it (A/B measurements; 16 only there).
 static int split_of(uint32_t mask, long long rays, int32_t flags) {
+  // camera / stepsize alone (no TF, no volume): 2 or 4 lanes per ray, not with the
+  // deterministic mode (its partials are per CTA of the one-thread-per-ray grid); by default
+  // 2 while one thread per ray would run under 4 waves of 4 CTAs/SM -- halving the CTAs'
+  // length halves the last wave's tail (C3: 1.7 waves, 82.4 -> 88.3 G samples/s)
+  const bool pos = mask && !(mask & ~(uint32_t)(DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE));
+  if (pos) {
+    if (flags & (DDVR_FLAG_DETERMINISTIC | DDVR_FLAG_RAY_SPLIT_OFF | DDVR_FLAG_RAY_SPLIT_8))
+      return 1;
+    if (flags & DDVR_FLAG_RAY_SPLIT_2) return 2;
+    if (flags & DDVR_FLAG_RAY_SPLIT_4) return 4;
+    return rays < 4ll * 148 * 4 * kThreads ? 2 : 1;
+  }
   if (mask != DDVR_TARGET_TF && mask != (DDVR_TARGET_TF | DDVR_TARGET_VOLUME)) return 1;
   if (flags & DDVR_FLAG_RAY_SPLIT_OFF) return 1;
   if (flags & DDVR_FLAG_RAY_SPLIT_2) return 2;
@@ -1164,7 +1176,7 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   }
   const int n_kernels =
       split > 1 ? launch_adjoint_split(mask, split, n_views, smem, st, V, T, G, d_volume, d_cells,
-                                       *fu)
+                                       d_camera, d_dt, *fu)
                 : launch(mask, cells, grid, smem, st, V, T, G, image, depth, seed, d_volume,
                          d_cells, d_camera, d_dt, fu);
   if ((rc = check_launch(fu ? "dvr_adjoint_kernel (fused)" : "dvr_adjoint_kernel"))) return rc;

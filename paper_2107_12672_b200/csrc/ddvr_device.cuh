@@ -223,7 +223,7 @@ DDVR_ADJ_LAUNCHER(launch_adjoint_g3);   // masks 12-15 (volume + tf [+ ...])
 // the kernels launched (0: not instantiated)
 int launch_adjoint_split(unsigned mask, int split, int n_views, size_t smem, cudaStream_t st,
                          const VolArgs& V, const TfArgs& T, const Geometry& G, float* dv,
-                         float* dcells, const FusedArgs& fu);
+                         float* dcells, double* dcam, double* ddt, const FusedArgs& fu);
 
 #ifndef DDVR_CARVEOUT
 #define DDVR_CARVEOUT -1
@@ -1268,12 +1268,15 @@ constexpr int adj_min_blocks(unsigned mask, int role, bool cells, bool fused) {
 #ifdef DDVR_ADJ_MINB
 #define DDVR_ADJ_BOUNDS __launch_bounds__(kThreads, DDVR_ADJ_MINB)
 #else
-// (segment-split steps are small: 2 CTAs/SM, the registers of the unsplit TF walk's spills)
+// (segment-split TF steps are small: 2 CTAs/SM, the registers of the unsplit TF walk's
+// spills; split camera / stepsize walks keep their 4 CTAs/SM)
 #ifndef DDVR_SPLIT_MINB
 #define DDVR_SPLIT_MINB 2
 #endif
-#define DDVR_ADJ_BOUNDS \
-  __launch_bounds__(kThreads, SPLIT > 1 ? DDVR_SPLIT_MINB : adj_min_blocks(MASK, ROLE, CELLS, FUSED))
+#define DDVR_ADJ_BOUNDS                                                                   \
+  __launch_bounds__(kThreads, SPLIT > 1 && !(MASK & (DDVR_TARGET_CAMERA | DDVR_TARGET_STEPSIZE)) \
+                                  ? DDVR_SPLIT_MINB                                         \
+                                  : adj_min_blocks(MASK, ROLE, CELLS, FUSED))
 #endif
 template <bool EARLY, bool CELLS, bool TAPE>
 __global__ void __launch_bounds__(kThreads, TAPE ? 4 : DDVR_FWD_MINB) dvr_forward_kernel(VolArgs V, TfArgs TFA, Geometry G,
@@ -1388,6 +1391,7 @@ struct AdjState {
   // camera / stepsize per-ray sums (grid units) in fp64: thousands of terms
   // with cancellation (the per-sample terms stay fp32)
   double s1x, s1y, s1z, s2x, s2y, s2z, dt_bl, dt_pos;
+  int i_off;   // sample index of the walk's first sample on the whole ray (segment-split rays)
 };
 
 // The backward walk of one ray (renderer.py:547-626).
@@ -1636,7 +1640,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
         st.acc8[6] += y11 * ex; st.acc8[7] += y11 * fx;
       }
       if (kPos && live) {   // renderer.py:609-623 (spatial gradient, field.py:446-484)
-        const float t = __fmul_rn((float)i, dt32);
+        const float t = __fmul_rn((float)(i + st.i_off), dt32);
         const float ddx = ip.gx;                     // field.py:446-484 from the partials
         const float ddy = interp_gy(c, v);
         const float ddz = interp_gz(c, ip);
@@ -1648,7 +1652,7 @@ __device__ __forceinline__ void adjoint_ray(const VolArgs& V, const TfArgs& TF, 
           st.s2x += (double)(t * bx); st.s2y += (double)(t * by); st.s2z += (double)(t * bz);
         }
         if (kStep)
-          st.dt_pos += (double)((float)i * (r.gw[0] * bx + r.gw[1] * by + r.gw[2] * bz));
+          st.dt_pos += (double)((float)(i + st.i_off) * (r.gw[0] * bx + r.gw[1] * by + r.gw[2] * bz));
       }
     }
     gx -= r.gs[0]; gy -= r.gs[1]; gz -= r.gs[2];
@@ -1891,8 +1895,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   // the tf target needs the rgb channels even when they are zero
   const bool emit = kTf || s_info[1] != 0u;
 
-  static_assert(SPLIT == 1 || (FUSED && !kPos && kThreads % (8 * SPLIT) == 0 && 32 % SPLIT == 0),
-                "segment-split rays: fused steps without camera / stepsize targets");
+  static_assert(SPLIT == 1 || (FUSED && kThreads % (8 * SPLIT) == 0 && 32 % SPLIT == 0),
+                "segment-split rays: fused steps");
   int px, py, seg = 0;
   if (SPLIT > 1) {   // ray (threadIdx / SPLIT) of an 8 x (kThreads / SPLIT / 8) tile
     const int rid = threadIdx.x / SPLIT;
@@ -1923,12 +1927,14 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     }
   }
   const bool warp_inside = CELLS && __all_sync(0xffffffffu, r.all_inside);
+  int seg_i0 = 0;   // the segment's first sample on the whole ray
   if (SPLIT > 1 && valid) {   // this lane's segment [i0, i1) of the ray's samples
     const int i0 = (int)((long long)r.n * seg / SPLIT);
     const int i1 = (int)((long long)r.n * (seg + 1) / SPLIT);
 #pragma unroll
     for (int k = 0; k < 3; ++k) r.g0[k] += (long long)i0 * r.gs[k];
     r.n = i1 - i0;
+    seg_i0 = i0;
   }
   // affine, non-negative tau column (the ramp), polynomial segment modes, no
   // stepsize target: the table-free walk
@@ -2016,6 +2022,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   st.tfa1 = make_float4(0, 0, 0, 0);
   st.tfp0 = st.tfp1 = 0.f;
   st.s1x = st.s1y = st.s1z = st.s2x = st.s2y = st.s2z = st.dt_bl = st.dt_pos = 0.0;
+  st.i_off = seg_i0;
 
 #define DDVR_WALK(SEG, INS, EM)                                                          \
   adjoint_ray<MASK, CELLS, SEG, INS, EM, kTfTexture, false, false, DET>(                   \

@@ -281,9 +281,10 @@ def test_band_tape_bytes_and_limits(lib):
 
 
 def test_ray_split_choice(lib):
-    """Segment-split rays (DDVR_FLAG_RAY_SPLIT_*): only fused TF-target masks without
-    camera / stepsize split, by default only when the rays alone would not fill the
-    GPU (C1's 16 K rays: 8 threads per ray; C2's 524 K: 1); the flags force it."""
+    """Segment-split rays (DDVR_FLAG_RAY_SPLIT_*): fused TF-target masks split by default
+    only when the rays alone would not fill the GPU (C1's 16 K rays: 8 threads per ray;
+    C2's 524 K: 1), camera / stepsize alone in two below four waves (C3), masks mixing
+    them with TF or volume never; the flags force it."""
     from paper_2107_12672_b200 import _native as N
     TF, VOL, CAM = N.TARGET_BITS["tf"], N.TARGET_BITS["volume"], N.TARGET_BITS["camera"]
     split = lib.ddvr_ray_split
@@ -296,3 +297,13 @@ def test_ray_split_choice(lib):
     for k, flag in N.FLAG_RAY_SPLIT.items():
         assert split(TF | VOL, 128 * 128, flag) == k
         assert split(TF, 10 ** 8, flag) == k
+    # camera / stepsize alone: 2 lanes below 4 waves (forced: 2 or 4), never deterministic
+    STEP = N.TARGET_BITS["stepsize"]
+    for mask in (CAM, STEP, CAM | STEP):
+        assert split(mask, 512 * 512, 0) == 2               # C3: 1.7 waves one thread per ray
+        assert split(mask, 8 * 1024 * 1024, 0) == 1
+        assert split(mask, 100, N.FLAG_RAY_SPLIT[1]) == 1
+        assert split(mask, 100, N.FLAG_RAY_SPLIT[2]) == 2
+        assert split(mask, 10 ** 6, N.FLAG_RAY_SPLIT[4]) == 4
+        assert split(mask, 100, N.FLAG_RAY_SPLIT[8]) == 1
+        assert split(mask, 100, N.FLAG_RAY_SPLIT[4] | N.FLAG_DETERMINISTIC) == 1

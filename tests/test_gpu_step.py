@@ -452,3 +452,39 @@ def test_fused_step_ray_split_matches_one_thread_per_ray(cuda, kind, targets):
         assert rel_l2(dtf, dtf1) <= 1e-5, (split, rel_l2(dtf, dtf1))
         if "volume" in targets:
             assert rel_l2(dvol, dvol1) <= 1e-5, (split, rel_l2(dvol, dvol1))
+
+
+@pytest.mark.parametrize("split", [2, 4])
+def test_fused_camera_step_ray_split_matches_one_thread_per_ray(cuda, split):
+    """Camera / stepsize targets with forced segment-split rays (DDVR_FLAG_RAY_SPLIT_2/4):
+    every segment walks with its samples' whole-ray indices (t = i dt) and its partial
+    sums go through the same per-ray Jacobian chain (linear in them), so the per-view
+    camera gradients, the stepsize gradient, the image and the loss agree with one thread
+    per ray up to the summation order."""
+    import torch
+    from paper_2107_12672_b200 import raymarch as R
+    from paper_2107_12672_b200.distributed import ShardedStep
+    rng = np.random.default_rng(31)
+    n = 20
+    vol = torch.from_numpy(rng.uniform(0.0, 1.0, (n, n, n)).astype(np.float32)).to(cuda)
+    tf = rng.uniform(0.1, 1.0, (16, 4)) * np.array([1, 1, 1, 6.0])
+    tx = torch.from_numpy(tf.astype(np.float32)).to(cuda)
+    ll = torch.tensor([[25.0, 10.0], [200.0, -40.0], [95.0, 65.0]], dtype=torch.float64,
+                      device=cuda)
+    W, H = 21, 19
+    refs = torch.from_numpy(rng.choice([-1.0, 2.0], (3, H, W, 4)).astype(np.float32)).to(cuda)
+    out = {}
+    for k in (1, split):
+        step = ShardedStep(vol, tx, ll, refs, 0.6 / n, R.Rig(W, H), targets=("camera", "stepsize"),
+                           radius=2.0, keep_images=True, fused=True, ray_split=k)
+        f = step.run()
+        torch.cuda.synchronize()
+        out[k] = (step.img.double().cpu().numpy(), float(f.loss),
+                  step.d_camera.double().cpu().numpy(), float(f.d_stepsize))
+    img1, loss1, cam1, dt1 = out[1]
+    img, loss, cam, dtk = out[split]
+    assert np.abs(cam1).max() > 0 and dt1 != 0.0
+    assert rel_l2(img, img1) <= 1e-6
+    assert abs(loss - loss1) <= 1e-6 * abs(loss1)
+    assert rel_l2(cam, cam1) <= 1e-5, rel_l2(cam, cam1)
+    assert abs(dtk - dt1) <= 1e-5 * abs(dt1)
