@@ -19,7 +19,7 @@ cap() {  # name, kernel regex, count, bench args...
 cap C4 'int\)1, \(bool\)1, \(bool\)0, \(int\)1>' 1
 cap C5 'dvr_adjoint_kernel' 1 --config C5 --views 16
 cap C2 'dvr_adjoint_kernel' 1 --config C2
-cap C3 'dvr_adjoint_kernel|dvr_forward_kernel' 3 --config C3
+cap C3 'dvr_adjoint_kernel' 1 --config C3
 cap C1 'dvr_adjoint_kernel' 1 --config C1 --graph off
 ls -la gpurun_out/final
 fi
