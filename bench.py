@@ -94,6 +94,9 @@ def parse(argv=None):
     p.add_argument("--ray-split", default="auto", choices=["auto", "1", "2", "4", "8"],
                    help="fused TF-target steps: threads per ray (DDVR_FLAG_RAY_SPLIT_*; auto "
                         "splits steps too small to fill the GPU, e.g. C1)")
+    p.add_argument("--sort-views", action="store_true",
+                   help="experiment: order the views by direction (latitude bands, then "
+                        "longitude) so that neighbouring views are similar")
     p.add_argument("--dry-run", action="store_true",
                    help="launcher / collective check without kernels (gloo on CPU if no GPU)")
     return p.parse_args(argv)
@@ -427,6 +430,11 @@ def run_own(args, cfg):
     truth = torch.from_numpy(cfg.volume()).to(dev)
     tex = torch.from_numpy(cfg.texels().astype(np.float32)).to(dev)
     poses = cfg.view_poses()
+    if args.sort_views:   # latitude bands of 22.5 degrees, serpentine in longitude
+        def _key(p):
+            band = int((p[1] + 90.0) // 22.5)
+            return (band, p[0] if band % 2 == 0 else -p[0])
+        poses = sorted(poses, key=_key)
     if args.views:
         poses = poses[: args.views]
     mine = shard_views(len(poses), rank, world)

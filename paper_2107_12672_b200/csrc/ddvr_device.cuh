@@ -170,6 +170,7 @@ struct Geometry {
                                // walk skipped, rays], one atomic per warp
   float* ray_k;           // band-tape step split into march + walk kernels (nullable): the
                           // march's per-ray walk weight abs_k, (V, rows, W)
+  int vgroup;             // CTAs cycle over groups of this many views per tile (1: view-major)
 };
 
 // Launchers with external linkage: each is defined (with its kernel
@@ -995,10 +996,29 @@ __device__ __forceinline__ int seg_mode(float dt32, unsigned maxtau_bits) {
   return xmax < 0.00896f ? kSegP3 : (xmax < 0.34657359f ? kSegP7 : kSegGen);
 }
 
-__device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
+__device__ __forceinline__ void pixel_of_tile(const Geometry& G, int tx, int ty, int& px, int& py) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  px = blockIdx.x * kTile + (warp & 1) * 8 + (lane & 7);
-  py = G.row0 + blockIdx.y * kTile + (warp >> 1) * 4 + (lane >> 3);
+  px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  py = G.row0 + ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+}
+__device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
+  pixel_of_tile(G, blockIdx.x, blockIdx.y, px, py);
+}
+
+// CTA -> (view, tile) with view groups (G.vgroup > 1): consecutive CTAs cycle over vgroup
+// consecutive views on the same tile, so views of similar direction (when the caller
+// orders them so) march nearly coincident ray tubes at the same time and share records
+// and gradient lines in L2.  Bijective; the last group may hold fewer views.
+__device__ __forceinline__ void cta_view_tile(int vg, int& view, int& tx, int& ty) {
+  const unsigned tiles = gridDim.x * gridDim.y;
+  const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned g0 = b / ((unsigned)vg * tiles) * (unsigned)vg;
+  const unsigned gs = min((unsigned)vg, gridDim.z - g0);
+  const unsigned r = b - g0 * tiles;
+  const unsigned tile = r / gs;
+  view = (int)(g0 + (r - tile * gs));
+  tx = (int)(tile % gridDim.x);
+  ty = (int)(tile / gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1875,7 +1895,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
                                          ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
                                            (size_t)blockIdx.z)) % TFA.nslot)
                        : nullptr;
-  const int view = blockIdx.z;
+  int view = blockIdx.z, tile_x = blockIdx.x, tile_y = blockIdx.y;
+  if (SPLIT == 1 && G.vgroup > 1) cta_view_tile(G.vgroup, view, tile_x, tile_y);
   if (threadIdx.x < 5) s_info[threadIdx.x] = 0u;
   __syncthreads();
   load_tf(TFA, s_info);
@@ -1904,7 +1925,7 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
     px = blockIdx.x * 8 + (rid & 7);
     py = G.row0 + blockIdx.y * (kThreads / SPLIT / 8) + (rid >> 3);
   } else {
-    pixel_of(G, px, py);
+    pixel_of_tile(G, tile_x, tile_y, px, py);
   }
   const bool valid = px < G.W && py < G.row1;
 
@@ -1946,9 +1967,11 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
   constexpr bool kBitsKernel = FUSED && ROLE == 1 && CELLS && MASK == DDVR_TARGET_VOLUME;
   // (the host keeps the tape under 2^32 words: 32-bit word indices)
   unsigned* bits = kBitsKernel && G.bits && aff_walk ? G.bits : nullptr;
+  // (by the logical CTA index tile + tiles * view: the same layout whatever order the CTAs
+  // ran in, and the same as the split march / walk kernels')
   const unsigned bits_off =
-      ((blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * kWarps +
-       (threadIdx.x >> 5)) * 32u * (unsigned)G.bits_words + (threadIdx.x & 31);
+      ((tile_x + gridDim.x * (tile_y + gridDim.y * view)) * kWarps + (threadIdx.x >> 5)) *
+          32u * (unsigned)G.bits_words + (threadIdx.x & 31);
   int march_skip = 0, walk_skip = 0;   // measurement counters (G.stats)
   if (FUSED) {   // forward march (renderer.py:306-357) + L1 seed (objectives.py:38-54)
     double loss_part = 0.0;
@@ -2142,8 +2165,8 @@ __global__ void DDVR_ADJ_BOUNDS dvr_adjoint_kernel(
       double t0 = 0, t1 = 0, t2 = 0;
       for (int k = 0; k < kWarps; ++k) { t0 += s_red[k][0]; t1 += s_red[k][1]; t2 += s_red[k][2]; }
       if (G.partials) {   // deterministic mode: reduced in CTA order afterwards
-        double* q = G.partials + 3 * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y *
-                                                                (size_t)blockIdx.z));
+        // (the logical CTA index tile + tiles * view, whatever order the CTAs ran in)
+        double* q = G.partials + 3 * (tile_x + gridDim.x * (tile_y + gridDim.y * (size_t)view));
         q[0] = t0; q[1] = t1; q[2] = t2;
       } else {
         if (kCam) { atomicAdd(d_camera + 2 * view, t0); atomicAdd(d_camera + 2 * view + 1, t1); }
