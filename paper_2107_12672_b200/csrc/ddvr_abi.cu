@@ -1097,12 +1097,12 @@ static int run_adjoint(const ddvr_volume* vol, const ddvr_tf* tf, VolArgs& V, Tf
   }
   // View groups (cta_view_tile): the adjoint / fused CTAs cycle over 4 views per tile
   // instead of running view after view (C4 263 -> 278 G samples/s, with or without views
-  // ordered by direction).  DDVR_VGROUP=1|2|4|8 in the environment overrides it (A/B).
+  // ordered by direction).  DDVR_VGROUP=<n> in the environment overrides it (A/B).
   {
     static const int vg = [] {
       const char* e = std::getenv("DDVR_VGROUP");
       const int v = e ? std::atoi(e) : 4;
-      return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+      return v >= 1 && v <= 4096 ? v : 4;
     }();
     G.vgroup = n_views > 1 ? vg : 1;
   }
