@@ -1006,9 +1006,10 @@ __device__ __forceinline__ void pixel_of(const Geometry& G, int& px, int& py) {
 }
 
 // CTA -> (view, tile) with view groups (G.vgroup > 1): consecutive CTAs cycle over vgroup
-// consecutive views on the same tile, so views of similar direction (when the caller
-// orders them so) march nearly coincident ray tubes at the same time and share records
-// and gradient lines in L2.  Bijective; the last group may hold fewer views.
+// consecutive views on the same tile instead of running view after view.  Measured: C4's
+// fused step 68.2 -> 64.8 ms with groups of 4, whether or not the views are ordered by
+// direction (so not by L2 sharing of similar ray tubes; DRAM traffic 103 -> 94 GB per
+// launch).  Bijective; the last group may hold fewer views.
 __device__ __forceinline__ void cta_view_tile(int vg, int& view, int& tx, int& ty) {
   const unsigned tiles = gridDim.x * gridDim.y;
   const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
