@@ -798,6 +798,9 @@ def report(args, cfg, step, runner, world, mine, total_samples, total_rays, loca
                                else "") +
                               (", march and walk as two kernels" if band and step.split_walk
                                else "") + (", CUDA-graph replay" if graphed else ""))
+    if len(mine) > 1:   # CTA order of the adjoint / fused kernels (cta_view_tile)
+        line["config"]["cta_order"] = (f"view groups of {os.environ.get('DDVR_VGROUP', '4')} "
+                                       f"views per tile")
     if fused:   # threads per ray of the fused kernel (DDVR_FLAG_RAY_SPLIT_*, ddvr_ray_split)
         from paper_2107_12672_b200 import _native as N
         sflags = (0 if step.ray_split == "auto" else N.FLAG_RAY_SPLIT[step.ray_split]) | \
